@@ -1,0 +1,156 @@
+/*
+ * libtdvp — B200-native hot path of the parallel two-site TDVP (p2TDVP) for
+ * matrix product states, Secular et al., arXiv:1912.06127.
+ *
+ * C-ABI boundary.  Plain pointers and sizes only.
+ *
+ * Conventions (SURVEY.md §8 "Conventions"):
+ *   - complex numbers are interleaved (re, im) doubles (= numpy complex128);
+ *   - all tensors are row-major;
+ *   - site tensor Psi_j: (chi_j, d, chi_{j+1}) where chi[] has L+1 entries,
+ *     chi[0] = chi[L] = 1 (chi[b+1] is the bond between sites b and b+1);
+ *   - MPO tensor W_j: (D[j], d_out, d_in, D[j+1]) with W[w,s,t,w'] = <s|O|t>,
+ *     D[] has L+1 entries with D[0] = D[L] = 1;
+ *   - Lambda_b (bond b between sites b, b+1, b = 0..L-2): chi[b+1] float64,
+ *     descending, strictly positive; V_b = 1/Lambda_b.
+ *
+ * Ownership: every input is copied; the caller keeps its buffers.  Outputs
+ * go to caller-allocated buffers.  A handle owns all device memory it
+ * allocates and is not thread-safe; distinct handles are independent.
+ *
+ * Errors: functions return 0 on success or a negative code, with a message
+ * in tdvp_last_error(handle).  No C++ exception crosses the ABI.
+ */
+#ifndef TDVP_H
+#define TDVP_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDVP_OK 0
+#define TDVP_EARG -1      /* bad argument: L<2, d<2, chi_max<1, dims mismatch, ends != 1 */
+#define TDVP_ENONFINITE -2 /* non-finite input or Lambda <= 0 */
+#define TDVP_EPARTITION -3 /* n_segments not 1 or even with 2 <= p <= L/2, segment < 2 sites,
+                              or p != world size in multi-process mode */
+#define TDVP_ECUDA -4     /* CUDA / NCCL failure (incl. no device) */
+#define TDVP_ENUMERIC -5  /* NaN after exp or SVD, or all singular values zero */
+#define TDVP_ESTATE -6    /* call order: MPO/MPS not set */
+
+typedef struct tdvp_ctx* tdvp_t;
+
+/* Truncation and Krylov knobs; defaults mirror PAPER.md:100 (S-IV). */
+typedef struct {
+  double eps;             /* relative SV cutoff epsilon, drop sigma < eps*sigma_1; default 1e-12 */
+  double w_max;           /* max discarded weight per SVD; 0 = off (default) */
+  int krylov_k;           /* Krylov vectors K, 1..15 ("maximum of 8"); default 8 */
+  double krylov_tol;      /* reserved: only 0 (fixed K, parity mode, SURVEY AMB-5) is implemented */
+  double multiplet_delta; /* AMB-9 multiplet guard at the chi_max cut; default 1e-6 */
+  int timing;             /* 1: record CUDA events around every H_eff matvec and SVD (stats) */
+} tdvp_params;
+
+typedef struct {
+  double w_step;          /* discarded weight summed over all SVDs of the last step (eq:discweight) */
+  double w_total;         /* cumulative over all steps */
+  int trunc_active;       /* chi_max / w_max / multiplet guard cut something in the last step */
+  int n_pair, n_back;     /* two-site and one-site updates in the last step */
+  int krylov_breakdowns;  /* cumulative Lanczos breakdowns (invariant subspace found) */
+  int svd_sweeps_max;     /* max Jacobi sweeps of any SVD in the last step */
+  double step_ms;         /* device time of the last step (CUDA events) */
+  double heff2_ms;        /* summed device time of all H_eff^(2) matvecs in the last step (timing=1) */
+  double heff2_flop;      /* algorithmic real flops of those matvecs */
+  int heff2_calls;
+  double heff1_ms, heff1_flop;
+  double svd_ms;          /* summed SVD time (timing=1) */
+  long long gemm_launches; /* DMMA GEMM kernel launches in the last step */
+  long long kernel_launches; /* all kernel launches of this library in the last step */
+} tdvp_stats;
+
+/* Create a handle for an L-site chain of local dimension d, MPO bond dimension
+ * up to D_mpo and bond dimension cap chi_max, on the current CUDA device.
+ * Allocates per-site buffers at chi_j^max = min(d^j, d^(L-j), chi_max). */
+int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out);
+
+int tdvp_set_params(tdvp_t h, const tdvp_params* p);
+int tdvp_get_params(tdvp_t h, tdvp_params* p);
+
+/* Copy the MPO.  D: L+1 bond dims (ends 1, each <= D_mpo); W[j] points to
+ * D[j]*d*d*D[j+1] complex values (interleaved). */
+int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W);
+
+/* Copy an inverse-canonical MPS (must be exactly
+ * inverse-canonical).  chi: L+1 bond dims (ends 1,
+ * chi[b] <= chi_j^max); Psi[j]: chi[j]*d*chi[j+1] complex; Lambda[b]:
+ * chi[b+1] doubles > 0 for b = 0..L-2.  Environments are rebuilt at the next
+ * tdvp_step (sequential initialisation). */
+int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const double* const* Lambda);
+
+/* One full timestep dt (two half-sweeps) with n_segments
+ * partitions (SURVEY App. A protocol).  n_segments = 1 is
+ * serial 2TDVP.  In single-process mode all segments run on this handle's
+ * device (BSP-equivalent order); after tdvp_comm_init each rank runs
+ * segment q = rank and n_segments must equal the world size.  Changing
+ * n_segments rebuilds the environments (sequential section). */
+int tdvp_step(tdvp_t h, double dt, int n_segments);
+
+/* Full-zipper measurements of Psi_0 V_0 Psi_1 ... Psi_{L-1} (any gauge,
+ * normalised by <psi|psi>).  Not on the timed path. */
+int tdvp_measure_sz(tdvp_t h, double* sz /* [L] */);
+int tdvp_measure_energy(tdvp_t h, double* E);
+int tdvp_measure_norm(tdvp_t h, double* norm2 /* <psi|psi> */);
+
+int tdvp_get_stats(tdvp_t h, tdvp_stats* s);
+/* Current bond dimensions (owner view): chi[L+1]. */
+int tdvp_get_chi(tdvp_t h, int* chi);
+/* Copy the current MPS (owner copies) into caller buffers sized by
+ * tdvp_get_chi (or at chi_j^max). */
+int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda);
+
+const char* tdvp_last_error(tdvp_t h);
+void tdvp_destroy(tdvp_t h);
+
+/* ---- multi-process (one rank per GPU, NCCL point-to-point over NVLink) ---- */
+/* Writes a 128-byte ncclUniqueId (call on rank 0, broadcast the bytes). */
+int tdvp_nccl_unique_id(unsigned char* id128);
+/* Join the rank group; afterwards tdvp_step(h, dt, world) runs segment `rank`. */
+int tdvp_comm_init(tdvp_t h, int rank, int world, const unsigned char* id128);
+
+/* ---- host-only schedule (no GPU needed; used by the CPU protocol tests) ----
+ * Writes the op list of segment q in half h (1 or 2) of a p-segment step
+ * into ops[4*i .. 4*i+3] = {kind, j, tau_full, build} and returns the number of
+ * ops (or a negative error).  kind: 1 PAIR(j,j+1), 2 BACK(j), 3 SEND_R
+ * (Psi_{e+1}, Lambda_e, beta_{e+1} -> q+1), 4 RECV_L, 5 SEND_L (Psi_s,
+ * gamma_s -> q-1), 6 RECV_R.  build: bit0 beta_{j+1}, bit1 gamma_j. */
+int tdvp_plan(int L, int p, int h, int q, int* ops, int max_ops);
+/* Segment bounds [s, e] of segment q (SURVEY O-3). */
+int tdvp_partition(int L, int p, int* s, int* e);
+
+/* ---- kernel-level entry points (host buffers; copies inside) -------------
+ * For parity tests of the individual contractions against the oracle.
+ * H_eff^(2) theta: Lenv (cl, Dl, cl), W1 (Dl, d, d, Dm),
+ * W2 (Dm, d, d, Dr), Renv (cr, Dr, cr), theta/out (cl, d, d, cr). */
+int tdvp_apply_heff2(int cl, int cr, int d, int Dl, int Dm, int Dr, const double* Lenv, const double* W1,
+                     const double* W2, const double* Renv, const double* theta, double* out);
+/* H_eff^(1) psi: psi/out (cl, d, cr). */
+int tdvp_apply_heff1(int cl, int cr, int d, int Dl, int Dr, const double* Lenv, const double* W, const double* Renv,
+                     const double* psi, double* out);
+/* beta' = env_left(beta, A, W): beta (cl,Dl,cl), A (cl,d,cr) -> (cr,Dr,cr).
+ * gamma' = env_right(gamma, B, W): gamma (cr,Dr,cr), B (cl,d,cr) -> (cl,Dl,cl). */
+int tdvp_env_left(int cl, int cr, int d, int Dl, int Dr, const double* beta, const double* A, const double* W,
+                  double* out);
+int tdvp_env_right(int cl, int cr, int d, int Dl, int Dr, const double* gamma, const double* B, const double* W,
+                   double* out);
+/* exp(tau H) v for a dense Hermitian n x n H by the device Lanczos (K vectors). */
+int tdvp_expm_lanczos_dense(int n, const double* H, const double* v, double tau_re, double tau_im, int K,
+                            double* out);
+/* Truncated SVD split of an m x n matrix:
+ * writes chi, w, Psi_L (m x chi), Lambda (chi), Psi_R (chi x n). */
+int tdvp_svd_split(int m, int n, const double* M, int chi_max, double eps, double w_max, double delta, int* chi,
+                   double* w, double* psiL, double* lam, double* psiR);
+/* C = op(A) op(B) complex GEMM on the DMMA path (op 0 N, 1 T, 2 C, 3 conj). */
+int tdvp_zgemm(int opA, int opB, int M, int N, int K, const double* A, const double* B, double* C);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDVP_H */

@@ -1,0 +1,66 @@
+// Sparse MPO-channel contraction (the W_j / W_{j+1} stages of H_eff and the
+// environment updates).  The MPO tensors are sparse finite-state machines
+// (nnz(W) = 12 of 100 entries for nearest-neighbour XXZ), so this stage is an
+// HBM-bound gather/FMA over the (chi x chi) plane, not a GEMM: one thread per
+// (outer, inner) point loops over all output channels; consecutive threads
+// walk the contiguous inner index so every load/store is coalesced.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int TPB = 128;
+
+__global__ void __launch_bounds__(TPB) chanmix_kernel(ChanMix cm, int n_inner, const cplx* __restrict__ in,
+                                                      long long so_in, long long si_in, Strides3 ich,
+                                                      cplx* __restrict__ out, long long so_out, long long si_out,
+                                                      Strides3 och) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  // stage the (small) sparse tables in shared memory
+  cplx* s_coef = reinterpret_cast<cplx*>(sm_raw);
+  long long* s_ioff = reinterpret_cast<long long*>(s_coef + cm.nnz);
+  long long* s_ooff = s_ioff + cm.nnz;
+  int* s_row = reinterpret_cast<int*>(s_ooff + cm.n_oc);
+  for (int e = threadIdx.x; e < cm.nnz; e += TPB) {
+    s_coef[e] = cm.coef[e];
+    const int4 c = cm.ic_idx[e];
+    s_ioff[e] = c.x * ich.s0 + c.y * ich.s1 + c.z * ich.s2;
+  }
+  for (int q = threadIdx.x; q < cm.n_oc; q += TPB) {
+    const int4 c = cm.oc_idx[q];
+    s_ooff[q] = c.x * och.s0 + c.y * och.s1 + c.z * och.s2;
+  }
+  for (int q = threadIdx.x; q <= cm.n_oc; q += TPB) s_row[q] = cm.rowptr[q];
+  __syncthreads();
+
+  const int i = blockIdx.x * TPB + threadIdx.x;
+  if (i >= n_inner) return;
+  const long long o = blockIdx.y;
+  const cplx* src = in + o * so_in + i * si_in;
+  cplx* dst = out + o * so_out + i * si_out;
+  for (int q = 0; q < cm.n_oc; ++q) {
+    cplx acc = cmk(0.0, 0.0);
+    const int e1 = s_row[q + 1];
+    for (int e = s_row[q]; e < e1; ++e) cfma(acc, s_coef[e], __ldg(src + s_ioff[e]));
+    dst[s_ooff[q]] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in,
+                    long long si_in, Strides3 in_ch, cplx* out, long long so_out, long long si_out,
+                    Strides3 out_ch) {
+  if (n_outer <= 0 || n_inner <= 0) return cudaSuccess;
+  const size_t sm = (size_t)cm.nnz * (sizeof(cplx) + sizeof(long long)) + (size_t)cm.n_oc * sizeof(long long) +
+                    (size_t)(cm.n_oc + 1) * sizeof(int);
+  static size_t configured = 48 * 1024;
+  if (sm > configured) {
+    cudaError_t e = cudaFuncSetAttribute(chanmix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
+  chanmix_kernel<<<grid, TPB, sm, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out, out_ch);
+  return cudaGetLastError();
+}

@@ -1,0 +1,1406 @@
+// libtdvp engine: device state, local updates, sweep executor, C-ABI.
+//
+// Hot path per two-site update:
+//   a1 merge   Theta = Psi_j diag(V_j) Psi_{j+1}            (row scale + DMMA GEMM)
+//   a2 H_eff   L.theta (DMMA GEMM) -> W_j, W_{j+1} (sparse channel mix) -> .R^T (DMMA GEMM)
+//   a3 Lanczos device-resident K-vector Krylov exp (lanczos.cu)
+//   a4 SVD     blocked one-sided Jacobi + truncation (svd.cu)
+//   a5 env     beta_{j+1} / gamma_j (GEMM, channel mix, GEMM)
+// a6 one-site backward update, a7 schedule (schedule.h), a8 boundary exchange
+// (device copies in single-process mode, NCCL send/recv across ranks).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tdvp.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "schedule.h"
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct TdvpError : std::runtime_error {
+  int code;
+  TdvpError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define CK(expr)                                                                                          \
+  do {                                                                                                    \
+    cudaError_t _e = (expr);                                                                              \
+    if (_e != cudaSuccess)                                                                                \
+      throw TdvpError(TDVP_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" +             \
+                                      std::to_string(__LINE__));                                          \
+  } while (0)
+#define NK(expr)                                                                                          \
+  do {                                                                                                    \
+    if (!nccl().ok) throw TdvpError(TDVP_ECUDA, "libnccl.so.2 could not be loaded");                      \
+    ncclResult_t _r = (expr);                                                                             \
+    if (_r != ncclSuccess) throw TdvpError(TDVP_ECUDA, std::string(#expr) + ": " + nccl().GetErrorString(_r)); \
+  } while (0)
+
+// NCCL is resolved at run time (dlopen) so that the library never pins a
+// libnccl.so.2 different from the one torch.distributed already loaded.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!hd) hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!hd) return api;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(hd, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(hd, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(hd, "ncclCommDestroy");
+  api.Send = (decltype(api.Send))dlsym(hd, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(hd, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(hd, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(hd, "ncclGroupEnd");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(hd, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+           api.GroupEnd && api.GetErrorString;
+  return api;
+}
+
+// ------------------------------------------------------------------ buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b) {
+    release();
+    if (b == 0) b = 16;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  cplx* c() const { return reinterpret_cast<cplx*>(p); }
+  double* d() const { return reinterpret_cast<double*>(p); }
+  int* i() const { return reinterpret_cast<int*>(p); }
+};
+using BufPtr = std::unique_ptr<DevBuf>;
+BufPtr make_buf(size_t bytes) {
+  BufPtr b(new DevBuf());
+  b->alloc(bytes);
+  return b;
+}
+
+// MPO site: CSR tables for the sparse channel stages (values copied from W)
+struct MpoSite {
+  int Dl = 1, Dr = 1;
+  ChanMix cmL;  // (w,t) -> (s,w'): H1, H2 stages, env_left
+  ChanMix cmR;  // (t,w') -> (w,s): env_right
+  std::vector<BufPtr> store;
+};
+
+// Segment: everything one process owns
+struct Segment {
+  int q = 0, s = 0, e = 0;
+  std::vector<int> cb;  // bond dims, L+1 (own view)
+  std::vector<BufPtr> psi, beta, gamma;  // per site (null if not held)
+  std::vector<BufPtr> lam, vinv;         // per bond
+};
+
+}  // namespace
+
+struct tdvp_ctx {
+  int L = 0, d = 0, Dmpo = 0, chi_max = 0;
+  tdvp_params prm{};
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  std::vector<int> cbmax;  // L+1
+  std::vector<MpoSite> mpo;
+  MpoSite mpo_id, mpo_sz;  // D = 1 identity / S^z (measurement)
+  bool have_mpo = false, have_mps = false, envs_valid = false;
+  int layout_p = 0;  // segments currently laid out
+  std::vector<std::pair<int, int>> bounds;
+  std::vector<Segment> segs;
+  // full-state host copy (multi-process initialisation)
+  std::vector<std::vector<double>> h_psi, h_lam;
+  std::vector<int> h_chi;
+  // workspace
+  long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
+  BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, gemm_work, partials;
+  BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
+  BufPtr svd_sigma, svd_order, svd_off, svd_ires, svd_dres, red_res, envA, envB;
+  double* h_pin = nullptr;
+  int* h_ipin = nullptr;
+  LanczosDev lz{};
+  SvdDev sv{};
+  // stats
+  tdvp_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, int>> ev_h2, ev_h1, ev_svd;
+  cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
+  // NCCL
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  BufPtr hdr;
+};
+
+long long g_launch_count = 0;
+long long g_gemm_count = 0;
+
+namespace {
+
+constexpr cplx ONE = {1.0, 0.0}, ZERO = {0.0, 0.0};
+
+// ------------------------------------------------------------ small helpers
+cudaEvent_t ev_get(tdvp_ctx* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->ev_pool.push_back(e);
+  }
+  return h->ev_pool[h->ev_used++];
+}
+int ev_record(tdvp_ctx* h) {
+  const int idx = (int)h->ev_used;
+  CK(cudaEventRecord(ev_get(h), h->st));
+  return idx;
+}
+
+void gemm(tdvp_ctx* h, int opA, int opB, int M, int N, int K, const cplx* A, long long lda, const cplx* B,
+          long long ldb, cplx* C, long long ldc) {
+  CK(zgemm(h->st, opA, opB, M, N, K, ONE, A, lda, B, ldb, ZERO, C, ldc, 1, 0, 0, 0, h->gemm_work->c(),
+           (size_t)h->work_elems));
+  g_gemm_count++;
+  g_launch_count++;
+}
+void cmix(tdvp_ctx* h, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in, long long si_in,
+          Strides3 ich, cplx* out, long long so_out, long long si_out, Strides3 och) {
+  CK(chanmix(h->st, cm, n_outer, n_inner, in, so_in, si_in, ich, out, so_out, si_out, och));
+  g_launch_count++;
+}
+
+// build CSR tables of one MPO site tensor W (Dl, d, d, Dr) (host structure pass;
+// the values are copied, not computed)
+void build_site(MpoSite& ms, int Dl, int Dr, int d, const std::vector<cplx>& W) {
+  ms.Dl = Dl;
+  ms.Dr = Dr;
+  ms.store.clear();
+  auto at = [&](int w, int s, int t, int w2) { return W[(((size_t)w * d + s) * d + t) * Dr + w2]; };
+  auto nz = [](cplx v) { return v.x != 0.0 || v.y != 0.0; };
+  auto upload = [&](ChanMix& cm, const std::vector<int>& rowptr, const std::vector<int4>& oc,
+                    const std::vector<int4>& ic, const std::vector<cplx>& coef) {
+    cm.n_oc = (int)oc.size();
+    cm.nnz = (int)ic.size();
+    BufPtr b1 = make_buf(rowptr.size() * sizeof(int));
+    BufPtr b2 = make_buf(std::max<size_t>(1, oc.size()) * sizeof(int4));
+    BufPtr b3 = make_buf(std::max<size_t>(1, ic.size()) * sizeof(int4));
+    BufPtr b4 = make_buf(std::max<size_t>(1, coef.size()) * sizeof(cplx));
+    CK(cudaMemcpy(b1->p, rowptr.data(), rowptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!oc.empty()) CK(cudaMemcpy(b2->p, oc.data(), oc.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    if (!ic.empty()) CK(cudaMemcpy(b3->p, ic.data(), ic.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    if (!coef.empty()) CK(cudaMemcpy(b4->p, coef.data(), coef.size() * sizeof(cplx), cudaMemcpyHostToDevice));
+    cm.rowptr = b1->i();
+    cm.oc_idx = reinterpret_cast<int4*>(b2->p);
+    cm.ic_idx = reinterpret_cast<int4*>(b3->p);
+    cm.coef = b4->c();
+    ms.store.push_back(std::move(b1));
+    ms.store.push_back(std::move(b2));
+    ms.store.push_back(std::move(b3));
+    ms.store.push_back(std::move(b4));
+  };
+  {  // cmL: out (s, w') <- in (w, t), coef W[w,s,t,w']
+    std::vector<int> rp{0};
+    std::vector<int4> oc, ic;
+    std::vector<cplx> cf;
+    for (int s = 0; s < d; ++s)
+      for (int w2 = 0; w2 < Dr; ++w2) {
+        oc.push_back(make_int4(s, w2, 0, 0));
+        for (int w = 0; w < Dl; ++w)
+          for (int t = 0; t < d; ++t)
+            if (nz(at(w, s, t, w2))) {
+              ic.push_back(make_int4(w, t, 0, 0));
+              cf.push_back(at(w, s, t, w2));
+            }
+        rp.push_back((int)ic.size());
+      }
+    upload(ms.cmL, rp, oc, ic, cf);
+  }
+  {  // cmR: out (w, s) <- in (t, w'), coef W[w,s,t,w']
+    std::vector<int> rp{0};
+    std::vector<int4> oc, ic;
+    std::vector<cplx> cf;
+    for (int w = 0; w < Dl; ++w)
+      for (int s = 0; s < d; ++s) {
+        oc.push_back(make_int4(w, s, 0, 0));
+        for (int t = 0; t < d; ++t)
+          for (int w2 = 0; w2 < Dr; ++w2)
+            if (nz(at(w, s, t, w2))) {
+              ic.push_back(make_int4(t, w2, 0, 0));
+              cf.push_back(at(w, s, t, w2));
+            }
+        rp.push_back((int)ic.size());
+      }
+    upload(ms.cmR, rp, oc, ic, cf);
+  }
+}
+
+size_t nnz_of(const MpoSite& ms) { return (size_t)ms.cmL.nnz; }
+
+// ---------------------------------------------------------- contractions
+// H_eff^(2) x: x, y (cl, d, d, cr)
+void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, const cplx* Renv, int cl, int cr,
+           const cplx* x, cplx* y) {
+  const int d = h->d, Dl = W1.Dl, Dm = W1.Dr, Dr = W2.Dr;
+  cplx* T1 = h->T1->c();
+  cplx* T2 = h->T2->c();
+  // stage 1: T1[(a,w),(t1,t2,b')] = L[(a,w),a'] x[a',(t1,t2,b')]
+  gemm(h, OP_N, OP_N, cl * Dl, d * d * cr, cl, Lenv, cl, x, (long long)d * d * cr, T1, (long long)d * d * cr);
+  // stage 2: T2[a][s1][w'][(t2,b')] = sum W1[w,s1,t1,w'] T1[a][w][t1][(t2,b')]
+  cmix(h, W1.cmL, cl, d * cr, T1, (long long)Dl * d * d * cr, 1, Strides3{(long long)d * d * cr, (long long)d * cr, 0},
+       T2, (long long)d * Dm * d * cr, 1, Strides3{(long long)Dm * d * cr, (long long)d * cr, 0});
+  // stage 3: T3[(a,s1)][s2][w''][b'] = sum W2[w',s2,t2,w''] T2[(a,s1)][w'][t2][b']   (T3 reuses T1)
+  cmix(h, W2.cmL, cl * d, cr, T2, (long long)Dm * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T1,
+       (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
+  // stage 4: y[(a,s1,s2), b] = T3[(a,s1,s2),(w'',b')] R[b,(w'',b')]^T
+  gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T1, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+}
+
+// H_eff^(1) x: x, y (cl, d, cr)
+void heff1(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W, const cplx* Renv, int cl, int cr, const cplx* x, cplx* y) {
+  const int d = h->d, Dl = W.Dl, Dr = W.Dr;
+  cplx* T1 = h->T1->c();
+  cplx* T2 = h->T2->c();
+  gemm(h, OP_N, OP_N, cl * Dl, d * cr, cl, Lenv, cl, x, (long long)d * cr, T1, (long long)d * cr);
+  cmix(h, W.cmL, cl, cr, T1, (long long)Dl * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T2,
+       (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
+  gemm(h, OP_N, OP_T, cl * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+}
+
+// beta'[b,w',b'] = sum conj(A[a,s,b]) beta[a,w,a'] W[w,s,t,w'] A[a',t,b']
+void env_left(tdvp_ctx* h, const cplx* beta, const cplx* A, const MpoSite& W, int cl, int cr, cplx* out) {
+  const int d = h->d, Dl = W.Dl, Dr = W.Dr;
+  cplx* X = h->T1->c();
+  cplx* Y = h->T2->c();
+  gemm(h, OP_N, OP_N, cl * Dl, d * cr, cl, beta, cl, A, (long long)d * cr, X, (long long)d * cr);
+  cmix(h, W.cmL, cl, cr, X, (long long)Dl * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, Y,
+       (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
+  gemm(h, OP_C, OP_N, cr, Dr * cr, cl * d, A, cr, Y, (long long)Dr * cr, out, (long long)Dr * cr);
+}
+
+// gamma'[a,w,a'] = sum conj(B[a,s,b]) W[w,s,t,w'] B[a',t,b'] gamma[b,w',b']
+void env_right(tdvp_ctx* h, const cplx* gamma, const cplx* B, const MpoSite& W, int cl, int cr, cplx* out) {
+  const int d = h->d, Dl = W.Dl, Dr = W.Dr;
+  cplx* X = h->T1->c();
+  cplx* Y = h->T2->c();
+  // X[(a',t),(b,w')] = B[(a',t),b'] gamma[(b,w'),b']
+  gemm(h, OP_N, OP_T, cl * d, cr * Dr, cr, B, cr, gamma, cr, X, (long long)cr * Dr);
+  // Y[w][a'][s][b] = sum W[w,s,t,w'] X[a'][t][b][w']
+  cmix(h, W.cmR, cl, cr, X, (long long)d * cr * Dr, Dr, Strides3{(long long)cr * Dr, 1, 0}, Y, (long long)d * cr, 1,
+       Strides3{(long long)cl * d * cr, (long long)cr, 0});
+  // out[a,(w,a')] = conj(B)[a,(s,b)] Y[(w,a'),(s,b)]^T
+  gemm(h, OP_R, OP_T, cl, Dl * cl, d * cr, B, (long long)d * cr, Y, (long long)d * cr, out, (long long)Dl * cl);
+}
+
+double flops_heff2(int cl, int cr, int d, int Dl, int Dr, size_t nnz1, size_t nnz2) {
+  // 8 [d^2 cl cr (Dl cl + Dr cr) + d cl cr (nnz W_j + nnz W_{j+1})]
+  return 8.0 * ((double)d * d * cl * cr * ((double)Dl * cl + (double)Dr * cr) +
+                (double)d * cl * cr * (double)(nnz1 + nnz2));
+}
+double flops_heff1(int cl, int cr, int d, int Dl, int Dr, size_t nnz) {
+  return 8.0 * ((double)d * cl * cr * ((double)Dl * cl + (double)Dr * cr) + (double)cl * cr * (double)nnz);
+}
+
+// exp(tau H) x -> out, device-resident Lanczos (SURVEY O-10)
+void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& matvec, const cplx* x, cplx* out,
+                  long long n, double tre, double tim, int K, int which /*2: heff2 1: heff1 0: other*/, double mv_flop) {
+  cplx* V = h->krylov->c();
+  cplx* w = h->wvec->c();
+  CK(lz_start(h->st, h->lz, x, V, n));
+  g_launch_count += 2;
+  for (int k = 0; k < K; ++k) {
+    int e0 = -1;
+    if (h->prm.timing && which) e0 = ev_record(h);
+    matvec(V + (long long)k * n, w);
+    if (e0 >= 0) {
+      const int e1 = ev_record(h);
+      (which == 2 ? h->ev_h2 : h->ev_h1).emplace_back(e0, e1);
+      if (which == 2) { h->stats.heff2_flop += mv_flop; h->stats.heff2_calls++; }
+      else h->stats.heff1_flop += mv_flop;
+    }
+    CK(lz_dots(h->st, h->lz, V, n, k + 1, w, n, k));
+    g_launch_count++;
+    if (k + 1 < K) {
+      CK(lz_update_dots(h->st, h->lz, V, n, k + 1, w, n));
+      CK(lz_update_norm(h->st, h->lz, V, n, k + 1, w, n, k));
+      CK(lz_next(h->st, h->lz, w, V + (long long)(k + 1) * n, n, k));
+      g_launch_count += 3;
+    }
+  }
+  CK(lz_tridiag_exp(h->st, h->lz, K, tre, tim));
+  CK(lz_combine(h->st, h->lz, V, n, K, out, n));
+  g_launch_count += 2;
+}
+
+// --------------------------------------------------------- local updates
+inline cplx* P(const BufPtr& b) { return b ? b->c() : nullptr; }
+
+void require_held(const Segment& g, int j) {
+  if (!g.psi[j] || !g.beta[j] || !g.gamma[j]) throw TdvpError(TDVP_ECUDA, "internal: site not held by segment");
+}
+
+// two-site forward update of (j, j+1) (SURVEY O-6)
+void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build) {
+  const int d = h->d;
+  const int cl = g.cb[j], cm = g.cb[j + 1], cr = g.cb[j + 2];
+  const MpoSite& W1 = h->mpo[j];
+  const MpoSite& W2 = h->mpo[j + 1];
+  cplx* th = h->theta->c();
+  // a1: Theta = Psi_j diag(V_j) Psi_{j+1}
+  CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), cm, (long long)d * cr));
+  g_launch_count++;
+  gemm(h, OP_N, OP_N, cl * d, d * cr, cm, P(g.psi[j]), cm, h->tmpA->c(), (long long)d * cr, th, (long long)d * cr);
+  // a2/a3: Theta' = exp(-i tau H_eff^(2)) Theta
+  const long long n = (long long)cl * d * d * cr;
+  const cplx* Lenv = P(g.beta[j]);
+  const cplx* Renv = P(g.gamma[j + 1]);
+  const double tau = full ? dt : 0.5 * dt;
+  const double fl = flops_heff2(cl, cr, d, W1.Dl, W2.Dr, nnz_of(W1), nnz_of(W2));
+  cplx* th2 = h->tmpB->c();
+  expm_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, 0.0, -tau,
+      h->prm.krylov_k, 2, fl);
+  // a4: truncated SVD split
+  int e0 = -1;
+  if (h->prm.timing) e0 = ev_record(h);
+  TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
+  int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
+  double w = 0.0;
+  cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
+                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps);
+  if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
+  CK(se);
+  g_launch_count += 3 + (long long)sweeps * std::max(1, ((std::min(cl * d, d * cr) + 15) / 16 + 1) / 2 * 2 - 1);
+  if (e0 >= 0) h->ev_svd.emplace_back(e0, ev_record(h));
+  if (chi > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: chi exceeds allocation");
+  g.cb[j + 1] = chi;
+  h->stats.w_step += w;
+  h->stats.n_pair++;
+  h->stats.svd_sweeps_max = std::max(h->stats.svd_sweeps_max, sweeps);
+  if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
+  // a5: environments for the next update
+  if (build & BUILD_BETA) {
+    CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
+    g_launch_count++;
+    env_left(h, P(g.beta[j]), h->tmpA->c(), W1, cl, chi, P(g.beta[j + 1]));
+  }
+  if (build & BUILD_GAMMA) {
+    CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), chi, (long long)d * cr));
+    g_launch_count++;
+    env_right(h, P(g.gamma[j + 1]), h->tmpA->c(), W2, chi, cr, P(g.gamma[j]));
+  }
+}
+
+// one-site backward update Psi_j <- exp(+i dt/2 H_eff^(1)) Psi_j
+void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
+  const int d = h->d, cl = g.cb[j], cr = g.cb[j + 1];
+  const MpoSite& W = h->mpo[j];
+  const long long n = (long long)cl * d * cr;
+  const cplx* Lenv = P(g.beta[j]);
+  const cplx* Renv = P(g.gamma[j]);
+  CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), n));
+  g_launch_count++;
+  const double fl = flops_heff1(cl, cr, d, W.Dl, W.Dr, nnz_of(W));
+  expm_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff1(h, Lenv, W, Renv, cl, cr, x, y); }, h->tmpB->c(), P(g.psi[j]), n, 0.0,
+      0.5 * dt, h->prm.krylov_k, 1, fl);
+  h->stats.n_back++;
+}
+
+// ------------------------------------------------------------ layout / init
+void alloc_segment(tdvp_ctx* h, Segment& g, int q, int s, int e) {
+  const int L = h->L, d = h->d;
+  g.q = q;
+  g.s = s;
+  g.e = e;
+  g.cb.assign(L + 1, 1);
+  g.psi.clear();
+  g.beta.clear();
+  g.gamma.clear();
+  g.lam.clear();
+  g.vinv.clear();
+  g.psi.resize(L);
+  g.beta.resize(L);
+  g.gamma.resize(L);
+  g.lam.resize(L - 1);
+  g.vinv.resize(L - 1);
+  const int hi = std::min(e + 1, L - 1);
+  for (int j = s; j <= hi; ++j) {
+    g.psi[j] = make_buf((size_t)h->cbmax[j] * d * h->cbmax[j + 1] * sizeof(cplx));
+    g.beta[j] = make_buf((size_t)h->cbmax[j] * h->mpo[j].Dl * h->cbmax[j] * sizeof(cplx));
+    g.gamma[j] = make_buf((size_t)h->cbmax[j + 1] * h->mpo[j].Dr * h->cbmax[j + 1] * sizeof(cplx));
+  }
+  for (int b = std::max(s - 1, 0); b <= std::min(e, L - 2); ++b) {
+    g.lam[b] = make_buf((size_t)h->cbmax[b + 1] * sizeof(double));
+    g.vinv[b] = make_buf((size_t)h->cbmax[b + 1] * sizeof(double));
+  }
+}
+
+__global__ void recip_kernel(const double* lam, double* vinv, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) vinv[i] = 1.0 / lam[i];
+}
+
+// owner segment of site j (single-process layout)
+int owner_of(tdvp_ctx* h, int j) {
+  for (size_t q = 0; q < h->bounds.size(); ++q)
+    if (j >= h->bounds[q].first && j <= h->bounds[q].second) return (int)q;
+  return -1;
+}
+bool local_mode(tdvp_ctx* h) { return h->world == 1; }
+
+// upload the full host MPS copy into the current layout
+void upload_state(tdvp_ctx* h) {
+  const int L = h->L;
+  for (auto& g : h->segs) {
+    g.cb = h->h_chi;
+    const int hi = std::min(g.e + 1, L - 1);
+    for (int j = g.s; j <= hi; ++j)
+      CK(cudaMemcpyAsync(g.psi[j]->p, h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double), cudaMemcpyHostToDevice,
+                         h->st));
+    for (int b = std::max(g.s - 1, 0); b <= std::min(g.e, L - 2); ++b) {
+      CK(cudaMemcpyAsync(g.lam[b]->p, h->h_lam[b].data(), h->h_lam[b].size() * sizeof(double),
+                         cudaMemcpyHostToDevice, h->st));
+      const int n = (int)h->h_lam[b].size();
+      recip_kernel<<<(n + 255) / 256, 256, 0, h->st>>>(g.lam[b]->d(), g.vinv[b]->d(), n);
+      CK(cudaGetLastError());
+    }
+  }
+  CK(cudaStreamSynchronize(h->st));
+}
+
+// download owner copies into the host MPS copy
+void download_state(tdvp_ctx* h) {
+  const int L = h->L, d = h->d;
+  if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "state download across ranks is not supported");
+  std::vector<int> chi(L + 1, 1);
+  for (int b = 0; b < L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];  // left owner owns bond b
+  h->h_chi = chi;
+  for (int j = 0; j < L; ++j) {
+    Segment& g = h->segs[owner_of(h, j)];
+    const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
+    h->h_psi[j].resize(n);
+    CK(cudaMemcpyAsync(h->h_psi[j].data(), g.psi[j]->p, n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  }
+  for (int b = 0; b < L - 1; ++b) {
+    Segment& g = h->segs[owner_of(h, b)];
+    h->h_lam[b].resize(chi[b + 1]);
+    CK(cudaMemcpyAsync(h->h_lam[b].data(), g.lam[b]->p, chi[b + 1] * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+}
+
+// Sequential initial environments (O-2) from the host
+// MPS copy: beta_{j+1} = env_left(beta_j, Psi_j V_j, W_j),
+// gamma_{j-1} = env_right(gamma_j, V_{j-1} Psi_j, W_j), stored wherever held.
+void build_envs(tdvp_ctx* h) {
+  const int L = h->L, d = h->d;
+  const std::vector<int>& chi = h->h_chi;
+  // scratch: running env (envA/envB ping-pong), site tensor upload (T2 reused), scaled tensor (tmpA)
+  DevBuf psi_tmp, lam_tmp, vinv_tmp;
+  psi_tmp.alloc((size_t)h->n1max * sizeof(cplx));
+  lam_tmp.alloc((size_t)h->chi_max * sizeof(double) + 64);
+  vinv_tmp.alloc((size_t)h->chi_max * sizeof(double) + 64);
+  auto upload_site = [&](int j) {
+    CK(cudaMemcpyAsync(psi_tmp.p, h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double), cudaMemcpyHostToDevice,
+                       h->st));
+  };
+  auto upload_bond = [&](int b) {
+    const int n = (int)h->h_lam[b].size();
+    CK(cudaMemcpyAsync(lam_tmp.p, h->h_lam[b].data(), n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    recip_kernel<<<(n + 255) / 256, 256, 0, h->st>>>(lam_tmp.d(), vinv_tmp.d(), n);
+    CK(cudaGetLastError());
+  };
+  const cplx one = ONE;
+  // left chain
+  cplx* cur = h->envA->c();
+  cplx* nxt = h->envB->c();
+  CK(cudaMemcpyAsync(cur, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+  auto store = [&](bool left, int j, const cplx* src, long long n) {
+    for (auto& g : h->segs) {
+      const BufPtr& b = left ? g.beta[j] : g.gamma[j];
+      if (b) CK(cudaMemcpyAsync(b->p, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, h->st));
+    }
+  };
+  store(true, 0, cur, 1);
+  for (int j = 0; j < L - 1; ++j) {
+    upload_site(j);
+    upload_bond(j);
+    CK(scale_cols(h->st, h->tmpA->c(), psi_tmp.c(), vinv_tmp.d(), (long long)chi[j] * d, chi[j + 1]));
+    env_left(h, cur, h->tmpA->c(), h->mpo[j], chi[j], chi[j + 1], nxt);
+    std::swap(cur, nxt);
+    store(true, j + 1, cur, (long long)chi[j + 1] * h->mpo[j].Dr * chi[j + 1]);
+    CK(cudaStreamSynchronize(h->st));  // host tmp buffers are reused
+  }
+  cur = h->envA->c();
+  nxt = h->envB->c();
+  CK(cudaMemcpyAsync(cur, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+  store(false, L - 1, cur, 1);
+  for (int j = L - 1; j > 0; --j) {
+    upload_site(j);
+    upload_bond(j - 1);
+    CK(scale_rows(h->st, h->tmpA->c(), psi_tmp.c(), vinv_tmp.d(), chi[j], (long long)d * chi[j + 1]));
+    env_right(h, cur, h->tmpA->c(), h->mpo[j], chi[j], chi[j + 1], nxt);
+    std::swap(cur, nxt);
+    store(false, j - 1, cur, (long long)chi[j] * h->mpo[j].Dl * chi[j]);
+    CK(cudaStreamSynchronize(h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+}
+
+void layout(tdvp_ctx* h, int p) {
+  std::vector<std::pair<int, int>> b;
+  std::string err;
+  if (!plan_partition(h->L, p, b, err)) throw TdvpError(TDVP_EPARTITION, err);
+  if (!local_mode(h) && p != h->world)
+    throw TdvpError(TDVP_EPARTITION, "n_segments must equal the world size in multi-process mode");
+  if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);  // keep the current state
+  h->segs.clear();
+  h->bounds = b;
+  if (local_mode(h)) {
+    h->segs.resize(p);
+    for (int q = 0; q < p; ++q) alloc_segment(h, h->segs[q], q, b[q].first, b[q].second);
+  } else {
+    h->segs.resize(1);
+    alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second);
+  }
+  h->layout_p = p;
+  upload_state(h);
+  build_envs(h);
+  h->envs_valid = true;
+}
+
+// ------------------------------------------------------------ exchanges
+// local mode: copy boundary data between segments (device to device)
+void copy_buf(tdvp_ctx* h, const BufPtr& dst, const BufPtr& src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst->p, src->p, bytes, cudaMemcpyDeviceToDevice, h->st));
+}
+
+// SEND_R: Psi'_{e+1}, Lambda'_e (and V), beta_{e+1} from q to q+1
+void send_right_local(tdvp_ctx* h, Segment& a, Segment& b) {
+  const int e = a.e, d = h->d;
+  const int chi = a.cb[e + 1], cr = a.cb[e + 2];
+  b.cb[e + 1] = chi;
+  copy_buf(h, b.psi[e + 1], a.psi[e + 1], (size_t)chi * d * cr * sizeof(cplx));
+  copy_buf(h, b.lam[e], a.lam[e], (size_t)chi * sizeof(double));
+  copy_buf(h, b.vinv[e], a.vinv[e], (size_t)chi * sizeof(double));
+  copy_buf(h, b.beta[e + 1], a.beta[e + 1], (size_t)chi * h->mpo[e + 1].Dl * chi * sizeof(cplx));
+}
+// SEND_L: Psi_s, gamma_s from q to q-1
+void send_left_local(tdvp_ctx* h, Segment& b, Segment& a) {
+  const int s = b.s, d = h->d;
+  const int cl = b.cb[s], cr = b.cb[s + 1];
+  a.cb[s + 1] = cr;
+  a.cb[s] = cl;
+  copy_buf(h, a.psi[s], b.psi[s], (size_t)cl * d * cr * sizeof(cplx));
+  copy_buf(h, a.gamma[s], b.gamma[s], (size_t)cr * h->mpo[s].Dr * cr * sizeof(cplx));
+}
+
+// NCCL mode
+void nccl_send_ints(tdvp_ctx* h, const int* v, int n, int peer) {
+  CK(cudaMemcpyAsync(h->hdr->p, v, n * sizeof(int), cudaMemcpyHostToDevice, h->st));
+  NK(nccl().Send(h->hdr->p, n, ncclInt32, peer, h->comm, h->st));
+  CK(cudaStreamSynchronize(h->st));
+}
+void nccl_recv_ints(tdvp_ctx* h, int* v, int n, int peer) {
+  NK(nccl().Recv(h->hdr->p, n, ncclInt32, peer, h->comm, h->st));
+  CK(cudaMemcpyAsync(v, h->hdr->p, n * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+}
+void send_right_nccl(tdvp_ctx* h, Segment& a) {
+  const int e = a.e, d = h->d, peer = a.q + 1;
+  const int chi = a.cb[e + 1], cr = a.cb[e + 2];
+  int hd[2] = {chi, cr};
+  nccl_send_ints(h, hd, 2, peer);
+  NK(nccl().GroupStart());
+  NK(nccl().Send(a.psi[e + 1]->p, (size_t)chi * d * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Send(a.lam[e]->p, (size_t)chi, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Send(a.beta[e + 1]->p, (size_t)chi * h->mpo[e + 1].Dl * chi * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().GroupEnd());
+}
+void recv_left_nccl(tdvp_ctx* h, Segment& b) {
+  const int s = b.s, d = h->d, peer = b.q - 1;
+  int hd[2];
+  nccl_recv_ints(h, hd, 2, peer);
+  const int chi = hd[0], cr = hd[1];
+  b.cb[s] = chi;
+  b.cb[s + 1] = cr;
+  NK(nccl().GroupStart());
+  NK(nccl().Recv(b.psi[s]->p, (size_t)chi * d * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Recv(b.lam[s - 1]->p, (size_t)chi, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Recv(b.beta[s]->p, (size_t)chi * h->mpo[s].Dl * chi * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().GroupEnd());
+  recip_kernel<<<(chi + 255) / 256, 256, 0, h->st>>>(b.lam[s - 1]->d(), b.vinv[s - 1]->d(), chi);
+  CK(cudaGetLastError());
+}
+void send_left_nccl(tdvp_ctx* h, Segment& b) {
+  const int s = b.s, d = h->d, peer = b.q - 1;
+  const int cl = b.cb[s], cr = b.cb[s + 1];
+  int hd[2] = {cl, cr};
+  nccl_send_ints(h, hd, 2, peer);
+  NK(nccl().GroupStart());
+  NK(nccl().Send(b.psi[s]->p, (size_t)cl * d * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Send(b.gamma[s]->p, (size_t)cr * h->mpo[s].Dr * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().GroupEnd());
+}
+void recv_right_nccl(tdvp_ctx* h, Segment& a) {
+  const int e = a.e, d = h->d, peer = a.q + 1;
+  int hd[2];
+  nccl_recv_ints(h, hd, 2, peer);
+  const int cl = hd[0], cr = hd[1];
+  a.cb[e + 1] = cl;
+  a.cb[e + 2] = cr;
+  NK(nccl().GroupStart());
+  NK(nccl().Recv(a.psi[e + 1]->p, (size_t)cl * d * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().Recv(a.gamma[e + 1]->p, (size_t)cr * h->mpo[e + 1].Dr * cr * 2, ncclFloat64, peer, h->comm, h->st));
+  NK(nccl().GroupEnd());
+}
+
+void exec_compute(tdvp_ctx* h, Segment& g, const SchedOp& op, double dt) {
+  if (op.kind == OP_PAIR) pair_update(h, g, op.j, dt, op.full, op.build);
+  else if (op.kind == OP_BACK) back_update(h, g, op.j, dt);
+}
+
+// one half-step
+void run_half(tdvp_ctx* h, int hh, double dt, const std::set<int>& merged) {
+  const int L = h->L, p = h->layout_p;
+  if (!local_mode(h)) {
+    Segment& g = h->segs[0];
+    for (const SchedOp& op : segment_program(L, p, hh, g.q, h->bounds[g.q], merged)) {
+      switch (op.kind) {
+        case OP_SEND_R: send_right_nccl(h, g); break;
+        case OP_RECV_L: recv_left_nccl(h, g); break;
+        case OP_SEND_L: send_left_nccl(h, g); break;
+        case OP_RECV_R: recv_right_nccl(h, g); break;
+        default: exec_compute(h, g, op, dt);
+      }
+    }
+    return;
+  }
+  // single process: cooperative round-robin executor over the segment
+  // programs; a SEND copies immediately, a RECV waits for its message.
+  std::vector<std::vector<SchedOp>> prog(p);
+  std::vector<size_t> pc(p, 0);
+  std::vector<int> msg_from_left(p, 0), msg_from_right(p, 0);
+  for (int q = 0; q < p; ++q) prog[q] = segment_program(L, p, hh, q, h->bounds[q], merged);
+  size_t done = 0;
+  while (done < (size_t)p) {
+    bool progress = false;
+    done = 0;
+    for (int q = 0; q < p; ++q) {
+      while (pc[q] < prog[q].size()) {
+        const SchedOp& op = prog[q][pc[q]];
+        Segment& g = h->segs[q];
+        if (op.kind == OP_RECV_L) {
+          if (!msg_from_left[q]) break;
+          msg_from_left[q]--;
+        } else if (op.kind == OP_RECV_R) {
+          if (!msg_from_right[q]) break;
+          msg_from_right[q]--;
+        } else if (op.kind == OP_SEND_R) {
+          send_right_local(h, g, h->segs[q + 1]);
+          msg_from_left[q + 1]++;
+        } else if (op.kind == OP_SEND_L) {
+          send_left_local(h, g, h->segs[q - 1]);
+          msg_from_right[q - 1]++;
+        } else {
+          exec_compute(h, g, op, dt);
+        }
+        pc[q]++;
+        progress = true;
+      }
+      if (pc[q] == prog[q].size()) done++;
+    }
+    if (done < (size_t)p && !progress) throw TdvpError(TDVP_ECUDA, "internal: schedule deadlock");
+  }
+}
+
+void finish_timing(tdvp_ctx* h) {
+  auto sum = [&](const std::vector<std::pair<int, int>>& v) {
+    double t = 0.0;
+    for (auto& pr : v) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h->ev_pool[pr.first], h->ev_pool[pr.second]));
+      t += ms;
+    }
+    return t;
+  };
+  h->stats.heff2_ms = sum(h->ev_h2);
+  h->stats.heff1_ms = sum(h->ev_h1);
+  h->stats.svd_ms = sum(h->ev_svd);
+}
+
+void do_step(tdvp_ctx* h, double dt, int p) {
+  if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step");
+  if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
+  if (p != h->layout_p || !h->envs_valid) layout(h, p);
+  h->stats.w_step = 0.0;
+  h->stats.trunc_active = 0;
+  h->stats.n_pair = h->stats.n_back = 0;
+  h->stats.svd_sweeps_max = 0;
+  h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
+  h->stats.heff2_calls = 0;
+  h->ev_used = 0;
+  h->ev_h2.clear();
+  h->ev_h1.clear();
+  h->ev_svd.clear();
+  const long long l0 = g_launch_count, g0 = g_gemm_count;
+  CK(cudaEventRecord(h->ev_step0, h->st));
+  const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
+  run_half(h, 1, dt, merged);
+  run_half(h, 2, dt, merged);
+  CK(cudaEventRecord(h->ev_step1, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev_step0, h->ev_step1));
+  h->stats.step_ms = ms;
+  h->stats.w_total += h->stats.w_step;
+  h->stats.kernel_launches = g_launch_count - l0;
+  h->stats.gemm_launches = g_gemm_count - g0;
+  if (h->prm.timing) finish_timing(h);
+}
+
+// ------------------------------------------------------------ measurement
+// Full zipper over M_j = Psi_j V_j (j < L-1), M_{L-1} = Psi_{L-1} (AMB-10).
+struct MeasureOut {
+  double norm = 0.0, energy = 0.0;
+  std::vector<double> sz;
+};
+void measure(tdvp_ctx* h, bool want_sz, bool want_E, MeasureOut& out) {
+  if (!h->have_mps || !h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set");
+  if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "measurement across ranks: gather the MPS to one rank");
+  if (h->layout_p == 0) layout(h, 1);
+  const int L = h->L, d = h->d;
+  std::vector<int> chi(L + 1, 1);
+  for (int j = 1; j < L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
+  // chain tensors M_j into a contiguous scratch set (owner copies)
+  std::vector<BufPtr> M(L);
+  for (int j = 0; j < L; ++j) {
+    Segment& g = h->segs[owner_of(h, j)];
+    const long long n = (long long)chi[j] * d * chi[j + 1];
+    M[j] = make_buf(n * sizeof(cplx));
+    if (j < L - 1) CK(scale_cols(h->st, M[j]->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)chi[j] * d, chi[j + 1]));
+    else CK(copy_cplx(h->st, M[j]->c(), P(g.psi[j]), n));
+  }
+  const cplx one = ONE;
+  // left norm envs E_j (j = 0..L) and right envs F_j (j = 0..L-1)
+  std::vector<BufPtr> E(L + 1), F(L);
+  E[0] = make_buf(sizeof(cplx));
+  CK(cudaMemcpyAsync(E[0]->p, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+  for (int j = 0; j < L; ++j) {
+    E[j + 1] = make_buf((size_t)chi[j + 1] * chi[j + 1] * sizeof(cplx));
+    env_left(h, E[j]->c(), M[j]->c(), h->mpo_id, chi[j], chi[j + 1], E[j + 1]->c());
+  }
+  F[L - 1] = make_buf(sizeof(cplx));
+  CK(cudaMemcpyAsync(F[L - 1]->p, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+  for (int j = L - 1; j > 0; --j) {
+    F[j - 1] = make_buf((size_t)chi[j] * chi[j] * sizeof(cplx));
+    env_right(h, F[j]->c(), M[j]->c(), h->mpo_id, chi[j], chi[j + 1], F[j - 1]->c());
+  }
+  cplx nrm;
+  CK(cudaMemcpyAsync(&nrm, E[L]->p, sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  out.norm = nrm.x;
+  if (!(out.norm > 0.0) || !std::isfinite(out.norm)) throw TdvpError(TDVP_ENUMERIC, "non-positive norm");
+  if (want_sz) {
+    out.sz.assign(L, 0.0);
+    BufPtr X = make_buf((size_t)h->chi_max * h->chi_max * sizeof(cplx) + 64);
+    BufPtr R = make_buf(sizeof(cplx) * L);
+    for (int j = 0; j < L; ++j) {
+      env_left(h, E[j]->c(), M[j]->c(), h->mpo_sz, chi[j], chi[j + 1], X->c());
+      CK(sum_products(h->st, X->c(), F[j]->c(), (long long)chi[j + 1] * chi[j + 1], R->c() + j, h->partials->d(),
+                      reinterpret_cast<unsigned*>(h->lz_counter->p)));
+    }
+    std::vector<cplx> r(L);
+    CK(cudaMemcpyAsync(r.data(), R->p, L * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int j = 0; j < L; ++j) out.sz[j] = r[j].x / out.norm;
+  }
+  if (want_E) {
+    BufPtr A = make_buf(h->envA->bytes), B = make_buf(h->envA->bytes);
+    cplx* cur = A->c();
+    cplx* nxt = B->c();
+    CK(cudaMemcpyAsync(cur, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+    for (int j = 0; j < L; ++j) {
+      env_left(h, cur, M[j]->c(), h->mpo[j], chi[j], chi[j + 1], nxt);
+      std::swap(cur, nxt);
+    }
+    cplx e;
+    CK(cudaMemcpyAsync(&e, cur, sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    out.energy = e.x / out.norm;
+  }
+}
+
+// ------------------------------------------------------------ workspace
+void alloc_workspace(tdvp_ctx* h) {
+  const int L = h->L, d = h->d, D = h->Dmpo;
+  long long n2 = 1, n1 = 1, scr = 1, svd = 1, env = 1;
+  for (int j = 0; j < L; ++j) {
+    const long long cl = h->cbmax[j], cr1 = h->cbmax[j + 1];
+    n1 = std::max(n1, cl * d * cr1);
+    env = std::max(env, std::max(cl * cl, cr1 * cr1) * D);
+    scr = std::max(scr, cl * d * cr1 * D * d);
+    if (j + 1 < L) {
+      const long long cr = h->cbmax[j + 2];
+      n2 = std::max(n2, cl * d * d * cr);
+      scr = std::max(scr, cl * d * d * cr * D);
+      svd = std::max(svd, (long long)svd_work_elems((int)(cl * d), (int)(d * cr)));
+    }
+  }
+  h->n2max = n2;
+  h->n1max = n1;
+  h->scratch = scr;
+  h->svdmax = svd;
+  h->work_elems = std::max<long long>(1 << 20, std::min<long long>(4 * scr, 1 << 23));
+  const int K = KMAX;
+  h->theta = make_buf(n2 * sizeof(cplx));
+  h->krylov = make_buf((size_t)K * n2 * sizeof(cplx));
+  h->wvec = make_buf(n2 * sizeof(cplx));
+  h->T1 = make_buf(scr * sizeof(cplx));
+  h->T2 = make_buf(scr * sizeof(cplx));
+  h->tmpA = make_buf(std::max(n2, n1) * sizeof(cplx));
+  h->tmpB = make_buf(std::max(n2, n1) * sizeof(cplx));
+  h->svdY = make_buf(svd * sizeof(cplx));
+  h->gemm_work = make_buf(h->work_elems * sizeof(cplx));
+  h->envA = make_buf(env * sizeof(cplx));
+  h->envB = make_buf(env * sizeof(cplx));
+  const int nblk = 4 * g_num_sms;
+  h->partials = make_buf((size_t)nblk * 2 * (KMAX + 1) * sizeof(double));
+  h->lz_scal = make_buf((2 * KMAX + 8) * sizeof(double));
+  h->lz_coef = make_buf(2 * (KMAX + 1) * sizeof(cplx));
+  h->lz_y = make_buf(KMAX * sizeof(cplx));
+  h->lz_counter = make_buf(64);
+  h->lz_brk = make_buf(64);
+  CK(cudaMemset(h->lz_counter->p, 0, 64));
+  CK(cudaMemset(h->lz_brk->p, 0, 64));
+  const long long ncmax = 2LL * h->chi_max;
+  h->svd_sigma = make_buf(ncmax * sizeof(double) + 64);
+  h->svd_order = make_buf(ncmax * sizeof(int) + 64);
+  h->svd_off = make_buf(64);
+  h->svd_ires = make_buf(64);
+  h->svd_dres = make_buf(64);
+  h->hdr = make_buf(64);
+  CK(cudaMallocHost(&h->h_pin, 16 * sizeof(double)));
+  CK(cudaMallocHost(&h->h_ipin, 16 * sizeof(int)));
+  h->lz = LanczosDev{h->lz_scal->d(), h->lz_coef->c(), h->lz_y->c(), h->partials->d(),
+                     reinterpret_cast<unsigned*>(h->lz_counter->p), h->lz_brk->i()};
+  h->sv = SvdDev{h->svdY->c(), 0, h->svd_sigma->d(), h->svd_order->i(), h->svd_off->d(), h->svd_ires->i(),
+                 h->svd_dres->d(), h->h_pin, h->h_ipin};
+}
+
+int fail(tdvp_ctx* h, const TdvpError& e) {
+  if (h) h->err = e.what();
+  return e.code;
+}
+
+void init_device_globals() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0) g_num_sms = sms;
+  }
+  done = true;
+}
+
+std::vector<cplx> to_cplx(const double* p, size_t n) {
+  std::vector<cplx> v(n);
+  for (size_t i = 0; i < n; ++i) v[i] = cmk(p[2 * i], p[2 * i + 1]);
+  return v;
+}
+
+// ------------------------------------------------------------ standalone kernels context
+tdvp_ctx* scratch_ctx(int maxchi, int D) {
+  // a small context for the kernel-level test entry points
+  static tdvp_ctx* sc = nullptr;
+  static int cap = 0, capD = 0;
+  if (sc && cap >= maxchi && capD >= D) return sc;
+  if (sc) {
+    if (sc->h_pin) cudaFreeHost(sc->h_pin);
+    if (sc->h_ipin) cudaFreeHost(sc->h_ipin);
+    if (sc->st) cudaStreamDestroy(sc->st);
+    delete sc;
+  }
+  sc = new tdvp_ctx();
+  init_device_globals();
+  CK(cudaStreamCreateWithFlags(&sc->st, cudaStreamNonBlocking));
+  sc->L = 2;
+  sc->d = 2;
+  sc->Dmpo = D;
+  sc->chi_max = maxchi;
+  sc->cbmax = {1, maxchi, 1};
+  // size the workspace for a (maxchi, d, d, maxchi) problem
+  sc->cbmax = {maxchi, maxchi, maxchi};
+  alloc_workspace(sc);
+  cap = maxchi;
+  capD = D;
+  return sc;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
+  if (!out) return TDVP_EARG;
+  *out = nullptr;
+  if (L < 2 || d < 2 || D_mpo < 1 || chi_max < 1) return TDVP_EARG;
+  tdvp_ctx* h = new tdvp_ctx();
+  try {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw TdvpError(TDVP_ECUDA, "no CUDA device");
+    init_device_globals();
+    CK(cudaGetDevice(&h->dev));
+    h->L = L;
+    h->d = d;
+    h->Dmpo = D_mpo;
+    h->chi_max = chi_max;
+    h->prm.eps = 1e-12;
+    h->prm.w_max = 0.0;
+    h->prm.krylov_k = 8;
+    h->prm.krylov_tol = 0.0;
+    h->prm.multiplet_delta = 1e-6;
+    h->prm.timing = 0;
+    h->cbmax.assign(L + 1, 1);
+    for (int j = 0; j <= L; ++j) {
+      double a = std::pow((double)d, std::min(j, 62)), b = std::pow((double)d, std::min(L - j, 62));
+      h->cbmax[j] = (int)std::min<double>(std::min(a, b), (double)chi_max);
+    }
+    CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev_step0));
+    CK(cudaEventCreate(&h->ev_step1));
+    alloc_workspace(h);
+    // measurement MPOs (D = 1): identity and S^z (d = 2 spin-1/2 convention)
+    std::vector<cplx> Id(d * d, ZERO), Sz(d * d, ZERO);
+    for (int s = 0; s < d; ++s) Id[s * d + s] = ONE;
+    Sz[0] = cmk(0.5, 0);
+    Sz[d * d - 1] = cmk(-0.5, 0);
+    build_site(h->mpo_id, 1, 1, d, Id);
+    build_site(h->mpo_sz, 1, 1, d, Sz);
+    h->h_psi.resize(L);
+    h->h_lam.resize(L - 1);
+  } catch (const TdvpError& e) {
+    std::fprintf(stderr, "tdvp_create: %s\n", e.what());
+    const int c = e.code;
+    tdvp_destroy(h);
+    return c;
+  }
+  *out = h;
+  return TDVP_OK;
+}
+
+int tdvp_set_params(tdvp_t h, const tdvp_params* p) {
+  if (!h || !p) return TDVP_EARG;
+  if (p->krylov_k < 1 || p->krylov_k >= KMAX || !(p->eps >= 0.0) || p->eps >= 1.0 || !(p->w_max >= 0.0) ||
+      !(p->multiplet_delta >= 0.0) || p->krylov_tol != 0.0) {
+    h->err = "invalid params (krylov_k in 1..15, 0 <= eps < 1, w_max >= 0, krylov_tol == 0)";
+    return TDVP_EARG;
+  }
+  h->prm = *p;
+  return TDVP_OK;
+}
+
+int tdvp_get_params(tdvp_t h, tdvp_params* p) {
+  if (!h || !p) return TDVP_EARG;
+  *p = h->prm;
+  return TDVP_OK;
+}
+
+int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W) {
+  if (!h || !D || !W) return TDVP_EARG;
+  try {
+    const int L = h->L, d = h->d;
+    if (D[0] != 1 || D[L] != 1) throw TdvpError(TDVP_EARG, "MPO boundary bond dims must be 1");
+    for (int j = 0; j <= L; ++j)
+      if (D[j] < 1 || D[j] > h->Dmpo) throw TdvpError(TDVP_EARG, "MPO bond dim out of range");
+    std::vector<MpoSite> mpo(L);
+    for (int j = 0; j < L; ++j) {
+      if (!W[j]) throw TdvpError(TDVP_EARG, "null MPO tensor");
+      const size_t n = (size_t)D[j] * d * d * D[j + 1];
+      for (size_t i = 0; i < 2 * n; ++i)
+        if (!std::isfinite(W[j][i])) throw TdvpError(TDVP_ENONFINITE, "non-finite MPO entry");
+      build_site(mpo[j], D[j], D[j + 1], d, to_cplx(W[j], n));
+    }
+    h->mpo = std::move(mpo);
+    h->have_mpo = true;
+    h->envs_valid = false;
+    if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);
+    h->layout_p = 0;
+    h->segs.clear();
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const double* const* Lambda) {
+  if (!h || !chi || !Psi || (h->L > 1 && !Lambda)) return TDVP_EARG;
+  try {
+    const int L = h->L, d = h->d;
+    if (chi[0] != 1 || chi[L] != 1) throw TdvpError(TDVP_EARG, "MPS boundary bond dims must be 1");
+    for (int j = 1; j < L; ++j)
+      if (chi[j] < 1 || chi[j] > h->cbmax[j]) throw TdvpError(TDVP_EARG, "bond dim exceeds min(d^j, d^(L-j), chi_max)");
+    std::vector<std::vector<double>> psi(L), lam(L - 1);
+    for (int j = 0; j < L; ++j) {
+      if (!Psi[j]) throw TdvpError(TDVP_EARG, "null Psi");
+      const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
+      psi[j].assign(Psi[j], Psi[j] + n);
+      for (double v : psi[j])
+        if (!std::isfinite(v)) throw TdvpError(TDVP_ENONFINITE, "non-finite Psi entry");
+    }
+    for (int b = 0; b < L - 1; ++b) {
+      if (!Lambda[b]) throw TdvpError(TDVP_EARG, "null Lambda");
+      lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
+      for (double v : lam[b])
+        if (!std::isfinite(v) || !(v > 0.0)) throw TdvpError(TDVP_ENONFINITE, "Lambda must be finite and > 0");
+    }
+    h->h_psi = std::move(psi);
+    h->h_lam = std::move(lam);
+    h->h_chi.assign(chi, chi + L + 1);
+    h->have_mps = true;
+    h->envs_valid = false;
+    h->layout_p = 0;  // re-layout (upload + env build) at the next step
+    h->segs.clear();
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_step(tdvp_t h, double dt, int n_segments) {
+  if (!h) return TDVP_EARG;
+  try {
+    do_step(h, dt, n_segments);
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_measure_sz(tdvp_t h, double* sz) {
+  if (!h || !sz) return TDVP_EARG;
+  try {
+    MeasureOut m;
+    measure(h, true, false, m);
+    for (int j = 0; j < h->L; ++j) sz[j] = m.sz[j];
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_measure_energy(tdvp_t h, double* E) {
+  if (!h || !E) return TDVP_EARG;
+  try {
+    MeasureOut m;
+    measure(h, false, true, m);
+    *E = m.energy;
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_measure_norm(tdvp_t h, double* n) {
+  if (!h || !n) return TDVP_EARG;
+  try {
+    MeasureOut m;
+    measure(h, false, false, m);
+    *n = m.norm;
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_get_stats(tdvp_t h, tdvp_stats* s) {
+  if (!h || !s) return TDVP_EARG;
+  int brk = 0;
+  if (h->lz_brk && cudaMemcpy(&brk, h->lz_brk->p, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess)
+    h->stats.krylov_breakdowns = brk;
+  *s = h->stats;
+  return TDVP_OK;
+}
+
+int tdvp_get_chi(tdvp_t h, int* chi) {
+  if (!h || !chi) return TDVP_EARG;
+  try {
+    if (!h->have_mps) throw TdvpError(TDVP_ESTATE, "MPS not set");
+    if (h->layout_p == 0) {
+      for (int j = 0; j <= h->L; ++j) chi[j] = h->h_chi[j];
+      return TDVP_OK;
+    }
+    if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "not available across ranks");
+    chi[0] = chi[h->L] = 1;
+    for (int j = 1; j < h->L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
+  if (!h || !Psi) return TDVP_EARG;
+  try {
+    if (!h->have_mps) throw TdvpError(TDVP_ESTATE, "MPS not set");
+    if (h->layout_p != 0) download_state(h);
+    for (int j = 0; j < h->L; ++j) std::memcpy(Psi[j], h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double));
+    if (Lambda)
+      for (int b = 0; b < h->L - 1; ++b) std::memcpy(Lambda[b], h->h_lam[b].data(), h->h_lam[b].size() * sizeof(double));
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+const char* tdvp_last_error(tdvp_t h) { return h ? h->err.c_str() : "null handle"; }
+
+void tdvp_destroy(tdvp_t h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  h->segs.clear();
+  h->mpo.clear();
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->ev_step0) cudaEventDestroy(h->ev_step0);
+  if (h->ev_step1) cudaEventDestroy(h->ev_step1);
+  if (h->h_pin) cudaFreeHost(h->h_pin);
+  if (h->h_ipin) cudaFreeHost(h->h_ipin);
+  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+int tdvp_nccl_unique_id(unsigned char* id128) {
+  if (!id128) return TDVP_EARG;
+  ncclUniqueId id;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return TDVP_ECUDA;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id128, &id, 128);
+  return TDVP_OK;
+}
+
+int tdvp_comm_init(tdvp_t h, int rank, int world, const unsigned char* id128) {
+  if (!h || !id128 || world < 1 || rank < 0 || rank >= world) return TDVP_EARG;
+  try {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    NK(nccl().CommInitRank(&h->comm, world, id, rank));
+    h->rank = rank;
+    h->world = world;
+    h->layout_p = 0;
+    h->segs.clear();
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_plan(int L, int p, int hh, int q, int* ops, int max_ops) {
+  std::vector<std::pair<int, int>> b;
+  std::string err;
+  if (!plan_partition(L, p, b, err)) return TDVP_EPARTITION;
+  if (hh < 1 || hh > 2 || q < 0 || q >= p) return TDVP_EARG;
+  const std::set<int> merged = merged_pairs(L, p, b);
+  const std::vector<SchedOp> prog = segment_program(L, p, hh, q, b[q], merged);
+  if ((int)prog.size() > max_ops) return TDVP_EARG;
+  for (size_t i = 0; i < prog.size(); ++i) {
+    ops[4 * i] = prog[i].kind;
+    ops[4 * i + 1] = prog[i].j;
+    ops[4 * i + 2] = prog[i].full;
+    ops[4 * i + 3] = prog[i].build;
+  }
+  return (int)prog.size();
+}
+
+int tdvp_partition(int L, int p, int* s, int* e) {
+  std::vector<std::pair<int, int>> b;
+  std::string err;
+  if (!plan_partition(L, p, b, err)) return TDVP_EPARTITION;
+  for (int q = 0; q < p; ++q) {
+    s[q] = b[q].first;
+    e[q] = b[q].second;
+  }
+  return TDVP_OK;
+}
+
+// ----------------------------------------------------- kernel-level entries
+static int upload_run_download(const std::function<void(tdvp_ctx*)>& fn) {
+  try {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw TdvpError(TDVP_ECUDA, "no CUDA device");
+    fn(nullptr);
+  } catch (const TdvpError& e) {
+    std::fprintf(stderr, "libtdvp: %s\n", e.what());
+    return e.code;
+  }
+  return TDVP_OK;
+}
+
+static BufPtr up(const double* p, size_t ncplx, cudaStream_t st) {
+  BufPtr b = make_buf(ncplx * sizeof(cplx));
+  CK(cudaMemcpyAsync(b->p, p, ncplx * sizeof(cplx), cudaMemcpyHostToDevice, st));
+  return b;
+}
+
+int tdvp_apply_heff2(int cl, int cr, int d, int Dl, int Dm, int Dr, const double* Lenv, const double* W1,
+                     const double* W2, const double* Renv, const double* theta, double* out) {
+  if (d != 2) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(cl, cr), std::max(Dl, std::max(Dm, Dr)));
+    MpoSite w1, w2;
+    build_site(w1, Dl, Dm, d, to_cplx(W1, (size_t)Dl * d * d * Dm));
+    build_site(w2, Dm, Dr, d, to_cplx(W2, (size_t)Dm * d * d * Dr));
+    BufPtr L_ = up(Lenv, (size_t)cl * Dl * cl, h->st), R_ = up(Renv, (size_t)cr * Dr * cr, h->st);
+    const size_t n = (size_t)cl * d * d * cr;
+    BufPtr x = up(theta, n, h->st), y = make_buf(n * sizeof(cplx));
+    heff2(h, L_->c(), w1, w2, R_->c(), cl, cr, x->c(), y->c());
+    CK(cudaMemcpyAsync(out, y->p, n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int tdvp_apply_heff1(int cl, int cr, int d, int Dl, int Dr, const double* Lenv, const double* W, const double* Renv,
+                     const double* psi, double* out) {
+  if (d != 2) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(cl, cr), std::max(Dl, Dr));
+    MpoSite w;
+    build_site(w, Dl, Dr, d, to_cplx(W, (size_t)Dl * d * d * Dr));
+    BufPtr L_ = up(Lenv, (size_t)cl * Dl * cl, h->st), R_ = up(Renv, (size_t)cr * Dr * cr, h->st);
+    const size_t n = (size_t)cl * d * cr;
+    BufPtr x = up(psi, n, h->st), y = make_buf(n * sizeof(cplx));
+    heff1(h, L_->c(), w, R_->c(), cl, cr, x->c(), y->c());
+    CK(cudaMemcpyAsync(out, y->p, n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int tdvp_env_left(int cl, int cr, int d, int Dl, int Dr, const double* beta, const double* A, const double* W,
+                  double* out) {
+  if (d != 2) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(cl, cr), std::max(Dl, Dr));
+    MpoSite w;
+    build_site(w, Dl, Dr, d, to_cplx(W, (size_t)Dl * d * d * Dr));
+    BufPtr b = up(beta, (size_t)cl * Dl * cl, h->st), a = up(A, (size_t)cl * d * cr, h->st);
+    const size_t n = (size_t)cr * Dr * cr;
+    BufPtr y = make_buf(n * sizeof(cplx));
+    env_left(h, b->c(), a->c(), w, cl, cr, y->c());
+    CK(cudaMemcpyAsync(out, y->p, n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int tdvp_env_right(int cl, int cr, int d, int Dl, int Dr, const double* gamma, const double* B, const double* W,
+                   double* out) {
+  if (d != 2) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(cl, cr), std::max(Dl, Dr));
+    MpoSite w;
+    build_site(w, Dl, Dr, d, to_cplx(W, (size_t)Dl * d * d * Dr));
+    BufPtr g = up(gamma, (size_t)cr * Dr * cr, h->st), b = up(B, (size_t)cl * d * cr, h->st);
+    const size_t n = (size_t)cl * Dl * cl;
+    BufPtr y = make_buf(n * sizeof(cplx));
+    env_right(h, g->c(), b->c(), w, cl, cr, y->c());
+    CK(cudaMemcpyAsync(out, y->p, n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int tdvp_expm_lanczos_dense(int n, const double* H, const double* v, double tau_re, double tau_im, int K, double* out) {
+  if (n < 1 || K < 1 || K >= KMAX) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    const int chi = std::max(1, (int)std::ceil(std::sqrt(n / 4.0)) + 1);
+    tdvp_ctx* h = scratch_ctx(std::max(chi, 8), 1);
+    if ((long long)n > h->n2max) throw TdvpError(TDVP_EARG, "n too large for scratch context");
+    BufPtr Hd = up(H, (size_t)n * n, h->st), x = up(v, n, h->st), y = make_buf((size_t)n * sizeof(cplx));
+    expm_lanczos(
+        h,
+        [&](const cplx* a, cplx* b) {
+          gemm(h, OP_N, OP_N, n, 1, n, Hd->c(), n, a, 1, b, 1);
+        },
+        x->c(), y->c(), n, tau_re, tau_im, K, 0, 0.0);
+    CK(cudaMemcpyAsync(out, y->p, (size_t)n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  });
+}
+
+int tdvp_svd_split(int m, int n, const double* M, int chi_max, double eps, double w_max, double delta, int* chi,
+                   double* w, double* psiL, double* lam, double* psiR) {
+  if (m < 1 || n < 1 || chi_max < 1) return TDVP_EARG;
+  int rc = upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(8, (std::max(m, n) + 1) / 2 + 1), 1);
+    if ((long long)svd_work_elems(m, n) > h->svdmax || (long long)m * n > h->n2max)
+      throw TdvpError(TDVP_EARG, "matrix too large for scratch context");
+    BufPtr a = up(M, (size_t)m * n, h->st);
+    const int k = std::min(m, n);
+    BufPtr pl = make_buf((size_t)m * k * sizeof(cplx)), pr = make_buf((size_t)k * n * sizeof(cplx));
+    BufPtr l = make_buf(k * sizeof(double)), vi = make_buf(k * sizeof(double));
+    TruncParams tp{chi_max, eps, w_max, delta};
+    int c = 0, r = 0, ce = 0, sw = 0;
+    double ww = 0.0;
+    cudaError_t se = svd_truncate_split(h->st, h->sv, a->c(), m, n, tp, pl->c(), pr->c(), l->d(), vi->d(), &c, &ww, &r,
+                                        &ce, &sw);
+    if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "SVD numerical failure");
+    CK(se);
+    CK(cudaMemcpyAsync(psiL, pl->p, (size_t)m * c * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(psiR, pr->p, (size_t)c * n * sizeof(cplx), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(lam, l->p, c * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    *chi = c;
+    *w = ww;
+  });
+  return rc;
+}
+
+int tdvp_zgemm(int opA, int opB, int M, int N, int K, const double* A, const double* B, double* C) {
+  if (M < 1 || N < 1 || K < 1 || opA < 0 || opA > 3 || opB < 0 || opB > 3) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    init_device_globals();
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    BufPtr a = up(A, (size_t)M * K, st), b = up(B, (size_t)K * N, st), c = make_buf((size_t)M * N * sizeof(cplx));
+    const bool ta = (opA == 1 || opA == 2), tb = (opB == 1 || opB == 2);
+    BufPtr work = make_buf((size_t)(1 << 22) * sizeof(cplx));
+    CK(zgemm(st, opA, opB, M, N, K, ONE, a->c(), ta ? M : K, b->c(), tb ? K : N, ZERO, c->c(), N, 1, 0, 0, 0,
+             work->c(), (size_t)1 << 22));
+    CK(cudaMemcpyAsync(C, c->p, (size_t)M * N * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamDestroy(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// Internal kernel launchers of libtdvp (not part of the public C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstddef>
+#include "common.cuh"
+
+extern int g_num_sms;
+
+// ---------------------------------------------------------------- zgemm.cu
+// C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], row-major complex128.
+// op: 0 = N, 1 = T, 2 = C (conj-transpose), 3 = R (conj, no transpose).
+// op(A) is M x K (A stored M x K for N/R, K x M for T/C); op(B) is K x N.
+// `work` (optional) enables deterministic split-K for small M x N.
+enum { OP_N = 0, OP_T = 1, OP_C = 2, OP_R = 3 };
+cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
+                  const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch = 1, long long sA = 0,
+                  long long sB = 0, long long sC = 0, cplx* work = nullptr, size_t work_elems = 0);
+
+// -------------------------------------------------------------- chanmix.cu
+// Sparse MPO-channel contraction:
+//   out[o*so_out + off_out(oc) + i*si_out] = sum_{e in row oc} coef[e] * in[o*so_in + off_in(e) + i*si_in]
+// with off(.) = c0*s0 + c1*s1 + c2*s2 from per-channel index triples.
+struct ChanMix {
+  int n_oc = 0, nnz = 0;
+  int* rowptr = nullptr;   // device [n_oc+1]
+  int4* oc_idx = nullptr;  // device [n_oc]   (c0, c1, c2, -)
+  int4* ic_idx = nullptr;  // device [nnz]    (c0, c1, c2, -)
+  cplx* coef = nullptr;    // device [nnz]
+};
+struct Strides3 {
+  long long s0, s1, s2;
+};
+cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in,
+                    long long si_in, Strides3 in_ch, cplx* out, long long so_out, long long si_out, Strides3 out_ch);
+
+// ---------------------------------------------------------------- vec.cu
+cudaError_t scale_rows(cudaStream_t st, cplx* out, const cplx* in, const double* v, int rows, long long cols);
+cudaError_t scale_cols(cudaStream_t st, cplx* out, const cplx* in, const double* v, long long rows, int cols);
+cudaError_t copy_cplx(cudaStream_t st, cplx* dst, const cplx* src, long long n);
+cudaError_t fill_cplx(cudaStream_t st, cplx* dst, cplx v, long long n);
+// result (device cplx) = sum_i x_i * y_i (no conjugation), deterministic.
+cudaError_t sum_products(cudaStream_t st, const cplx* x, const cplx* y, long long n, cplx* result, double* partials,
+                         unsigned* counter);
+cudaError_t any_nonfinite(cudaStream_t st, const cplx* x, long long n, int* flag);
+
+// ------------------------------------------------------------- lanczos.cu
+constexpr int KMAX = 16;
+struct LanczosDev {
+  double* scal;       // [ALPHA 0..KMAX) [BETA KMAX..2KMAX) [N0 2KMAX] [BRK 2KMAX+1]
+  cplx* coef;         // [2][KMAX+1] multi-dot results
+  cplx* y;            // [KMAX] exp(tau T) e1 * n0
+  double* partials;   // reduction scratch [nblk_max * 2 * (KMAX+1)]
+  unsigned* counter;  // last-block counter (self-resetting)
+  int* brk_count;     // number of Lanczos runs that hit breakdown
+};
+enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1 };
+int lanczos_nblk(long long n);
+cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* v0, long long n);
+cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
+                    long long n, int k);
+cudaError_t lz_update_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
+                           long long n);
+cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
+                           long long n, int k);
+cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k);
+cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im);
+cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
+                       long long n);
+
+// ----------------------------------------------------------------- svd.cu
+struct SvdDev {
+  cplx* Y;            // (mr + nc) x nc, column-major, ld = ldy
+  long long ldy;
+  double* sigma;      // [nc]
+  int* order;         // [nc]
+  double* offmax;     // [1]
+  int* ires;          // [4] : chi, chi_eps, nonfinite, r
+  double* dres;       // [4] : w (discarded weight), sigma_1
+  double* h_buf;      // pinned host mirror [8] (offmax, dres..)
+  int* h_ibuf;        // pinned host mirror [4]
+};
+struct TruncParams {
+  int chi_max;
+  double eps, w_max, delta;
+};
+// Full SVD by blocked one-sided Jacobi, then truncation (SURVEY O-7) and the split
+// Psi_L = U S, Lambda = S, V = 1/S, Psi_R = S W^dagger.  theta is m x n row-major.
+// Returns chi via *chi_out (host), discarded weight via *w_out (host).
+cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
+                               const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
+                               int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out);
+size_t svd_work_elems(int m, int n);

@@ -1,0 +1,273 @@
+// Device-resident Lanczos exponentiation exp(tau H) v (PAPER.md:447 + footnote,
+// :100 "max 8 Krylov vectors").
+//
+// No host synchronisation: alpha_k, beta_k, the breakdown flag and the
+// Krylov coefficients live in device memory.  Each vector pass is a single
+// HBM-bound kernel with a deterministic two-level reduction (per-block
+// partials, the last block to finish reduces them in block order):
+//   lz_dots         c = V^H w                  (alpha_k = Re c_k)
+//   lz_update_dots  w -= V c ;   c' = V^H w    (3-term recurrence + CGS pass 1, fused)
+//   lz_update_norm  w -= V c' ;  ||w||^2       (CGS pass 2; beta_k, breakdown)
+//   lz_next         v_{k+1} = w / beta_k       (hard zero after breakdown)
+// then an on-device K x K symmetric tridiagonal eigen-decomposition
+// (cyclic Jacobi) for y = n0 Q exp(tau mu) Q^T e_1 and v' = V y.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int TPB = 256;
+constexpr int NW = TPB / 32;
+
+int nblk_for(long long n) {
+  long long b = (n + TPB - 1) / TPB;
+  return (int)std::max<long long>(1, std::min<long long>(b, 2LL * g_num_sms));
+}
+
+enum { M_DOTS = 0, M_UPD_DOTS = 1, M_UPD_NORM = 2 };
+
+template <int NV, int MODE>
+__global__ void __launch_bounds__(TPB) lz_pass_kernel(LanczosDev d, const cplx* __restrict__ V, long long ldv,
+                                                      cplx* w, long long n, int k) {
+  constexpr int NQ = (MODE == M_UPD_NORM) ? 1 : NV;  // number of complex quantities reduced
+  __shared__ cplx s_c[NV];
+  __shared__ double s_red[NW][2 * NQ];
+  __shared__ bool s_last;
+  if (MODE != M_DOTS) {
+    if (threadIdx.x < NV) s_c[threadIdx.x] = d.coef[(MODE == M_UPD_DOTS ? 0 : (KMAX + 1)) + threadIdx.x];
+    __syncthreads();
+  }
+  double acc[2 * NQ];
+#pragma unroll
+  for (int q = 0; q < 2 * NQ; ++q) acc[q] = 0.0;
+
+  for (long long e = blockIdx.x * (long long)TPB + threadIdx.x; e < n; e += (long long)gridDim.x * TPB) {
+    cplx we = w[e];
+    cplx v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[i * ldv + e];
+    if (MODE != M_DOTS) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], v[i]));
+      w[e] = we;
+    }
+    if (MODE == M_UPD_NORM) {
+      acc[0] += cabs2(we);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const cplx p = cdotc(v[i], we);
+        acc[2 * i] += p.x;
+        acc[2 * i + 1] += p.y;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 2 * NQ; ++q) {
+    const double t = warp_sum(acc[q]);
+    if (lane == 0) s_red[wid][q] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * NQ) {
+    double t = 0.0;
+    for (int ww = 0; ww < NW; ++ww) t += s_red[ww][threadIdx.x];
+    d.partials[(long long)blockIdx.x * (2 * NQ) + threadIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(d.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ double s_tot[2 * NQ];
+  if (threadIdx.x < 2 * NQ) {
+    double t = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)d.partials)[(long long)b * (2 * NQ) + threadIdx.x];
+    s_tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *d.counter = 0u;
+    if (MODE == M_DOTS) {
+      for (int i = 0; i < NV; ++i) d.coef[i] = cmk(s_tot[2 * i], s_tot[2 * i + 1]);
+      d.scal[k] = s_tot[2 * k];  // alpha_k = Re <v_k, H v_k>
+    } else if (MODE == M_UPD_DOTS) {
+      for (int i = 0; i < NV; ++i) d.coef[KMAX + 1 + i] = cmk(s_tot[2 * i], s_tot[2 * i + 1]);
+    } else {
+      const double b = sqrt(s_tot[0]);
+      double s = 1.0;
+      for (int i = 0; i <= k; ++i) s = fmax(s, fabs(d.scal[i]));
+      for (int i = 0; i < k; ++i) s = fmax(s, d.scal[KMAX + i]);
+      const bool was = d.scal[LZ_BRK] != 0.0;
+      if (was || !(b > 1e-12 * s)) {
+        d.scal[LZ_BRK] = 1.0;
+        d.scal[KMAX + k] = 0.0;
+        if (!was) atomicAdd(d.brk_count, 1);
+      } else {
+        d.scal[KMAX + k] = b;
+      }
+    }
+  }
+}
+
+template <int MODE>
+cudaError_t pass_dispatch(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
+                          long long n, int k) {
+  const int nb = nblk_for(n);
+#define LZ_CASE(NVV) \
+  case NVV: lz_pass_kernel<NVV, MODE><<<nb, TPB, 0, st>>>(d, V, ldv, w, n, k); break;
+  switch (nv) {
+    LZ_CASE(1) LZ_CASE(2) LZ_CASE(3) LZ_CASE(4) LZ_CASE(5) LZ_CASE(6) LZ_CASE(7) LZ_CASE(8)
+    LZ_CASE(9) LZ_CASE(10) LZ_CASE(11) LZ_CASE(12) LZ_CASE(13) LZ_CASE(14) LZ_CASE(15) LZ_CASE(16)
+    default: return cudaErrorInvalidValue;
+  }
+#undef LZ_CASE
+  return cudaGetLastError();
+}
+
+// n0 = ||x||, reset scalars
+__global__ void __launch_bounds__(TPB) lz_norm_kernel(LanczosDev d, const cplx* __restrict__ x, long long n) {
+  __shared__ double s_red[NW];
+  __shared__ bool s_last;
+  double acc = 0.0;
+  for (long long e = blockIdx.x * (long long)TPB + threadIdx.x; e < n; e += (long long)gridDim.x * TPB)
+    acc += cabs2(x[e]);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int ww = 0; ww < NW; ++ww) t += s_red[ww];
+    d.partials[blockIdx.x] = t;
+    __threadfence();
+    s_last = (atomicAdd(d.counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)d.partials)[b];
+    for (int i = 0; i < 2 * KMAX; ++i) d.scal[i] = 0.0;
+    d.scal[LZ_N0] = sqrt(t);
+    d.scal[LZ_BRK] = 0.0;
+    *d.counter = 0u;
+  }
+}
+
+__global__ void lz_scale_kernel(const double* scal, int which, bool brk_zero, const cplx* __restrict__ x,
+                                cplx* __restrict__ out, long long n) {
+  const double nrm = scal[which];
+  const bool zero = (brk_zero && scal[LZ_BRK] != 0.0) || !(nrm > 0.0);
+  const double inv = zero ? 0.0 : 1.0 / nrm;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    out[e] = cscale(x[e], inv);
+}
+
+// symmetric tridiagonal T (K x K) = Q mu Q^T by cyclic Jacobi; y = n0 Q (e^{tau mu} * Q^T e1)
+__global__ void lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double A[KMAX][KMAX], Q[KMAX][KMAX];
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j) {
+      A[i][j] = 0.0;
+      Q[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+  for (int i = 0; i < K; ++i) A[i][i] = d.scal[i];
+  for (int i = 0; i + 1 < K; ++i) A[i][i + 1] = A[i + 1][i] = d.scal[KMAX + i];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, nrm = 0.0;
+    for (int i = 0; i < K; ++i)
+      for (int j = 0; j < K; ++j) {
+        if (i != j) off += A[i][j] * A[i][j];
+        nrm += A[i][j] * A[i][j];
+      }
+    if (off <= 1e-34 * nrm || off == 0.0) break;
+    for (int p = 0; p < K - 1; ++p)
+      for (int q = p + 1; q < K; ++q) {
+        const double apq = A[p][q];
+        if (apq == 0.0) continue;
+        const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int r = 0; r < K; ++r) {
+          const double arp = A[r][p], arq = A[r][q];
+          A[r][p] = c * arp - s * arq;
+          A[r][q] = s * arp + c * arq;
+        }
+        for (int r = 0; r < K; ++r) {
+          const double apr = A[p][r], aqr = A[q][r];
+          A[p][r] = c * apr - s * aqr;
+          A[q][r] = s * apr + c * aqr;
+        }
+        A[p][q] = A[q][p] = 0.0;
+        for (int r = 0; r < K; ++r) {
+          const double qrp = Q[r][p], qrq = Q[r][q];
+          Q[r][p] = c * qrp - s * qrq;
+          Q[r][q] = s * qrp + c * qrq;
+        }
+      }
+  }
+  const double n0 = d.scal[LZ_N0];
+  cplx f[KMAX];
+  for (int j = 0; j < K; ++j) {
+    const double mu = A[j][j];
+    const double mag = exp(tre * mu);
+    double sn, cs;
+    sincos(tim * mu, &sn, &cs);
+    f[j] = cmk(mag * cs * Q[0][j], mag * sn * Q[0][j]);
+  }
+  for (int i = 0; i < K; ++i) {
+    cplx acc = cmk(0, 0);
+    for (int j = 0; j < K; ++j) acc = cadd(acc, cscale(f[j], Q[i][j]));
+    d.y[i] = cscale(acc, n0);
+  }
+}
+
+__global__ void lz_combine_kernel(const cplx* __restrict__ y, const cplx* __restrict__ V, long long ldv, int K,
+                                  cplx* __restrict__ out, long long n) {
+  __shared__ cplx s_y[KMAX];
+  if (threadIdx.x < K) s_y[threadIdx.x] = y[threadIdx.x];
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    cplx acc = cmk(0, 0);
+    for (int i = 0; i < K; ++i) cfma(acc, s_y[i], V[i * ldv + e]);
+    out[e] = acc;
+  }
+}
+
+}  // namespace
+
+int lanczos_nblk(long long n) { return nblk_for(n); }
+
+cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* v0, long long n) {
+  lz_norm_kernel<<<nblk_for(n), TPB, 0, st>>>(d, x, n);
+  lz_scale_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.scal, LZ_N0, false, x, v0, n);
+  return cudaGetLastError();
+}
+cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
+                    long long n, int k) {
+  return pass_dispatch<M_DOTS>(st, d, V, ldv, nv, const_cast<cplx*>(w), n, k);
+}
+cudaError_t lz_update_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
+                           long long n) {
+  return pass_dispatch<M_UPD_DOTS>(st, d, V, ldv, nv, w, n, 0);
+}
+cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
+                           long long n, int k) {
+  return pass_dispatch<M_UPD_NORM>(st, d, V, ldv, nv, w, n, k);
+}
+cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k) {
+  lz_scale_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.scal, KMAX + k, true, w, vnext, n);
+  return cudaGetLastError();
+}
+cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im) {
+  if (K > KMAX) return cudaErrorInvalidValue;
+  lz_tridiag_exp_kernel<<<1, 32, 0, st>>>(d, K, tau_re, tau_im);
+  return cudaGetLastError();
+}
+cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
+                       long long n) {
+  lz_combine_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.y, V, ldv, K, out, n);
+  return cudaGetLastError();
+}

@@ -1,0 +1,300 @@
+// Complex-FP64 GEMM on the sm_100a FP64 tensor pipe (DMMA.8x8x4).
+//
+// tcgen05.mma has no f64 kind, so the FP64 tensor path on B200 is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA).  One complex product is four
+// real DMMAs on separate re/im accumulators.  Operands are staged through a
+// 4-stage cp.async (LDGSTS) shared-memory pipeline; tiles are 64x64 complex
+// per CTA, 32x32 per warp.  op(A), op(B) in {N, T, C, R(conj only)};
+// everything is row-major.  Used for every dense contraction on the hot path
+// (H_eff stages 1 and 4, H1, environment updates, Theta merge, measurement).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 8, STAGES = 4, NT = 128;
+constexpr int PA = BK + 4;   // [BM][PA]  k contiguous   (conflict-free fragment reads)
+constexpr int PAT = BM + 2;  // [BK][PAT] m contiguous
+constexpr int PB = BN + 2;   // [BK][PB]  n contiguous
+constexpr int PBT = BK + 4;  // [BN][PBT] k contiguous
+
+struct GemmArgs {
+  int M, N, K;
+  cplx alpha, beta;
+  const cplx* A;
+  long long lda, sA;
+  const cplx* B;
+  long long ldb, sB;
+  cplx* C;
+  long long ldc, sC;
+  int ksplit, kchunk;
+  cplx* work;  // split-K partials [batch*ksplit][M][N]
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int OPA, int OPB>
+__global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
+  constexpr bool TA = (OPA == 1 || OPA == 2), CA = (OPA == 2 || OPA == 3);
+  constexpr bool TB = (OPB == 1 || OPB == 2), CB = (OPB == 2 || OPB == 3);
+  constexpr int A_ST = TA ? BK * PAT : BM * PA;
+  constexpr int B_ST = TB ? BN * PBT : BK * PB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* sA = reinterpret_cast<cplx*>(smem_raw);
+  cplx* sB = sA + STAGES * A_ST;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int z = blockIdx.z;
+  const int batch = z / g.ksplit, split = z - batch * g.ksplit;
+  const int kbeg = split * g.kchunk;
+  const int kend = min(g.K, kbeg + g.kchunk);
+  const cplx* A = g.A + batch * g.sA;
+  const cplx* B = g.B + batch * g.sB;
+  const int M = g.M, N = g.N;
+  const long long lda = g.lda, ldb = g.ldb;
+
+  auto load_tile = [&](int stage, int kt) {
+    const int k0 = kbeg + kt * BK;
+    cplx* a_dst = sA + stage * A_ST;
+    cplx* b_dst = sB + stage * B_ST;
+#pragma unroll
+    for (int i = 0; i < (BM * BK) / NT; ++i) {
+      const int c = tid + i * NT;
+      if (!TA) {
+        const int r = c >> 3, kk = c & 7;
+        const int gm = m0 + r, gk = k0 + kk;
+        const bool v = (gm < M) && (gk < kend);
+        cp_async16(a_dst + r * PA + kk, v ? (const void*)(A + gm * lda + gk) : (const void*)A, v);
+      } else {
+        const int kr = c >> 6, mm = c & 63;
+        const int gm = m0 + mm, gk = k0 + kr;
+        const bool v = (gm < M) && (gk < kend);
+        cp_async16(a_dst + kr * PAT + mm, v ? (const void*)(A + gk * lda + gm) : (const void*)A, v);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < (BN * BK) / NT; ++i) {
+      const int c = tid + i * NT;
+      if (!TB) {
+        const int kr = c >> 6, nn = c & 63;
+        const int gn = n0 + nn, gk = k0 + kr;
+        const bool v = (gn < N) && (gk < kend);
+        cp_async16(b_dst + kr * PB + nn, v ? (const void*)(B + gk * ldb + gn) : (const void*)B, v);
+      } else {
+        const int r = c >> 3, kk = c & 7;
+        const int gn = n0 + r, gk = k0 + kk;
+        const bool v = (gn < N) && (gk < kend);
+        cp_async16(b_dst + r * PBT + kk, v ? (const void*)(B + gn * ldb + gk) : (const void*)B, v);
+      }
+    }
+  };
+
+  double accR[4][4][2], accI[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
+
+  const int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_tile(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = kt + STAGES - 1;
+      if (nt < nk) load_tile(nt % STAGES, nt);
+      cp_commit();
+    }
+    const cplx* a_s = sA + (kt % STAGES) * A_ST;
+    const cplx* b_s = sB + (kt % STAGES) * B_ST;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      const int kq = ks + (lane & 3);
+      cplx af[4], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int row = wm * 32 + mt * 8 + (lane >> 2);
+        af[mt] = TA ? a_s[kq * PAT + row] : a_s[row * PA + kq];
+        if (CA) af[mt].y = -af[mt].y;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int col = wn * 32 + nt * 8 + (lane >> 2);
+        bf[nt] = TB ? b_s[col * PBT + kq] : b_s[kq * PB + col];
+        if (CB) bf[nt].y = -bf[nt].y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double nai = -af[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          dmma(accR[mt][nt][0], accR[mt][nt][1], af[mt].x, bf[nt].x);
+          dmma(accR[mt][nt][0], accR[mt][nt][1], nai, bf[nt].y);
+          dmma(accI[mt][nt][0], accI[mt][nt][1], af[mt].x, bf[nt].y);
+          dmma(accI[mt][nt][0], accI[mt][nt][1], af[mt].y, bf[nt].x);
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue
+  const bool partial = g.ksplit > 1;
+  cplx* C = partial ? g.work + (long long)z * M * N : g.C + batch * g.sC;
+  const long long ldc = partial ? (long long)N : g.ldc;
+  const cplx alpha = g.alpha, beta = g.beta;
+  const bool use_beta = (beta.x != 0.0 || beta.y != 0.0);
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int r = m0 + wm * 32 + mt * 8 + (lane >> 2);
+    if (r >= M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = n0 + wn * 32 + nt * 8 + 2 * (lane & 3) + h;
+        if (c >= N) continue;
+        cplx v = cmk(accR[mt][nt][h], accI[mt][nt][h]);
+        cplx* p = C + r * ldc + c;
+        if (partial) {
+          *p = v;
+        } else {
+          cplx out = cmul(alpha, v);
+          if (use_beta) out = cadd(out, cmul(beta, *p));
+          *p = out;
+        }
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(int M, int N, int ksplit, int batch, const cplx* __restrict__ work, cplx alpha,
+                                     cplx beta, cplx* C, long long ldc, long long sC) {
+  const long long MN = (long long)M * N;
+  const long long total = MN * batch;
+  const bool use_beta = (beta.x != 0.0 || beta.y != 0.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / MN, rc = e - b * MN;
+    const int r = (int)(rc / N), c = (int)(rc - (long long)r * N);
+    cplx s = cmk(0, 0);
+    for (int k = 0; k < ksplit; ++k) s = cadd(s, work[(b * ksplit + k) * MN + rc]);
+    cplx* p = C + b * sC + (long long)r * ldc + c;
+    cplx out = cmul(alpha, s);
+    if (use_beta) out = cadd(out, cmul(beta, *p));
+    *p = out;
+  }
+}
+
+__global__ void scale_matrix_kernel(int M, int N, cplx beta, cplx* C, long long ldc) {
+  const long long total = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / N), c = (int)(e - (long long)r * N);
+    cplx* p = C + (long long)r * ldc + c;
+    *p = (beta.x == 0.0 && beta.y == 0.0) ? cmk(0, 0) : cmul(beta, *p);
+  }
+}
+
+template <int OPA, int OPB>
+constexpr size_t smem_bytes() {
+  constexpr bool TA = (OPA == 1 || OPA == 2);
+  constexpr bool TB = (OPB == 1 || OPB == 2);
+  return (size_t)STAGES * ((TA ? BK * PAT : BM * PA) + (TB ? BN * PBT : BK * PB)) * sizeof(cplx);
+}
+
+template <int OPA, int OPB>
+cudaError_t launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  static bool configured = false;
+  constexpr size_t sm = smem_bytes<OPA, OPB>();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  zgemm_dmma_kernel<OPA, OPB><<<grid, NT, sm, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <int OPA>
+cudaError_t launch_b(int opB, const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  switch (opB) {
+    case 0: return launch_t<OPA, 0>(g, grid, st);
+    case 1: return launch_t<OPA, 1>(g, grid, st);
+    case 2: return launch_t<OPA, 2>(g, grid, st);
+    default: return launch_t<OPA, 3>(g, grid, st);
+  }
+}
+
+}  // namespace
+
+int g_num_sms = 148;
+
+cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
+                  const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch, long long sA,
+                  long long sB, long long sC, cplx* work, size_t work_elems) {
+  if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
+  if (K <= 0) {
+    for (int b = 0; b < batch; ++b) {
+      scale_matrix_kernel<<<std::max(1, std::min(4096, (M * N + 255) / 256)), 256, 0, st>>>(M, N, beta, C + b * sC, ldc);
+    }
+    return cudaGetLastError();
+  }
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.alpha = alpha; g.beta = beta;
+  g.A = A; g.lda = lda; g.sA = sA;
+  g.B = B; g.ldb = ldb; g.sB = sB;
+  g.C = C; g.ldc = ldc; g.sC = sC;
+  g.work = work;
+  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+  int ksplit = 1;
+  const long long target = 2LL * g_num_sms;
+  if (work != nullptr && tiles < target && K >= 256) {
+    ksplit = (int)std::min<long long>((target + tiles - 1) / tiles, K / 128);
+    ksplit = std::min(ksplit, 16);
+    while (ksplit > 1 && (size_t)ksplit * batch * (size_t)M * N > work_elems) --ksplit;
+  }
+  int kchunk = K;
+  if (ksplit > 1) {
+    kchunk = ((K + ksplit - 1) / ksplit + BK - 1) / BK * BK;
+    ksplit = (K + kchunk - 1) / kchunk;
+  }
+  g.ksplit = ksplit;
+  g.kchunk = kchunk;
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch * ksplit);
+  cudaError_t e;
+  switch (opA) {
+    case 0: e = launch_b<0>(opB, g, grid, st); break;
+    case 1: e = launch_b<1>(opB, g, grid, st); break;
+    case 2: e = launch_b<2>(opB, g, grid, st); break;
+    default: e = launch_b<3>(opB, g, grid, st); break;
+  }
+  if (e != cudaSuccess || ksplit == 1) return e;
+  const long long total = (long long)M * N * batch;
+  const int blocks = (int)std::min<long long>(4LL * g_num_sms, (total + 255) / 256);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ksplit, batch, work, alpha, beta, C, ldc, sC);
+  return cudaGetLastError();
+}

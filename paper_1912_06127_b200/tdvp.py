@@ -1,0 +1,271 @@
+"""Thin ctypes binding of libtdvp.so (include/tdvp.h).  Argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libtdvp.so; there is no
+CPU fallback.  If the library is missing or has no GPU, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtdvp.so")
+_lib = None
+
+TDVP_ERRORS = {-1: "bad argument", -2: "non-finite input", -3: "invalid partition", -4: "CUDA/NCCL failure",
+               -5: "numerical failure", -6: "call order"}
+
+
+class TdvpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libtdvp error {code} ({TDVP_ERRORS.get(code, '?')}): {msg}")
+        self.code = code
+
+
+class tdvp_params(C.Structure):
+    _fields_ = [("eps", C.c_double), ("w_max", C.c_double), ("krylov_k", C.c_int), ("krylov_tol", C.c_double),
+                ("multiplet_delta", C.c_double), ("timing", C.c_int)]
+
+
+class tdvp_stats(C.Structure):
+    _fields_ = [("w_step", C.c_double), ("w_total", C.c_double), ("trunc_active", C.c_int), ("n_pair", C.c_int),
+                ("n_back", C.c_int), ("krylov_breakdowns", C.c_int), ("svd_sweeps_max", C.c_int),
+                ("step_ms", C.c_double), ("heff2_ms", C.c_double), ("heff2_flop", C.c_double),
+                ("heff2_calls", C.c_int), ("heff1_ms", C.c_double), ("heff1_flop", C.c_double),
+                ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+_PD = C.POINTER(_D)
+
+_SIGS = {
+    "tdvp_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "tdvp_set_params": (C.c_int, [C.c_void_p, C.POINTER(tdvp_params)]),
+    "tdvp_get_params": (C.c_int, [C.c_void_p, C.POINTER(tdvp_params)]),
+    "tdvp_set_mpo": (C.c_int, [C.c_void_p, _I, _PD]),
+    "tdvp_set_mps": (C.c_int, [C.c_void_p, _I, _PD, _PD]),
+    "tdvp_step": (C.c_int, [C.c_void_p, C.c_double, C.c_int]),
+    "tdvp_measure_sz": (C.c_int, [C.c_void_p, _D]),
+    "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
+    "tdvp_measure_norm": (C.c_int, [C.c_void_p, _D]),
+    "tdvp_get_stats": (C.c_int, [C.c_void_p, C.POINTER(tdvp_stats)]),
+    "tdvp_get_chi": (C.c_int, [C.c_void_p, _I]),
+    "tdvp_get_mps": (C.c_int, [C.c_void_p, _PD, _PD]),
+    "tdvp_last_error": (C.c_char_p, [C.c_void_p]),
+    "tdvp_destroy": (None, [C.c_void_p]),
+    "tdvp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "tdvp_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
+    "tdvp_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, C.c_int]),
+    "tdvp_partition": (C.c_int, [C.c_int, C.c_int, _I, _I]),
+    "tdvp_apply_heff2": (C.c_int, [C.c_int] * 6 + [_D] * 6),
+    "tdvp_apply_heff1": (C.c_int, [C.c_int] * 5 + [_D] * 5),
+    "tdvp_env_left": (C.c_int, [C.c_int] * 5 + [_D] * 4),
+    "tdvp_env_right": (C.c_int, [C.c_int] * 5 + [_D] * 4),
+    "tdvp_expm_lanczos_dense": (C.c_int, [C.c_int, _D, _D, C.c_double, C.c_double, C.c_int, _D]),
+    "tdvp_svd_split": (C.c_int, [C.c_int, C.c_int, _D, C.c_int, C.c_double, C.c_double, C.c_double, _I, _D, _D, _D,
+                                 _D]),
+    "tdvp_zgemm": (C.c_int, [C.c_int] * 5 + [_D] * 3),
+}
+
+
+def lib():
+    """Load libtdvp.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_1912_06127_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _c(a):
+    """contiguous complex128 array -> double pointer"""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    return a, a.ctypes.data_as(_D)
+
+
+def _check(rc, h=None):
+    if rc != 0:
+        msg = lib().tdvp_last_error(h).decode() if h else ""
+        raise TdvpError(rc, msg)
+
+
+class Tdvp:
+    """Handle over one libtdvp context (one device, or one rank)."""
+
+    def __init__(self, L, d, D_mpo, chi_max):
+        self.L, self.d = L, d
+        h = C.c_void_p()
+        _check(lib().tdvp_create(L, d, D_mpo, chi_max, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tdvp_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False):
+        p = tdvp_params(eps, w_max, krylov_k, 0.0, multiplet_delta, int(bool(timing)))
+        _check(lib().tdvp_set_params(self.h, C.byref(p)), self.h)
+
+    def set_mpo(self, W):
+        D = [1] + [w.shape[3] for w in W]
+        Ws = [_c(w)[0] for w in W]
+        arr = (_D * len(Ws))(*[w.ctypes.data_as(_D) for w in Ws])
+        _check(lib().tdvp_set_mpo(self.h, (C.c_int * len(D))(*D), arr), self.h)
+
+    def set_mps(self, psi, lam):
+        chi = [1] + [p.shape[2] for p in psi[:-1]] + [1]
+        P = [_c(p)[0] for p in psi]
+        Lm = [np.ascontiguousarray(l, dtype=np.float64) for l in lam]
+        pa = (_D * len(P))(*[p.ctypes.data_as(_D) for p in P])
+        la = (_D * max(1, len(Lm)))(*[l.ctypes.data_as(_D) for l in Lm])
+        _check(lib().tdvp_set_mps(self.h, (C.c_int * len(chi))(*chi), pa, la), self.h)
+
+    def step(self, dt, n_segments=1):
+        _check(lib().tdvp_step(self.h, float(dt), int(n_segments)), self.h)
+
+    def measure_sz(self):
+        out = np.zeros(self.L)
+        _check(lib().tdvp_measure_sz(self.h, out.ctypes.data_as(_D)), self.h)
+        return out
+
+    def measure_energy(self):
+        e = C.c_double()
+        _check(lib().tdvp_measure_energy(self.h, C.byref(e)), self.h)
+        return e.value
+
+    def measure_norm(self):
+        e = C.c_double()
+        _check(lib().tdvp_measure_norm(self.h, C.byref(e)), self.h)
+        return e.value
+
+    def stats(self):
+        s = tdvp_stats()
+        _check(lib().tdvp_get_stats(self.h, C.byref(s)), self.h)
+        return s.as_dict()
+
+    def chi(self):
+        out = (C.c_int * (self.L + 1))()
+        _check(lib().tdvp_get_chi(self.h, out), self.h)
+        return list(out)
+
+    def get_mps(self):
+        chi = self.chi()
+        psi = [np.zeros((chi[j], self.d, chi[j + 1]), dtype=np.complex128) for j in range(self.L)]
+        lam = [np.zeros(chi[b + 1]) for b in range(self.L - 1)]
+        pa = (_D * self.L)(*[p.ctypes.data_as(_D) for p in psi])
+        la = (_D * max(1, self.L - 1))(*[l.ctypes.data_as(_D) for l in lam])
+        _check(lib().tdvp_get_mps(self.h, pa, la), self.h)
+        return psi, lam
+
+    def comm_init(self, rank, world, uid: bytes):
+        _check(lib().tdvp_comm_init(self.h, rank, world, uid), self.h)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().tdvp_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ---------------------------------------------------------------- host-only
+def plan(L, p, h, q):
+    buf = (C.c_int * (4 * 8 * (L + 8)))()
+    n = lib().tdvp_plan(L, p, h, q, buf, 8 * (L + 8))
+    if n < 0:
+        raise TdvpError(n, f"tdvp_plan(L={L}, p={p})")
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]
+
+
+def partition(L, p):
+    s = (C.c_int * p)()
+    e = (C.c_int * p)()
+    _check(lib().tdvp_partition(L, p, s, e))
+    return list(zip(list(s), list(e)))
+
+
+# ------------------------------------------------------- kernel-level entries
+def apply_heff2(Lenv, W1, W2, Renv, theta):
+    cl, d, _, cr = theta.shape
+    Dl, Dm, Dr = W1.shape[0], W1.shape[3], W2.shape[3]
+    out = np.zeros_like(theta, dtype=np.complex128)
+    args = [_c(x) for x in (Lenv, W1, W2, Renv, theta)]
+    _check(lib().tdvp_apply_heff2(cl, cr, d, Dl, Dm, Dr, *[a[1] for a in args], out.ctypes.data_as(_D)))
+    return out
+
+
+def apply_heff1(Lenv, W, Renv, psi):
+    cl, d, cr = psi.shape
+    out = np.zeros_like(psi, dtype=np.complex128)
+    args = [_c(x) for x in (Lenv, W, Renv, psi)]
+    _check(lib().tdvp_apply_heff1(cl, cr, d, W.shape[0], W.shape[3], *[a[1] for a in args], out.ctypes.data_as(_D)))
+    return out
+
+
+def env_left(beta, A, W):
+    cl, d, cr = A.shape
+    out = np.zeros((cr, W.shape[3], cr), dtype=np.complex128)
+    args = [_c(x) for x in (beta, A, W)]
+    _check(lib().tdvp_env_left(cl, cr, d, W.shape[0], W.shape[3], *[a[1] for a in args], out.ctypes.data_as(_D)))
+    return out
+
+
+def env_right(gamma, B, W):
+    cl, d, cr = B.shape
+    out = np.zeros((cl, W.shape[0], cl), dtype=np.complex128)
+    args = [_c(x) for x in (gamma, B, W)]
+    _check(lib().tdvp_env_right(cl, cr, d, W.shape[0], W.shape[3], *[a[1] for a in args], out.ctypes.data_as(_D)))
+    return out
+
+
+def expm_lanczos_dense(H, v, tau, K=8):
+    n = v.shape[0]
+    out = np.zeros(n, dtype=np.complex128)
+    (hH, pH), (hv, pv) = _c(H), _c(v)
+    _check(lib().tdvp_expm_lanczos_dense(n, pH, pv, float(np.real(tau)), float(np.imag(tau)), K,
+                                         out.ctypes.data_as(_D)))
+    return out
+
+
+def svd_split(M, chi_max, eps=1e-12, w_max=0.0, delta=1e-6):
+    m, n = M.shape
+    k = min(m, n)
+    pl = np.zeros((m, k), dtype=np.complex128)
+    pr = np.zeros((k, n), dtype=np.complex128)
+    lam = np.zeros(k)
+    chi = C.c_int()
+    w = C.c_double()
+    hM, pM = _c(M)
+    _check(lib().tdvp_svd_split(m, n, pM, chi_max, eps, w_max, delta, C.byref(chi), C.byref(w),
+                                pl.ctypes.data_as(_D), lam.ctypes.data_as(_D), pr.ctypes.data_as(_D)))
+    c = chi.value
+    # psiL was written with row stride chi
+    pl = pl.reshape(-1)[: m * c].reshape(m, c)
+    pr = pr.reshape(-1)[: c * n].reshape(c, n)
+    return pl, lam[:c], pr, w.value
+
+
+def zgemm(opA, opB, A, B):
+    ops = {"N": 0, "T": 1, "C": 2, "R": 3}
+    a, b = ops[opA], ops[opB]
+    M = A.shape[1] if a in (1, 2) else A.shape[0]
+    K = A.shape[0] if a in (1, 2) else A.shape[1]
+    N = B.shape[0] if b in (1, 2) else B.shape[1]
+    out = np.zeros((M, N), dtype=np.complex128)
+    (hA, pA), (hB, pB) = _c(A), _c(B)
+    _check(lib().tdvp_zgemm(a, b, M, N, K, pA, pB, out.ctypes.data_as(_D)))
+    return out

@@ -1,0 +1,212 @@
+"""GPU parity: libtdvp (CUDA, through the C-ABI) against the CPU oracle.
+
+Kernel level: every contraction of the hot path on random operands at ragged
+sizes (several 64x64 tiles plus a tail), <= 1e-12 relative Frobenius.
+Integrator level: <S^z_i>, E, norm and the chi profile after every step of
+the same seeded runs with the same segment partition; 1e-9 absolute when no
+truncation is active, 1e-6 otherwise (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+import tdvp_inputs as ti
+from oracle import tdvp as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1912_06127_b200 as pkg
+    return pkg
+
+
+def rc(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ------------------------------------------------------------------ kernels
+@pytest.mark.parametrize("opA", "NTCR")
+@pytest.mark.parametrize("opB", "NTCR")
+def test_zgemm_all_ops(B, opA, opB):
+    rng = np.random.default_rng(0)
+    M, N, K = 131, 77, 203
+    A = rc(rng, K, M) if opA in "TC" else rc(rng, M, K)
+    Bm = rc(rng, N, K) if opB in "TC" else rc(rng, K, N)
+    f = {"N": lambda x: x, "T": lambda x: x.T, "C": lambda x: x.conj().T, "R": lambda x: x.conj()}
+    ref = f[opA](A) @ f[opB](Bm)
+    out = B.zgemm(opA, opB, A, Bm)
+    assert rel(out, ref) < 1e-14
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 4), (64, 64, 8), (65, 129, 257), (5, 3, 4096), (2048, 16, 640)])
+def test_zgemm_shapes(B, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    A, Bm = rc(rng, M, K), rc(rng, K, N)
+    assert rel(B.zgemm("N", "N", A, Bm), A @ Bm) < 1e-14
+
+
+def _mpo_site(kind, rng):
+    if kind == "nn":
+        W = ti.mpo_xxz_nn(4, 0.7)[1]
+    elif kind == "lr":
+        a, lam, _, _ = ti.fit_expsum(100, 9, 2.0)
+        W = ti.mpo_xxz_expsum(4, a, lam, 1.0)[1]
+    else:
+        W = rc(rng, 3, 2, 2, 4)
+    return W
+
+
+@pytest.mark.parametrize("cl,cr,kind", [(1, 2, "nn"), (37, 53, "nn"), (70, 66, "nn"), (33, 17, "lr"), (24, 24, "rand")])
+def test_heff2_matches_oracle(B, cl, cr, kind):
+    rng = np.random.default_rng(cl * 100 + cr)
+    W1 = _mpo_site(kind, rng)
+    W2 = _mpo_site(kind, rng) if kind != "rand" else rc(rng, 4, 2, 2, 3)
+    Lenv = rc(rng, cl, W1.shape[0], cl)
+    Renv = rc(rng, cr, W2.shape[3], cr)
+    th = rc(rng, cl, 2, 2, cr)
+    ref = O.apply_h2(Lenv, W1, W2, Renv, th)
+    assert rel(B.apply_heff2(Lenv, W1, W2, Renv, th), ref) < 1e-13
+
+
+@pytest.mark.parametrize("cl,cr,kind", [(1, 2, "nn"), (45, 70, "nn"), (19, 33, "lr"), (16, 9, "rand")])
+def test_heff1_and_envs_match_oracle(B, cl, cr, kind):
+    rng = np.random.default_rng(cl * 7 + cr)
+    W = _mpo_site(kind, rng)
+    Dl, Dr = W.shape[0], W.shape[3]
+    Lenv, Renv = rc(rng, cl, Dl, cl), rc(rng, cr, Dr, cr)
+    psi = rc(rng, cl, 2, cr)
+    assert rel(B.apply_heff1(Lenv, W, Renv, psi), O.apply_h1(Lenv, W, Renv, psi)) < 1e-13
+    assert rel(B.env_left(Lenv, psi, W), O.env_left(Lenv, psi, W)) < 1e-13
+    assert rel(B.env_right(Renv, psi, W), O.env_right(Renv, psi, W)) < 1e-13
+
+
+@pytest.mark.parametrize("n,K", [(32, 8), (300, 8), (7, 8), (64, 12)])
+def test_lanczos_matches_oracle(B, n, K):
+    rng = np.random.default_rng(n)
+    A = rc(rng, n, n)
+    H = (A + A.conj().T) / 2
+    v = rc(rng, n)
+    for tau in (-0.05j, 0.025j, -0.1j):
+        ref = O.expm_lanczos(lambda x: H @ x, v, tau, K=K)
+        out = B.expm_lanczos_dense(H, v, tau, K=K)
+        assert rel(out, ref) < 1e-12
+
+
+@pytest.mark.parametrize("m,n,chi_max", [(2, 2, 2), (8, 6, 6), (40, 72, 20), (128, 128, 64), (256, 200, 128),
+                                         (66, 34, 40)])
+def test_svd_split_matches_oracle(B, m, n, chi_max):
+    rng = np.random.default_rng(m * n)
+    M = rc(rng, m, n) * np.exp(-np.linspace(0, 30, n))[None, :]  # graded spectrum down to ~1e-13
+    p = O.Params(chi_max=chi_max, eps=1e-10)
+    pl_o, S_o, pr_o, w_o, _, _ = O.svd_truncate(M.reshape(m, 1, 1, n), p)
+    pl, S, pr, w = B.svd_split(M, chi_max, eps=1e-10)
+    assert len(S) == len(S_o)
+    assert np.allclose(S, S_o, rtol=1e-11, atol=1e-14 * S_o[0])
+    assert abs(w - w_o) <= 1e-12 * np.linalg.norm(M) ** 2
+    # gauge-invariant: the truncated matrix Psi_L V Psi_R
+    rec = (pl / S[None, :]) @ pr
+    rec_o = pl_o.reshape(m, -1) @ np.diag(1 / S_o) @ pr_o.reshape(-1, n)
+    assert rel(rec, rec_o) < 1e-10
+    U = pl / S[None, :]
+    assert np.abs(U.conj().T @ U - np.eye(len(S))).max() < 1e-12
+
+
+def test_svd_degenerate_and_rank_deficient(B):
+    rng = np.random.default_rng(5)
+    Q1, _ = np.linalg.qr(rc(rng, 20, 20))
+    Q2, _ = np.linalg.qr(rc(rng, 12, 12))
+    s = np.array([3.0, 2.0, 2.0, 2.0, 1.0, 0.5] + [0.0] * 6)
+    M = Q1[:, :12] @ np.diag(s) @ Q2.conj().T
+    for chi_max in (3, 4, 12):
+        p = O.Params(chi_max=chi_max, eps=1e-12)
+        _, S_o, _, w_o, _, _ = O.svd_truncate(M.reshape(20, 1, 1, 12), p)
+        _, S, _, w = B.svd_split(M, chi_max, eps=1e-12)
+        assert len(S) == len(S_o) and np.allclose(S, S_o, rtol=1e-12)
+        assert abs(w - w_o) < 1e-12
+
+
+# --------------------------------------------------------------- integrator
+def gpu_run(B, mps, W, chi_max, eps, dt, steps, p, krylov_k=8, every=1):
+    D = max(w.shape[3] for w in W)
+    t = B.Tdvp(len(W), 2, max(D, max(w.shape[0] for w in W)), chi_max)
+    t.set_params(eps=eps, krylov_k=krylov_k)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    out = []
+    for n in range(steps):
+        t.step(dt, p)
+        if (n + 1) % every == 0 or n + 1 == steps:
+            out.append(dict(sz=t.measure_sz(), E=t.measure_energy(), norm=t.measure_norm(), chi=t.chi(),
+                            stats=t.stats()))
+    t.close()
+    return out
+
+
+def oracle_run(mps, W, chi_max, eps, dt, steps, p, krylov_k=8, every=1):
+    st = O.init_state(mps, W, O.Params(chi_max=chi_max, eps=eps, krylov_k=krylov_k), p)
+    out = []
+    for n in range(steps):
+        O.step(st, dt)
+        if (n + 1) % every == 0 or n + 1 == steps:
+            m = O.measure(st)
+            out.append(dict(sz=m["sz"], E=m["energy"], norm=m["norm"], chi=O.chi_profile(st),
+                            trunc=st.stats.trunc_active, w=st.stats.w_step))
+    return out
+
+
+def compare(g, o, tol_untrunc=1e-9, tol_trunc=1e-6):
+    trunc = False
+    for a, b in zip(g, o):
+        trunc = trunc or b["trunc"]
+        tol = tol_trunc if trunc else tol_untrunc
+        assert a["chi"] == b["chi"], (a["chi"], b["chi"])
+        assert np.abs(a["sz"] - b["sz"]).max() < tol
+        assert abs(a["E"] - b["E"]) < tol
+        assert abs(a["norm"] - b["norm"]) < tol
+
+
+def test_config1_serial_untruncated(B):
+    cfg = ti.config("c1")
+    args = (cfg["mps"], cfg["mpo"], cfg["chi_max"], cfg["eps"], cfg["dt"], cfg["steps"], 1)
+    g, o = gpu_run(B, *args), oracle_run(*args)
+    compare(g, o)
+    assert not any(x["trunc"] for x in o)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_segmented_small(B, p):
+    L = 16
+    mps, W = ti.neel_mps(L), ti.mpo_xxz_nn(L, 0.5)
+    args = (mps, W, 32, 1e-12, 0.05, 10, p)
+    compare(gpu_run(B, *args), oracle_run(*args))
+
+
+def test_long_range_random_state(B):
+    L = 20
+    a, lam, _, _ = ti.fit_expsum(100, 9, 2.0)
+    args = (ti.bloch_mps(L, 0), ti.mpo_xxz_expsum(L, a, lam, 1.0), 16, 1e-12, 0.02, 4, 2)
+    compare(gpu_run(B, *args), oracle_run(*args))
+
+
+def test_truncated_saturated(B):
+    L = 12
+    mps = ti.random_canonical_mps(L, 8, seed=2)
+    args = (mps, ti.mpo_xxz_nn(L, 0.5), 8, 1e-10, 0.05, 3, 1)
+    g, o = gpu_run(B, *args), oracle_run(*args)
+    assert o[0]["trunc"]
+    compare(g, o)
+
+
+def test_one_body_exact_on_gpu(B):
+    L, h = 8, 0.7
+    g = gpu_run(B, ti.neel_mps(L), ti.mpo_onsite(L, h * ti.SX), 8, 1e-12, 0.1, 10, 2)
+    exact = np.array([0.5 if i % 2 == 0 else -0.5 for i in range(L)]) * np.cos(h * 1.0)
+    assert np.abs(g[-1]["sz"] - exact).max() < 1e-12
