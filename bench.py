@@ -157,8 +157,8 @@ def cpu_baseline(wl, budget_s=12.0):
     done_w, n = 0.0, 0
     j = L // 2 - 4
     while time.perf_counter() - t0 < budget_s and j < L - 2:
-        O.tdvp._pair(st, seg, j, -0.5j * dt, True, False)
-        O.tdvp._back(st, seg, j + 1, dt)
+        O._pair(st, seg, j, -0.5j * dt, True, False)
+        O._back(st, seg, j + 1, dt)
         done_w += w_pair(j) + w_back(j + 1)
         n += 1
         j += 1
