@@ -1,0 +1,87 @@
+"""GPU-vs-oracle parity on BASELINE.json's configs at their full sizes, in
+the launch configuration bench.py uses (one handle, the config's segment
+count), same seeded inputs and partition.  Observables after every few steps:
+1e-9 absolute while no truncation is active, 1e-6 once it is.  The chi
+profile must match except for isolated eps-threshold flips (|dchi| = 1 at a
+bond where a singular value sits within rounding of eps*sigma_1), which are
+counted and bounded."""
+import numpy as np
+import pytest
+
+import tdvp_inputs as ti
+from oracle import tdvp as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1912_06127_b200 as pkg
+    return pkg
+
+
+def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
+    D = max(max(w.shape[0], w.shape[3]) for w in W)
+    t = B.Tdvp(len(W), 2, D, chi_max)
+    t.set_params(eps=eps)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    st = O.init_state(mps, W, O.Params(chi_max=chi_max, eps=eps), p)
+    flips, trunc, worst = 0, False, 0.0
+    for n in range(steps):
+        t.step(dt, p)
+        O.step(st, dt)
+        trunc = trunc or st.stats.trunc_active
+        if (n + 1) % every and n + 1 != steps:
+            continue
+        m = O.measure(st)
+        sz, E, nrm, chi = t.measure_sz(), t.measure_energy(), t.measure_norm(), t.chi()
+        ochi = O.chi_profile(st)
+        d = [abs(a - b) for a, b in zip(chi, ochi)]
+        assert max(d) <= 1, (chi, ochi)
+        flips += sum(1 for x in d if x)
+        tol = 1e-6 if trunc else 1e-9
+        err = max(np.abs(sz - m["sz"]).max(), abs(E - m["energy"]), abs(nrm - m["norm"]))
+        worst = max(worst, err)
+        assert err < tol, (n + 1, err, tol)
+    s = t.stats()
+    t.close()
+    return dict(flips=flips, trunc=trunc, worst=worst, stats=s, chi=ochi)
+
+
+def test_config2_serial_full(B):
+    c = ti.config("c2")
+    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], 1, every=5)
+    assert r["flips"] <= 4
+
+
+def test_config3_eight_segments_full(B):
+    c = ti.config("c3")
+    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], 8, every=5)
+    assert r["flips"] <= 4
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_config4_long_range(B, p):
+    c = ti.config("c4")
+    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], 3, p, every=1)
+    assert r["flips"] <= 6
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_config5_scaling_partitions(B, p):
+    c = ti.config("c5")
+    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], p, every=5)
+    assert r["flips"] <= 4
+
+
+def test_bench_workload_saturated_chi(B):
+    """bench.py's default workload (c2sat) for one step: chi_max binds everywhere."""
+    L = 64
+    mps = ti.random_canonical_mps(L, 128, seed=2)
+    r = run_both(B, mps, ti.mpo_xxz_nn(L, 0.5), 128, 1e-10, 0.05, 1, 1, every=1)
+    assert r["trunc"]
+    assert max(r["chi"]) == 128
