@@ -96,6 +96,8 @@ def merge_theta(psi_l, v, psi_r):
     return np.tensordot(psi_l * v[None, None, :], psi_r, axes=(2, 0))
 
 
+MULTIPLET_ABS = 1e-13  # absolute degeneracy floor of the multiplet guard (reading R-9b)
+
 # ----------------------------------------------------------------------------
 # truncated SVD (PAPER.md:455 Fig 6; :493-499 eq:discweight; :510 epsilon)
 # ----------------------------------------------------------------------------
@@ -108,7 +110,12 @@ def truncation_rank(sigma, p: Params):
     chi_w   = min chi with sum_{k>chi} sigma_k^2 <= w_max
               (w_max = 0 -> chi_w = #nonzero)
     chi     = min(chi_eps, chi_w, chi_max), then the multiplet guard:
-              while 1 < chi < r and sigma_{chi+1} >= (1-delta) sigma_chi: chi -= 1
+              while 1 < chi < r and sigma_chi - sigma_{chi+1} <= delta sigma_chi + tau sigma_1:
+                  chi -= 1
+              with tau = MULTIPLET_ABS = 1e-13: values closer than the absolute accuracy of
+              any backward-stable SVD (O(u sigma_1)) are one multiplet, so a
+              numerically degenerate multiplet (e.g. SU(2) at Delta = 1) straddling
+              the eps cut is kept or dropped whole (reading R-9b).
     eps = 0 is floored at 1e-14 (SPEC.md linalg-core design decision) so that
     V = 1/Lambda never overflows (PAPER.md:365 footnote).
     """
@@ -130,7 +137,7 @@ def truncation_rank(sigma, p: Params):
     else:
         chi_w = nz
     chi = max(1, min(chi_eps, chi_w, p.chi_max))
-    while 1 < chi < r and sigma[chi] >= (1.0 - p.multiplet_delta) * sigma[chi - 1]:
+    while 1 < chi < r and sigma[chi - 1] - sigma[chi] <= p.multiplet_delta * sigma[chi - 1] + MULTIPLET_ABS * s1:
         chi -= 1
     return chi
 

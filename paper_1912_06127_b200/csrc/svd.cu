@@ -301,7 +301,8 @@ __global__ void svd_truncate_kernel(const double* __restrict__ sigma, int nc, in
     chi_w = max(chi_w, 1);
   }
   int chi = max(1, min(min(chi_eps, chi_w), tp.chi_max));
-  while (chi > 1 && chi < r && s_sorted[chi] >= (1.0 - tp.delta) * s_sorted[chi - 1]) --chi;
+  // multiplet guard (AMB-9 + reading R-9b: absolute floor 1e-13 sigma_1)
+  while (chi > 1 && chi < r && s_sorted[chi - 1] - s_sorted[chi] <= tp.delta * s_sorted[chi - 1] + 1e-13 * s1) --chi;
   double w = 0.0;
   for (int k = chi; k < r; ++k) w += s_sorted[k] * s_sorted[k];
   ires[0] = chi;

@@ -147,6 +147,11 @@ def test_truncation_rules():
     assert O.truncation_rank(sig, O.Params(chi_max=6, w_max=0.0101 + 1e-6)) == 4
     # eps rule
     assert O.truncation_rank(sig, O.Params(chi_max=6, eps=2e-3)) == 5
+    # R-9b: a numerically degenerate pair (gap < 1e-13 sigma_1) straddling the eps cut is dropped whole
+    sig2 = np.array([1.0, 0.2, 1.0e-12 + 3e-14, 1.0e-12 - 2e-14, 5e-13])
+    assert O.truncation_rank(sig2, O.Params(chi_max=5, eps=1e-12)) == 2
+    sig3 = np.array([1.0, 0.2, 1.0e-12 + 3e-13, 1.0e-12 - 2e-14, 5e-13])
+    assert O.truncation_rank(sig3, O.Params(chi_max=5, eps=1e-12)) == 3
 
 
 # --------------------------------------------------------------------------
