@@ -150,6 +150,15 @@ int tdvp_svd_split(int m, int n, const double* M, int chi_max, double eps, doubl
 /* C = op(A) op(B) complex GEMM on the DMMA path (op 0 N, 1 T, 2 C, 3 conj). */
 int tdvp_zgemm(int opA, int opB, int M, int N, int K, const double* A, const double* B, double* C);
 
+/* ---- microbenchmarks (device-resident operands, CUDA-event / wall timed) ---- */
+/* Mean device time (ms) of one H_eff^(2) matvec at chi_L = chi_R = chi with the
+ * given MPO site tensors, and its algorithmic real flop count. */
+int tdvp_bench_heff2(int chi, int Dl, int Dm, int Dr, const double* W1, const double* W2, int reps, double* ms,
+                     double* flop);
+/* Mean wall time (ms, includes the host read of chi) of one truncated SVD split
+ * of the m x n matrix M; *sweeps = Jacobi sweeps of the last run. */
+int tdvp_bench_svd(int m, int n, const double* M, int reps, double* ms, int* sweeps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -400,7 +401,7 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
                                       g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps);
   if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
   CK(se);
-  g_launch_count += 3 + (long long)sweeps * std::max(1, ((std::min(cl * d, d * cr) + 15) / 16 + 1) / 2 * 2 - 1);
+  g_launch_count += 5;
   if (e0 >= 0) h->ev_svd.emplace_back(e0, ev_record(h));
   if (chi > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: chi exceeds allocation");
   g.cb[j + 1] = chi;
@@ -1400,6 +1401,63 @@ int tdvp_zgemm(int opA, int opB, int M, int N, int K, const double* A, const dou
     CK(cudaMemcpyAsync(C, c->p, (size_t)M * N * sizeof(cplx), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaStreamDestroy(st));
+  });
+}
+
+
+// ----------------------------------------------------- microbenchmarks (device-resident operands)
+int tdvp_bench_heff2(int chi, int Dl, int Dm, int Dr, const double* W1, const double* W2, int reps, double* ms,
+                     double* flop) {
+  if (chi < 1 || reps < 1) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(chi, std::max(Dl, std::max(Dm, Dr)));
+    const int d = 2;
+    MpoSite w1, w2;
+    build_site(w1, Dl, Dm, d, to_cplx(W1, (size_t)Dl * d * d * Dm));
+    build_site(w2, Dm, Dr, d, to_cplx(W2, (size_t)Dm * d * d * Dr));
+    const size_t nL = (size_t)chi * Dl * chi, nR = (size_t)chi * Dr * chi, n = (size_t)chi * d * d * chi;
+    BufPtr L_ = make_buf(nL * sizeof(cplx)), R_ = make_buf(nR * sizeof(cplx)), x = make_buf(n * sizeof(cplx)),
+           y = make_buf(n * sizeof(cplx));
+    CK(fill_cplx(h->st, L_->c(), cmk(0.01, -0.02), (long long)nL));
+    CK(fill_cplx(h->st, R_->c(), cmk(-0.03, 0.01), (long long)nR));
+    CK(fill_cplx(h->st, x->c(), cmk(0.5, 0.25), (long long)n));
+    heff2(h, L_->c(), w1, w2, R_->c(), chi, chi, x->c(), y->c());  // warm-up
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->st));
+    for (int r = 0; r < reps; ++r) heff2(h, L_->c(), w1, w2, R_->c(), chi, chi, (r & 1) ? y->c() : x->c(), (r & 1) ? x->c() : y->c());
+    CK(cudaEventRecord(e1, h->st));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / reps;
+    *flop = flops_heff2(chi, chi, d, Dl, Dr, nnz_of(w1), nnz_of(w2));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+int tdvp_bench_svd(int m, int n, const double* M, int reps, double* ms, int* sweeps) {
+  if (m < 1 || n < 1 || reps < 1) return TDVP_EARG;
+  return upload_run_download([&](tdvp_ctx*) {
+    tdvp_ctx* h = scratch_ctx(std::max(8, (std::max(m, n) + 1) / 2 + 1), 1);
+    BufPtr a = up(M, (size_t)m * n, h->st);
+    const int k = std::min(m, n);
+    BufPtr pl = make_buf((size_t)m * k * sizeof(cplx)), pr = make_buf((size_t)k * n * sizeof(cplx));
+    BufPtr l = make_buf(k * sizeof(double)), vi = make_buf(k * sizeof(double));
+    TruncParams tp{k, 1e-12, 0.0, 1e-6};
+    int c = 0, r = 0, ce = 0, sw = 0;
+    double ww = 0.0;
+    CK(svd_truncate_split(h->st, h->sv, a->c(), m, n, tp, pl->c(), pr->c(), l->d(), vi->d(), &c, &ww, &r, &ce, &sw));
+    CK(cudaStreamSynchronize(h->st));
+    const auto t0 = std::chrono::high_resolution_clock::now();
+    for (int i = 0; i < reps; ++i)
+      CK(svd_truncate_split(h->st, h->sv, a->c(), m, n, tp, pl->c(), pr->c(), l->d(), vi->d(), &c, &ww, &r, &ce, &sw));
+    CK(cudaStreamSynchronize(h->st));
+    const auto t1 = std::chrono::high_resolution_clock::now();
+    *ms = std::chrono::duration<double, std::milli>(t1 - t0).count() / reps;
+    *sweeps = sw;
   });
 }
 

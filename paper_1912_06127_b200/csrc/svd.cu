@@ -4,9 +4,9 @@
 // The matrix (or its conjugate transpose, so that rows >= cols) is held
 // column-major together with the accumulated right rotations:
 //   Y = [X ; V]  (mr + nc rows, nc columns),  X = M V  ->  columns U_c sigma_c.
-// A sweep is a round-robin tournament over column blocks of b = 16; in each
-// round one CTA per block pair
-//   1. forms the 32 x 32 Gram matrix of its columns (X rows only),
+// A sweep is a round-robin tournament over column blocks of b (4 or 8); in
+// each round one CTA per block pair
+//   1. forms the 2b x 2b Gram matrix of its columns (X rows only),
 //   2. measures max |g_ij| / sqrt(g_ii g_jj) (convergence, relative),
 //   3. diagonalises the Gram matrix by parallel-ordered complex Jacobi
 //      rotations in shared memory, accumulating the unitary Q,
@@ -19,14 +19,13 @@
 #include <cmath>
 #include "common.cuh"
 #include "kernels.h"
+#include <cooperative_groups.h>
+#include <cstdlib>
+namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int TB = 16;     // columns per block
-constexpr int PC = 2 * TB; // columns per block pair
 constexpr int NTH = 256;
-constexpr int TR = 16;     // row tile
-constexpr int OPT = TR * PC / NTH;  // apply outputs per thread
 
 __device__ __forceinline__ void rr_pair(int n, int round, int i, int& a, int& b) {
   // circle method on n (even) players: player n-1 fixed
@@ -58,196 +57,242 @@ __global__ void svd_init_kernel(cplx* Y, long long ldy, const cplx* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(NTH) svd_round_kernel(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe,
-                                                        int round, double tol, double* offmax) {
+// ---------------------------------------------------------------------------
+// Cooperative single-launch variant: all sweeps and rounds in one persistent
+// kernel, grid-wide barrier between rounds, convergence decided on device
+// (no host round trips).  Block pair = 2*BW columns per CTA; the inner
+// Hermitian 2BW x 2BW Gram eigenproblem is solved by one warp.
+template <int BW>
+struct CoopCfg {
+  static constexpr int PC = 2 * BW;
+  static constexpr int TRc = (PC <= 8) ? 32 : 16;  // rows per staged tile
+  static constexpr int E = PC * PC;                // Gram entries
+  static constexpr int EPT = (E + NTH - 1) / NTH;  // entries per thread
+  static constexpr int S = (E >= NTH) ? 1 : NTH / E;  // row slices per entry
+};
+
+template <int BW>
+__device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe, int round, int pair, double tol,
+                          double* off_cur, cplx (*G)[2 * BW + 1], cplx (*Qm)[2 * BW + 1], cplx (*tile)[2 * BW + 1],
+                          cplx* red, int* cols, int* s_ncols, int* rp, int* rq, double* rc, cplx* rs,
+                          double* s_off) {
+  using Cf = CoopCfg<BW>;
+  constexpr int PC = Cf::PC, TRc = Cf::TRc;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    int a, b;
+    rr_pair(nbe, round, pair, a, b);
+    int k = 0;
+    for (int blk : {a, b}) {
+      if (blk >= nb) continue;
+      for (int c = blk * BW; c < min(nc, blk * BW + BW); ++c) cols[k++] = c;
+    }
+    *s_ncols = k;
+  }
+  __syncthreads();
+  const int ncols = *s_ncols;
+  if (ncols < 2) return;
+
+  // ---- Gram matrix over the X rows
+  cplx acc[Cf::EPT];
+#pragma unroll
+  for (int u = 0; u < Cf::EPT; ++u) acc[u] = cmk(0, 0);
+  const int slice = (Cf::S > 1) ? (tid % Cf::S) : 0;
+  const int ebase = (Cf::S > 1) ? (tid / Cf::S) : tid;
+  for (int r0 = 0; r0 < mr; r0 += TRc) {
+    for (int e = tid; e < TRc * PC; e += NTH) {
+      const int c = e / TRc, rr = e - c * TRc;
+      cplx v = cmk(0, 0);
+      if (c < ncols && r0 + rr < mr) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
+      tile[rr][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < Cf::EPT; ++u) {
+      const int e = ebase + u * NTH;
+      if (e < Cf::E) {
+        const int i = e / PC, j = e - i * PC;
+        for (int rr = slice; rr < TRc; rr += Cf::S) {
+          const cplx a = tile[rr][i], b = tile[rr][j];
+          acc[u].x = fma(a.x, b.x, acc[u].x);
+          acc[u].x = fma(a.y, b.y, acc[u].x);
+          acc[u].y = fma(a.x, b.y, acc[u].y);
+          acc[u].y = fma(-a.y, b.x, acc[u].y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (Cf::S > 1) {
+    red[tid] = acc[0];
+    __syncthreads();
+    if (tid < Cf::E) {
+      cplx t = cmk(0, 0);
+      for (int q = 0; q < Cf::S; ++q) t = cadd(t, red[tid * Cf::S + q]);
+      G[tid / PC][tid % PC] = t;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < Cf::EPT; ++u) {
+      const int e = ebase + u * NTH;
+      if (e < Cf::E) G[e / PC][e % PC] = acc[u];
+    }
+  }
+  for (int e = tid; e < PC * PC; e += NTH) Qm[e / PC][e % PC] = cmk((e / PC) == (e % PC) ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+
+  // ---- relative off-diagonal measure (whole CTA)
+  double off = 0.0;
+  for (int e = tid; e < PC * PC; e += NTH) {
+    const int i = e / PC, j = e - i * PC;
+    if (i < j && j < ncols) {
+      const double di = G[i][i].x, dj = G[j][j].x;
+      if (di > 0.0 && dj > 0.0) off = fmax(off, sqrt(cabs2(G[i][j]) / (di * dj)));
+    }
+  }
+  off = warp_max(off);
+  if (lane == 0) s_off[wid] = off;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NTH / 32; ++w) t = fmax(t, s_off[w]);
+    s_off[0] = t;
+    atomic_max_nonneg(off_cur, t);
+  }
+  __syncthreads();
+  const double off0 = s_off[0];
+  __syncthreads();
+  if (off0 <= tol) return;
+
+  // ---- inner Jacobi on G by warp 0 (parallel ordering, Q accumulates)
+  if (wid == 0) {
+    const int n2 = ncols + (ncols & 1);
+    for (int sweep = 0; sweep < 6; ++sweep) {
+      for (int r = 0; r < n2 - 1; ++r) {
+        if (lane < n2 / 2) {
+          int p, q;
+          rr_pair(n2, r, lane, p, q);
+          double cs = 1.0;
+          cplx sn = cmk(0, 0);
+          if (q < ncols) {
+            const double a = G[p][p].x, c = G[q][q].x;
+            const cplx g = G[p][q];
+            const double ag = sqrt(cabs2(g));
+            if (ag > 1e-300 && !(ag <= 0.25 * tol * sqrt(fmax(a, 0.0) * fmax(c, 0.0)))) {
+              const double zeta = (c - a) / (2.0 * ag);
+              const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              cs = 1.0 / sqrt(1.0 + t * t);
+              const double sv = cs * t;
+              sn = cmk(sv * g.x / ag, sv * g.y / ag);
+            }
+          }
+          rp[lane] = p;
+          rq[lane] = q;
+          rc[lane] = cs;
+          rs[lane] = sn;
+        }
+        __syncwarp();
+        for (int e = lane; e < (n2 / 2) * PC; e += 32) {
+          const int pi = e / PC, row = e - pi * PC;
+          const int p = rp[pi], q = rq[pi];
+          if (q >= ncols || row >= ncols || rc[pi] == 1.0) continue;
+          const double cs = rc[pi];
+          const cplx sn = rs[pi];
+          const cplx gp = G[row][p], gq = G[row][q];
+          G[row][p] = csub(cscale(gp, cs), cmul(cconj(sn), gq));
+          G[row][q] = cadd(cmul(sn, gp), cscale(gq, cs));
+          const cplx qp = Qm[row][p], qq = Qm[row][q];
+          Qm[row][p] = csub(cscale(qp, cs), cmul(cconj(sn), qq));
+          Qm[row][q] = cadd(cmul(sn, qp), cscale(qq, cs));
+        }
+        __syncwarp();
+        for (int e = lane; e < (n2 / 2) * PC; e += 32) {
+          const int pi = e / PC, col = e - pi * PC;
+          const int p = rp[pi], q = rq[pi];
+          if (q >= ncols || col >= ncols || rc[pi] == 1.0) continue;
+          const double cs = rc[pi];
+          const cplx sn = rs[pi];
+          const cplx gp = G[p][col], gq = G[q][col];
+          G[p][col] = csub(cscale(gp, cs), cmul(sn, gq));
+          G[q][col] = cadd(cmul(cconj(sn), gp), cscale(gq, cs));
+        }
+        __syncwarp();
+        if (lane < n2 / 2) {
+          const int p = rp[lane], q = rq[lane];
+          if (q < ncols && rc[lane] != 1.0) {
+            G[p][q] = cmk(0, 0);
+            G[q][p] = cmk(0, 0);
+            G[p][p].y = 0.0;
+            G[q][q].y = 0.0;
+          }
+        }
+        __syncwarp();
+      }
+      double o = 0.0;
+      for (int e = lane; e < PC * PC; e += 32) {
+        const int i = e / PC, j = e - i * PC;
+        if (i < j && j < ncols) {
+          const double di = G[i][i].x, dj = G[j][j].x;
+          if (di > 0.0 && dj > 0.0) o = fmax(o, sqrt(cabs2(G[i][j]) / (di * dj)));
+        }
+      }
+      if (warp_max(o) <= 0.25 * tol) break;
+    }
+  }
+  __syncthreads();
+
+  // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows
+  const int rows = mr + nc;
+  for (int r0 = 0; r0 < rows; r0 += TRc) {
+    for (int e = tid; e < TRc * PC; e += NTH) {
+      const int c = e / TRc, rr = e - c * TRc;
+      cplx v = cmk(0, 0);
+      if (c < ncols && r0 + rr < rows) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
+      tile[rr][c] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < TRc * PC; e += NTH) {
+      const int c = e / TRc, rr = e - c * TRc;
+      if (c < ncols && r0 + rr < rows) {
+        cplx a = cmk(0, 0);
+        for (int k = 0; k < ncols; ++k) cfma(a, tile[rr][k], Qm[k][c]);
+        __stcg(Y + (long long)cols[c] * ldy + r0 + rr, a);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int BW>
+__global__ void __launch_bounds__(NTH) svd_coop_kernel(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe,
+                                                       double tol, int max_sweeps, double* offbuf, int* sweeps_out) {
+  constexpr int PC = 2 * BW;
+  using Cf = CoopCfg<BW>;
   __shared__ cplx G[PC][PC + 1];
   __shared__ cplx Qm[PC][PC + 1];
-  __shared__ cplx tile[TR][PC + 1];
+  __shared__ cplx tile[Cf::TRc][PC + 1];
+  __shared__ cplx red[NTH];
   __shared__ int cols[PC];
   __shared__ int s_ncols;
   __shared__ int rp[PC / 2], rq[PC / 2];
   __shared__ double rc[PC / 2];
   __shared__ cplx rs[PC / 2];
   __shared__ double s_off[NTH / 32];
-  __shared__ double s_offall;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-
-  if (tid == 0) {
-    int a, b;
-    rr_pair(nbe, round, blockIdx.x, a, b);
-    int k = 0;
-    for (int blk : {a, b}) {
-      if (blk >= nb) continue;
-      for (int c = blk * TB; c < min(nc, blk * TB + TB); ++c) cols[k++] = c;
+  cg::grid_group grid = cg::this_grid();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    double* off_cur = offbuf + (sweep % 3);
+    if (blockIdx.x == 0 && threadIdx.x == 0) offbuf[(sweep + 1) % 3] = 0.0;
+    for (int round = 0; round < nbe - 1; ++round) {
+      for (int pair = blockIdx.x; pair < nbe / 2; pair += gridDim.x)
+        coop_pair<BW>(Y, ldy, mr, nc, nb, nbe, round, pair, tol, off_cur, G, Qm, tile, red, cols, &s_ncols, rp, rq,
+                      rc, rs, s_off);
+      grid.sync();
     }
-    s_ncols = k;
+    const double off = __ldcg(off_cur);
+    if (!(off > tol)) break;
   }
-  __syncthreads();
-  const int ncols = s_ncols;
-  if (ncols < 2) return;
-
-  // ---- 1. Gram matrix of the X rows
-  cplx acc[4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) acc[s] = cmk(0, 0);
-  for (int r0 = 0; r0 < mr; r0 += TR) {
-    for (int e = tid; e < TR * PC; e += NTH) {
-      const int c = e / TR, rr = e - c * TR;
-      cplx v = cmk(0, 0);
-      if (c < ncols && r0 + rr < mr) v = Y[(long long)cols[c] * ldy + r0 + rr];
-      tile[rr][c] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int i = wid + 8 * s, j = lane;
-#pragma unroll 8
-      for (int rr = 0; rr < TR; ++rr) {
-        const cplx a = tile[rr][i], b = tile[rr][j];
-        acc[s].x = fma(a.x, b.x, acc[s].x);
-        acc[s].x = fma(a.y, b.y, acc[s].x);
-        acc[s].y = fma(a.x, b.y, acc[s].y);
-        acc[s].y = fma(-a.y, b.x, acc[s].y);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int s = 0; s < 4; ++s) G[wid + 8 * s][lane] = acc[s];
-  for (int e = tid; e < PC * PC; e += NTH) {
-    const int i = e / PC, j = e - i * PC;
-    Qm[i][j] = cmk(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-
-  // ---- 2. relative off-diagonal measure
-  auto measure_off = [&]() -> double {
-    double off = 0.0;
-    for (int e = tid; e < PC * PC; e += NTH) {
-      const int i = e / PC, j = e - i * PC;
-      if (i < j && j < ncols) {
-        const double di = G[i][i].x, dj = G[j][j].x;
-        if (di > 0.0 && dj > 0.0) off = fmax(off, sqrt(cabs2(G[i][j])) / sqrt(di * dj));
-      }
-    }
-    off = warp_max(off);
-    if (lane == 0) s_off[wid] = off;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < NTH / 32; ++w) t = fmax(t, s_off[w]);
-      s_offall = t;
-    }
-    __syncthreads();
-    return s_offall;
-  };
-  const double off0 = measure_off();
-  if (tid == 0) atomic_max_nonneg(offmax, off0);
-  if (off0 <= tol) return;
-
-  // ---- 3. parallel-ordered Jacobi diagonalisation of G, Q accumulates
-  const int n2 = ncols + (ncols & 1);
-  for (int sweep = 0; sweep < 10; ++sweep) {
-    for (int r = 0; r < n2 - 1; ++r) {
-      if (tid < n2 / 2) {
-        int p, q;
-        rr_pair(n2, r, tid, p, q);
-        double cs = 1.0;
-        cplx sn = cmk(0, 0);  // sn * e^{i phi}
-        if (q < ncols) {
-          const double a = G[p][p].x, c = G[q][q].x;
-          const cplx g = G[p][q];
-          const double ag = sqrt(cabs2(g));
-          if (ag > 0.0 && ag > 1e-300 && !(ag <= 0.25 * tol * sqrt(fmax(a, 0.0) * fmax(c, 0.0)))) {
-            const double zeta = (c - a) / (2.0 * ag);
-            const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            cs = 1.0 / sqrt(1.0 + t * t);
-            const double s = cs * t;
-            sn = cmk(s * g.x / ag, s * g.y / ag);
-          }
-        }
-        rp[tid] = p;
-        rq[tid] = q;
-        rc[tid] = cs;
-        rs[tid] = sn;
-      }
-      __syncthreads();
-      // column updates of G and Q:  X_p' = cs X_p - conj(sn) X_q ; X_q' = sn X_p + cs X_q
-      for (int e = tid; e < (n2 / 2) * PC; e += NTH) {
-        const int pi = e / PC, row = e - pi * PC;
-        const int p = rp[pi], q = rq[pi];
-        if (q >= ncols || row >= ncols) continue;
-        const double cs = rc[pi];
-        const cplx sn = rs[pi];
-        if (cs == 1.0 && sn.x == 0.0 && sn.y == 0.0) continue;
-        {
-          const cplx gp = G[row][p], gq = G[row][q];
-          G[row][p] = csub(cscale(gp, cs), cmul(cconj(sn), gq));
-          G[row][q] = cadd(cmul(sn, gp), cscale(gq, cs));
-        }
-        {
-          const cplx qp = Qm[row][p], qq = Qm[row][q];
-          Qm[row][p] = csub(cscale(qp, cs), cmul(cconj(sn), qq));
-          Qm[row][q] = cadd(cmul(sn, qp), cscale(qq, cs));
-        }
-      }
-      __syncthreads();
-      // row updates of G:  G_p' = cs G_p - sn G_q ; G_q' = conj(sn) G_p + cs G_q
-      for (int e = tid; e < (n2 / 2) * PC; e += NTH) {
-        const int pi = e / PC, col = e - pi * PC;
-        const int p = rp[pi], q = rq[pi];
-        if (q >= ncols || col >= ncols) continue;
-        const double cs = rc[pi];
-        const cplx sn = rs[pi];
-        if (cs == 1.0 && sn.x == 0.0 && sn.y == 0.0) continue;
-        const cplx gp = G[p][col], gq = G[q][col];
-        G[p][col] = csub(cscale(gp, cs), cmul(sn, gq));
-        G[q][col] = cadd(cmul(cconj(sn), gp), cscale(gq, cs));
-      }
-      __syncthreads();
-      if (tid < n2 / 2) {
-        const int p = rp[tid], q = rq[tid];
-        if (q < ncols && !(rc[tid] == 1.0 && rs[tid].x == 0.0 && rs[tid].y == 0.0)) {
-          G[p][q] = cmk(0, 0);
-          G[q][p] = cmk(0, 0);
-          G[p][p].y = 0.0;
-          G[q][q].y = 0.0;
-        }
-      }
-      __syncthreads();
-    }
-    if (measure_off() <= 0.25 * tol) break;
-  }
-
-  // ---- 4. Y_pair <- Y_pair Q over all rows (X and accumulated V)
-  const int rows = mr + nc;
-  for (int r0 = 0; r0 < rows; r0 += TR) {
-    for (int e = tid; e < TR * PC; e += NTH) {
-      const int c = e / TR, rr = e - c * TR;
-      cplx v = cmk(0, 0);
-      if (c < ncols && r0 + rr < rows) v = Y[(long long)cols[c] * ldy + r0 + rr];
-      tile[rr][c] = v;
-    }
-    __syncthreads();
-    cplx outv[OPT];
-#pragma unroll
-    for (int s = 0; s < OPT; ++s) {
-      const int e = tid + s * NTH;
-      const int c = e / TR, rr = e - c * TR;
-      cplx a = cmk(0, 0);
-      if (c < ncols) {
-        for (int k = 0; k < ncols; ++k) cfma(a, tile[rr][k], Qm[k][c]);
-      }
-      outv[s] = a;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < OPT; ++s) {
-      const int e = tid + s * NTH;
-      const int c = e / TR, rr = e - c * TR;
-      if (c < ncols && r0 + rr < rows) Y[(long long)cols[c] * ldy + r0 + rr] = outv[s];
-    }
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
 
 __global__ void svd_colnorm_kernel(const cplx* __restrict__ Y, long long ldy, int mr, int nc, double* sigma,
@@ -358,27 +403,39 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
     svd_init_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, theta, m, n, mr, nc, transposed);
   }
-  const int nb = (nc + TB - 1) / TB;
-  const int nbe = std::max(2, nb + (nb & 1));
   const double tol = std::max(4.0 * DBL_EPSILON * std::sqrt((double)mr), 1e-15);
   int sweeps = 0;
   if (nc >= 2) {
-    for (sweeps = 1; sweeps <= 40; ++sweeps) {
-      if ((e = cudaMemsetAsync(d.offmax, 0, sizeof(double), st)) != cudaSuccess) return e;
-      for (int r = 0; r < nbe - 1; ++r) svd_round_kernel<<<nbe / 2, NTH, 0, st>>>(d.Y, ldy, mr, nc, nb, nbe, r, tol, d.offmax);
-      if ((e = cudaMemcpyAsync(d.h_buf, d.offmax, sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-      if (!(d.h_buf[0] > tol)) break;
+    static int forced = -1;
+    if (forced < 0) {
+      const char* ev = std::getenv("TDVP_SVD_BW");
+      forced = ev ? std::atoi(ev) : 0;
     }
+    int bw = forced > 0 ? forced : (nc <= 1024 ? 4 : 8);
+    if (bw != 4 && bw != 8 && bw != 16) bw = 4;
+    const int nb = (nc + bw - 1) / bw;
+    const int nbe = std::max(2, nb + (nb & 1));
+    if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
+    int max_sweeps = 60;
+    int* sweeps_dev = d.ires + 4;
+    void* args[] = {(void*)&d.Y, (void*)&ldy, (void*)&mr, (void*)&nc, (void*)&nb, (void*)&nbe, (void*)&tol,
+                    (void*)&max_sweeps, (void*)&d.offmax, (void*)&sweeps_dev};
+    void* fn = bw == 4 ? (void*)svd_coop_kernel<4> : bw == 8 ? (void*)svd_coop_kernel<8> : (void*)svd_coop_kernel<16>;
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NTH, 0)) != cudaSuccess) return e;
+    const int grid = std::max(1, std::min(nbe / 2, occ * g_num_sms));
+    if ((e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTH), args, 0, st)) != cudaSuccess) return e;
+    sweeps = -1;  // read back with the truncation results
   }
   if ((e = cudaMemsetAsync(d.ires, 0, 4 * sizeof(int), st)) != cudaSuccess) return e;
   svd_colnorm_kernel<<<(nc + 7) / 8, 256, 0, st>>>(d.Y, ldy, mr, nc, d.sigma, d.ires + 2);
   svd_truncate_kernel<<<1, 1024, (2 * nc + 1) * sizeof(double), st>>>(d.sigma, nc, d.order, tp, d.ires, d.dres);
-  if ((e = cudaMemcpyAsync(d.h_ibuf, d.ires, 4 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(d.h_ibuf, d.ires, 8 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaMemcpyAsync(d.h_buf + 1, d.dres, 2 * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   if (d.h_ibuf[2] != 0 || !std::isfinite(d.h_buf[1]) || !(d.h_buf[2] > 0.0)) return cudaErrorUnknown;
   const int chi = d.h_ibuf[0];
+  if (sweeps < 0) sweeps = d.h_ibuf[4];
   {
     const long long total = (long long)m * chi + (long long)chi * n + chi;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));

@@ -71,6 +71,8 @@ _SIGS = {
     "tdvp_svd_split": (C.c_int, [C.c_int, C.c_int, _D, C.c_int, C.c_double, C.c_double, C.c_double, _I, _D, _D, _D,
                                  _D]),
     "tdvp_zgemm": (C.c_int, [C.c_int] * 5 + [_D] * 3),
+    "tdvp_bench_heff2": (C.c_int, [C.c_int] * 4 + [_D, _D, C.c_int, _D, _D]),
+    "tdvp_bench_svd": (C.c_int, [C.c_int, C.c_int, _D, C.c_int, _D, _I]),
 }
 
 
@@ -269,3 +271,18 @@ def zgemm(opA, opB, A, B):
     (hA, pA), (hB, pB) = _c(A), _c(B)
     _check(lib().tdvp_zgemm(a, b, M, N, K, pA, pB, out.ctypes.data_as(_D)))
     return out
+
+
+# ---------------------------------------------------------------- microbench
+def bench_heff2(chi, W1, W2, reps=20):
+    ms, fl = C.c_double(), C.c_double()
+    (h1, p1), (h2, p2) = _c(W1), _c(W2)
+    _check(lib().tdvp_bench_heff2(chi, W1.shape[0], W1.shape[3], W2.shape[3], p1, p2, reps, C.byref(ms), C.byref(fl)))
+    return ms.value, fl.value
+
+
+def bench_svd(M, reps=5):
+    ms, sw = C.c_double(), C.c_int()
+    hM, pM = _c(M)
+    _check(lib().tdvp_bench_svd(M.shape[0], M.shape[1], pM, reps, C.byref(ms), C.byref(sw)))
+    return ms.value, sw.value
