@@ -65,7 +65,7 @@ __global__ void svd_init_kernel(cplx* Y, long long ldy, const cplx* __restrict__
 template <int BW>
 struct CoopCfg {
   static constexpr int PC = 2 * BW;
-  static constexpr int TRc = (PC <= 8) ? 32 : 16;  // rows per staged tile
+  static constexpr int TRc = 1536 / PC;             // rows per staged tile (6 loads in flight per thread)
   static constexpr int E = PC * PC;                // Gram entries
   static constexpr int EPT = (E + NTH - 1) / NTH;  // entries per thread
   static constexpr int S = (E >= NTH) ? 1 : NTH / E;  // row slices per entry
@@ -100,7 +100,9 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   const int slice = (Cf::S > 1) ? (tid % Cf::S) : 0;
   const int ebase = (Cf::S > 1) ? (tid / Cf::S) : tid;
   for (int r0 = 0; r0 < mr; r0 += TRc) {
-    for (int e = tid; e < TRc * PC; e += NTH) {
+#pragma unroll
+    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
+      const int e = tid + u * NTH;
       const int c = e / TRc, rr = e - c * TRc;
       cplx v = cmk(0, 0);
       if (c < ncols && r0 + rr < mr) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
@@ -195,7 +197,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
         for (int e = lane; e < (n2 / 2) * PC; e += 32) {
           const int pi = e / PC, row = e - pi * PC;
           const int p = rp[pi], q = rq[pi];
-          if (q >= ncols || row >= ncols || rc[pi] == 1.0) continue;
+          if (q >= ncols || row >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
           const double cs = rc[pi];
           const cplx sn = rs[pi];
           const cplx gp = G[row][p], gq = G[row][q];
@@ -209,7 +211,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
         for (int e = lane; e < (n2 / 2) * PC; e += 32) {
           const int pi = e / PC, col = e - pi * PC;
           const int p = rp[pi], q = rq[pi];
-          if (q >= ncols || col >= ncols || rc[pi] == 1.0) continue;
+          if (q >= ncols || col >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
           const double cs = rc[pi];
           const cplx sn = rs[pi];
           const cplx gp = G[p][col], gq = G[q][col];
@@ -219,7 +221,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
         __syncwarp();
         if (lane < n2 / 2) {
           const int p = rp[lane], q = rq[lane];
-          if (q < ncols && rc[lane] != 1.0) {
+          if (q < ncols && !(rs[lane].x == 0.0 && rs[lane].y == 0.0)) {
             G[p][q] = cmk(0, 0);
             G[q][p] = cmk(0, 0);
             G[p][p].y = 0.0;
@@ -244,14 +246,18 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows
   const int rows = mr + nc;
   for (int r0 = 0; r0 < rows; r0 += TRc) {
-    for (int e = tid; e < TRc * PC; e += NTH) {
+#pragma unroll
+    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
+      const int e = tid + u * NTH;
       const int c = e / TRc, rr = e - c * TRc;
       cplx v = cmk(0, 0);
       if (c < ncols && r0 + rr < rows) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
       tile[rr][c] = v;
     }
     __syncthreads();
-    for (int e = tid; e < TRc * PC; e += NTH) {
+#pragma unroll
+    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
+      const int e = tid + u * NTH;
       const int c = e / TRc, rr = e - c * TRc;
       if (c < ncols && r0 + rr < rows) {
         cplx a = cmk(0, 0);
@@ -412,7 +418,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
       forced = ev ? std::atoi(ev) : 0;
     }
     int bw = forced > 0 ? forced : (nc <= 1024 ? 4 : 8);
-    if (bw != 4 && bw != 8 && bw != 16) bw = 4;
+    if (bw != 4 && bw != 8) bw = 4;
     const int nb = (nc + bw - 1) / bw;
     const int nbe = std::max(2, nb + (nb & 1));
     if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
@@ -420,7 +426,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     int* sweeps_dev = d.ires + 4;
     void* args[] = {(void*)&d.Y, (void*)&ldy, (void*)&mr, (void*)&nc, (void*)&nb, (void*)&nbe, (void*)&tol,
                     (void*)&max_sweeps, (void*)&d.offmax, (void*)&sweeps_dev};
-    void* fn = bw == 4 ? (void*)svd_coop_kernel<4> : bw == 8 ? (void*)svd_coop_kernel<8> : (void*)svd_coop_kernel<16>;
+    void* fn = bw == 4 ? (void*)svd_coop_kernel<4> : (void*)svd_coop_kernel<8>;
     int occ = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NTH, 0)) != cudaSuccess) return e;
     const int grid = std::max(1, std::min(nbe / 2, occ * g_num_sms));
