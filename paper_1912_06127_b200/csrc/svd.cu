@@ -26,6 +26,9 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int NTH = 256;
+#ifndef INNER_SWEEPS
+#define INNER_SWEEPS 2
+#endif
 
 __device__ __forceinline__ void rr_pair(int n, int round, int i, int& a, int& b) {
   // circle method on n (even) players: player n-1 fixed
@@ -149,7 +152,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
     const int i = e / PC, j = e - i * PC;
     if (i < j && j < ncols) {
       const double di = G[i][i].x, dj = G[j][j].x;
-      if (di > 0.0 && dj > 0.0) off = fmax(off, sqrt(cabs2(G[i][j]) / (di * dj)));
+      if (di > 0.0 && dj > 0.0) off = fmax(off, cabs2(G[i][j]) / (di * dj));  // squared
     }
   }
   off = warp_max(off);
@@ -158,6 +161,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < NTH / 32; ++w) t = fmax(t, s_off[w]);
+    t = sqrt(t);
     s_off[0] = t;
     atomic_max_nonneg(off_cur, t);
   }
@@ -169,7 +173,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   // ---- inner Jacobi on G by warp 0 (parallel ordering, Q accumulates)
   if (wid == 0) {
     const int n2 = ncols + (ncols & 1);
-    for (int sweep = 0; sweep < 6; ++sweep) {
+    for (int sweep = 0; sweep < INNER_SWEEPS; ++sweep) {
       for (int r = 0; r < n2 - 1; ++r) {
         if (lane < n2 / 2) {
           int p, q;
@@ -179,13 +183,14 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
           if (q < ncols) {
             const double a = G[p][p].x, c = G[q][q].x;
             const cplx g = G[p][q];
-            const double ag = sqrt(cabs2(g));
-            if (ag > 1e-300 && !(ag <= 0.25 * tol * sqrt(fmax(a, 0.0) * fmax(c, 0.0)))) {
-              const double zeta = (c - a) / (2.0 * ag);
-              const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              cs = 1.0 / sqrt(1.0 + t * t);
-              const double sv = cs * t;
-              sn = cmk(sv * g.x / ag, sv * g.y / ag);
+            const double ag2 = cabs2(g);
+            if (ag2 > 1e-300 && ag2 > 0.0625 * tol * tol * fmax(a, 0.0) * fmax(c, 0.0)) {
+              const double inv_ag = rsqrt(ag2);
+              const double zeta = 0.5 * (c - a) * inv_ag;
+              const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              cs = rsqrt(fma(t, t, 1.0));
+              const double sv = cs * t * inv_ag;
+              sn = cmk(sv * g.x, sv * g.y);
             }
           }
           rp[lane] = p;
@@ -235,10 +240,10 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
         const int i = e / PC, j = e - i * PC;
         if (i < j && j < ncols) {
           const double di = G[i][i].x, dj = G[j][j].x;
-          if (di > 0.0 && dj > 0.0) o = fmax(o, sqrt(cabs2(G[i][j]) / (di * dj)));
+          if (di > 0.0 && dj > 0.0) o = fmax(o, cabs2(G[i][j]) - 0.0625 * tol * tol * di * dj);
         }
       }
-      if (warp_max(o) <= 0.25 * tol) break;
+      if (warp_max(o) <= 0.0) break;
     }
   }
   __syncthreads();
