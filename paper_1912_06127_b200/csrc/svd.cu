@@ -306,6 +306,131 @@ __global__ void __launch_bounds__(NTH) svd_coop_kernel(cplx* Y, long long ldy, i
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory-resident variant (used when a block pair's full columns fit):
+// the CTA stages all mr + nc rows of its 2*BW columns in shared memory and
+// runs plain one-sided Hestenes rotations on them (dot products of the
+// actual columns, no Gram matrix, no inner eigenproblem), one warp per
+// column pair, INNER_SWEEPS inner sweeps, then writes the columns back.
+template <int BW>
+__global__ void __launch_bounds__(32 * BW) svd_coop_smem_kernel(cplx* Y, long long ldy, int mr, int nc, int nb,
+                                                               int nbe, double tol, int max_sweeps, double* offbuf,
+                                                               int* sweeps_out) {
+  constexpr int PC = 2 * BW, NT = 32 * BW;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx* sm = reinterpret_cast<cplx*>(smraw);
+  __shared__ int cols[PC];
+  __shared__ int s_ncols;
+  __shared__ double s_off[BW];
+  __shared__ int s_any;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rows = mr + nc;
+  const int lds = rows;  // column stride in shared memory
+  const double tol2q = 0.0625 * tol * tol;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    double* off_cur = offbuf + (sweep % 3);
+    if (blockIdx.x == 0 && tid == 0) offbuf[(sweep + 1) % 3] = 0.0;
+    for (int round = 0; round < nbe - 1; ++round) {
+      for (int pair = blockIdx.x; pair < nbe / 2; pair += gridDim.x) {
+        if (tid == 0) {
+          int a, b;
+          rr_pair(nbe, round, pair, a, b);
+          int k = 0;
+          for (int blk : {a, b}) {
+            if (blk >= nb) continue;
+            for (int c = blk * BW; c < min(nc, blk * BW + BW); ++c) cols[k++] = c;
+          }
+          s_ncols = k;
+          s_any = 0;
+        }
+        if (tid < BW) s_off[tid] = 0.0;
+        __syncthreads();
+        const int ncols = s_ncols;
+        if (ncols >= 2) {
+          for (int c = 0; c < ncols; ++c) {
+            const cplx* src = Y + (long long)cols[c] * ldy;
+            for (int r = tid; r < rows; r += NT) sm[c * lds + r] = __ldcg(src + r);
+          }
+          __syncthreads();
+          const int n2 = ncols + (ncols & 1);
+          for (int isw = 0; isw < INNER_SWEEPS; ++isw) {
+            for (int r = 0; r < n2 - 1; ++r) {
+              if (wid < n2 / 2) {
+                int p, q;
+                rr_pair(n2, r, wid, p, q);
+                if (q < ncols) {
+                  cplx* xp = sm + p * lds;
+                  cplx* xq = sm + q * lds;
+                  double a0 = 0, a1 = 0, c0 = 0, c1 = 0, gr0 = 0, gr1 = 0, gi0 = 0, gi1 = 0;
+                  int rr = lane;
+                  for (; rr + 32 < mr; rr += 64) {
+                    const cplx u0 = xp[rr], v0 = xq[rr], u1 = xp[rr + 32], v1 = xq[rr + 32];
+                    a0 += cabs2(u0); a1 += cabs2(u1);
+                    c0 += cabs2(v0); c1 += cabs2(v1);
+                    gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0)); gr1 = fma(u1.x, v1.x, fma(u1.y, v1.y, gr1));
+                    gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0)); gi1 = fma(u1.x, v1.y, fma(-u1.y, v1.x, gi1));
+                  }
+                  for (; rr < mr; rr += 32) {
+                    const cplx u0 = xp[rr], v0 = xq[rr];
+                    a0 += cabs2(u0);
+                    c0 += cabs2(v0);
+                    gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0));
+                    gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0));
+                  }
+                  const double a = warp_sum(a0 + a1), c = warp_sum(c0 + c1);
+                  const double gr = warp_sum(gr0 + gr1), gi = warp_sum(gi0 + gi1);
+                  const double ag2 = gr * gr + gi * gi;
+                  double cs = 1.0;
+                  cplx sn = cmk(0, 0);
+                  if (a > 0.0 && c > 0.0) {
+                    if (isw == 0 && lane == 0) s_off[wid] = fmax(s_off[wid], ag2 / (a * c));
+                    if (ag2 > 1e-300 && ag2 > tol2q * a * c) {
+                      const double inv_ag = rsqrt(ag2);
+                      const double zeta = 0.5 * (c - a) * inv_ag;
+                      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                      cs = rsqrt(fma(t, t, 1.0));
+                      const double sv = cs * t * inv_ag;
+                      sn = cmk(sv * gr, sv * gi);
+                    }
+                  }
+                  if (sn.x != 0.0 || sn.y != 0.0) {
+                    if (lane == 0) s_any = 1;
+                    const cplx snc = cconj(sn);
+                    for (int r2 = lane; r2 < rows; r2 += 32) {
+                      const cplx u = xp[r2], v = xq[r2];
+                      xp[r2] = csub(cscale(u, cs), cmul(snc, v));
+                      xq[r2] = cadd(cmul(sn, u), cscale(v, cs));
+                    }
+                  }
+                }
+              }
+              __syncthreads();
+            }
+          }
+          if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < BW; ++w) t = fmax(t, s_off[w]);
+            atomic_max_nonneg(off_cur, sqrt(t));
+          }
+          if (s_any) {
+            for (int c = 0; c < ncols; ++c) {
+              cplx* dst = Y + (long long)cols[c] * ldy;
+              for (int r = tid; r < rows; r += NT) __stcg(dst + r, sm[c * lds + r]);
+            }
+          }
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    const double off = __ldcg(off_cur);
+    if (!(off > tol)) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = min(sweep + 1, max_sweeps);
+}
+
 __global__ void svd_colnorm_kernel(const cplx* __restrict__ Y, long long ldy, int mr, int nc, double* sigma,
                                    int* nonfinite) {
   const int warps = blockDim.x >> 5;
@@ -422,8 +547,26 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
       const char* ev = std::getenv("TDVP_SVD_BW");
       forced = ev ? std::atoi(ev) : 0;
     }
-    int bw = forced > 0 ? forced : (nc <= 1024 ? 4 : 8);
-    if (bw != 4 && bw != 8) bw = 4;
+    // shared-memory-resident block pairs when the columns fit (<= 200 KB), else Gram variant
+    const long long rows = (long long)mr + nc;
+    int bw;
+    bool smem_path;
+    if (forced == 104 || forced == 108) {
+      bw = forced - 100;
+      smem_path = true;
+    } else if (forced > 0) {
+      bw = forced == 8 ? 8 : 4;
+      smem_path = false;
+    } else if (rows * 16 * 16 <= 200 * 1024) {
+      bw = 8;
+      smem_path = true;
+    } else if (rows * 8 * 16 <= 200 * 1024) {
+      bw = 4;
+      smem_path = true;
+    } else {
+      bw = nc <= 1024 ? 4 : 8;
+      smem_path = false;
+    }
     const int nb = (nc + bw - 1) / bw;
     const int nbe = std::max(2, nb + (nb & 1));
     if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
@@ -431,11 +574,28 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     int* sweeps_dev = d.ires + 4;
     void* args[] = {(void*)&d.Y, (void*)&ldy, (void*)&mr, (void*)&nc, (void*)&nb, (void*)&nbe, (void*)&tol,
                     (void*)&max_sweeps, (void*)&d.offmax, (void*)&sweeps_dev};
-    void* fn = bw == 4 ? (void*)svd_coop_kernel<4> : (void*)svd_coop_kernel<8>;
+    void* fn;
+    int nth;
+    size_t dsm = 0;
+    if (smem_path) {
+      fn = bw == 4 ? (void*)svd_coop_smem_kernel<4> : (void*)svd_coop_smem_kernel<8>;
+      nth = 32 * bw;
+      dsm = (size_t)rows * 2 * bw * sizeof(cplx);
+      static size_t configured[2] = {0, 0};
+      size_t& cf = configured[bw == 4 ? 0 : 1];
+      if (dsm > cf) {
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024)) != cudaSuccess)
+          return e;
+        cf = 210 * 1024;
+      }
+    } else {
+      fn = bw == 4 ? (void*)svd_coop_kernel<4> : (void*)svd_coop_kernel<8>;
+      nth = NTH;
+    }
     int occ = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NTH, 0)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nth, dsm)) != cudaSuccess) return e;
     const int grid = std::max(1, std::min(nbe / 2, occ * g_num_sms));
-    if ((e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTH), args, 0, st)) != cudaSuccess) return e;
+    if ((e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nth), args, dsm, st)) != cudaSuccess) return e;
     sweeps = -1;  // read back with the truncation results
   }
   if ((e = cudaMemsetAsync(d.ires, 0, 4 * sizeof(int), st)) != cudaSuccess) return e;
