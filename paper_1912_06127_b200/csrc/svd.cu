@@ -74,6 +74,130 @@ struct CoopCfg {
   static constexpr int S = (E >= NTH) ? 1 : NTH / E;  // row slices per entry
 };
 
+// Inner block-pair solve, one warp, register resident (PC = 8 or 16 columns).
+// G = D C D (D = sqrt diag G); C = L L^H (Cholesky, clamped pivots); R = L^H D
+// satisfies R^H R = G, so one-sided Jacobi on the columns of R (held in
+// registers: lane (c, h) owns rows [h*RC, (h+1)*RC) of column c of R and of
+// Q) yields the rotation Q that orthogonalises the block pair.  Only column
+// operations: partner chunks arrive by shuffle, dots reduce across the H
+// chunk-lanes of a column.  Writes Q (PC x PC) to Qm.
+template <int PC>
+__device__ __forceinline__ void inner_reg(cplx (*G)[PC + 1], cplx (*Qm)[PC + 1], int ncols, double tol) {
+  constexpr int H = 32 / PC, RC = PC / H;
+  const int lane = threadIdx.x & 31;
+  const int c = lane % PC, h = lane / PC;
+  // --- scaled Cholesky of the leading ncols x ncols block, L stored in Qm (lower)
+  __shared__ double s_d[PC];
+  if (lane < PC) {
+    const double gd = (lane < ncols) ? G[lane][lane].x : 0.0;
+    s_d[lane] = gd > 0.0 ? sqrt(gd) : 0.0;
+  }
+  __syncwarp();
+  for (int k = 0; k < PC; ++k) {
+    // lane i >= k computes L[i][k]
+    if (lane < PC) {
+      const int i = lane;
+      cplx l = cmk(0, 0);
+      if (k < ncols && i < ncols && i >= k && s_d[k] > 0.0 && s_d[i] > 0.0) {
+        const cplx cik = cscale(G[i][k], 1.0 / (s_d[i] * s_d[k]));
+        cplx acc = cik;
+        for (int m = 0; m < k; ++m) acc = csub(acc, cmul(Qm[i][m], cconj(Qm[k][m])));
+        if (i == k) {
+          l = cmk(sqrt(fmax(acc.x, 1e-28)), 0.0);
+        }
+        Qm[i][k] = (i == k) ? l : acc;  // off-diagonal: numerator, divided below
+      } else if (i >= k) {
+        Qm[i][k] = cmk(0, 0);
+      }
+    }
+    __syncwarp();
+    if (lane < PC && lane > k) {
+      const double lkk = Qm[k][k].x;
+      if (lkk > 0.0) Qm[lane][k] = cscale(Qm[lane][k], 1.0 / lkk);
+    }
+    __syncwarp();
+  }
+  // --- registers: R[rho][c] = conj(L[c][rho]) d_c (rho <= c), Q = I
+  cplx r[RC], q[RC];
+#pragma unroll
+  for (int k = 0; k < RC; ++k) {
+    const int rho = h * RC + k;
+    r[k] = (rho <= c && c < ncols) ? cscale(cconj(Qm[c][rho]), s_d[c]) : cmk(0, 0);
+    q[k] = cmk(rho == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncwarp();
+  const double tol2q = 0.0625 * tol * tol;
+  for (int sweep = 0; sweep < 3; ++sweep) {
+    double offs = 0.0;
+#pragma unroll 1
+    for (int rd = 0; rd < PC - 1; ++rd) {
+      int pa, pb;
+      // partner of column c in round rd (circle method, player PC-1 fixed)
+      {
+        const int m = PC - 1;
+        int partner;
+        if (c == PC - 1) partner = rd % m;
+        else if (c == rd % m) partner = PC - 1;
+        else partner = (2 * rd - c + 2 * m) % m;
+        pa = min(c, partner);
+        pb = max(c, partner);
+      }
+      const bool is_p = (c == pa);
+      const int plane = (is_p ? pb : pa) + PC * h;
+      cplx pr[RC], pq[RC];
+#pragma unroll
+      for (int k = 0; k < RC; ++k) {
+        pr[k].x = __shfl_sync(0xffffffffu, r[k].x, plane);
+        pr[k].y = __shfl_sync(0xffffffffu, r[k].y, plane);
+        pq[k].x = __shfl_sync(0xffffffffu, q[k].x, plane);
+        pq[k].y = __shfl_sync(0xffffffffu, q[k].y, plane);
+      }
+      double a = 0.0, cc = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int k = 0; k < RC; ++k) {
+        const cplx xp = is_p ? r[k] : pr[k];
+        const cplx xq = is_p ? pr[k] : r[k];
+        a += cabs2(xp);
+        cc += cabs2(xq);
+        gr = fma(xp.x, xq.x, fma(xp.y, xq.y, gr));
+        gi = fma(xp.x, xq.y, fma(-xp.y, xq.x, gi));
+      }
+#pragma unroll
+      for (int o = PC; o < 32; o <<= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        cc += __shfl_xor_sync(0xffffffffu, cc, o);
+        gr += __shfl_xor_sync(0xffffffffu, gr, o);
+        gi += __shfl_xor_sync(0xffffffffu, gi, o);
+      }
+      const double ag2 = gr * gr + gi * gi;
+      if (a > 0.0 && cc > 0.0 && pb < ncols) {
+        offs = fmax(offs, ag2 / (a * cc));
+        if (ag2 > 1e-300 && ag2 > tol2q * a * cc) {
+          const double inv_ag = rsqrt(ag2);
+          const double zeta = 0.5 * (cc - a) * inv_ag;
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sv = cs * t * inv_ag;
+          const cplx sn = cmk(sv * gr, sv * gi);
+          // p: x_p' = cs x_p - conj(sn) x_q ;  q: x_q' = sn x_p + cs x_q
+          const cplx f = is_p ? cmk(-sn.x, sn.y) : sn;
+#pragma unroll
+          for (int k = 0; k < RC; ++k) {
+            r[k] = cadd(cscale(r[k], cs), cmul(f, pr[k]));
+            q[k] = cadd(cscale(q[k], cs), cmul(f, pq[k]));
+          }
+        }
+      }
+    }
+    offs = warp_max(offs);
+    if (offs <= tol2q) break;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < RC; ++k) Qm[h * RC + k][c] = q[k];
+  __syncwarp();
+}
+
 template <int BW>
 __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe, int round, int pair, double tol,
                           double* off_cur, cplx (*G)[2 * BW + 1], cplx (*Qm)[2 * BW + 1], cplx (*tile)[2 * BW + 1],
@@ -170,82 +294,8 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   __syncthreads();
   if (off0 <= tol) return;
 
-  // ---- inner Jacobi on G by warp 0 (parallel ordering, Q accumulates)
-  if (wid == 0) {
-    const int n2 = ncols + (ncols & 1);
-    for (int sweep = 0; sweep < INNER_SWEEPS; ++sweep) {
-      for (int r = 0; r < n2 - 1; ++r) {
-        if (lane < n2 / 2) {
-          int p, q;
-          rr_pair(n2, r, lane, p, q);
-          double cs = 1.0;
-          cplx sn = cmk(0, 0);
-          if (q < ncols) {
-            const double a = G[p][p].x, c = G[q][q].x;
-            const cplx g = G[p][q];
-            const double ag2 = cabs2(g);
-            if (ag2 > 1e-300 && ag2 > 0.0625 * tol * tol * fmax(a, 0.0) * fmax(c, 0.0)) {
-              const double inv_ag = rsqrt(ag2);
-              const double zeta = 0.5 * (c - a) * inv_ag;
-              const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-              cs = rsqrt(fma(t, t, 1.0));
-              const double sv = cs * t * inv_ag;
-              sn = cmk(sv * g.x, sv * g.y);
-            }
-          }
-          rp[lane] = p;
-          rq[lane] = q;
-          rc[lane] = cs;
-          rs[lane] = sn;
-        }
-        __syncwarp();
-        for (int e = lane; e < (n2 / 2) * PC; e += 32) {
-          const int pi = e / PC, row = e - pi * PC;
-          const int p = rp[pi], q = rq[pi];
-          if (q >= ncols || row >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
-          const double cs = rc[pi];
-          const cplx sn = rs[pi];
-          const cplx gp = G[row][p], gq = G[row][q];
-          G[row][p] = csub(cscale(gp, cs), cmul(cconj(sn), gq));
-          G[row][q] = cadd(cmul(sn, gp), cscale(gq, cs));
-          const cplx qp = Qm[row][p], qq = Qm[row][q];
-          Qm[row][p] = csub(cscale(qp, cs), cmul(cconj(sn), qq));
-          Qm[row][q] = cadd(cmul(sn, qp), cscale(qq, cs));
-        }
-        __syncwarp();
-        for (int e = lane; e < (n2 / 2) * PC; e += 32) {
-          const int pi = e / PC, col = e - pi * PC;
-          const int p = rp[pi], q = rq[pi];
-          if (q >= ncols || col >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
-          const double cs = rc[pi];
-          const cplx sn = rs[pi];
-          const cplx gp = G[p][col], gq = G[q][col];
-          G[p][col] = csub(cscale(gp, cs), cmul(sn, gq));
-          G[q][col] = cadd(cmul(cconj(sn), gp), cscale(gq, cs));
-        }
-        __syncwarp();
-        if (lane < n2 / 2) {
-          const int p = rp[lane], q = rq[lane];
-          if (q < ncols && !(rs[lane].x == 0.0 && rs[lane].y == 0.0)) {
-            G[p][q] = cmk(0, 0);
-            G[q][p] = cmk(0, 0);
-            G[p][p].y = 0.0;
-            G[q][q].y = 0.0;
-          }
-        }
-        __syncwarp();
-      }
-      double o = 0.0;
-      for (int e = lane; e < PC * PC; e += 32) {
-        const int i = e / PC, j = e - i * PC;
-        if (i < j && j < ncols) {
-          const double di = G[i][i].x, dj = G[j][j].x;
-          if (di > 0.0 && dj > 0.0) o = fmax(o, cabs2(G[i][j]) - 0.0625 * tol * tol * di * dj);
-        }
-      }
-      if (warp_max(o) <= 0.0) break;
-    }
-  }
+  // ---- inner solve by warp 0: Q with (X Q)^H (X Q) diagonal, from G = X^H X
+  if (wid == 0) inner_reg<PC>(G, Qm, ncols, tol);
   __syncthreads();
 
   // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows
