@@ -21,13 +21,20 @@
 #include "kernels.h"
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <cstdio>
 namespace cg = cooperative_groups;
 
 namespace {
 
+__device__ unsigned long long g_svd_prof[8];  // cycles per phase (block 0), debug
+#define PROF_MARK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const unsigned long long _t = clock64(); g_svd_prof[i] += _t - prof_t; prof_t = _t; } } while (0)
+
 constexpr int NTH = 256;
 #ifndef INNER_SWEEPS
-#define INNER_SWEEPS 2
+#define INNER_SWEEPS 1
+#endif
+#ifndef INNER_MODE
+#define INNER_MODE 0
 #endif
 
 __device__ __forceinline__ void rr_pair(int n, int round, int i, int& a, int& b) {
@@ -73,6 +80,24 @@ struct CoopCfg {
   static constexpr int EPT = (E + NTH - 1) / NTH;  // entries per thread
   static constexpr int S = (E >= NTH) ? 1 : NTH / E;  // row slices per entry
 };
+
+// Complex Jacobi rotation zeroing g = x_p^H x_q for column norms a = |x_p|^2,
+// c = |x_q|^2 (3 long-latency ops): w = c - a, D = sqrt(w^2 + 4|g|^2),
+// t e^{i phi} = 2 sgn(w) g / (|w| + D), cs = 1/sqrt(1 + t^2), sn = cs t e^{i phi}.
+// x_p' = cs x_p - conj(sn) x_q ;  x_q' = sn x_p + cs x_q.  Returns false if
+// |g|^2 <= tol2q a c (already orthogonal to the requested tolerance).
+__device__ __forceinline__ bool rot_params(double a, double c, double gr, double gi, double tol2q, double& cs,
+                                           cplx& sn) {
+  const double ag2 = gr * gr + gi * gi;
+  if (!(ag2 > 1e-300) || !(ag2 > tol2q * a * c)) return false;
+  const double w = c - a;
+  const double den = fabs(w) + sqrt(fma(w, w, 4.0 * ag2));
+  const double f = copysign(2.0, w) / den;  // t e^{i phi} = f g
+  const double t2 = f * f * ag2;
+  cs = rsqrt(1.0 + t2);
+  sn = cmk(cs * f * gr, cs * f * gi);
+  return true;
+}
 
 // Inner block-pair solve, one warp, register resident (PC = 8 or 16 columns).
 // G = D C D (D = sqrt diag G); C = L L^H (Cholesky, clamped pivots); R = L^H D
@@ -127,7 +152,7 @@ __device__ __forceinline__ void inner_reg(cplx (*G)[PC + 1], cplx (*Qm)[PC + 1],
   }
   __syncwarp();
   const double tol2q = 0.0625 * tol * tol;
-  for (int sweep = 0; sweep < 3; ++sweep) {
+  for (int sweep = 0; sweep < INNER_SWEEPS; ++sweep) {
     double offs = 0.0;
 #pragma unroll 1
     for (int rd = 0; rd < PC - 1; ++rd) {
@@ -172,13 +197,9 @@ __device__ __forceinline__ void inner_reg(cplx (*G)[PC + 1], cplx (*Qm)[PC + 1],
       const double ag2 = gr * gr + gi * gi;
       if (a > 0.0 && cc > 0.0 && pb < ncols) {
         offs = fmax(offs, ag2 / (a * cc));
-        if (ag2 > 1e-300 && ag2 > tol2q * a * cc) {
-          const double inv_ag = rsqrt(ag2);
-          const double zeta = 0.5 * (cc - a) * inv_ag;
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double cs = rsqrt(fma(t, t, 1.0));
-          const double sv = cs * t * inv_ag;
-          const cplx sn = cmk(sv * gr, sv * gi);
+        double cs;
+        cplx sn;
+        if (rot_params(a, cc, gr, gi, tol2q, cs, sn)) {
           // p: x_p' = cs x_p - conj(sn) x_q ;  q: x_q' = sn x_p + cs x_q
           const cplx f = is_p ? cmk(-sn.x, sn.y) : sn;
 #pragma unroll
@@ -198,6 +219,75 @@ __device__ __forceinline__ void inner_reg(cplx (*G)[PC + 1], cplx (*Qm)[PC + 1],
   __syncwarp();
 }
 
+// Alternative inner solve (INNER_MODE 0): two-sided Jacobi on the Gram
+// matrix in shared memory by one warp (one task per lane per phase).
+template <int PC>
+__device__ __forceinline__ void inner_smem(cplx (*G)[PC + 1], cplx (*Qm)[PC + 1], int ncols, double tol, int* rp,
+                                           int* rq, double* rc, cplx* rs) {
+  const int lane = threadIdx.x & 31;
+  const double tol2q = 0.0625 * tol * tol;
+  for (int e = lane; e < PC * PC; e += 32) Qm[e / PC][e % PC] = cmk((e / PC) == (e % PC) ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  const int n2 = ncols + (ncols & 1);
+  for (int sweep = 0; sweep < INNER_SWEEPS; ++sweep) {
+    for (int r = 0; r < n2 - 1; ++r) {
+      if (lane < n2 / 2) {
+        int p, q;
+        rr_pair(n2, r, lane, p, q);
+        double cs = 1.0;
+        cplx sn = cmk(0, 0);
+        if (q < ncols) {
+          const double a = G[p][p].x, c = G[q][q].x;
+          if (a > 0.0 && c > 0.0 && !rot_params(a, c, G[p][q].x, G[p][q].y, tol2q, cs, sn)) {
+            cs = 1.0;
+            sn = cmk(0, 0);
+          }
+        }
+        rp[lane] = p;
+        rq[lane] = q;
+        rc[lane] = cs;
+        rs[lane] = sn;
+      }
+      __syncwarp();
+      for (int e = lane; e < (n2 / 2) * PC; e += 32) {
+        const int pi = e / PC, row = e - pi * PC;
+        const int p = rp[pi], q = rq[pi];
+        if (q >= ncols || row >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
+        const double cs = rc[pi];
+        const cplx sn = rs[pi];
+        const cplx gp = G[row][p], gq = G[row][q];
+        G[row][p] = csub(cscale(gp, cs), cmul(cconj(sn), gq));
+        G[row][q] = cadd(cmul(sn, gp), cscale(gq, cs));
+        const cplx qp = Qm[row][p], qq = Qm[row][q];
+        Qm[row][p] = csub(cscale(qp, cs), cmul(cconj(sn), qq));
+        Qm[row][q] = cadd(cmul(sn, qp), cscale(qq, cs));
+      }
+      __syncwarp();
+      for (int e = lane; e < (n2 / 2) * PC; e += 32) {
+        const int pi = e / PC, col = e - pi * PC;
+        const int p = rp[pi], q = rq[pi];
+        if (q >= ncols || col >= ncols || (rs[pi].x == 0.0 && rs[pi].y == 0.0)) continue;
+        const double cs = rc[pi];
+        const cplx sn = rs[pi];
+        const cplx gp = G[p][col], gq = G[q][col];
+        G[p][col] = csub(cscale(gp, cs), cmul(sn, gq));
+        G[q][col] = cadd(cmul(cconj(sn), gp), cscale(gq, cs));
+      }
+      __syncwarp();
+      if (lane < n2 / 2) {
+        const int p = rp[lane], q = rq[lane];
+        if (q < ncols && !(rs[lane].x == 0.0 && rs[lane].y == 0.0)) {
+          G[p][q] = cmk(0, 0);
+          G[q][p] = cmk(0, 0);
+          G[p][p].y = 0.0;
+          G[q][q].y = 0.0;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int BW>
 __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe, int round, int pair, double tol,
                           double* off_cur, cplx (*G)[2 * BW + 1], cplx (*Qm)[2 * BW + 1], cplx (*tile)[2 * BW + 1],
@@ -206,6 +296,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   using Cf = CoopCfg<BW>;
   constexpr int PC = Cf::PC, TRc = Cf::TRc;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned long long prof_t = clock64();
   if (tid == 0) {
     int a, b;
     rr_pair(nbe, round, pair, a, b);
@@ -220,38 +311,61 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   const int ncols = *s_ncols;
   if (ncols < 2) return;
 
-  // ---- Gram matrix over the X rows
-  cplx acc[Cf::EPT];
+  // ---- Gram matrix over the X rows (next tile prefetched into registers)
+  constexpr int LPT = (TRc * PC) / NTH;  // loads per thread per tile
+  cplx acc[Cf::EPT], acc2[Cf::EPT];
 #pragma unroll
-  for (int u = 0; u < Cf::EPT; ++u) acc[u] = cmk(0, 0);
+  for (int u = 0; u < Cf::EPT; ++u) acc[u] = acc2[u] = cmk(0, 0);
   const int slice = (Cf::S > 1) ? (tid % Cf::S) : 0;
   const int ebase = (Cf::S > 1) ? (tid / Cf::S) : tid;
-  for (int r0 = 0; r0 < mr; r0 += TRc) {
+  cplx pre[LPT];
+  auto fetch = [&](int r0, int limit) {
 #pragma unroll
-    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
+    for (int u = 0; u < LPT; ++u) {
       const int e = tid + u * NTH;
       const int c = e / TRc, rr = e - c * TRc;
-      cplx v = cmk(0, 0);
-      if (c < ncols && r0 + rr < mr) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
-      tile[rr][c] = v;
+      pre[u] = (c < ncols && r0 + rr < limit) ? __ldcg(Y + (long long)cols[c] * ldy + r0 + rr) : cmk(0, 0);
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) {
+      const int e = tid + u * NTH;
+      tile[e - (e / TRc) * TRc][e / TRc] = pre[u];
+    }
+  };
+  fetch(0, mr);
+  for (int r0 = 0; r0 < mr; r0 += TRc) {
+    stash();
     __syncthreads();
+    if (r0 + TRc < mr) fetch(r0 + TRc, mr);
 #pragma unroll
     for (int u = 0; u < Cf::EPT; ++u) {
       const int e = ebase + u * NTH;
       if (e < Cf::E) {
         const int i = e / PC, j = e - i * PC;
-        for (int rr = slice; rr < TRc; rr += Cf::S) {
+#pragma unroll 4
+        for (int rr = slice; rr < TRc; rr += 2 * Cf::S) {
           const cplx a = tile[rr][i], b = tile[rr][j];
           acc[u].x = fma(a.x, b.x, acc[u].x);
           acc[u].x = fma(a.y, b.y, acc[u].x);
           acc[u].y = fma(a.x, b.y, acc[u].y);
           acc[u].y = fma(-a.y, b.x, acc[u].y);
+          const int r2 = rr + Cf::S;
+          if (r2 < TRc) {
+            const cplx a2 = tile[r2][i], b2 = tile[r2][j];
+            acc2[u].x = fma(a2.x, b2.x, acc2[u].x);
+            acc2[u].x = fma(a2.y, b2.y, acc2[u].x);
+            acc2[u].y = fma(a2.x, b2.y, acc2[u].y);
+            acc2[u].y = fma(-a2.y, b2.x, acc2[u].y);
+          }
         }
       }
     }
     __syncthreads();
   }
+#pragma unroll
+  for (int u = 0; u < Cf::EPT; ++u) acc[u] = cadd(acc[u], acc2[u]);
   if (Cf::S > 1) {
     red[tid] = acc[0];
     __syncthreads();
@@ -270,6 +384,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   for (int e = tid; e < PC * PC; e += NTH) Qm[e / PC][e % PC] = cmk((e / PC) == (e % PC) ? 1.0 : 0.0, 0.0);
   __syncthreads();
 
+  PROF_MARK(0);
   // ---- relative off-diagonal measure (whole CTA)
   double off = 0.0;
   for (int e = tid; e < PC * PC; e += NTH) {
@@ -294,34 +409,41 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
   __syncthreads();
   if (off0 <= tol) return;
 
+  PROF_MARK(1);
   // ---- inner solve by warp 0: Q with (X Q)^H (X Q) diagonal, from G = X^H X
+#if INNER_MODE == 1
   if (wid == 0) inner_reg<PC>(G, Qm, ncols, tol);
+#else
+  if (wid == 0) inner_smem<PC>(G, Qm, ncols, tol, rp, rq, rc, rs);
+#endif
   __syncthreads();
+  PROF_MARK(2);
 
-  // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows
+  // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows (next tile prefetched)
   const int rows = mr + nc;
+  fetch(0, rows);
   for (int r0 = 0; r0 < rows; r0 += TRc) {
-#pragma unroll
-    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
-      const int e = tid + u * NTH;
-      const int c = e / TRc, rr = e - c * TRc;
-      cplx v = cmk(0, 0);
-      if (c < ncols && r0 + rr < rows) v = __ldcg(Y + (long long)cols[c] * ldy + r0 + rr);
-      tile[rr][c] = v;
-    }
+    stash();
     __syncthreads();
+    if (r0 + TRc < rows) fetch(r0 + TRc, rows);
 #pragma unroll
-    for (int u = 0; u < (TRc * PC) / NTH; ++u) {
+    for (int u = 0; u < LPT; ++u) {
       const int e = tid + u * NTH;
       const int c = e / TRc, rr = e - c * TRc;
       if (c < ncols && r0 + rr < rows) {
-        cplx a = cmk(0, 0);
-        for (int k = 0; k < ncols; ++k) cfma(a, tile[rr][k], Qm[k][c]);
-        __stcg(Y + (long long)cols[c] * ldy + r0 + rr, a);
+        cplx a = cmk(0, 0), b = cmk(0, 0);
+        int k = 0;
+        for (; k + 1 < ncols; k += 2) {
+          cfma(a, tile[rr][k], Qm[k][c]);
+          cfma(b, tile[rr][k + 1], Qm[k + 1][c]);
+        }
+        if (k < ncols) cfma(a, tile[rr][k], Qm[k][c]);
+        __stcg(Y + (long long)cols[c] * ldy + r0 + rr, cadd(a, b));
       }
     }
     __syncthreads();
   }
+  PROF_MARK(3);
 }
 
 template <int BW>
@@ -348,7 +470,11 @@ __global__ void __launch_bounds__(NTH) svd_coop_kernel(cplx* Y, long long ldy, i
       for (int pair = blockIdx.x; pair < nbe / 2; pair += gridDim.x)
         coop_pair<BW>(Y, ldy, mr, nc, nb, nbe, round, pair, tol, off_cur, G, Qm, tile, red, cols, &s_ncols, rp, rq,
                       rc, rs, s_off);
-      grid.sync();
+      {
+        unsigned long long prof_t = clock64();
+        grid.sync();
+        PROF_MARK(4);
+      }
     }
     const double off = __ldcg(off_cur);
     if (!(off > tol)) break;
@@ -436,14 +562,7 @@ __global__ void __launch_bounds__(32 * BW) svd_coop_smem_kernel(cplx* Y, long lo
                   cplx sn = cmk(0, 0);
                   if (a > 0.0 && c > 0.0) {
                     if (isw == 0 && lane == 0) s_off[wid] = fmax(s_off[wid], ag2 / (a * c));
-                    if (ag2 > 1e-300 && ag2 > tol2q * a * c) {
-                      const double inv_ag = rsqrt(ag2);
-                      const double zeta = 0.5 * (c - a) * inv_ag;
-                      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-                      cs = rsqrt(fma(t, t, 1.0));
-                      const double sv = cs * t * inv_ag;
-                      sn = cmk(sv * gr, sv * gi);
-                    }
+                    rot_params(a, c, gr, gi, tol2q, cs, sn);
                   }
                   if (sn.x != 0.0 || sn.y != 0.0) {
                     if (lane == 0) s_any = 1;
@@ -645,7 +764,20 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     int occ = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nth, dsm)) != cudaSuccess) return e;
     const int grid = std::max(1, std::min(nbe / 2, occ * g_num_sms));
+    static int prof = -1;
+    if (prof < 0) prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;
+    if (prof) {
+      unsigned long long z[8] = {0};
+      cudaMemcpyToSymbolAsync(g_svd_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    }
     if ((e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nth), args, dsm, st)) != cudaSuccess) return e;
+    if (prof) {
+      unsigned long long z[8];
+      cudaMemcpyFromSymbolAsync(z, g_svd_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "svd prof n=%d grid=%d bw=%d smem=%d cycles: setup+gram %llu off %llu inner %llu apply %llu gsync %llu\n",
+                   nc, grid, bw, (int)smem_path, z[0], z[1], z[2], z[3], z[4]);
+    }
     sweeps = -1;  // read back with the truncation results
   }
   if ((e = cudaMemsetAsync(d.ires, 0, 4 * sizeof(int), st)) != cudaSuccess) return e;

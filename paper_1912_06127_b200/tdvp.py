@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtdvp.so")
+LIB_PATH = os.environ.get("TDVP_LIB") or os.path.join(_HERE, "libtdvp.so")
 _lib = None
 
 TDVP_ERRORS = {-1: "bad argument", -2: "non-finite input", -3: "invalid partition", -4: "CUDA/NCCL failure",
