@@ -726,13 +726,15 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     } else if (forced > 0) {
       bw = forced == 8 ? 8 : 4;
       smem_path = false;
+    } else if (rows * 8 * 16 <= 200 * 1024) {
+      // measured on B200 (microbench.py --svd, profiles/r1_microbench.md): the
+      // shared-memory block-pair variant with b = 4 is fastest where it fits
+      bw = 4;
+      smem_path = true;
     } else {
-      // measured on B200 (microbench.py --svd): the Gram variant with b = 4 is
-      // fastest up to n = 1024 (14.9 ms vs 16.3 ms smem variant at n = 256)
       bw = nc <= 1024 ? 4 : 8;
       smem_path = false;
     }
-    (void)rows;
     const int nb = (nc + bw - 1) / bw;
     const int nbe = std::max(2, nb + (nb & 1));
     if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
