@@ -489,12 +489,13 @@ __global__ void __launch_bounds__(NTH) svd_coop_kernel(cplx* Y, long long ldy, i
 // actual columns, no Gram matrix, no inner eigenproblem), one warp per
 // column pair, INNER_SWEEPS inner sweeps, then writes the columns back.
 template <int BW>
-__global__ void __launch_bounds__(32 * BW) svd_coop_smem_kernel(cplx* Y, long long ldy, int mr, int nc, int nb,
+__global__ void __launch_bounds__(256) svd_coop_smem_kernel(cplx* Y, long long ldy, int mr, int nc, int nb,
                                                                int nbe, double tol, int max_sweeps, double* offbuf,
                                                                int* sweeps_out) {
-  constexpr int PC = 2 * BW, NT = 32 * BW;
+  constexpr int PC = 2 * BW, NT = 256, WPP = 8 / BW;  // warps per column pair
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx* sm = reinterpret_cast<cplx*>(smraw);
+  __shared__ double s_part[8][4];
   __shared__ int cols[PC];
   __shared__ int s_ncols;
   __shared__ double s_off[BW];
@@ -525,53 +526,90 @@ __global__ void __launch_bounds__(32 * BW) svd_coop_smem_kernel(cplx* Y, long lo
         __syncthreads();
         const int ncols = s_ncols;
         if (ncols >= 2) {
-          for (int c = 0; c < ncols; ++c) {
-            const cplx* src = Y + (long long)cols[c] * ldy;
-            for (int r = tid; r < rows; r += NT) sm[c * lds + r] = __ldcg(src + r);
+          {
+            // 8 independent loads in flight per thread
+            const int total = ncols * rows;
+            for (int base = tid; base < total; base += 8 * NT) {
+              cplx v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int e = base + u * NT;
+                if (e < total) {
+                  const int c = e / rows, r = e - c * rows;
+                  v[u] = __ldcg(Y + (long long)cols[c] * ldy + r);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int e = base + u * NT;
+                if (e < total) sm[e] = v[u];  // sm[c * lds + r] with lds == rows
+              }
+            }
           }
           __syncthreads();
           const int n2 = ncols + (ncols & 1);
           for (int isw = 0; isw < INNER_SWEEPS; ++isw) {
             for (int r = 0; r < n2 - 1; ++r) {
-              if (wid < n2 / 2) {
-                int p, q;
-                rr_pair(n2, r, wid, p, q);
-                if (q < ncols) {
-                  cplx* xp = sm + p * lds;
-                  cplx* xq = sm + q * lds;
-                  double a0 = 0, a1 = 0, c0 = 0, c1 = 0, gr0 = 0, gr1 = 0, gi0 = 0, gi1 = 0;
-                  int rr = lane;
-                  for (; rr + 32 < mr; rr += 64) {
-                    const cplx u0 = xp[rr], v0 = xq[rr], u1 = xp[rr + 32], v1 = xq[rr + 32];
-                    a0 += cabs2(u0); a1 += cabs2(u1);
-                    c0 += cabs2(v0); c1 += cabs2(v1);
-                    gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0)); gr1 = fma(u1.x, v1.x, fma(u1.y, v1.y, gr1));
-                    gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0)); gi1 = fma(u1.x, v1.y, fma(-u1.y, v1.x, gi1));
-                  }
-                  for (; rr < mr; rr += 32) {
-                    const cplx u0 = xp[rr], v0 = xq[rr];
-                    a0 += cabs2(u0);
-                    c0 += cabs2(v0);
-                    gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0));
-                    gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0));
-                  }
-                  const double a = warp_sum(a0 + a1), c = warp_sum(c0 + c1);
-                  const double gr = warp_sum(gr0 + gr1), gi = warp_sum(gi0 + gi1);
-                  const double ag2 = gr * gr + gi * gi;
-                  double cs = 1.0;
-                  cplx sn = cmk(0, 0);
-                  if (a > 0.0 && c > 0.0) {
-                    if (isw == 0 && lane == 0) s_off[wid] = fmax(s_off[wid], ag2 / (a * c));
-                    rot_params(a, c, gr, gi, tol2q, cs, sn);
-                  }
-                  if (sn.x != 0.0 || sn.y != 0.0) {
-                    if (lane == 0) s_any = 1;
-                    const cplx snc = cconj(sn);
-                    for (int r2 = lane; r2 < rows; r2 += 32) {
-                      const cplx u = xp[r2], v = xq[r2];
-                      xp[r2] = csub(cscale(u, cs), cmul(snc, v));
-                      xq[r2] = cadd(cmul(sn, u), cscale(v, cs));
-                    }
+              const int pi = wid / WPP, part = wid - pi * WPP;
+              int p = 0, q = 0;
+              bool active = pi < n2 / 2;
+              if (active) {
+                rr_pair(n2, r, pi, p, q);
+                active = q < ncols;
+              }
+              cplx* xp = sm + p * lds;
+              cplx* xq = sm + q * lds;
+              if (active) {
+                double a0 = 0, a1 = 0, c0 = 0, c1 = 0, gr0 = 0, gr1 = 0, gi0 = 0, gi1 = 0;
+                constexpr int STR = 32 * WPP;
+                int rr = lane + 32 * part;
+                for (; rr + STR < mr; rr += 2 * STR) {
+                  const cplx u0 = xp[rr], v0 = xq[rr], u1 = xp[rr + STR], v1 = xq[rr + STR];
+                  a0 += cabs2(u0); a1 += cabs2(u1);
+                  c0 += cabs2(v0); c1 += cabs2(v1);
+                  gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0)); gr1 = fma(u1.x, v1.x, fma(u1.y, v1.y, gr1));
+                  gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0)); gi1 = fma(u1.x, v1.y, fma(-u1.y, v1.x, gi1));
+                }
+                for (; rr < mr; rr += STR) {
+                  const cplx u0 = xp[rr], v0 = xq[rr];
+                  a0 += cabs2(u0);
+                  c0 += cabs2(v0);
+                  gr0 = fma(u0.x, v0.x, fma(u0.y, v0.y, gr0));
+                  gi0 = fma(u0.x, v0.y, fma(-u0.y, v0.x, gi0));
+                }
+                const double pa = warp_sum(a0 + a1), pc = warp_sum(c0 + c1);
+                const double pgr = warp_sum(gr0 + gr1), pgi = warp_sum(gi0 + gi1);
+                if (lane == 0) {
+                  s_part[wid][0] = pa;
+                  s_part[wid][1] = pc;
+                  s_part[wid][2] = pgr;
+                  s_part[wid][3] = pgi;
+                }
+              }
+              if (WPP > 1) __syncthreads(); else __syncwarp();
+              if (active) {
+                double a = 0, c = 0, gr = 0, gi = 0;
+#pragma unroll
+                for (int u = 0; u < WPP; ++u) {
+                  a += s_part[pi * WPP + u][0];
+                  c += s_part[pi * WPP + u][1];
+                  gr += s_part[pi * WPP + u][2];
+                  gi += s_part[pi * WPP + u][3];
+                }
+                const double ag2 = gr * gr + gi * gi;
+                double cs = 1.0;
+                cplx sn = cmk(0, 0);
+                if (a > 0.0 && c > 0.0) {
+                  if (isw == 0 && part == 0 && lane == 0) s_off[pi] = fmax(s_off[pi], ag2 / (a * c));
+                  rot_params(a, c, gr, gi, tol2q, cs, sn);
+                }
+                if (sn.x != 0.0 || sn.y != 0.0) {
+                  if (lane == 0) s_any = 1;
+                  const cplx snc = cconj(sn);
+                  for (int r2 = lane + 32 * part; r2 < rows; r2 += 32 * WPP) {
+                    const cplx u = xp[r2], v = xq[r2];
+                    xp[r2] = csub(cscale(u, cs), cmul(snc, v));
+                    xq[r2] = cadd(cmul(sn, u), cscale(v, cs));
                   }
                 }
               }
@@ -584,9 +622,11 @@ __global__ void __launch_bounds__(32 * BW) svd_coop_smem_kernel(cplx* Y, long lo
             atomic_max_nonneg(off_cur, sqrt(t));
           }
           if (s_any) {
-            for (int c = 0; c < ncols; ++c) {
-              cplx* dst = Y + (long long)cols[c] * ldy;
-              for (int r = tid; r < rows; r += NT) __stcg(dst + r, sm[c * lds + r]);
+            const int total = ncols * rows;
+#pragma unroll 4
+            for (int e = tid; e < total; e += NT) {
+              const int c = e / rows, r = e - c * rows;
+              __stcg(Y + (long long)cols[c] * ldy + r, sm[e]);
             }
           }
         }
@@ -747,7 +787,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     size_t dsm = 0;
     if (smem_path) {
       fn = bw == 4 ? (void*)svd_coop_smem_kernel<4> : (void*)svd_coop_smem_kernel<8>;
-      nth = 32 * bw;
+      nth = 256;
       dsm = (size_t)rows * 2 * bw * sizeof(cplx);
       static size_t configured[2] = {0, 0};
       size_t& cf = configured[bw == 4 ? 0 : 1];

@@ -4,7 +4,8 @@
 // warp-level mma.sync.m8n8k4.f64 (SASS DMMA).  One complex product is four
 // real DMMAs on separate re/im accumulators.  Operands are staged through a
 // 4-stage cp.async (LDGSTS) shared-memory pipeline; tiles are 64x64 complex
-// per CTA, 32x32 per warp.  op(A), op(B) in {N, T, C, R(conj only)};
+// per CTA (32x32 per warp), or 32x32 per CTA when 64x64 tiles would give
+// fewer than two waves on the 148 SMs; deterministic split-K on top.  op(A), op(B) in {N, T, C, R(conj only)};
 // everything is row-major.  Used for every dense contraction on the hot path
 // (H_eff stages 1 and 4, H1, environment updates, Theta merge, measurement).
 #include "common.cuh"
@@ -12,11 +13,10 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 8, STAGES = 4, NT = 128;
+constexpr int BK = 8, STAGES = 4, NT = 128;
 constexpr int PA = BK + 4;   // [BM][PA]  k contiguous   (conflict-free fragment reads)
-constexpr int PAT = BM + 2;  // [BK][PAT] m contiguous
-constexpr int PB = BN + 2;   // [BK][PB]  n contiguous
 constexpr int PBT = BK + 4;  // [BN][PBT] k contiguous
+// [BK][BM + 2] (m contiguous) and [BK][BN + 2] (n contiguous) for the other layouts
 
 struct GemmArgs {
   int M, N, K;
@@ -48,10 +48,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int OPA, int OPB>
+template <int OPA, int OPB, int BM, int BN>
 __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
   constexpr bool TA = (OPA == 1 || OPA == 2), CA = (OPA == 2 || OPA == 3);
   constexpr bool TB = (OPB == 1 || OPB == 2), CB = (OPB == 2 || OPB == 3);
+  constexpr int PAT = BM + 2, PB = BN + 2;
+  constexpr int MT = BM / 16, NTL = BN / 16;  // 8x8 sub-tiles per warp (2x2 warps)
   constexpr int A_ST = TA ? BK * PAT : BM * PA;
   constexpr int B_ST = TB ? BN * PBT : BK * PB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
         const bool v = (gm < M) && (gk < kend);
         cp_async16(a_dst + r * PA + kk, v ? (const void*)(A + gm * lda + gk) : (const void*)A, v);
       } else {
-        const int kr = c >> 6, mm = c & 63;
+        const int kr = c / BM, mm = c % BM;
         const int gm = m0 + mm, gk = k0 + kr;
         const bool v = (gm < M) && (gk < kend);
         cp_async16(a_dst + kr * PAT + mm, v ? (const void*)(A + gk * lda + gm) : (const void*)A, v);
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
     for (int i = 0; i < (BN * BK) / NT; ++i) {
       const int c = tid + i * NT;
       if (!TB) {
-        const int kr = c >> 6, nn = c & 63;
+        const int kr = c / BN, nn = c % BN;
         const int gn = n0 + nn, gk = k0 + kr;
         const bool v = (gn < N) && (gk < kend);
         cp_async16(b_dst + kr * PB + nn, v ? (const void*)(B + gk * ldb + gn) : (const void*)B, v);
@@ -106,11 +108,11 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
     }
   };
 
-  double accR[4][4][2], accI[4][4][2];
+  double accR[MT][NTL][2], accI[MT][NTL][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
+    for (int j = 0; j < NTL; ++j) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
 
   const int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
 #pragma unroll
@@ -131,24 +133,24 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
       const int kq = ks + (lane & 3);
-      cplx af[4], bf[4];
+      cplx af[MT], bf[NTL];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int row = wm * 32 + mt * 8 + (lane >> 2);
+      for (int mt = 0; mt < MT; ++mt) {
+        const int row = wm * (BM / 2) + mt * 8 + (lane >> 2);
         af[mt] = TA ? a_s[kq * PAT + row] : a_s[row * PA + kq];
         if (CA) af[mt].y = -af[mt].y;
       }
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int col = wn * 32 + nt * 8 + (lane >> 2);
+      for (int nt = 0; nt < NTL; ++nt) {
+        const int col = wn * (BN / 2) + nt * 8 + (lane >> 2);
         bf[nt] = TB ? b_s[col * PBT + kq] : b_s[kq * PB + col];
         if (CB) bf[nt].y = -bf[nt].y;
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         const double nai = -af[mt].y;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
+        for (int nt = 0; nt < NTL; ++nt) {
           dmma(accR[mt][nt][0], accR[mt][nt][1], af[mt].x, bf[nt].x);
           dmma(accR[mt][nt][0], accR[mt][nt][1], nai, bf[nt].y);
           dmma(accI[mt][nt][0], accI[mt][nt][1], af[mt].x, bf[nt].y);
@@ -166,14 +168,14 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
   const cplx alpha = g.alpha, beta = g.beta;
   const bool use_beta = (beta.x != 0.0 || beta.y != 0.0);
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int r = m0 + wm * 32 + mt * 8 + (lane >> 2);
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = m0 + wm * (BM / 2) + mt * 8 + (lane >> 2);
     if (r >= M) continue;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
+    for (int nt = 0; nt < NTL; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = n0 + wn * 32 + nt * 8 + 2 * (lane & 3) + h;
+        const int c = n0 + wn * (BN / 2) + nt * 8 + 2 * (lane & 3) + h;
         if (c >= N) continue;
         cplx v = cmk(accR[mt][nt][h], accI[mt][nt][h]);
         cplx* p = C + r * ldc + c;
@@ -217,34 +219,44 @@ __global__ void scale_matrix_kernel(int M, int N, cplx beta, cplx* C, long long 
   }
 }
 
-template <int OPA, int OPB>
+template <int OPA, int OPB, int BM, int BN>
 constexpr size_t smem_bytes() {
   constexpr bool TA = (OPA == 1 || OPA == 2);
   constexpr bool TB = (OPB == 1 || OPB == 2);
-  return (size_t)STAGES * ((TA ? BK * PAT : BM * PA) + (TB ? BN * PBT : BK * PB)) * sizeof(cplx);
+  return (size_t)STAGES * ((TA ? BK * (BM + 2) : BM * PA) + (TB ? BN * PBT : BK * (BN + 2))) * sizeof(cplx);
 }
 
-template <int OPA, int OPB>
+template <int OPA, int OPB, int BM, int BN>
 cudaError_t launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
   static bool configured = false;
-  constexpr size_t sm = smem_bytes<OPA, OPB>();
+  constexpr size_t sm = smem_bytes<OPA, OPB, BM, BN>();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<OPA, OPB, BM, BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  zgemm_dmma_kernel<OPA, OPB><<<grid, NT, sm, st>>>(g);
+  zgemm_dmma_kernel<OPA, OPB, BM, BN><<<grid, NT, sm, st>>>(g);
   return cudaGetLastError();
 }
 
-template <int OPA>
+template <int BM, int BN, int OPA>
 cudaError_t launch_b(int opB, const GemmArgs& g, dim3 grid, cudaStream_t st) {
   switch (opB) {
-    case 0: return launch_t<OPA, 0>(g, grid, st);
-    case 1: return launch_t<OPA, 1>(g, grid, st);
-    case 2: return launch_t<OPA, 2>(g, grid, st);
-    default: return launch_t<OPA, 3>(g, grid, st);
+    case 0: return launch_t<OPA, 0, BM, BN>(g, grid, st);
+    case 1: return launch_t<OPA, 1, BM, BN>(g, grid, st);
+    case 2: return launch_t<OPA, 2, BM, BN>(g, grid, st);
+    default: return launch_t<OPA, 3, BM, BN>(g, grid, st);
+  }
+}
+
+template <int BM, int BN>
+cudaError_t launch_ab(int opA, int opB, const GemmArgs& g, dim3 grid, cudaStream_t st) {
+  switch (opA) {
+    case 0: return launch_b<BM, BN, 0>(opB, g, grid, st);
+    case 1: return launch_b<BM, BN, 1>(opB, g, grid, st);
+    case 2: return launch_b<BM, BN, 2>(opB, g, grid, st);
+    default: return launch_b<BM, BN, 3>(opB, g, grid, st);
   }
 }
 
@@ -269,7 +281,11 @@ cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx a
   g.B = B; g.ldb = ldb; g.sB = sB;
   g.C = C; g.ldc = ldc; g.sC = sC;
   g.work = work;
-  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN) * batch;
+  // tile choice: 64x64 when that gives >= 2 waves of CTAs, else 32x32 (4x more CTAs)
+  const long long tiles64 = (long long)((M + 63) / 64) * ((N + 63) / 64) * batch;
+  const bool small = tiles64 < 2LL * g_num_sms;
+  const int bm = small ? 32 : 64, bn = bm;
+  const long long tiles = (long long)((M + bm - 1) / bm) * ((N + bn - 1) / bn) * batch;
   int ksplit = 1;
   const long long target = 2LL * g_num_sms;
   if (work != nullptr && tiles < target && K >= 256) {
@@ -284,14 +300,8 @@ cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx a
   }
   g.ksplit = ksplit;
   g.kchunk = kchunk;
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch * ksplit);
-  cudaError_t e;
-  switch (opA) {
-    case 0: e = launch_b<0>(opB, g, grid, st); break;
-    case 1: e = launch_b<1>(opB, g, grid, st); break;
-    case 2: e = launch_b<2>(opB, g, grid, st); break;
-    default: e = launch_b<3>(opB, g, grid, st); break;
-  }
+  dim3 grid((N + bn - 1) / bn, (M + bm - 1) / bm, batch * ksplit);
+  cudaError_t e = small ? launch_ab<32, 32>(opA, opB, g, grid, st) : launch_ab<64, 64>(opA, opB, g, grid, st);
   if (e != cudaSuccess || ksplit == 1) return e;
   const long long total = (long long)M * N * batch;
   const int blocks = (int)std::min<long long>(4LL * g_num_sms, (total + 255) / 256);

@@ -46,7 +46,8 @@ def test_zgemm_all_ops(B, opA, opB):
     assert rel(out, ref) < 1e-14
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 4), (64, 64, 8), (65, 129, 257), (5, 3, 4096), (2048, 16, 640)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 4), (64, 64, 8), (65, 129, 257), (5, 3, 4096), (2048, 16, 640),
+                                   (1024, 1280, 96), (1100, 1090, 300)])
 def test_zgemm_shapes(B, M, N, K):
     rng = np.random.default_rng(M + N + K)
     A, Bm = rc(rng, M, K), rc(rng, K, N)
