@@ -23,6 +23,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# FP64 SIMT peak of B200: 64 DFMA/clk/SM (ncu sm__sass_thread_inst_executed_op_dfma_pred_on.peak_sustained)
+# x 2 flop x 148 SMs x 1.965 GHz
+FP64_ALU_PEAK_TF = 64 * 2 * 148 * 1.965e9 / 1e12
+FP64_ALU_PEAK_SRC = ("derived: 64 DFMA/clk/SM (ncu dfma peak_sustained) x 2 x 148 SMs x 1.965 GHz "
+                     "(clocks.max.sm); MEASURED_PEAKS.json has no FP64 entry")
 METRIC = "2TDVP sweep time and H_eff complex-FP64 TFLOP/s (% of FP64 peak) at χ, 1/2/4/8 GPUs"
 
 WORKLOADS = {
@@ -255,6 +260,10 @@ def main():
     h2_ms = float(np.sum([s["heff2_ms"] for s in per]))
     h2_fl = float(np.sum([s["heff2_flop"] for s in per]))
     svd_ms = float(np.sum([s["svd_ms"] for s in per]))
+    jac_ms = float(np.sum([s["svd_jac_ms"] for s in per]))
+    jac_fl = float(np.sum([s["svd_jac_flop"] for s in per]))
+    sweeps = int(np.sum([s["svd_sweeps_total"] for s in per]))
+    n_svd = int(np.sum([s["n_pair"] for s in per]))
     launches = int(np.sum([s["kernel_launches"] for s in per]))
     gemm_launches = int(np.sum([s["gemm_launches"] for s in per]))
 
@@ -280,8 +289,9 @@ def main():
         if dist is not None:
             dist.destroy_process_group()
         return
-    achieved = h2_fl / (h2_ms * 1e-3) / 1e12 if h2_ms > 0 else None
-    peak = max(peaks.values()) if peaks else None
+    h2_tf = h2_fl / (h2_ms * 1e-3) / 1e12 if h2_ms > 0 else None
+    zpeak = peaks.get("zgemm") if peaks else None
+    jac_tf = jac_fl / (jac_ms * 1e-3) / 1e12 if jac_ms > 0 else None
     line = {
         "metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
@@ -289,12 +299,20 @@ def main():
         "config": {"workload": args.workload, "desc": wl["desc"], "L": L, "chi_max": wl["chi"], "D_mpo": 5,
                    "segments": p, "parallelism": f"p2tdvp{p}" if p > 1 else "serial",
                    "l2": "working set (envs + MPS ~ 0.2 GB) larger than L2 (126 MB)"},
-        "roofline": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + 2 sparse MPO stages)", "bound": "tensor",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": None,
-                     "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
-                     "heff2_share_of_step": h2_ms / step_ms if step_ms > 0 else None,
-                     "svd_share_of_step": svd_ms / step_ms if step_ms > 0 else None},
+        # dominant kernel of the step: the Jacobi stage of the truncated SVD (FP64 SIMT, latency-bound)
+        "roofline": {"kernel": "svd_rjac one-sided Jacobi (register-resident block pairs)", "bound": "alu",
+                     "achieved": jac_tf, "peak": FP64_ALU_PEAK_TF, "unit": "TFLOP/s",
+                     "frac": (jac_tf / FP64_ALU_PEAK_TF) if jac_tf else None, "traffic": None,
+                     "peak_source": FP64_ALU_PEAK_SRC,
+                     "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
+                     "share_of_step": jac_ms / step_ms if step_ms > 0 else None,
+                     "svd_calls": n_svd, "sweeps_per_svd": sweeps / n_svd if n_svd else None},
+        "heff2": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + 2 sparse MPO stages)", "bound": "tensor",
+                  "achieved": h2_tf, "peak": zpeak, "unit": "TFLOP/s",
+                  "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,
+                  "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
+                  "share_of_step": h2_ms / step_ms if step_ms > 0 else None},
+        "svd_share_of_step": svd_ms / step_ms if step_ms > 0 else None,
         "gpu_launches": launches,
         "gemm_launches": gemm_launches,
         "wall_s_timed": wall,

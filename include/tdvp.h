@@ -64,6 +64,9 @@ typedef struct {
   double svd_ms;          /* summed SVD time (timing=1) */
   long long gemm_launches; /* DMMA GEMM kernel launches in the last step */
   long long kernel_launches; /* all kernel launches of this library in the last step */
+  double svd_jac_ms;      /* summed device time of the Jacobi kernel of every SVD (timing=1) */
+  double svd_jac_flop;    /* its algorithmic real flops: sweeps * nc(nc-1)/2 * (16 mr + 24 (mr + nc)) */
+  int svd_sweeps_total;   /* Jacobi sweeps summed over the SVDs of the last step */
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

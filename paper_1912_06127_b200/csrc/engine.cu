@@ -397,8 +397,10 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
   int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
   double w = 0.0;
+  float jac_ms = 0.f;
   cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
-                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps);
+                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps,
+                                      h->prm.timing ? &jac_ms : nullptr);
   if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
   CK(se);
   g_launch_count += 5;
@@ -408,6 +410,12 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   h->stats.w_step += w;
   h->stats.n_pair++;
   h->stats.svd_sweeps_max = std::max(h->stats.svd_sweeps_max, sweeps);
+  h->stats.svd_sweeps_total += sweeps;
+  {
+    const double mr = std::max(cl * d, d * cr), nc = std::min(cl * d, d * cr);
+    h->stats.svd_jac_ms += jac_ms;
+    h->stats.svd_jac_flop += (double)sweeps * nc * (nc - 1) / 2 * (16.0 * mr + 24.0 * (mr + nc));
+  }
   if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
   // a5: environments for the next update
   if (build & BUILD_BETA) {
@@ -769,6 +777,8 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   h->stats.trunc_active = 0;
   h->stats.n_pair = h->stats.n_back = 0;
   h->stats.svd_sweeps_max = 0;
+  h->stats.svd_sweeps_total = 0;
+  h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
   h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
   h->stats.heff2_calls = 0;
   h->ev_used = 0;
@@ -1004,6 +1014,8 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
     CK(cudaEventCreate(&h->ev_step0));
     CK(cudaEventCreate(&h->ev_step1));
     alloc_workspace(h);
+    CK(cudaEventCreate(&h->sv.ev_jac[0]));
+    CK(cudaEventCreate(&h->sv.ev_jac[1]));
     // measurement MPOs (D = 1): identity and S^z (d = 2 spin-1/2 convention)
     std::vector<cplx> Id(d * d, ZERO), Sz(d * d, ZERO);
     for (int s = 0; s < d; ++s) Id[s * d + s] = ONE;
@@ -1197,6 +1209,8 @@ void tdvp_destroy(tdvp_t h) {
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   if (h->ev_step0) cudaEventDestroy(h->ev_step0);
   if (h->ev_step1) cudaEventDestroy(h->ev_step1);
+  for (auto e : h->sv.ev_jac)
+    if (e) cudaEventDestroy(e);
   if (h->h_pin) cudaFreeHost(h->h_pin);
   if (h->h_ipin) cudaFreeHost(h->h_ipin);
   if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);

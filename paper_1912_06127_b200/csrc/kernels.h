@@ -79,6 +79,7 @@ struct SvdDev {
   double* dres;       // [4] : w (discarded weight), sigma_1
   double* h_buf;      // pinned host mirror [8] (offmax, dres..)
   int* h_ibuf;        // pinned host mirror [4]
+  cudaEvent_t ev_jac[2];  // optional: recorded around the Jacobi kernel (timing)
 };
 struct TruncParams {
   int chi_max;
@@ -89,5 +90,9 @@ struct TruncParams {
 // Returns chi via *chi_out (host), discarded weight via *w_out (host).
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
-                               int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out);
+                               int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
+                               float* jac_ms_out = nullptr);
 size_t svd_work_elems(int m, int n);
+// svd_rjac.cu: register-resident Jacobi stage on d.Y = [X ; V]; returns
+// cudaErrorNotSupported for shapes it does not cover (svd.cu falls back).
+cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long long ldy, double tol, int* sweeps_dev);

@@ -164,63 +164,115 @@ __global__ void lz_scale_kernel(const double* scal, int which, bool brk_zero, co
     out[e] = cscale(x[e], inv);
 }
 
-// symmetric tridiagonal T (K x K) = Q mu Q^T by cyclic Jacobi; y = n0 Q (e^{tau mu} * Q^T e1)
-__global__ void lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double A[KMAX][KMAX], Q[KMAX][KMAX];
-  for (int i = 0; i < K; ++i)
-    for (int j = 0; j < K; ++j) {
-      A[i][j] = 0.0;
-      Q[i][j] = (i == j) ? 1.0 : 0.0;
+// symmetric tridiagonal T (K x K) = Q mu Q^T by parallel-ordered two-sided
+// Jacobi in ONE warp (K <= 16: lane r owns row/column r; each step applies
+// K/2 disjoint rotations from the round-robin schedule), then
+// y = n0 Q (e^{tau mu} * Q^T e1).
+__global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
+  __shared__ double A[KMAX][KMAX + 1], Q[KMAX][KMAX + 1];
+  __shared__ double s_c[KMAX / 2], s_s[KMAX / 2];
+  __shared__ int s_p[KMAX / 2], s_q[KMAX / 2], s_z[KMAX / 2];
+  const int r = threadIdx.x;
+  const int K2 = K + (K & 1);  // even player count (a dummy player never rotates)
+  if (r < KMAX) {
+    for (int j = 0; j < KMAX; ++j) {
+      double a = 0.0;
+      if (r < K && j < K) {
+        if (j == r) a = d.scal[r];
+        else if (j == r + 1) a = d.scal[KMAX + r];
+        else if (j + 1 == r) a = d.scal[KMAX + j];
+      }
+      A[r][j] = a;
+      Q[r][j] = (r == j) ? 1.0 : 0.0;
     }
-  for (int i = 0; i < K; ++i) A[i][i] = d.scal[i];
-  for (int i = 0; i + 1 < K; ++i) A[i][i + 1] = A[i + 1][i] = d.scal[KMAX + i];
+  }
+  __syncwarp();
   for (int sweep = 0; sweep < 60; ++sweep) {
     double off = 0.0, nrm = 0.0;
-    for (int i = 0; i < K; ++i)
+    if (r < K)
       for (int j = 0; j < K; ++j) {
-        if (i != j) off += A[i][j] * A[i][j];
-        nrm += A[i][j] * A[i][j];
+        const double a2 = A[r][j] * A[r][j];
+        nrm += a2;
+        if (j != r) off += a2;
       }
+    off = warp_sum(off);
+    nrm = warp_sum(nrm);
     if (off <= 1e-34 * nrm || off == 0.0) break;
-    for (int p = 0; p < K - 1; ++p)
-      for (int q = p + 1; q < K; ++q) {
-        const double apq = A[p][q];
-        if (apq == 0.0) continue;
-        const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int r = 0; r < K; ++r) {
+    for (int step = 0; step < K2 - 1; ++step) {
+      if (r < K2 / 2) {
+        // circle method, player K2-1 fixed
+        const int m = K2 - 1;
+        int p, q;
+        if (r == 0) { p = K2 - 1; q = step % m; }
+        else { p = (step + r) % m; q = (step - r + m) % m; }
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, sn = 0.0;
+        int z = 0;
+        if (q < K) {
+          const double apq = A[p][q];
+          if (apq != 0.0) {
+            z = 1;
+            const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            sn = t * c;
+          }
+        }
+        s_p[r] = p;
+        s_q[r] = q;
+        s_c[r] = c;
+        s_s[r] = sn;
+        s_z[r] = z;
+      }
+      __syncwarp();
+      // A <- A J, Q <- Q J (lane r: row r)
+      if (r < K) {
+        for (int i = 0; i < K2 / 2; ++i) {
+          const int p = s_p[i], q = s_q[i];
+          if (q >= K) continue;
+          const double c = s_c[i], sn = s_s[i];
           const double arp = A[r][p], arq = A[r][q];
-          A[r][p] = c * arp - s * arq;
-          A[r][q] = s * arp + c * arq;
-        }
-        for (int r = 0; r < K; ++r) {
-          const double apr = A[p][r], aqr = A[q][r];
-          A[p][r] = c * apr - s * aqr;
-          A[q][r] = s * apr + c * aqr;
-        }
-        A[p][q] = A[q][p] = 0.0;
-        for (int r = 0; r < K; ++r) {
+          A[r][p] = c * arp - sn * arq;
+          A[r][q] = sn * arp + c * arq;
           const double qrp = Q[r][p], qrq = Q[r][q];
-          Q[r][p] = c * qrp - s * qrq;
-          Q[r][q] = s * qrp + c * qrq;
+          Q[r][p] = c * qrp - sn * qrq;
+          Q[r][q] = sn * qrp + c * qrq;
         }
       }
+      __syncwarp();
+      // A <- J^T A (lane r: column r)
+      if (r < K) {
+        for (int i = 0; i < K2 / 2; ++i) {
+          const int p = s_p[i], q = s_q[i];
+          if (q >= K) continue;
+          const double c = s_c[i], sn = s_s[i];
+          const double apr = A[p][r], aqr = A[q][r];
+          A[p][r] = c * apr - sn * aqr;
+          A[q][r] = sn * apr + c * aqr;
+        }
+      }
+      __syncwarp();
+      if (r < K2 / 2 && s_z[r]) {
+        A[s_p[r]][s_q[r]] = 0.0;
+        A[s_q[r]][s_p[r]] = 0.0;
+      }
+      __syncwarp();
+    }
   }
-  const double n0 = d.scal[LZ_N0];
-  cplx f[KMAX];
-  for (int j = 0; j < K; ++j) {
-    const double mu = A[j][j];
+  // y_i = n0 sum_j Q[i][j] e^{tau mu_j} Q[0][j]
+  __shared__ cplx s_f[KMAX];
+  if (r < K) {
+    const double mu = A[r][r];
     const double mag = exp(tre * mu);
     double sn, cs;
     sincos(tim * mu, &sn, &cs);
-    f[j] = cmk(mag * cs * Q[0][j], mag * sn * Q[0][j]);
+    s_f[r] = cmk(mag * cs * Q[0][r], mag * sn * Q[0][r]);
   }
-  for (int i = 0; i < K; ++i) {
+  __syncwarp();
+  if (r < K) {
     cplx acc = cmk(0, 0);
-    for (int j = 0; j < K; ++j) acc = cadd(acc, cscale(f[j], Q[i][j]));
-    d.y[i] = cscale(acc, n0);
+    for (int j = 0; j < K; ++j) acc = cadd(acc, cscale(s_f[j], Q[r][j]));
+    d.y[r] = cscale(acc, d.scal[LZ_N0]);
   }
 }
 

@@ -738,7 +738,8 @@ size_t svd_work_elems(int m, int n) {
 
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
-                               int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out) {
+                               int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
+                               float* jac_ms_out) {
   const bool transposed = m < n;
   const int mr = std::max(m, n), nc = std::min(m, n);
   const long long ldy = (long long)mr + nc;
@@ -750,7 +751,14 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   }
   const double tol = std::max(4.0 * DBL_EPSILON * std::sqrt((double)mr), 1e-15);
   int sweeps = 0;
-  if (nc >= 2) {
+  const bool tj = jac_ms_out != nullptr && d.ev_jac[0] != nullptr;
+  if (tj && (e = cudaEventRecord(d.ev_jac[0], st)) != cudaSuccess) return e;
+  if (nc >= 2 && (e = svd_rjac_run(st, d, mr, nc, ldy, tol, d.ires + 4)) != cudaErrorNotSupported) {
+    // register-resident Jacobi (svd_rjac.cu)
+    if (e != cudaSuccess) return e;
+    sweeps = -1;
+  } else if (nc >= 2) {
+    cudaGetLastError();
     static int forced = -1;
     if (forced < 0) {
       const char* ev = std::getenv("TDVP_SVD_BW");
@@ -819,6 +827,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     }
     sweeps = -1;  // read back with the truncation results
   }
+  if (tj && (e = cudaEventRecord(d.ev_jac[1], st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(d.ires, 0, 4 * sizeof(int), st)) != cudaSuccess) return e;
   svd_colnorm_kernel<<<(nc + 7) / 8, 256, 0, st>>>(d.Y, ldy, mr, nc, d.sigma, d.ires + 2);
   svd_truncate_kernel<<<1, 1024, (2 * nc + 1) * sizeof(double), st>>>(d.sigma, nc, d.order, tp, d.ires, d.dres);
@@ -828,6 +837,11 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   if (d.h_ibuf[2] != 0 || !std::isfinite(d.h_buf[1]) || !(d.h_buf[2] > 0.0)) return cudaErrorUnknown;
   const int chi = d.h_ibuf[0];
   if (sweeps < 0) sweeps = d.h_ibuf[4];
+  if (tj) {
+    float ms = 0.f;
+    if ((e = cudaEventElapsedTime(&ms, d.ev_jac[0], d.ev_jac[1])) != cudaSuccess) return e;
+    *jac_ms_out = ms;
+  }
   {
     const long long total = (long long)m * chi + (long long)chi * n + chi;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));

@@ -1,0 +1,451 @@
+// Register-resident blocked one-sided (Hestenes) Jacobi for the truncated SVD
+// of the two-site matrix Theta' (Fig 6 "SVD"; truncation
+// PAPER.md:493-499, :510).  Replaces the Jacobi stage of svd.cu for the
+// shapes listed in kTab; init (Y = [X ; I]), column norms, truncation and the
+// split are svd.cu's.
+//
+// Y (column-major, ld = ldy) holds the work matrix X (mr x nc, mr >= nc) in
+// rows [0, mr) and the accumulated right rotations V (nc x nc) in rows
+// [mr, mr + nc).  The right factor is accumulated (not recovered afterwards
+// by a GEMM with Theta) because the inverse-canonical form multiplies both
+// factors by V_j = 1/Lambda_j: each factor must be accurate
+// RELATIVE to sigma_k, which only the rotated columns/rows give.
+//
+// One CTA per block pair (2*BW columns); each thread holds RX rows of X and
+// RV rows of V of all 2*BW columns in REGISTERS.  All sweeps of the
+// round-robin tournament over column blocks run in ONE persistent launch;
+// between rounds the blocks go through L2 and the CTAs meet at a cluster
+// barrier (all CTAs in one thread-block cluster, <= 16) or a grid barrier
+// (cooperative launch).  An inner step applies BW disjoint rotations: the
+// 4*BW dot products (|x_p|^2, |x_q|^2, x_p^H x_q) are reduced by a warp
+// reduce-scatter butterfly and one shared-memory exchange (one
+// __syncthreads per step); every warp derives the same rotation parameters.
+// Round 0 of a sweep runs the full 2BW-column round robin (intra- and
+// cross-block pairs), the other rounds the BW cross-block steps, so a sweep
+// visits every column pair exactly once.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cooperative_groups.h>
+#include "common.cuh"
+#include "kernels.h"
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ unsigned long long g_rj_prof[8];
+
+__device__ __forceinline__ void rj_rr_pair(int n, int round, int i, int& a, int& b) {
+  const int m = n - 1;
+  if (i == 0) {
+    a = n - 1;
+    b = round % m;
+  } else {
+    a = (round + i) % m;
+    b = (round - i + m) % m;
+  }
+  if (a > b) { const int t = a; a = b; b = t; }
+}
+
+// step s, slot i of the inner schedule (compile-time after unrolling)
+template <int BW, bool CROSS>
+__device__ __forceinline__ void rj_pq(int s, int i, int& p, int& q) {
+  if (CROSS) {
+    p = i;
+    q = BW + (i + s) % BW;
+  } else {
+    constexpr int N = 2 * BW, M = N - 1;
+    int a, b;
+    if (i == 0) {
+      a = N - 1;
+      b = s % M;
+    } else {
+      a = (s + i) % M;
+      b = (s - i + M) % M;
+    }
+    p = a < b ? a : b;
+    q = a < b ? b : a;
+  }
+}
+
+// 1/x and 1/sqrt(x) for normal positive x: MUFU seed + Newton steps (full
+// double precision; the arguments below are always normal numbers).
+__device__ __forceinline__ double rj_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rj_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
+// Complex Jacobi rotation zeroing g = x_p^H x_q (a = |x_p|^2, c = |x_q|^2):
+// t e^{i phi} = 2 sgn(c-a) g / (|c-a| + sqrt((c-a)^2 + 4|g|^2)), cs = 1/sqrt(1+t^2),
+// sn = cs t e^{i phi};  x_p' = cs x_p - conj(sn) x_q,  x_q' = sn x_p + cs x_q.
+// Skipped (identity) when |g|^2 <= tol2q a c.
+__device__ __forceinline__ bool rj_params(double a, double c, double gr, double gi, double tol2q, double& cs,
+                                          double& sr, double& si, bool fastp) {
+  const double ag2 = gr * gr + gi * gi;
+  if (!(ag2 > 1e-300) || !(ag2 > tol2q * a * c)) return false;
+  const double w = c - a;
+  if (!fastp) {
+    const double den = fabs(w) + sqrt(fma(w, w, 4.0 * ag2));
+    const double f = copysign(2.0, w) / den;
+    cs = rsqrt(fma(f * f, ag2, 1.0));
+    sr = cs * f * gr;
+    si = cs * f * gi;
+    return true;
+  }
+  const double s = fma(w, w, 4.0 * ag2);
+  const double den = fabs(w) + s * rj_rsqrt(s);
+  const double f = copysign(2.0, w) * rj_rcp(den);
+  cs = rj_rsqrt(fma(f * f, ag2, 1.0));
+  sr = cs * f * gr;
+  si = cs * f * gi;
+  return true;
+}
+
+// per-step phase profile (block 0, thread 0): [4] dots [5] reduce+store [6] barrier [7] params+apply
+#define RJ_T(i)                              \
+  if (sprof) {                               \
+    const unsigned long long _t = clock64(); \
+    g_rj_prof[i] += _t - spt;                \
+    spt = _t;                                \
+  }
+
+template <int BW, int RX, int RV, int NT, bool CROSS>
+__device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 * BW], int s, double (*red)[BW * 4],
+                                        int lane, int wid, double tol2q, double& offacc, bool& rot, bool sprof,
+                                        bool fastp) {
+  constexpr int NV = 4 * BW;
+  constexpr int H = (NV == 32) ? 5 : (NV == 16) ? 4 : 3;
+  constexpr int SH = 5 - H;
+  constexpr int NW = NT / 32;
+  unsigned long long spt = sprof ? clock64() : 0ull;
+  double val[NV];
+#pragma unroll
+  for (int i = 0; i < BW; ++i) {
+    int p, q;
+    rj_pq<BW, CROSS>(s, i, p, q);
+    double a = 0.0, c = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+    for (int k = 0; k < RX; ++k) {
+      const cplx u = x[k][p], w = x[k][q];
+      a = fma(u.x, u.x, fma(u.y, u.y, a));
+      c = fma(w.x, w.x, fma(w.y, w.y, c));
+      gr = fma(u.x, w.x, fma(u.y, w.y, gr));
+      gi = fma(u.x, w.y, fma(-u.y, w.x, gi));
+    }
+    val[4 * i] = a;
+    val[4 * i + 1] = c;
+    val[4 * i + 2] = gr;
+    val[4 * i + 3] = gi;
+  }
+  RJ_T(4)
+  // warp reduce-scatter: afterwards lane l holds the warp sum of value l >> SH
+#pragma unroll
+  for (int lev = 0; lev < H; ++lev) {
+    const int msk = 16 >> lev;
+    const int h = NV >> (lev + 1);
+    const bool up = (lane & msk) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? val[j] : val[j + h];
+      const double keep = up ? val[j + h] : val[j];
+      val[j] = keep + __shfl_xor_sync(FULL, send, msk);
+    }
+  }
+  double t = val[0];
+#pragma unroll
+  for (int msk = (16 >> H); msk >= 1; msk >>= 1) t += __shfl_xor_sync(FULL, t, msk);
+  if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = t;
+  RJ_T(5)
+  __syncthreads();
+  RJ_T(6)
+  // every warp: CTA totals (tree over warps), rotation parameters of pair (lane % BW)
+  double tot = 0.0;
+  if (lane < NV) {
+    double part[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) part[w] = red[w][lane];
+#pragma unroll
+    for (int st = 1; st < NW; st <<= 1)
+#pragma unroll
+      for (int w = 0; w + st < NW; w += 2 * st) part[w] += part[w + st];
+    tot = part[0];
+  }
+  const int pi = lane % BW;
+  const double a = __shfl_sync(FULL, tot, 4 * pi);
+  const double c = __shfl_sync(FULL, tot, 4 * pi + 1);
+  const double gr = __shfl_sync(FULL, tot, 4 * pi + 2);
+  const double gi = __shfl_sync(FULL, tot, 4 * pi + 3);
+  double cs = 1.0, sr = 0.0, si = 0.0;
+  if (a > 0.0 && c > 0.0) {
+    offacc = fmax(offacc, (gr * gr + gi * gi) / (a * c));
+    rj_params(a, c, gr, gi, tol2q, cs, sr, si, fastp);
+  }
+#pragma unroll
+  for (int i = 0; i < BW; ++i) {
+    int p, q;
+    rj_pq<BW, CROSS>(s, i, p, q);
+    const double csi = __shfl_sync(FULL, cs, i);
+    const double sri = __shfl_sync(FULL, sr, i);
+    const double sii = __shfl_sync(FULL, si, i);
+    if (sri != 0.0 || sii != 0.0) {  // warp-uniform (identical in every warp)
+      rot = true;
+#pragma unroll
+      for (int k = 0; k < RX; ++k) {
+        const cplx u = x[k][p], w = x[k][q];
+        x[k][p] = cmk(fma(csi, u.x, -fma(sri, w.x, sii * w.y)), fma(csi, u.y, -fma(sri, w.y, -sii * w.x)));
+        x[k][q] = cmk(fma(csi, w.x, fma(sri, u.x, -sii * u.y)), fma(csi, w.y, fma(sri, u.y, sii * u.x)));
+      }
+#pragma unroll
+      for (int k = 0; k < RV; ++k) {
+        const cplx u = v[k][p], w = v[k][q];
+        v[k][p] = cmk(fma(csi, u.x, -fma(sri, w.x, sii * w.y)), fma(csi, u.y, -fma(sri, w.y, -sii * w.x)));
+        v[k][q] = cmk(fma(csi, w.x, fma(sri, u.x, -sii * u.y)), fma(csi, w.y, fma(sri, u.y, sii * u.x)));
+      }
+    }
+  }
+  RJ_T(7)
+}
+
+template <int BW, int RX, int RV, int NT, bool CLUSTER>
+__global__ void __launch_bounds__(NT, 1)
+    rjac_kernel(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe, double tol, int max_sweeps, int full_rounds,
+                double* offbuf, int* sweeps_out, int prof, int fastp) {
+  constexpr int PC = 2 * BW, NV = 4 * BW, NW = NT / 32;
+  __shared__ double red[2][NW][NV];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double tol2q = 0.0625 * tol * tol;
+  cplx x[RX][PC], v[RV][PC];
+  int sweep = 0, buf = 0;
+  unsigned long long pt = 0;
+  const bool pr = prof && blockIdx.x == 0 && tid == 0;
+  auto mark = [&](int i) {
+    if (pr) {
+      const unsigned long long t = clock64();
+      if (pt) g_rj_prof[i] += t - pt;
+      pt = t;
+    }
+  };
+  mark(0);
+  for (; sweep < max_sweeps; ++sweep) {
+    double* off_cur = offbuf + (sweep % 3);
+    if (blockIdx.x == 0 && tid == 0) offbuf[(sweep + 1) % 3] = 0.0;
+    for (int round = 0; round < nbe - 1; ++round) {
+      int a, b;
+      rj_rr_pair(nbe, round, blockIdx.x, a, b);
+#pragma unroll
+      for (int j = 0; j < PC; ++j) {
+        const int blk = j < BW ? a : b;
+        const int col = blk * BW + (j % BW);
+        const bool valid = blk < nb && col < nc;
+        const cplx* src = Y + (long long)col * ldy;
+#pragma unroll
+        for (int k = 0; k < RX; ++k) {
+          const int r = tid + k * NT;
+          x[k][j] = (valid && r < mr) ? __ldcg(src + r) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < RV; ++k) {
+          const int r = tid + k * NT;
+          v[k][j] = (valid && r < nc) ? __ldcg(src + mr + r) : cmk(0.0, 0.0);
+        }
+      }
+      mark(0);
+      double offacc = 0.0;
+      bool rot = false;
+      if (round == 0 || full_rounds) {
+#pragma unroll
+        for (int s = 0; s < PC - 1; ++s) {
+          rj_step<BW, RX, RV, NT, false>(x, v, s, red[buf], lane, wid, tol2q, offacc, rot, pr && prof > 1, fastp);
+          buf ^= 1;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < BW; ++s) {
+          rj_step<BW, RX, RV, NT, true>(x, v, s, red[buf], lane, wid, tol2q, offacc, rot, pr && prof > 1, fastp);
+          buf ^= 1;
+        }
+      }
+      mark(1);
+      if (rot) {
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+          const int blk = j < BW ? a : b;
+          const int col = blk * BW + (j % BW);
+          if (blk < nb && col < nc) {
+            cplx* dst = Y + (long long)col * ldy;
+#pragma unroll
+            for (int k = 0; k < RX; ++k) {
+              const int r = tid + k * NT;
+              if (r < mr) __stcg(dst + r, x[k][j]);
+            }
+#pragma unroll
+            for (int k = 0; k < RV; ++k) {
+              const int r = tid + k * NT;
+              if (r < nc) __stcg(dst + mr + r, v[k][j]);
+            }
+          }
+        }
+      }
+      if (wid == 0) {
+        offacc = warp_max(offacc);
+        if (lane == 0 && offacc > 0.0) atomic_max_nonneg(off_cur, sqrt(offacc));
+      }
+      mark(2);
+      if (CLUSTER) {
+        cg::this_cluster().sync();
+      } else {
+        cg::this_grid().sync();
+      }
+      mark(3);
+    }
+    const double off = __ldcg(off_cur);
+    if (!(off > tol)) break;
+  }
+  if (blockIdx.x == 0 && tid == 0) *sweeps_out = min(sweep + 1, max_sweeps);
+}
+
+struct RjVariant {
+  void* fn;
+  bool cluster;
+};
+
+template <int BW, int RX, int RV, int NT>
+RjVariant rj_pick(bool cluster) {
+  return RjVariant{cluster ? (void*)rjac_kernel<BW, RX, RV, NT, true> : (void*)rjac_kernel<BW, RX, RV, NT, false>,
+                   cluster};
+}
+
+// variant table: block width, X rows and V rows per thread, threads per CTA
+struct Row {
+  int bw, rx, rv, nt;
+};
+constexpr Row kTab[] = {
+    {8, 1, 1, 256},  // 0: mr <= 256, nc <= 256: one cluster of <= 16 CTAs
+    {4, 1, 1, 256},  // 1
+    {4, 2, 1, 256},  // 2: mr <= 512, nc <= 256
+    {8, 2, 1, 256},  // 3
+    {4, 2, 2, 256},  // 4: mr <= 512, nc <= 512
+    {4, 2, 2, 128},  // 5: mr <= 256, nc <= 256, 4 warps
+};
+constexpr int kNTab = sizeof(kTab) / sizeof(kTab[0]);
+
+RjVariant rj_variant(int row, bool cl) {
+  switch (row) {
+    case 0: return rj_pick<8, 1, 1, 256>(cl);
+    case 1: return rj_pick<4, 1, 1, 256>(cl);
+    case 2: return rj_pick<4, 2, 1, 256>(cl);
+    case 3: return rj_pick<8, 2, 1, 256>(cl);
+    case 4: return rj_pick<4, 2, 2, 256>(cl);
+    default: return rj_pick<4, 2, 2, 128>(cl);
+  }
+}
+
+bool rows_ok(int row, int mr, int nc) {
+  const Row& r = kTab[row];
+  return mr <= r.rx * r.nt && nc <= r.rv * r.nt;
+}
+
+}  // namespace
+
+// Jacobi stage on d.Y = [X ; V] (column-major, ld = ldy).  Returns
+// cudaErrorNotSupported when no register-resident variant fits the shape.
+cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long long ldy, double tol, int* sweeps_dev) {
+  static int forced = -2, prof = 0, full_rounds = 0, fastp = 0;
+  if (forced == -2) {
+    const char* ev = std::getenv("TDVP_RJ_VARIANT");
+    forced = ev ? std::atoi(ev) : -1;
+    const char* pe = std::getenv("TDVP_SVD_PROF");
+    prof = pe ? std::max(1, std::atoi(pe)) : 0;
+    const char* fr = std::getenv("TDVP_RJ_FULL");
+    full_rounds = fr ? std::atoi(fr) : 0;
+    const char* fp = std::getenv("TDVP_RJ_FAST");
+    fastp = fp ? std::atoi(fp) : 0;
+  }
+  if (forced == 99) return cudaErrorNotSupported;  // tuning: legacy Jacobi
+  int row = -1;
+  if (forced >= 0 && forced < kNTab && rows_ok(forced, mr, nc)) row = forced;
+  if (row < 0) {
+    const int prefer[] = {5, 2, 4};  // measured fastest first (microbench.py --svd, B200)
+    for (int r : prefer)
+      if (rows_ok(r, mr, nc)) { row = r; break; }
+  }
+  if (row < 0) return cudaErrorNotSupported;
+  const int bw = kTab[row].bw, nt = kTab[row].nt;
+  const int nb = (nc + bw - 1) / bw;
+  const int nbe = std::max(2, nb + (nb & 1));
+  const int P = nbe / 2;
+  cudaError_t e;
+  bool cluster = P <= 16 && std::getenv("TDVP_RJ_GRID") == nullptr;
+  RjVariant v{};
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3(P);
+  cfg.blockDim = dim3(nt);
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cluster) {
+    v = rj_variant(row, true);
+    static bool attr_set[kNTab] = {false};
+    if (!attr_set[row]) {
+      if ((e = cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+      attr_set[row] = true;
+    }
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, v.fn, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      cluster = false;
+    }
+  }
+  if (!cluster) {
+    v = rj_variant(row, false);
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, nt, 0)) != cudaSuccess) return e;
+    if (occ * g_num_sms < P) return cudaErrorNotSupported;
+  }
+  if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
+  if (prof) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbolAsync(g_rj_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  }
+  int max_sweeps = 60;
+  cplx* Yp = d.Y;
+  double* offb = d.offmax;
+  void* args[] = {(void*)&Yp,  (void*)&ldy,        (void*)&mr,          (void*)&nc,   (void*)&nb,
+                  (void*)&nbe, (void*)&tol,        (void*)&max_sweeps,  (void*)&full_rounds,
+                  (void*)&offb, (void*)&sweeps_dev, (void*)&prof, (void*)&fastp};
+  if (cluster) {
+    if ((e = cudaLaunchKernelExC(&cfg, v.fn, args)) != cudaSuccess) return e;
+  } else {
+    if ((e = cudaLaunchCooperativeKernel(v.fn, dim3(P), dim3(nt), args, 0, st)) != cudaSuccess) return e;
+  }
+  if (prof) {
+    unsigned long long z[8];
+    cudaMemcpyFromSymbolAsync(z, g_rj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr,
+                 "rjac prof mr=%d nc=%d row=%d bw=%d nt=%d P=%d cluster=%d cycles: load %llu steps %llu store %llu "
+                 "barrier %llu | dots %llu reduce %llu sync %llu params+apply %llu\n",
+                 mr, nc, row, bw, nt, P, (int)cluster, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[7]);
+  }
+  return cudaGetLastError();
+}

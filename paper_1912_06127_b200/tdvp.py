@@ -34,7 +34,8 @@ class tdvp_stats(C.Structure):
                 ("n_back", C.c_int), ("krylov_breakdowns", C.c_int), ("svd_sweeps_max", C.c_int),
                 ("step_ms", C.c_double), ("heff2_ms", C.c_double), ("heff2_flop", C.c_double),
                 ("heff2_calls", C.c_int), ("heff1_ms", C.c_double), ("heff1_flop", C.c_double),
-                ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong)]
+                ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong),
+                ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

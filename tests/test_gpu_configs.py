@@ -52,7 +52,11 @@ def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
             k = min(len(a), len(b))
             assert np.abs(a[:k] - b[:k]).max() <= tol * b[0], (len(a), len(b))
             extra = np.concatenate([a[k:], b[k:]])
-            assert extra.size == 0 or extra.max() <= max(10 * eps, tol) * b[0]
+            # a chi difference is an eps-threshold flip: every value kept by one
+            # side only sits at the eps * sigma_1 cut (within the multiplet floor
+            # of reading R-9b) while no truncation beyond eps is active
+            band = tol if trunc else 2 * eps
+            assert extra.size == 0 or extra.max() <= band * b[0], (extra.max() / b[0], band)
         flips += sum(1 for x, y in zip(chi, ochi) if x != y)
     s = t.stats()
     t.close()
@@ -82,7 +86,12 @@ def test_config4_long_range(B, p):
 def test_config5_scaling_partitions(B, p):
     c = ti.config("c5")
     r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], p, every=5)
-    assert r["flips"] <= 64  # eps-level flips at many bonds of the L=256 SU(2) chain
+    # No bound on the NUMBER of flips here: at eps = 1e-12 the cut sits where the
+    # singular values of the 2048 x 2048 two-site matrices carry absolute errors
+    # ~ sqrt(n) u sigma_1 ~ 1e-14 sigma_1 (1% of the cut) on BOTH sides, and the
+    # SU(2) chain has dense multiplets there, so many bonds flip; run_both checks
+    # that each flip is such a near-cut value (reading R-F).
+    assert not r["trunc"] or r["flips"] <= 64
 
 
 def test_bench_workload_saturated_chi(B):
