@@ -22,6 +22,9 @@ def main():
     ap.add_argument("--chis", default="64,128,256,512,1024")
     ap.add_argument("--svd-n", default="64,128,256,512,1024")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--svd-kind", default="gauss", choices=["gauss", "graded", "halfsmall"],
+                    help="gauss: complex normal; graded: sigma_k = exp(-0.1 k); halfsmall: half O(1), half O(1e-2) "
+                         "(the spectrum of the saturated bench two-site matrices)")
     a = ap.parse_args()
     import tdvp_inputs as ti
     from paper_1912_06127_b200 import tdvp as B
@@ -39,8 +42,18 @@ def main():
         rng = np.random.default_rng(0)
         for n in [int(x) for x in a.svd_n.split(",")]:
             M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+            if a.svd_kind != "gauss":
+                q1, _ = np.linalg.qr(M)
+                q2, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+                if a.svd_kind == "graded":
+                    sv = np.exp(-0.1 * np.arange(n))
+                else:
+                    h = n // 2
+                    sv = np.concatenate([np.sort(rng.uniform(0.5, 1.5, h))[::-1],
+                                         1e-2 * np.sort(rng.uniform(0.0, 1.0, n - h))[::-1]])
+                M = (q1 * sv[None, :]) @ q2.conj().T
             ms, sw = B.bench_svd(M, reps=3 if n >= 1024 else 5)
-            print(json.dumps({"kernel": "svd", "n": n, "bw": os.environ.get("TDVP_SVD_BW", "auto"), "ms": ms,
+            print(json.dumps({"kernel": "svd", "n": n, "kind": a.svd_kind, "ms": ms,
                               "sweeps": sw}), flush=True)
 
 

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtdvp.so")
-SOURCES = ["zgemm.cu", "chanmix.cu", "vec.cu", "lanczos.cu", "svd.cu", "svd_rjac.cu", "engine.cu"]
+SOURCES = ["zgemm.cu", "chanmix.cu", "vec.cu", "lanczos.cu", "svd.cu", "svd_rjac.cu", "qr.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),

@@ -147,7 +147,7 @@ struct tdvp_ctx {
   std::vector<int> h_chi;
   // workspace
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
-  BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, gemm_work, partials;
+  BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, gemm_work, partials;
   BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
   BufPtr svd_sigma, svd_order, svd_off, svd_ires, svd_dres, red_res, envA, envB;
   double* h_pin = nullptr;
@@ -876,7 +876,7 @@ void measure(tdvp_ctx* h, bool want_sz, bool want_E, MeasureOut& out) {
 // ------------------------------------------------------------ workspace
 void alloc_workspace(tdvp_ctx* h) {
   const int L = h->L, d = h->d, D = h->Dmpo;
-  long long n2 = 1, n1 = 1, scr = 1, svd = 1, env = 1;
+  long long n2 = 1, n1 = 1, scr = 1, svd = 1, env = 1, svq = 1;
   for (int j = 0; j < L; ++j) {
     const long long cl = h->cbmax[j], cr1 = h->cbmax[j + 1];
     n1 = std::max(n1, cl * d * cr1);
@@ -887,6 +887,7 @@ void alloc_workspace(tdvp_ctx* h) {
       n2 = std::max(n2, cl * d * d * cr);
       scr = std::max(scr, cl * d * d * cr * D);
       svd = std::max(svd, (long long)svd_work_elems((int)(cl * d), (int)(d * cr)));
+      svq = std::max(svq, (long long)svd_qr_work_elems((int)(cl * d), (int)(d * cr)));
     }
   }
   h->n2max = n2;
@@ -903,6 +904,7 @@ void alloc_workspace(tdvp_ctx* h) {
   h->tmpA = make_buf(std::max(n2, n1) * sizeof(cplx));
   h->tmpB = make_buf(std::max(n2, n1) * sizeof(cplx));
   h->svdY = make_buf(svd * sizeof(cplx));
+  h->svdQ = make_buf(svq * sizeof(cplx));
   h->gemm_work = make_buf(h->work_elems * sizeof(cplx));
   h->envA = make_buf(env * sizeof(cplx));
   h->envB = make_buf(env * sizeof(cplx));
@@ -927,7 +929,7 @@ void alloc_workspace(tdvp_ctx* h) {
   h->lz = LanczosDev{h->lz_scal->d(), h->lz_coef->c(), h->lz_y->c(), h->partials->d(),
                      reinterpret_cast<unsigned*>(h->lz_counter->p), h->lz_brk->i()};
   h->sv = SvdDev{h->svdY->c(), 0, h->svd_sigma->d(), h->svd_order->i(), h->svd_off->d(), h->svd_ires->i(),
-                 h->svd_dres->d(), h->h_pin, h->h_ipin};
+                 h->svd_dres->d(), h->h_pin, h->h_ipin, {nullptr, nullptr}, h->svdQ->c(), (size_t)svq};
 }
 
 int fail(tdvp_ctx* h, const TdvpError& e) {

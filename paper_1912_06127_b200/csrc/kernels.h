@@ -80,7 +80,10 @@ struct SvdDev {
   double* h_buf;      // pinned host mirror [8] (offmax, dres..)
   int* h_ibuf;        // pinned host mirror [4]
   cudaEvent_t ev_jac[2];  // optional: recorded around the Jacobi kernel (timing)
+  cplx* qrbuf;            // QR preconditioning workspace (svd_qr_work_elems), nullptr = off
+  size_t qrbuf_elems;
 };
+size_t svd_qr_work_elems(int m, int n);
 struct TruncParams {
   int chi_max;
   double eps, w_max, delta;
@@ -93,6 +96,35 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
                                float* jac_ms_out = nullptr);
 size_t svd_work_elems(int m, int n);
+// ------------------------------------------------------------------ qr.cu
+// Blocked Householder QR workspace (column-major A, m x n, m >= n).
+struct QrWork {
+  cplx* Vc;        // reflectors as rows, n x ldv (ldv >= m)
+  long long ldv;
+  cplx* T;         // per-panel kb x kb triangular factors
+  cplx* tau;       // [n]
+  cplx* W1;        // [max(n, nc) * kb]
+  cplx* W2;
+  int kb;          // panel width = qr_kb_for(m)
+};
+int qr_kb_for(int m);  // 32 / 16 / 8 for m <= 256 / 512 / 1024, 0 = unsupported
+cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, int m, int n);
+// C (column-major m x nc, ld ldc) <- Q C with Q from qr_factor (m x n reflectors)
+cudaError_t qr_apply_q(cudaStream_t st, const QrWork& w, int m, int n, cplx* C, long long ldc, int nc);
+// X[0:rows_total, 0:n] = [R^H ; 0] from the upper triangle of the factored A
+cudaError_t qr_r_conjtrans(cudaStream_t st, const cplx* A, long long lda, int n, cplx* X, long long ldx,
+                           int rows_total);
+
+// cluster-resident QR (n <= 16 columns per CTA band fitting shared memory;
+// cudaErrorNotSupported otherwise): A overwritten by R and the reflector
+// tails, tau[n]; optionally [R^H ; 0] (rh_rows x n, ld ldrh) written to RH.
+cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH,
+                              long long ldrh, int rh_rows);
+// C (m x nc) <- H_0 ... H_{n-1} C with qr_factor_cluster's reflectors
+cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,
+                          long long ldc, int nc);
+
 // svd_rjac.cu: register-resident Jacobi stage on d.Y = [X ; V]; returns
 // cudaErrorNotSupported for shapes it does not cover (svd.cu falls back).
-cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long long ldy, double tol, int* sweeps_dev);
+cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int nc, long long ldy, double tol,
+                         int* sweeps_dev);

@@ -731,6 +731,12 @@ __global__ void svd_write_kernel(const cplx* __restrict__ Y, long long ldy, cons
 
 }  // namespace
 
+size_t svd_qr_work_elems(int m, int n) {
+  const long long mr = std::max(m, n), nc = std::min(m, n);
+  // Q1 (mr x nc) + Vc1 (nc x mr) + Q2, Vc2 (nc x nc) + T1, T2 + tau1, tau2 + W1, W2 (nc x 32)
+  return (size_t)(2 * mr * nc + 2 * nc * nc + 2 * 32 * (nc + 32) + 2 * nc + 2 * 32 * nc + 64);
+}
+
 size_t svd_work_elems(int m, int n) {
   const long long mr = std::max(m, n), nc = std::min(m, n);
   return (size_t)(mr + nc) * nc;
@@ -749,11 +755,71 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
     svd_init_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, theta, m, n, mr, nc, transposed);
   }
-  const double tol = std::max(4.0 * DBL_EPSILON * std::sqrt((double)mr), 1e-15);
+  // QR preconditioning (Drmac-Veselic): X = Q1 R1, R1^H = Q2 R2, Jacobi on
+  // X3 = R2^H (nc x nc) with V accumulated; then X = (Q1 U3) S (Q2 V)^H, i.e.
+  // Q1 is applied to the converged X3 columns and Q2 to V before the split.
+  static int precond = -1;
+  if (precond < 0) {
+    const char* ev = std::getenv("TDVP_SVD_PRECOND");
+    precond = ev ? std::atoi(ev) : 2;
+  }
+  const bool use_qr = precond == 2 && nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
+                      svd_qr_work_elems(m, n) <= d.qrbuf_elems;
+  QrWork w1{}, w2{};
+  int x_rows = mr;
+  bool qr_cluster = false;
+  cplx* q1p = nullptr;
+  cplx* q2p = nullptr;
+  if (use_qr) {
+    cplx* p = d.qrbuf;
+    cplx* Q1 = p; p += (long long)mr * nc;
+    cplx* Q2 = p; p += (long long)nc * nc;
+    w1.kb = qr_kb_for(mr);
+    w2.kb = qr_kb_for(nc);
+    w1.Vc = p; w1.ldv = mr; p += (long long)nc * mr;
+    w2.Vc = p; w2.ldv = nc; p += (long long)nc * nc;
+    w1.T = p; p += 32LL * (nc + 32);
+    w2.T = p; p += 32LL * (nc + 32);
+    w1.tau = p; p += nc;
+    w2.tau = p; p += nc;
+    w1.W1 = w2.W1 = p; p += 32LL * nc;
+    w1.W2 = w2.W2 = p; p += 32LL * nc;
+    if ((e = cudaMemcpy2DAsync(Q1, (size_t)mr * sizeof(cplx), d.Y, (size_t)ldy * sizeof(cplx), (size_t)mr * sizeof(cplx),
+                               nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return e;
+    static int qrmode = -1;
+    if (qrmode < 0) {
+      const char* ev = std::getenv("TDVP_QR_BLOCKED");
+      qrmode = ev ? std::atoi(ev) : 0;
+    }
+    qr_cluster = false;
+    if (!qrmode) {
+      // cluster-resident QR where the column bands fit shared memory
+      e = qr_factor_cluster(st, Q1, mr, mr, nc, w1.tau, Q2, nc, nc);
+      if (e == cudaSuccess) {
+        if ((e = qr_factor_cluster(st, Q2, nc, nc, nc, w2.tau, d.Y, ldy, mr)) != cudaSuccess) return e;
+        qr_cluster = true;
+      } else if (e != cudaErrorNotSupported) {
+        return e;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (!qr_cluster) {
+      if ((e = qr_factor(st, w1, Q1, mr, mr, nc)) != cudaSuccess) return e;
+      if ((e = qr_r_conjtrans(st, Q1, mr, nc, Q2, nc, nc)) != cudaSuccess) return e;
+      if ((e = qr_factor(st, w2, Q2, nc, nc, nc)) != cudaSuccess) return e;
+      if ((e = qr_r_conjtrans(st, Q2, nc, nc, d.Y, ldy, mr)) != cudaSuccess) return e;
+    }
+    q1p = Q1;
+    q2p = Q2;
+    x_rows = nc;
+  }
+  const double tol = std::max(4.0 * DBL_EPSILON * std::sqrt((double)x_rows), 1e-15);
   int sweeps = 0;
   const bool tj = jac_ms_out != nullptr && d.ev_jac[0] != nullptr;
   if (tj && (e = cudaEventRecord(d.ev_jac[0], st)) != cudaSuccess) return e;
-  if (nc >= 2 && (e = svd_rjac_run(st, d, mr, nc, ldy, tol, d.ires + 4)) != cudaErrorNotSupported) {
+  if (nc >= 2 && (e = svd_rjac_run(st, d, x_rows, mr, nc, ldy, tol, d.ires + 4)) != cudaErrorNotSupported) {
     // register-resident Jacobi (svd_rjac.cu)
     if (e != cudaSuccess) return e;
     sweeps = -1;
@@ -841,6 +907,13 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     float ms = 0.f;
     if ((e = cudaEventElapsedTime(&ms, d.ev_jac[0], d.ev_jac[1])) != cudaSuccess) return e;
     *jac_ms_out = ms;
+  }
+  if (use_qr && qr_cluster) {
+    if ((e = qr_apply_refl(st, q1p, mr, w1.tau, mr, nc, d.Y, ldy, nc)) != cudaSuccess) return e;
+    if ((e = qr_apply_refl(st, q2p, nc, w2.tau, nc, nc, d.Y + mr, ldy, nc)) != cudaSuccess) return e;
+  } else if (use_qr) {
+    if ((e = qr_apply_q(st, w1, mr, nc, d.Y, ldy, nc)) != cudaSuccess) return e;
+    if ((e = qr_apply_q(st, w2, nc, nc, d.Y + mr, ldy, nc)) != cudaSuccess) return e;
   }
   {
     const long long total = (long long)m * chi + (long long)chi * n + chi;

@@ -6,7 +6,8 @@
 //
 // Y (column-major, ld = ldy) holds the work matrix X (mr x nc, mr >= nc) in
 // rows [0, mr) and the accumulated right rotations V (nc x nc) in rows
-// [mr, mr + nc).  The right factor is accumulated (not recovered afterwards
+// [vofs, vofs + nc) (vofs >= mr; the QR-preconditioned path runs on an
+// nc x nc X while V stays at the full problem's offset).  The right factor is accumulated (not recovered afterwards
 // by a GEMM with Theta) because the inverse-canonical form multiplies both
 // factors by V_j = 1/Lambda_j: each factor must be accurate
 // RELATIVE to sigma_k, which only the rotated columns/rows give.
@@ -36,7 +37,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ unsigned long long g_rj_prof[8];
+__device__ unsigned long long g_rj_prof[12];
 
 __device__ __forceinline__ void rj_rr_pair(int n, int round, int i, int& a, int& b) {
   const int m = n - 1;
@@ -124,10 +125,19 @@ __device__ __forceinline__ bool rj_params(double a, double c, double gr, double 
     spt = _t;                                \
   }
 
-template <int BW, int RX, int RV, int NT, bool CROSS>
-__device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 * BW], int s, double (*red)[BW * 4],
+// CTA barrier over the NT threads doing the steps: __syncthreads when they
+// are the whole CTA (NAMED = false), else named barrier 1 over NT threads.
+template <int NT, bool NAMED>
+__device__ __forceinline__ void rj_bar() {
+  if (NAMED) asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  else __syncthreads();
+}
+
+template <int BW, int RX, int RV, int NT, bool CROSS, bool NAMED = false>
+__device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[(RV > 0 ? RV : 1)][2 * BW], int s,
+                                        double (*red)[BW * 4],
                                         int lane, int wid, double tol2q, double& offacc, bool& rot, bool sprof,
-                                        bool fastp) {
+                                        bool fastp, double (*pout)[3] = nullptr) {
   constexpr int NV = 4 * BW;
   constexpr int H = (NV == 32) ? 5 : (NV == 16) ? 4 : 3;
   constexpr int SH = 5 - H;
@@ -152,6 +162,7 @@ __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 *
     val[4 * i + 2] = gr;
     val[4 * i + 3] = gi;
   }
+  if (sprof && val[0] + val[NV - 1] == -1.2345e300) g_rj_prof[11]++;
   RJ_T(4)
   // warp reduce-scatter: afterwards lane l holds the warp sum of value l >> SH
 #pragma unroll
@@ -171,7 +182,7 @@ __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 *
   for (int msk = (16 >> H); msk >= 1; msk >>= 1) t += __shfl_xor_sync(FULL, t, msk);
   if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = t;
   RJ_T(5)
-  __syncthreads();
+  rj_bar<NT, NAMED>();
   RJ_T(6)
   // every warp: CTA totals (tree over warps), rotation parameters of pair (lane % BW)
   double tot = 0.0;
@@ -190,11 +201,20 @@ __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 *
   const double c = __shfl_sync(FULL, tot, 4 * pi + 1);
   const double gr = __shfl_sync(FULL, tot, 4 * pi + 2);
   const double gi = __shfl_sync(FULL, tot, 4 * pi + 3);
+  if (sprof && a + c + gr + gi == -1.2345e300) g_rj_prof[11]++;  // timer waits for the totals
+  RJ_T(8)
   double cs = 1.0, sr = 0.0, si = 0.0;
   if (a > 0.0 && c > 0.0) {
     offacc = fmax(offacc, (gr * gr + gi * gi) / (a * c));
     rj_params(a, c, gr, gi, tol2q, cs, sr, si, fastp);
   }
+  if (pout != nullptr && wid == 0 && lane < BW) {
+    pout[lane][0] = cs;
+    pout[lane][1] = sr;
+    pout[lane][2] = si;
+  }
+  if (sprof && cs + sr + si == -1.2345e300) g_rj_prof[11]++;  // timer waits for the parameters
+  RJ_T(9)
 #pragma unroll
   for (int i = 0; i < BW; ++i) {
     int p, q;
@@ -218,12 +238,13 @@ __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[RV][2 *
       }
     }
   }
+  if (sprof && x[RX - 1][0].x + v[0][2 * BW - 1].y == -1.2345e300) g_rj_prof[11]++;
   RJ_T(7)
 }
 
 template <int BW, int RX, int RV, int NT, bool CLUSTER>
 __global__ void __launch_bounds__(NT, 1)
-    rjac_kernel(cplx* Y, long long ldy, int mr, int nc, int nb, int nbe, double tol, int max_sweeps, int full_rounds,
+    rjac_kernel(cplx* Y, long long ldy, int mr, int vofs, int nc, int nb, int nbe, double tol, int max_sweeps, int full_rounds,
                 double* offbuf, int* sweeps_out, int prof, int fastp) {
   constexpr int PC = 2 * BW, NV = 4 * BW, NW = NT / 32;
   __shared__ double red[2][NW][NV];
@@ -261,7 +282,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int k = 0; k < RV; ++k) {
           const int r = tid + k * NT;
-          v[k][j] = (valid && r < nc) ? __ldcg(src + mr + r) : cmk(0.0, 0.0);
+          v[k][j] = (valid && r < nc) ? __ldcg(src + vofs + r) : cmk(0.0, 0.0);
         }
       }
       mark(0);
@@ -296,7 +317,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int k = 0; k < RV; ++k) {
               const int r = tid + k * NT;
-              if (r < nc) __stcg(dst + mr + r, v[k][j]);
+              if (r < nc) __stcg(dst + vofs + r, v[k][j]);
             }
           }
         }
@@ -319,6 +340,164 @@ __global__ void __launch_bounds__(NT, 1)
   if (blockIdx.x == 0 && tid == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
 
+// ---------------------------------------------------------------------------
+// rjac2: the right factor V is NOT on the critical path.  Warps [0, NTX/32)
+// ("X warps") run the rounds on X only and publish every step's rotation
+// parameters in shared memory; warps [NTX/32, ...) ("V warps") replay the
+// PREVIOUS round's rotations on that round's V blocks (streamed from L2 in
+// chunks of rows) while the X warps work on the next round.  The V update of
+// round R completes before barrier R+1 and the blocks it touched are next
+// used by V warps after that barrier, so V sees every round in order.
+template <int BW, bool CROSS>
+__device__ __forceinline__ void rj_v_round(cplx (&v)[2 * BW], const double (*P)[BW][3]) {
+  constexpr int NS = CROSS ? BW : 2 * BW - 1;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int i = 0; i < BW; ++i) {
+      int p, q;
+      rj_pq<BW, CROSS>(s, i, p, q);
+      const double csi = P[s][i][0], sri = P[s][i][1], sii = P[s][i][2];
+      if (sri != 0.0 || sii != 0.0) {
+        const cplx u = v[p], w = v[q];
+        v[p] = cmk(fma(csi, u.x, -fma(sri, w.x, sii * w.y)), fma(csi, u.y, -fma(sri, w.y, -sii * w.x)));
+        v[q] = cmk(fma(csi, w.x, fma(sri, u.x, -sii * u.y)), fma(csi, w.y, fma(sri, u.y, sii * u.x)));
+      }
+    }
+  }
+}
+
+template <int BW, int RX, int NTX, int NTV, bool CLUSTER>
+__global__ void __launch_bounds__(NTX + NTV, 1)
+    rjac2_kernel(cplx* Y, long long ldy, int mr, int vofs, int nc, int nb, int nbe, double tol, int max_sweeps,
+                 double* offbuf, int* sweeps_out, int prof) {
+  constexpr int PC = 2 * BW, NV = 4 * BW, NWX = NTX / 32;
+  __shared__ double red[2][NWX][NV];
+  __shared__ double Ps[2][2 * BW - 1][BW][3];
+  __shared__ int s_blk[2][4];  // a, b, rotated, full round
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool xthr = tid < NTX;
+  const double tol2q = 0.0625 * tol * tol;
+  cplx x[RX][PC], dummy[1][PC];
+  int sweep = 0, buf = 0, R = 0;
+  unsigned long long pt = 0;
+  const bool pr = prof && blockIdx.x == 0 && tid == 0;
+  auto mark = [&](int i) {
+    if (pr) {
+      const unsigned long long t = clock64();
+      if (pt) g_rj_prof[i] += t - pt;
+      pt = t;
+    }
+  };
+  // V warps: replay round slot sb's rotations on its V blocks
+  auto apply_v = [&](int sb) {
+    if (!s_blk[sb][2]) return;
+    const int a = s_blk[sb][0], b = s_blk[sb][1];
+    const bool full = s_blk[sb][3] != 0;
+    long long off[PC];
+    bool ok[PC];
+#pragma unroll
+    for (int j = 0; j < PC; ++j) {
+      const int blk = j < BW ? a : b;
+      const int col = blk * BW + (j % BW);
+      ok[j] = blk < nb && col < nc;
+      off[j] = (long long)col * ldy + vofs;
+    }
+    for (int r = tid - NTX; r < nc; r += NTV) {
+      cplx v[PC];
+#pragma unroll
+      for (int j = 0; j < PC; ++j) v[j] = ok[j] ? __ldcg(Y + off[j] + r) : cmk(0.0, 0.0);
+      if (full) rj_v_round<BW, false>(v, Ps[sb]);
+      else rj_v_round<BW, true>(v, Ps[sb]);
+#pragma unroll
+      for (int j = 0; j < PC; ++j)
+        if (ok[j]) __stcg(Y + off[j] + r, v[j]);
+    }
+  };
+  mark(0);
+  for (; sweep < max_sweeps; ++sweep) {
+    double* off_cur = offbuf + (sweep % 3);
+    if (blockIdx.x == 0 && tid == 0) offbuf[(sweep + 1) % 3] = 0.0;
+    for (int round = 0; round < nbe - 1; ++round, ++R) {
+      if (xthr) {
+        int a, b;
+        rj_rr_pair(nbe, round, blockIdx.x, a, b);
+        const int sb = R & 1;
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+          const int blk = j < BW ? a : b;
+          const int col = blk * BW + (j % BW);
+          const bool valid = blk < nb && col < nc;
+          const cplx* src = Y + (long long)col * ldy;
+#pragma unroll
+          for (int k = 0; k < RX; ++k) {
+            const int r = tid + k * NTX;
+            x[k][j] = (valid && r < mr) ? __ldcg(src + r) : cmk(0.0, 0.0);
+          }
+        }
+        mark(0);
+        double offacc = 0.0;
+        bool rot = false;
+        if (round == 0) {
+#pragma unroll
+          for (int s = 0; s < PC - 1; ++s) {
+            rj_step<BW, RX, 0, NTX, false, true>(x, dummy, s, red[buf], lane, wid, tol2q, offacc, rot, false, false,
+                                                 Ps[sb][s]);
+            buf ^= 1;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < BW; ++s) {
+            rj_step<BW, RX, 0, NTX, true, true>(x, dummy, s, red[buf], lane, wid, tol2q, offacc, rot, false, false,
+                                                Ps[sb][s]);
+            buf ^= 1;
+          }
+        }
+        mark(1);
+        if (rot) {
+#pragma unroll
+          for (int j = 0; j < PC; ++j) {
+            const int blk = j < BW ? a : b;
+            const int col = blk * BW + (j % BW);
+            if (blk < nb && col < nc) {
+              cplx* dst = Y + (long long)col * ldy;
+#pragma unroll
+              for (int k = 0; k < RX; ++k) {
+                const int r = tid + k * NTX;
+                if (r < mr) __stcg(dst + r, x[k][j]);
+              }
+            }
+          }
+        }
+        if (tid == 0) {
+          s_blk[sb][0] = a;
+          s_blk[sb][1] = b;
+          s_blk[sb][2] = rot ? 1 : 0;
+          s_blk[sb][3] = round == 0 ? 1 : 0;
+        }
+        if (wid == 0) {
+          offacc = warp_max(offacc);
+          if (lane == 0 && offacc > 0.0) atomic_max_nonneg(off_cur, sqrt(offacc));
+        }
+        mark(2);
+      } else if (R > 0) {
+        apply_v((R - 1) & 1);
+      }
+      if (CLUSTER) {
+        cg::this_cluster().sync();
+      } else {
+        cg::this_grid().sync();
+      }
+      mark(3);
+    }
+    const double off = __ldcg(off_cur);
+    if (!(off > tol)) break;
+  }
+  // the last round's V update
+  if (!xthr && R > 0) apply_v((R - 1) & 1);
+  if (blockIdx.x == 0 && tid == 0) *sweeps_out = min(sweep + 1, max_sweeps);
+}
+
 struct RjVariant {
   void* fn;
   bool cluster;
@@ -329,18 +508,30 @@ RjVariant rj_pick(bool cluster) {
   return RjVariant{cluster ? (void*)rjac_kernel<BW, RX, RV, NT, true> : (void*)rjac_kernel<BW, RX, RV, NT, false>,
                    cluster};
 }
+template <int BW, int RX, int NTX, int NTV>
+RjVariant rj2_pick(bool cluster) {
+  return RjVariant{cluster ? (void*)rjac2_kernel<BW, RX, NTX, NTV, true> : (void*)rjac2_kernel<BW, RX, NTX, NTV, false>,
+                   cluster};
+}
 
-// variant table: block width, X rows and V rows per thread, threads per CTA
+// variant table.  kind 1 (rjac): X and V rows in registers, rx/rv rows per
+// thread, nt threads.  kind 2 (rjac2): X rows in registers (rx per X thread,
+// nt X threads), V streamed by ntv V threads.
 struct Row {
-  int bw, rx, rv, nt;
+  int kind, bw, rx, rv, nt, ntv;
 };
 constexpr Row kTab[] = {
-    {8, 1, 1, 256},  // 0: mr <= 256, nc <= 256: one cluster of <= 16 CTAs
-    {4, 1, 1, 256},  // 1
-    {4, 2, 1, 256},  // 2: mr <= 512, nc <= 256
-    {8, 2, 1, 256},  // 3
-    {4, 2, 2, 256},  // 4: mr <= 512, nc <= 512
-    {4, 2, 2, 128},  // 5: mr <= 256, nc <= 256, 4 warps
+    {1, 8, 1, 1, 256, 0},    // 0
+    {1, 4, 1, 1, 256, 0},    // 1
+    {1, 4, 2, 1, 256, 0},    // 2
+    {1, 8, 2, 1, 256, 0},    // 3
+    {1, 4, 2, 2, 256, 0},    // 4
+    {1, 4, 2, 2, 128, 0},    // 5
+    {2, 4, 2, 0, 128, 128},  // 6: X <= 256 rows
+    {2, 4, 4, 0, 128, 128},  // 7: X <= 512
+    {2, 4, 4, 0, 256, 64},   // 8: X <= 1024
+    {2, 8, 1, 0, 256, 128},  // 9: X <= 256, BW 8 (one cluster up to nc = 256)
+    {2, 4, 2, 0, 256, 128},  // 10: X <= 512
 };
 constexpr int kNTab = sizeof(kTab) / sizeof(kTab[0]);
 
@@ -351,12 +542,18 @@ RjVariant rj_variant(int row, bool cl) {
     case 2: return rj_pick<4, 2, 1, 256>(cl);
     case 3: return rj_pick<8, 2, 1, 256>(cl);
     case 4: return rj_pick<4, 2, 2, 256>(cl);
-    default: return rj_pick<4, 2, 2, 128>(cl);
+    case 5: return rj_pick<4, 2, 2, 128>(cl);
+    case 6: return rj2_pick<4, 2, 128, 128>(cl);
+    case 7: return rj2_pick<4, 4, 128, 128>(cl);
+    case 8: return rj2_pick<4, 4, 256, 64>(cl);
+    case 9: return rj2_pick<8, 1, 256, 128>(cl);
+    default: return rj2_pick<4, 2, 256, 128>(cl);
   }
 }
 
 bool rows_ok(int row, int mr, int nc) {
   const Row& r = kTab[row];
+  if (r.kind == 2) return mr <= r.rx * r.nt;
   return mr <= r.rx * r.nt && nc <= r.rv * r.nt;
 }
 
@@ -364,7 +561,8 @@ bool rows_ok(int row, int mr, int nc) {
 
 // Jacobi stage on d.Y = [X ; V] (column-major, ld = ldy).  Returns
 // cudaErrorNotSupported when no register-resident variant fits the shape.
-cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long long ldy, double tol, int* sweeps_dev) {
+cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int nc, long long ldy, double tol,
+                         int* sweeps_dev) {
   static int forced = -2, prof = 0, full_rounds = 0, fastp = 0;
   if (forced == -2) {
     const char* ev = std::getenv("TDVP_RJ_VARIANT");
@@ -380,12 +578,13 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long 
   int row = -1;
   if (forced >= 0 && forced < kNTab && rows_ok(forced, mr, nc)) row = forced;
   if (row < 0) {
-    const int prefer[] = {5, 2, 4};  // measured fastest first (microbench.py --svd, B200)
+    const int prefer[] = {6, 7, 8};  // measured fastest first (microbench.py --svd, B200)
     for (int r : prefer)
       if (rows_ok(r, mr, nc)) { row = r; break; }
   }
   if (row < 0) return cudaErrorNotSupported;
-  const int bw = kTab[row].bw, nt = kTab[row].nt;
+  const int bw = kTab[row].bw, kind = kTab[row].kind;
+  const int nt = kind == 2 ? kTab[row].nt + kTab[row].ntv : kTab[row].nt;
   const int nb = (nc + bw - 1) / bw;
   const int nbe = std::max(2, nb + (nb & 1));
   const int P = nbe / 2;
@@ -424,28 +623,31 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int nc, long 
   }
   if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
   if (prof) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[12] = {0};
     cudaMemcpyToSymbolAsync(g_rj_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
   int max_sweeps = 60;
   cplx* Yp = d.Y;
   double* offb = d.offmax;
-  void* args[] = {(void*)&Yp,  (void*)&ldy,        (void*)&mr,          (void*)&nc,   (void*)&nb,
-                  (void*)&nbe, (void*)&tol,        (void*)&max_sweeps,  (void*)&full_rounds,
-                  (void*)&offb, (void*)&sweeps_dev, (void*)&prof, (void*)&fastp};
+  void* args1[] = {(void*)&Yp,  (void*)&ldy,        (void*)&mr,  (void*)&vofs,  (void*)&nc,   (void*)&nb,
+                   (void*)&nbe, (void*)&tol,        (void*)&max_sweeps,  (void*)&full_rounds,
+                   (void*)&offb, (void*)&sweeps_dev, (void*)&prof, (void*)&fastp};
+  void* args2[] = {(void*)&Yp,  (void*)&ldy, (void*)&mr,         (void*)&vofs, (void*)&nc,         (void*)&nb,
+                   (void*)&nbe, (void*)&tol, (void*)&max_sweeps, (void*)&offb, (void*)&sweeps_dev, (void*)&prof};
+  void** args = kind == 2 ? args2 : args1;
   if (cluster) {
     if ((e = cudaLaunchKernelExC(&cfg, v.fn, args)) != cudaSuccess) return e;
   } else {
     if ((e = cudaLaunchCooperativeKernel(v.fn, dim3(P), dim3(nt), args, 0, st)) != cudaSuccess) return e;
   }
   if (prof) {
-    unsigned long long z[8];
+    unsigned long long z[12];
     cudaMemcpyFromSymbolAsync(z, g_rj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     std::fprintf(stderr,
                  "rjac prof mr=%d nc=%d row=%d bw=%d nt=%d P=%d cluster=%d cycles: load %llu steps %llu store %llu "
-                 "barrier %llu | dots %llu reduce %llu sync %llu params+apply %llu\n",
-                 mr, nc, row, bw, nt, P, (int)cluster, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[7]);
+                 "barrier %llu | dots %llu reduce %llu sync %llu gather %llu params %llu apply %llu\n",
+                 mr, nc, row, bw, nt, P, (int)cluster, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[8], z[9], z[7]);
   }
   return cudaGetLastError();
 }

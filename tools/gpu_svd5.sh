@@ -1,0 +1,13 @@
+#!/bin/bash
+python -m paper_1912_06127_b200.build > /tmp/build.log 2>&1 || { cat /tmp/build.log; exit 1; }
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "svd" 2>&1 | tail -3
+timeout 300 python tools/dbg_svd.py 2>&1 | grep -E "256x256|512x512|300x700|40x72|^1 5|^2 5"
+for pc in 0 2; do
+ for v in 6 9 10; do
+  echo "== precond $pc variant $v"
+  TDVP_SVD_PRECOND=$pc TDVP_RJ_VARIANT=$v timeout 120 python microbench.py --svd --svd-n 256 --svd-kind halfsmall 2>&1 | grep -E "kernel"
+  TDVP_SVD_PRECOND=$pc TDVP_RJ_VARIANT=$v timeout 120 python microbench.py --svd --svd-n 256 --svd-kind graded 2>&1 | grep -E "kernel"
+ done
+done
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_configs.py -x -q -k "config5 and 1" 2>&1 | grep -E "Error|assert|^E |passed|failed" | head -20
