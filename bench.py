@@ -264,6 +264,7 @@ def main():
     jac_fl = float(np.sum([s["svd_jac_flop"] for s in per]))
     sweeps = int(np.sum([s["svd_sweeps_total"] for s in per]))
     n_svd = int(np.sum([s["n_pair"] for s in per]))
+    n_warm = int(np.sum([s["svd_warm"] for s in per]))
     launches = int(np.sum([s["kernel_launches"] for s in per]))
     gemm_launches = int(np.sum([s["gemm_launches"] for s in per]))
 
@@ -306,7 +307,8 @@ def main():
                      "peak_source": FP64_ALU_PEAK_SRC,
                      "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
                      "share_of_step": jac_ms / step_ms if step_ms > 0 else None,
-                     "svd_calls": n_svd, "sweeps_per_svd": sweeps / n_svd if n_svd else None},
+                     "svd_calls": n_svd, "svd_warm_started": n_warm,
+                     "sweeps_per_svd": sweeps / n_svd if n_svd else None},
         "heff2": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + 2 sparse MPO stages)", "bound": "tensor",
                   "achieved": h2_tf, "peak": zpeak, "unit": "TFLOP/s",
                   "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,

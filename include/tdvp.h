@@ -67,6 +67,7 @@ typedef struct {
   double svd_jac_ms;      /* summed device time of the Jacobi kernel of every SVD (timing=1) */
   double svd_jac_flop;    /* its algorithmic real flops: sweeps * nc(nc-1)/2 * (16 mr + 24 (mr + nc)) */
   int svd_sweeps_total;   /* Jacobi sweeps summed over the SVDs of the last step */
+  int svd_warm;           /* SVDs of the last step warm-started from the previous visit of their bond */
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

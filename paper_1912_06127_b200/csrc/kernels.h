@@ -88,13 +88,24 @@ struct TruncParams {
   int chi_max;
   double eps, w_max, delta;
 };
+// Warm start of the Jacobi SVD from the previous visit of the same bond
+// (square matrices): X = Theta (orient 0) or Theta^H (orient 1); `pre` (nc x nc,
+// column-major, unitary to the Jacobi tolerance) is a basis of X's column
+// space from the previous SVD, X0 = X pre and V0 = pre; `store` receives this
+// SVD's left factor of X (columns X_c / sigma_c) when every sigma_c > 0.
+struct SvdWarm {
+  int orient;
+  const cplx* pre;
+  cplx* store;
+  int* store_ok;
+};
 // Full SVD by blocked one-sided Jacobi, then truncation (SURVEY O-7) and the split
 // Psi_L = U S, Lambda = S, V = 1/S, Psi_R = S W^dagger.  theta is m x n row-major.
 // Returns chi via *chi_out (host), discarded weight via *w_out (host).
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out = nullptr);
+                               float* jac_ms_out = nullptr, const SvdWarm* warm = nullptr);
 size_t svd_work_elems(int m, int n);
 // ------------------------------------------------------------------ qr.cu
 // Blocked Householder QR workspace (column-major A, m x n, m >= n).

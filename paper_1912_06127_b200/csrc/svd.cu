@@ -698,6 +698,7 @@ __global__ void svd_truncate_kernel(const double* __restrict__ sigma, int nc, in
   ires[0] = chi;
   ires[1] = chi_eps;
   ires[3] = r;
+  ires[5] = nz;
   dres[0] = w;
   dres[1] = s1;
 }
@@ -742,15 +743,38 @@ size_t svd_work_elems(int m, int n) {
   return (size_t)(mr + nc) * nc;
 }
 
+// store[c][r] = X[r][c] / sigma_c (column-major nc x nc): the left factor of X, whose
+// columns are orthonormal to the Jacobi tolerance (relative orthogonality)
+__global__ void svd_store_kernel(const cplx* __restrict__ Y, long long ldy, const double* __restrict__ sigma, int nr,
+                                 int nc, cplx* store) {
+  const long long total = (long long)nr * nc;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / nr), r = (int)(e - (long long)c * nr);
+    store[e] = cscale(Y[(long long)c * ldy + r], 1.0 / sigma[c]);
+  }
+}
+
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out) {
-  const bool transposed = m < n;
+                               float* jac_ms_out, const SvdWarm* warm) {
+  // warm start only for square matrices (orientation forced by the caller)
+  if (warm != nullptr && m != n) warm = nullptr;
+  const bool transposed = warm ? warm->orient == 1 : m < n;
   const int mr = std::max(m, n), nc = std::min(m, n);
   const long long ldy = (long long)mr + nc;
   cudaError_t e;
-  {
+  const bool use_warm = warm != nullptr && warm->pre != nullptr;
+  if (use_warm) {
+    // X0 = X P (X = Theta or Theta^H), V0 = P: the previous visit's basis of X's column space
+    const cplx one = cmk(1.0, 0.0), zero = cmk(0.0, 0.0);
+    if ((e = zgemm(st, OP_N, transposed ? OP_R : OP_T, nc, mr, nc, one, warm->pre, nc, theta, n, zero, d.Y, ldy)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaMemcpy2DAsync(d.Y + mr, (size_t)ldy * sizeof(cplx), warm->pre, (size_t)nc * sizeof(cplx),
+                               (size_t)nc * sizeof(cplx), nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return e;
+  } else {
     const long long total = ldy * nc;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
     svd_init_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, theta, m, n, mr, nc, transposed);
@@ -763,7 +787,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     const char* ev = std::getenv("TDVP_SVD_PRECOND");
     precond = ev ? std::atoi(ev) : 2;
   }
-  const bool use_qr = precond == 2 && nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
+  const bool use_qr = !use_warm && precond == 2 && nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
                       svd_qr_work_elems(m, n) <= d.qrbuf_elems;
   QrWork w1{}, w2{};
   int x_rows = mr;
@@ -907,6 +931,16 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     float ms = 0.f;
     if ((e = cudaEventElapsedTime(&ms, d.ev_jac[0], d.ev_jac[1])) != cudaSuccess) return e;
     *jac_ms_out = ms;
+  }
+  if (warm != nullptr && warm->store != nullptr) {
+    // keep this SVD's left factor of X for the next visit of the bond (all columns nonzero)
+    *warm->store_ok = 0;
+    if (d.h_ibuf[5] == nc) {
+      const long long total = (long long)mr * nc;
+      const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 4LL * g_num_sms));
+      svd_store_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, d.sigma, mr, nc, warm->store);
+      *warm->store_ok = 1;
+    }
   }
   if (use_qr && qr_cluster) {
     if ((e = qr_apply_refl(st, q1p, mr, w1.tau, mr, nc, d.Y, ldy, nc)) != cudaSuccess) return e;

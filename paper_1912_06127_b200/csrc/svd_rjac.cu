@@ -341,6 +341,187 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Norm-tracked step (rjac2 MODE 1).  The column norms a_j = |x_j|^2 are
+// reduced once per round and then updated by every rotation (a_p' = a_p - d,
+// a_q' = a_q + d with d = t |g|, exact for the zeroing rotation), so a step
+// reduces only the BW inner products g = x_p^H x_q.  A norm that loses more
+// than 99% in one rotation is marked stale: its pairs are skipped for the rest
+// of the round and the sweep is not allowed to converge (the next round
+// recomputes the norms from the data).  The rotation angle is formed in FP32
+// from zeta = (c - a) / (2|g|); cs = 1/sqrt(1 + t^2) and sn = cs t g/|g| are
+// FP64, so the rotation is unitary to FP64 rounding whatever t is (an angle
+// off by ~1e-7 only leaves a ~1e-7 residual for the next sweep).
+__device__ __forceinline__ void rj2_params(double a, double c, double gr, double gi, double& cs, double& sr,
+                                           double& si, double& dnorm) {
+  const double ag2 = gr * gr + gi * gi;
+  const double rg = rj_rsqrt(ag2);  // 1/|g|
+  const double zeta = 0.5 * (c - a) * rg;
+  double t;
+  if (fabs(zeta) < 1e15) {
+    const float z = (float)zeta;
+    const float az = fabsf(z);
+    const float tf = copysignf(1.0f, z) / (az + sqrtf(fmaf(z, z, 1.0f)));
+    t = (double)tf;
+  } else {
+    t = 0.5 / zeta;
+  }
+  cs = rj_rsqrt(fma(t, t, 1.0));
+  const double f = cs * t * rg;
+  sr = f * gr;
+  si = f * gi;
+  dnorm = t * ag2 * rg;  // t |g|
+}
+
+template <int BW, int RX, int NT, bool CROSS>
+__device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 * BW], unsigned& stale, int s,
+                                         double (*red)[BW * 4], int lane, int wid, double tol2q, double tolc2,
+                                         bool& notconv, bool& rot, double (*pout)[3]) {
+  constexpr int NV = 2 * BW;
+  constexpr int H = (NV == 16) ? 4 : (NV == 8) ? 3 : 2;
+  constexpr int SH = 5 - H;
+  constexpr int NW = NT / 32;
+  double val[NV];
+#pragma unroll
+  for (int i = 0; i < BW; ++i) {
+    int p, q;
+    rj_pq<BW, CROSS>(s, i, p, q);
+    double gr = 0.0, gi = 0.0;
+#pragma unroll
+    for (int k = 0; k < RX; ++k) {
+      const cplx u = x[k][p], w = x[k][q];
+      gr = fma(u.x, w.x, fma(u.y, w.y, gr));
+      gi = fma(u.x, w.y, fma(-u.y, w.x, gi));
+    }
+    val[2 * i] = gr;
+    val[2 * i + 1] = gi;
+  }
+#pragma unroll
+  for (int lev = 0; lev < H; ++lev) {
+    const int msk = 16 >> lev;
+    const int h = NV >> (lev + 1);
+    const bool up = (lane & msk) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? val[j] : val[j + h];
+      const double keep = up ? val[j + h] : val[j];
+      val[j] = keep + __shfl_xor_sync(FULL, send, msk);
+    }
+  }
+  double tt = val[0];
+#pragma unroll
+  for (int msk = (16 >> H); msk >= 1; msk >>= 1) tt += __shfl_xor_sync(FULL, tt, msk);
+  if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = tt;
+  rj_bar<NT, true>();
+  double tot = 0.0;
+  if (lane < NV) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tot += red[w][lane];
+  }
+  // lane pi (mod BW) forms the rotation of pair pi
+  const int pi = lane % BW;
+  const double gr = __shfl_sync(FULL, tot, 2 * pi);
+  const double gi = __shfl_sync(FULL, tot, 2 * pi + 1);
+  double a = 0.0, c = 0.0;
+  int pidx = 0, qidx = 0;
+#pragma unroll
+  for (int i = 0; i < BW; ++i) {
+    int p, q;
+    rj_pq<BW, CROSS>(s, i, p, q);
+    if (pi == i) {
+      a = nrm[p];
+      c = nrm[q];
+      pidx = p;
+      qidx = q;
+    }
+  }
+  double cs = 1.0, sr = 0.0, si = 0.0, dn = 0.0;
+  int flag = 0;  // 1: not converged, 2: a norm went stale
+  const bool st = ((stale >> pidx) | (stale >> qidx)) & 1u;
+  if (a > 0.0 && c > 0.0) {
+    const double ag2 = gr * gr + gi * gi;
+    if (st) {
+      flag = 1;
+    } else if (ag2 > 1e-300 && ag2 > tol2q * a * c) {
+      rj2_params(a, c, gr, gi, cs, sr, si, dn);
+      if (ag2 > tolc2 * a * c) flag = 1;
+      if (a - dn < 0.01 * a || c + dn < 0.01 * c) flag |= 2;
+    } else if (ag2 > tolc2 * a * c) {
+      flag = 1;
+    }
+  }
+  if (pout != nullptr && wid == 0 && lane < BW) {
+    pout[lane][0] = cs;
+    pout[lane][1] = sr;
+    pout[lane][2] = si;
+  }
+#pragma unroll
+  for (int i = 0; i < BW; ++i) {
+    int p, q;
+    rj_pq<BW, CROSS>(s, i, p, q);
+    const double csi = __shfl_sync(FULL, cs, i);
+    const double sri = __shfl_sync(FULL, sr, i);
+    const double sii = __shfl_sync(FULL, si, i);
+    const double dni = __shfl_sync(FULL, dn, i);
+    const int fl = __shfl_sync(FULL, flag, i);
+    if (fl & 1) notconv = true;
+    if (sri != 0.0 || sii != 0.0) {  // warp-uniform
+      rot = true;
+#pragma unroll
+      for (int k = 0; k < RX; ++k) {
+        const cplx u = x[k][p], w = x[k][q];
+        x[k][p] = cmk(fma(csi, u.x, -fma(sri, w.x, sii * w.y)), fma(csi, u.y, -fma(sri, w.y, -sii * w.x)));
+        x[k][q] = cmk(fma(csi, w.x, fma(sri, u.x, -sii * u.y)), fma(csi, w.y, fma(sri, u.y, sii * u.x)));
+      }
+      nrm[p] -= dni;
+      nrm[q] += dni;
+      if (fl & 2) stale |= (1u << p) | (1u << q);
+    }
+  }
+}
+
+// column norms of the 2BW register columns, reduced over the NT X threads
+template <int BW, int RX, int NT>
+__device__ __forceinline__ void rj2_norms(const cplx (&x)[RX][2 * BW], double (&nrm)[2 * BW], double (*red)[BW * 4],
+                                          int lane, int wid) {
+  constexpr int NV = 2 * BW;
+  constexpr int H = (NV == 16) ? 4 : (NV == 8) ? 3 : 2;
+  constexpr int SH = 5 - H;
+  constexpr int NW = NT / 32;
+  double val[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < RX; ++k) t = fma(x[k][j].x, x[k][j].x, fma(x[k][j].y, x[k][j].y, t));
+    val[j] = t;
+  }
+#pragma unroll
+  for (int lev = 0; lev < H; ++lev) {
+    const int msk = 16 >> lev;
+    const int h = NV >> (lev + 1);
+    const bool up = (lane & msk) != 0;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const double send = up ? val[j] : val[j + h];
+      const double keep = up ? val[j + h] : val[j];
+      val[j] = keep + __shfl_xor_sync(FULL, send, msk);
+    }
+  }
+  double tt = val[0];
+#pragma unroll
+  for (int msk = (16 >> H); msk >= 1; msk >>= 1) tt += __shfl_xor_sync(FULL, tt, msk);
+  if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = tt;
+  rj_bar<NT, true>();
+  double tot = 0.0;
+  if (lane < NV) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tot += red[w][lane];
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) nrm[j] = __shfl_sync(FULL, tot, j);
+}
+
+// ---------------------------------------------------------------------------
 // rjac2: the right factor V is NOT on the critical path.  Warps [0, NTX/32)
 // ("X warps") run the rounds on X only and publish every step's rotation
 // parameters in shared memory; warps [NTX/32, ...) ("V warps") replay the
@@ -367,7 +548,7 @@ __device__ __forceinline__ void rj_v_round(cplx (&v)[2 * BW], const double (*P)[
   }
 }
 
-template <int BW, int RX, int NTX, int NTV, bool CLUSTER>
+template <int BW, int RX, int NTX, int NTV, bool CLUSTER, int MODE>
 __global__ void __launch_bounds__(NTX + NTV, 1)
     rjac2_kernel(cplx* Y, long long ldy, int mr, int vofs, int nc, int nb, int nbe, double tol, int max_sweeps,
                  double* offbuf, int* sweeps_out, int prof) {
@@ -438,7 +619,29 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
         mark(0);
         double offacc = 0.0;
         bool rot = false;
-        if (round == 0) {
+        if (MODE == 1) {
+          double nrm[PC];
+          unsigned stale = 0u;
+          bool notconv = false;
+          rj2_norms<BW, RX, NTX>(x, nrm, red[buf], lane, wid);
+          buf ^= 1;
+          if (round == 0) {
+#pragma unroll
+            for (int s = 0; s < PC - 1; ++s) {
+              rj2_step<BW, RX, NTX, false>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
+                                           Ps[sb][s]);
+              buf ^= 1;
+            }
+          } else {
+#pragma unroll
+            for (int s = 0; s < BW; ++s) {
+              rj2_step<BW, RX, NTX, true>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
+                                          Ps[sb][s]);
+              buf ^= 1;
+            }
+          }
+          offacc = notconv ? 1.0 : 0.0;
+        } else if (round == 0) {
 #pragma unroll
           for (int s = 0; s < PC - 1; ++s) {
             rj_step<BW, RX, 0, NTX, false, true>(x, dummy, s, red[buf], lane, wid, tol2q, offacc, rot, false, false,
@@ -508,9 +711,10 @@ RjVariant rj_pick(bool cluster) {
   return RjVariant{cluster ? (void*)rjac_kernel<BW, RX, RV, NT, true> : (void*)rjac_kernel<BW, RX, RV, NT, false>,
                    cluster};
 }
-template <int BW, int RX, int NTX, int NTV>
+template <int BW, int RX, int NTX, int NTV, int MODE = 1>
 RjVariant rj2_pick(bool cluster) {
-  return RjVariant{cluster ? (void*)rjac2_kernel<BW, RX, NTX, NTV, true> : (void*)rjac2_kernel<BW, RX, NTX, NTV, false>,
+  return RjVariant{cluster ? (void*)rjac2_kernel<BW, RX, NTX, NTV, true, MODE>
+                           : (void*)rjac2_kernel<BW, RX, NTX, NTV, false, MODE>,
                    cluster};
 }
 
@@ -532,6 +736,9 @@ constexpr Row kTab[] = {
     {2, 4, 4, 0, 256, 64},   // 8: X <= 1024
     {2, 8, 1, 0, 256, 128},  // 9: X <= 256, BW 8 (one cluster up to nc = 256)
     {2, 4, 2, 0, 256, 128},  // 10: X <= 512
+    {2, 4, 2, 0, 128, 128},  // 11: as 6 with exact (non-tracked) norms and FP64 angles
+    {2, 8, 2, 0, 128, 128},  // 12: X <= 256, BW 8: one cluster up to nc = 256
+    {2, 8, 2, 0, 128, 128},  // 13: as 12, exact norms
 };
 constexpr int kNTab = sizeof(kTab) / sizeof(kTab[0]);
 
@@ -547,7 +754,10 @@ RjVariant rj_variant(int row, bool cl) {
     case 7: return rj2_pick<4, 4, 128, 128>(cl);
     case 8: return rj2_pick<4, 4, 256, 64>(cl);
     case 9: return rj2_pick<8, 1, 256, 128>(cl);
-    default: return rj2_pick<4, 2, 256, 128>(cl);
+    case 10: return rj2_pick<4, 2, 256, 128>(cl);
+    case 11: return rj2_pick<4, 2, 128, 128, 0>(cl);
+    case 12: return rj2_pick<8, 2, 128, 128>(cl);
+    default: return rj2_pick<8, 2, 128, 128, 0>(cl);
   }
 }
 

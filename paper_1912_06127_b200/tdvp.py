@@ -35,7 +35,8 @@ class tdvp_stats(C.Structure):
                 ("step_ms", C.c_double), ("heff2_ms", C.c_double), ("heff2_flop", C.c_double),
                 ("heff2_calls", C.c_int), ("heff1_ms", C.c_double), ("heff1_flop", C.c_double),
                 ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong),
-                ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int)]
+                ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int),
+                ("svd_warm", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
