@@ -15,6 +15,8 @@
 // Conventions follow LAPACK zgeqr2/zlarfg/zlarft: H = I - tau v v^H,
 // R = H_n^H ... H_1^H A, beta = -sign(Re alpha) ||x||.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "kernels.h"
@@ -329,6 +331,207 @@ __global__ void __launch_bounds__(NT, 1)
   cluster.sync();  // keep shared memory alive until every CTA finished its DSMEM reads
 }
 
+// Look-ahead variant (default).  CTA c owns columns [c*cw, (c+1)*cw).  No
+// cluster-wide barrier per reflector: reflectors are published point to point.
+//  phase 1: CTA c applies the reflectors 0 .. c*cw-1 of the earlier CTAs to its
+//           columns as they appear: it spins on a counter in its own shared
+//           memory that the producer raises with a cluster-scope release store,
+//           then copies v_k and tau_k through DSMEM (batches of up to NB).
+//  phase 2: CTA c factors its band: warp 0 (the panel warp) forms v_k from
+//           column k, publishes it, and applies it to column k+1 (look-ahead)
+//           while warps 1.. apply it to the band's remaining columns; one named
+//           barrier per reflector.
+// flag in CTA `rank`'s shared memory (shared::cluster window), release/acquire at cluster scope
+__device__ __forceinline__ void st_release_cluster_rank(const unsigned* local, unsigned rank, unsigned v) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(local);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cluster_local(const unsigned* local) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(local);
+  unsigned v;
+  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(la) : "memory");
+  return v;
+}
+
+__device__ unsigned long long g_qr_prof[16][4];
+__device__ unsigned long long g_qr_ph[8];
+__constant__ int qr_ph_cta = 15;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+#ifndef QR_PUB
+#define QR_PUB 4
+#endif
+template <int NT, int NB>
+__global__ void __launch_bounds__(NT, 1)
+    qrc3_factor_kernel(cplx* A, long long lda, int m, int n, int cw, cplx* tau, cplx* RH, long long ldrh, int rh_rows) {
+  namespace cgq = cooperative_groups;
+  cgq::cluster_group cluster = cgq::this_cluster();
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char qc_sm[];
+  cplx* Aloc = reinterpret_cast<cplx*>(qc_sm);  // cw columns x m rows (own band)
+  cplx* vb = Aloc + (long long)cw * m;          // NB received reflectors x m rows
+  cplx* s_tau = vb + (long long)NB * m;         // [cw] published taus of the own band
+  __shared__ cplx s_vt[NB];
+  __shared__ unsigned s_npub;  // reflectors published to this CTA (written remotely)
+  __shared__ int s_nav;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int crank = (int)cluster.block_rank(), ncta = (int)cluster.num_blocks();
+  const int c0 = crank * cw, c1 = min(n, c0 + cw), ncl = max(0, c1 - c0);
+  for (int e = tid; e < ncl * m; e += NT) {
+    const int j = e / m, r = e - j * m;
+    Aloc[e] = A[(long long)(c0 + j) * lda + r];
+  }
+  if (tid == 0) s_npub = 0u;
+  cluster.sync();  // every counter initialised before any remote release
+  if (tid == 0 && crank < 16) g_qr_prof[crank][0] = gtime();
+  int nbatches = 0;
+  // ---------------- phase 1: apply the earlier CTAs' reflectors 0 .. c0-1
+  for (int k = 0; k < c0;) {
+    if (tid == 0) {
+      unsigned a;
+      while ((a = ld_acquire_cluster_local(&s_npub)) <= (unsigned)k) __nanosleep(64);
+      s_nav = min((int)a, min(c0, k + NB)) - k;  // batch of available reflectors
+    }
+    __syncthreads();
+    const int nb = s_nav;
+    // copy v_{k..k+nb-1} (rows >= k) and their taus from the owners
+    for (int e = tid; e < nb * (m - k); e += NT) {
+      const int b = e / (m - k), r = k + (e - b * (m - k));
+      const int kk = k + b;
+      vb[(long long)b * m + r] =
+          (r < kk) ? cmk(0.0, 0.0) : (r == kk) ? cmk(1.0, 0.0) : __ldcg(A + (long long)kk * lda + r);
+    }
+    if (tid < nb) s_vt[tid] = __ldcg(tau + k + tid);
+    __syncthreads();
+    for (int jl = wid; jl < ncl; jl += NW) {
+      cplx* aj = Aloc + (long long)jl * m;
+      for (int b = 0; b < nb; ++b) {
+        const cplx ct = cconj(s_vt[b]);
+        if (ct.x == 0.0 && ct.y == 0.0) continue;
+        const int kk = k + b;
+        const cplx* v = vb + (long long)b * m;
+        double dr = 0.0, di = 0.0;
+        for (int r = kk + lane; r < m; r += 32) {
+          const cplx x = cdotc(v[r], aj[r]);
+          dr += x.x;
+          di += x.y;
+        }
+        dr = warp_sum(dr);
+        di = warp_sum(di);
+        const cplx f = cmul(ct, cmk(dr, di));
+        for (int r = kk + lane; r < m; r += 32) aj[r] = csub(aj[r], cmul(v[r], f));
+      }
+    }
+    __syncthreads();  // vb reused by the next batch
+    k += nb;
+    ++nbatches;
+  }
+  if (tid == 0 && crank < 16) g_qr_prof[crank][1] = gtime();
+  // ---------------- phase 2: factor the own band with look-ahead
+  for (int i = 0; i < ncl; ++i) {
+    const int k = c0 + i;
+    cplx* col = Aloc + (long long)i * m;
+    const bool ph = (crank == qr_ph_cta && tid == 0);
+    unsigned long long pt0 = ph ? clock64() : 0ull;
+#define QPH(i) if (ph) { const unsigned long long _t = clock64(); g_qr_ph[i] += _t - pt0; pt0 = _t; }
+    if (wid == 0) {
+      double xn2 = 0.0;
+      for (int r = k + 1 + lane; r < m; r += 32) xn2 += cabs2(col[r]);
+      xn2 = warp_sum(xn2);
+      if (ph && xn2 == -1.0) g_qr_ph[7]++;
+      QPH(0)
+      const double ar = col[k].x, ai = col[k].y;
+      cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
+      double beta = ar;
+      const bool refl = !(xn2 == 0.0 && ai == 0.0);
+      if (refl) {
+        beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        const double ib = 1.0 / beta;
+        t_i = cmk((beta - ar) * ib, -ai * ib);
+        const double dr = ar - beta, di = ai;
+        const double iden = 1.0 / (dr * dr + di * di);
+        scale = cmk(dr * iden, -di * iden);
+        if (ph && scale.x == -1.0) g_qr_ph[7]++;
+        QPH(1)
+        for (int r = k + 1 + lane; r < m; r += 32) col[r] = cmul(col[r], scale);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        col[k] = cmk(beta, 0.0);
+        s_tau[i] = t_i;
+        __stcg(tau + k, t_i);
+      }
+      // the consumers read the reflector from L2, not through DSMEM: a
+      // producer's shared-memory port would otherwise serve every later CTA
+      for (int r = k + 1 + lane; r < m; r += 32) __stcg(A + (long long)k * lda + r, col[r]);
+      __syncwarp();
+      // publish v_k to every later CTA (release orders the warp's writes
+      // above); inside the band only every QR_PUB-th reflector, the band's
+      // last one always
+      if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl)
+        for (int c = crank + 1 + lane; c < ncta; c += 32)
+          st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
+      QPH(2)
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+    QPH(3)
+    const cplx ct = cconj(s_tau[i]);
+    if (ct.x != 0.0 || ct.y != 0.0) {
+      // warp 0: column i+1 (the next pivot); warps 1..: columns i+2, ...
+      const int jstart = (wid == 0) ? i + 1 : i + 1 + wid;
+      const int jstep = (wid == 0) ? ncl : NW - 1;
+      for (int jl = jstart; jl < ncl; jl += jstep) {
+        cplx* aj = Aloc + (long long)jl * m;
+        double dr = 0.0, di = 0.0;
+        for (int r = k + lane; r < m; r += 32) {
+          const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
+          const cplx x = cdotc(v, aj[r]);
+          dr += x.x;
+          di += x.y;
+        }
+        dr = warp_sum(dr);
+        di = warp_sum(di);
+        const cplx f = cmul(ct, cmk(dr, di));
+        for (int r = k + lane; r < m; r += 32) {
+          const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
+          aj[r] = csub(aj[r], cmul(v, f));
+        }
+        if (wid == 0) {
+          if (ph && aj[m - 1].x == -1.2345) g_qr_ph[7]++;
+          break;
+        }
+      }
+    }
+    QPH(4)
+    // next iteration: warp 0 reads column i+1 (updated by itself); the workers'
+    // updates of column i+2 are ordered before warp 0 touches it by the next
+    // bar.sync 2
+  }
+  __syncthreads();
+  if (tid == 0 && crank < 16) {
+    g_qr_prof[crank][2] = gtime();
+    g_qr_prof[crank][3] = nbatches;
+  }
+  for (int e = tid; e < ncl * m; e += NT) {
+    const int j = e / m, r = e - j * m;
+    A[(long long)(c0 + j) * lda + r] = Aloc[e];
+  }
+  if (RH != nullptr) {
+    for (int e = tid; e < ncl * rh_rows; e += NT) {
+      const int j = e / rh_rows, r = e - j * rh_rows;
+      const int c = c0 + j;
+      if (r <= c && r < n) RH[(long long)r * ldrh + c] = cconj(Aloc[(long long)j * m + r]);
+    }
+  }
+  cluster.sync();  // keep shared memory alive until every CTA finished its DSMEM reads
+}
+
 // C (m x nc, column-major, ld ldc) <- H_0 H_1 ... H_{n-1} C with the
 // reflectors of qrc_factor_kernel / zgeqr2 (v_k = [0..0, 1, A[k+1:, k]]).
 // One CTA per 8 columns of C held in registers (RPT rows per thread); per
@@ -351,15 +554,31 @@ __global__ void __launch_bounds__(NT)
       c[q][j] = (r < m && cb0 + j < nc) ? C[(long long)(cb0 + j) * ldc + r] : cmk(0.0, 0.0);
   }
   int buf = 0;
+  // software prefetch of the next reflector (L2 latency off the chain)
+  cplx vn[RPT];
+  cplx tn = (n > 0) ? tau[n - 1] : cmk(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = tid + q * NT, k = n - 1;
+    vn[q] = (k >= 0 && r > k && r < m) ? __ldg(A + (long long)k * lda + r) : cmk(0.0, 0.0);
+  }
   for (int k = n - 1; k >= 0; --k) {
-    const cplx tk = tau[k];
-    if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform across the CTA
+    const cplx tk = tn;
     cplx v[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int r = tid + q * NT;
-      v[q] = (r == k) ? cmk(1.0, 0.0) : (r > k && r < m) ? __ldg(A + (long long)k * lda + r) : cmk(0.0, 0.0);
+      v[q] = (r == k) ? cmk(1.0, 0.0) : vn[q];
     }
+    if (k > 0) {
+      tn = tau[k - 1];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * NT;
+        vn[q] = (r > k - 1 && r < m) ? __ldg(A + (long long)(k - 1) * lda + r) : cmk(0.0, 0.0);
+      }
+    }
+    if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform across the CTA
     double val[NV];
 #pragma unroll
     for (int j = 0; j < CB; ++j) {
@@ -421,15 +640,18 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   const int C = std::min(16, n);
   const int cw = (n + C - 1) / C;
   const int Cu = (n + cw - 1) / cw;
-  const size_t smem = ((size_t)cw * m + m) * sizeof(cplx);
+  if (cw > 32) return cudaErrorNotSupported;
+  constexpr int NB = 8;
+  // >= 116 KB so that the 16 CTAs land on 16 different SMs (2 per SM halves the producer's pace)
+  const size_t smem = std::max<size_t>(((size_t)cw * m + (size_t)NB * m + cw) * sizeof(cplx), 116 * 1024);
   if (smem > 200 * 1024) return cudaErrorNotSupported;
   cudaError_t e;
   static bool attr = false;
   if (!attr) {
-    if ((e = cudaFuncSetAttribute(qrc_factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) !=
-        cudaSuccess)
+    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024)) != cudaSuccess)
       return e;
-    if ((e = cudaFuncSetAttribute(qrc_factor_kernel<256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
         cudaSuccess)
       return e;
     attr = true;
@@ -452,7 +674,26 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
         cudaSuccess)
       return e;
   }
-  return cudaLaunchKernelEx(&cfg, qrc_factor_kernel<256>, A, lda, m, n, cw, tau, RH, ldrh, rh_rows);
+  e = cudaLaunchKernelEx(&cfg, qrc3_factor_kernel<256, NB>, A, lda, m, n, cw, tau, RH, ldrh, rh_rows);
+  static int prof = -1;
+  if (prof < 0) prof = std::getenv("TDVP_QR_PROF") ? 1 : 0;
+  if (prof && e == cudaSuccess) {
+    unsigned long long z[16][4];
+    cudaMemcpyFromSymbolAsync(z, g_qr_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long ph[8];
+    cudaMemcpyFromSymbolAsync(ph, g_qr_ph, sizeof(ph), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr, "qrc3 cta1 phase-2 cycles: norm %llu params %llu scale+publish %llu bar %llu lookahead %llu\n",
+                 ph[0], ph[1], ph[2], ph[3], ph[4]);
+    unsigned long long zz[8] = {0};
+    cudaMemcpyToSymbolAsync(g_qr_ph, zz, sizeof(zz), 0, cudaMemcpyHostToDevice, st);
+    std::fprintf(stderr, "qrc3 m=%d n=%d cw=%d ctas=%d (us from start: phase1 end / phase2 end / batches)\n", m, n, cw, Cu);
+    for (int c = 0; c < Cu && c < 16; ++c)
+      std::fprintf(stderr, "  cta %2d: %8.1f %8.1f %4llu\n", c, (z[c][1] - z[0][0]) * 1e-3, (z[c][2] - z[0][0]) * 1e-3,
+                   z[c][3]);
+  }
+  return e;
 }
 
 cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,
