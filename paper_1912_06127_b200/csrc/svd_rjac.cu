@@ -128,8 +128,8 @@ __device__ __forceinline__ bool rj_params(double a, double c, double gr, double 
 // CTA barrier over the NT threads doing the steps: __syncthreads when they
 // are the whole CTA (NAMED = false), else named barrier 1 over NT threads.
 template <int NT, bool NAMED>
-__device__ __forceinline__ void rj_bar() {
-  if (NAMED) asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+__device__ __forceinline__ void rj_bar(int barid = 1) {
+  if (NAMED) asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NT) : "memory");
   else __syncthreads();
 }
 
@@ -137,7 +137,7 @@ template <int BW, int RX, int RV, int NT, bool CROSS, bool NAMED = false>
 __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[(RV > 0 ? RV : 1)][2 * BW], int s,
                                         double (*red)[BW * 4],
                                         int lane, int wid, double tol2q, double& offacc, bool& rot, bool sprof,
-                                        bool fastp, double (*pout)[3] = nullptr) {
+                                        bool fastp, double (*pout)[3] = nullptr, int barid = 1) {
   constexpr int NV = 4 * BW;
   constexpr int H = (NV == 32) ? 5 : (NV == 16) ? 4 : 3;
   constexpr int SH = 5 - H;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void rj_step(cplx (&x)[RX][2 * BW], cplx (&v)[(RV > 0
   for (int msk = (16 >> H); msk >= 1; msk >>= 1) t += __shfl_xor_sync(FULL, t, msk);
   if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = t;
   RJ_T(5)
-  rj_bar<NT, NAMED>();
+  rj_bar<NT, NAMED>(barid);
   RJ_T(6)
   // every warp: CTA totals (tree over warps), rotation parameters of pair (lane % BW)
   double tot = 0.0;
@@ -375,7 +375,7 @@ __device__ __forceinline__ void rj2_params(double a, double c, double gr, double
 template <int BW, int RX, int NT, bool CROSS>
 __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 * BW], unsigned& stale, int s,
                                          double (*red)[BW * 4], int lane, int wid, double tol2q, double tolc2,
-                                         bool& notconv, bool& rot, double (*pout)[3]) {
+                                         bool& notconv, bool& rot, double (*pout)[3], int barid = 1) {
   constexpr int NV = 2 * BW;
   constexpr int H = (NV == 16) ? 4 : (NV == 8) ? 3 : 2;
   constexpr int SH = 5 - H;
@@ -411,7 +411,7 @@ __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 
 #pragma unroll
   for (int msk = (16 >> H); msk >= 1; msk >>= 1) tt += __shfl_xor_sync(FULL, tt, msk);
   if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = tt;
-  rj_bar<NT, true>();
+  rj_bar<NT, true>(barid);
   double tot = 0.0;
   if (lane < NV) {
 #pragma unroll
@@ -482,7 +482,7 @@ __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 
 // column norms of the 2BW register columns, reduced over the NT X threads
 template <int BW, int RX, int NT>
 __device__ __forceinline__ void rj2_norms(const cplx (&x)[RX][2 * BW], double (&nrm)[2 * BW], double (*red)[BW * 4],
-                                          int lane, int wid) {
+                                          int lane, int wid, int barid = 1) {
   constexpr int NV = 2 * BW;
   constexpr int H = (NV == 16) ? 4 : (NV == 8) ? 3 : 2;
   constexpr int SH = 5 - H;
@@ -511,7 +511,7 @@ __device__ __forceinline__ void rj2_norms(const cplx (&x)[RX][2 * BW], double (&
 #pragma unroll
   for (int msk = (16 >> H); msk >= 1; msk >>= 1) tt += __shfl_xor_sync(FULL, tt, msk);
   if ((lane & ((1 << SH) - 1)) == 0) red[wid][lane >> SH] = tt;
-  rj_bar<NT, true>();
+  rj_bar<NT, true>(barid);
   double tot = 0.0;
   if (lane < NV) {
 #pragma unroll
@@ -548,21 +548,32 @@ __device__ __forceinline__ void rj_v_round(cplx (&v)[2 * BW], const double (*P)[
   }
 }
 
-template <int BW, int RX, int NTX, int NTV, bool CLUSTER, int MODE>
-__global__ void __launch_bounds__(NTX + NTV, 1)
+template <int BW, int RX, int NTX, int NTV, bool CLUSTER, int MODE, int G>
+__global__ void __launch_bounds__(G * NTX + NTV, 1)
     rjac2_kernel(cplx* Y, long long ldy, int mr, int vofs, int nc, int nb, int nbe, double tol, int max_sweeps,
                  double* offbuf, int* sweeps_out, int prof) {
+  // G block pairs per CTA ("pair groups" of NTX X threads each, named barrier
+  // 1 + g), one set of NTV V threads serving all groups
   constexpr int PC = 2 * BW, NV = 4 * BW, NWX = NTX / 32;
-  __shared__ double red[2][NWX][NV];
-  __shared__ double Ps[2][2 * BW - 1][BW][3];
-  __shared__ int s_blk[2][4];  // a, b, rotated, full round
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool xthr = tid < NTX;
+  __shared__ double red_all[G][2][NWX][NV];
+  __shared__ double Ps_all[G][2][2 * BW - 1][BW][3];
+  __shared__ int s_blk_all[G][2][4];  // a, b, rotated, full round
+  const int tid0 = threadIdx.x, lane = tid0 & 31;
+  const bool xthr = tid0 < G * NTX;
+  const int grp = xthr ? tid0 / NTX : 0;
+  const int tid = xthr ? tid0 - grp * NTX : tid0 - (G - 1) * NTX;  // V threads: tid - NTX >= 0
+  const int wid = tid >> 5;
+  const int barid = 1 + grp;
+  const int pair = blockIdx.x * G + grp;
+  const int npairs = nbe / 2;
+  auto& red = red_all[grp];
+  auto& Ps = Ps_all[grp];
+  auto& s_blk = s_blk_all[grp];
   const double tol2q = 0.0625 * tol * tol;
   cplx x[RX][PC], dummy[1][PC];
   int sweep = 0, buf = 0, R = 0;
   unsigned long long pt = 0;
-  const bool pr = prof && blockIdx.x == 0 && tid == 0;
+  const bool pr = prof && blockIdx.x == 0 && tid0 == 0;
   auto mark = [&](int i) {
     if (pr) {
       const unsigned long long t = clock64();
@@ -572,9 +583,10 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
   };
   // V warps: replay round slot sb's rotations on its V blocks
   auto apply_v = [&](int sb) {
-    if (!s_blk[sb][2]) return;
-    const int a = s_blk[sb][0], b = s_blk[sb][1];
-    const bool full = s_blk[sb][3] != 0;
+   for (int g = 0; g < G; ++g) {
+    if (!s_blk_all[g][sb][2]) continue;
+    const int a = s_blk_all[g][sb][0], b = s_blk_all[g][sb][1];
+    const bool full = s_blk_all[g][sb][3] != 0;
     long long off[PC];
     bool ok[PC];
 #pragma unroll
@@ -588,21 +600,24 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
       cplx v[PC];
 #pragma unroll
       for (int j = 0; j < PC; ++j) v[j] = ok[j] ? __ldcg(Y + off[j] + r) : cmk(0.0, 0.0);
-      if (full) rj_v_round<BW, false>(v, Ps[sb]);
-      else rj_v_round<BW, true>(v, Ps[sb]);
+      if (full) rj_v_round<BW, false>(v, Ps_all[g][sb]);
+      else rj_v_round<BW, true>(v, Ps_all[g][sb]);
 #pragma unroll
       for (int j = 0; j < PC; ++j)
         if (ok[j]) __stcg(Y + off[j] + r, v[j]);
     }
+   }
   };
   mark(0);
   for (; sweep < max_sweeps; ++sweep) {
     double* off_cur = offbuf + (sweep % 3);
-    if (blockIdx.x == 0 && tid == 0) offbuf[(sweep + 1) % 3] = 0.0;
+    if (blockIdx.x == 0 && tid0 == 0) offbuf[(sweep + 1) % 3] = 0.0;
     for (int round = 0; round < nbe - 1; ++round, ++R) {
-      if (xthr) {
+      if (xthr && pair >= npairs) {
+        if (tid == 0) s_blk[R & 1][2] = 0;  // idle group (odd pair count)
+      } else if (xthr) {
         int a, b;
-        rj_rr_pair(nbe, round, blockIdx.x, a, b);
+        rj_rr_pair(nbe, round, pair, a, b);
         const int sb = R & 1;
 #pragma unroll
         for (int j = 0; j < PC; ++j) {
@@ -623,20 +638,20 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
           double nrm[PC];
           unsigned stale = 0u;
           bool notconv = false;
-          rj2_norms<BW, RX, NTX>(x, nrm, red[buf], lane, wid);
+          rj2_norms<BW, RX, NTX>(x, nrm, red[buf], lane, wid, barid);
           buf ^= 1;
           if (round == 0) {
 #pragma unroll
             for (int s = 0; s < PC - 1; ++s) {
               rj2_step<BW, RX, NTX, false>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
-                                           Ps[sb][s]);
+                                           Ps[sb][s], barid);
               buf ^= 1;
             }
           } else {
 #pragma unroll
             for (int s = 0; s < BW; ++s) {
               rj2_step<BW, RX, NTX, true>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
-                                          Ps[sb][s]);
+                                          Ps[sb][s], barid);
               buf ^= 1;
             }
           }
@@ -645,14 +660,14 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
 #pragma unroll
           for (int s = 0; s < PC - 1; ++s) {
             rj_step<BW, RX, 0, NTX, false, true>(x, dummy, s, red[buf], lane, wid, tol2q, offacc, rot, false, false,
-                                                 Ps[sb][s]);
+                                                 Ps[sb][s], barid);
             buf ^= 1;
           }
         } else {
 #pragma unroll
           for (int s = 0; s < BW; ++s) {
             rj_step<BW, RX, 0, NTX, true, true>(x, dummy, s, red[buf], lane, wid, tol2q, offacc, rot, false, false,
-                                                Ps[sb][s]);
+                                                Ps[sb][s], barid);
             buf ^= 1;
           }
         }
@@ -698,7 +713,7 @@ __global__ void __launch_bounds__(NTX + NTV, 1)
   }
   // the last round's V update
   if (!xthr && R > 0) apply_v((R - 1) & 1);
-  if (blockIdx.x == 0 && tid == 0) *sweeps_out = min(sweep + 1, max_sweeps);
+  if (blockIdx.x == 0 && tid0 == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
 
 struct RjVariant {
@@ -711,10 +726,10 @@ RjVariant rj_pick(bool cluster) {
   return RjVariant{cluster ? (void*)rjac_kernel<BW, RX, RV, NT, true> : (void*)rjac_kernel<BW, RX, RV, NT, false>,
                    cluster};
 }
-template <int BW, int RX, int NTX, int NTV, int MODE = 1>
+template <int BW, int RX, int NTX, int NTV, int MODE = 1, int G = 1>
 RjVariant rj2_pick(bool cluster) {
-  return RjVariant{cluster ? (void*)rjac2_kernel<BW, RX, NTX, NTV, true, MODE>
-                           : (void*)rjac2_kernel<BW, RX, NTX, NTV, false, MODE>,
+  return RjVariant{cluster ? (void*)rjac2_kernel<BW, RX, NTX, NTV, true, MODE, G>
+                           : (void*)rjac2_kernel<BW, RX, NTX, NTV, false, MODE, G>,
                    cluster};
 }
 
@@ -722,7 +737,7 @@ RjVariant rj2_pick(bool cluster) {
 // thread, nt threads.  kind 2 (rjac2): X rows in registers (rx per X thread,
 // nt X threads), V streamed by ntv V threads.
 struct Row {
-  int kind, bw, rx, rv, nt, ntv;
+  int kind, bw, rx, rv, nt, ntv, groups = 1;
 };
 constexpr Row kTab[] = {
     {1, 8, 1, 1, 256, 0},    // 0
@@ -739,6 +754,11 @@ constexpr Row kTab[] = {
     {2, 4, 2, 0, 128, 128},  // 11: as 6 with exact (non-tracked) norms and FP64 angles
     {2, 8, 2, 0, 128, 128},  // 12: X <= 256, BW 8: one cluster up to nc = 256
     {2, 8, 2, 0, 128, 128},  // 13: as 12, exact norms
+    {2, 4, 2, 0, 128, 128, 2},  // 14: as 6 with 2 block pairs per CTA (one cluster up to nc = 256)
+    {2, 4, 1, 0, 256, 128},     // 15: X <= 256 rows, 8 X warps (1 row each)
+    {2, 4, 1, 0, 256, 256},     // 16: as 15 with 8 V warps
+    {2, 4, 4, 0, 64, 128},      // 17: X <= 256 rows, 2 X warps (4 rows each)
+    {2, 4, 8, 0, 32, 128},      // 18: X <= 256 rows, 1 X warp (8 rows each)
 };
 constexpr int kNTab = sizeof(kTab) / sizeof(kTab[0]);
 
@@ -757,7 +777,12 @@ RjVariant rj_variant(int row, bool cl) {
     case 10: return rj2_pick<4, 2, 256, 128>(cl);
     case 11: return rj2_pick<4, 2, 128, 128, 0>(cl);
     case 12: return rj2_pick<8, 2, 128, 128>(cl);
-    default: return rj2_pick<8, 2, 128, 128, 0>(cl);
+    case 13: return rj2_pick<8, 2, 128, 128, 0>(cl);
+    case 14: return rj2_pick<4, 2, 128, 128, 1, 2>(cl);
+    case 15: return rj2_pick<4, 1, 256, 128>(cl);
+    case 16: return rj2_pick<4, 1, 256, 256>(cl);
+    case 17: return rj2_pick<4, 4, 64, 128>(cl);
+    default: return rj2_pick<4, 8, 32, 128>(cl);
   }
 }
 
@@ -793,11 +818,11 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
       if (rows_ok(r, mr, nc)) { row = r; break; }
   }
   if (row < 0) return cudaErrorNotSupported;
-  const int bw = kTab[row].bw, kind = kTab[row].kind;
-  const int nt = kind == 2 ? kTab[row].nt + kTab[row].ntv : kTab[row].nt;
+  const int bw = kTab[row].bw, kind = kTab[row].kind, grp = kTab[row].groups;
+  const int nt = kind == 2 ? grp * kTab[row].nt + kTab[row].ntv : kTab[row].nt;
   const int nb = (nc + bw - 1) / bw;
   const int nbe = std::max(2, nb + (nb & 1));
-  const int P = nbe / 2;
+  const int P = (nbe / 2 + grp - 1) / grp;  // CTAs
   cudaError_t e;
   bool cluster = P <= 16 && std::getenv("TDVP_RJ_GRID") == nullptr;
   RjVariant v{};
