@@ -259,6 +259,9 @@ def main():
     ms_per_step = step_ms / args.steps
     h2_ms = float(np.sum([s["heff2_ms"] for s in per]))
     h1_ms = float(np.sum([s["heff1_ms"] for s in per]))
+    lz2_ms = float(np.sum([s["lanczos2_ms"] for s in per]))
+    lz1_ms = float(np.sum([s["lanczos1_ms"] for s in per]))
+    env_ms = float(np.sum([s["env_ms"] for s in per]))
     h2_fl = float(np.sum([s["heff2_flop"] for s in per]))
     svd_ms = float(np.sum([s["svd_ms"] for s in per]))
     jac_ms = float(np.sum([s["svd_jac_ms"] for s in per]))
@@ -317,8 +320,10 @@ def main():
                   "share_of_step": h2_ms / step_ms if step_ms > 0 else None},
         "svd_share_of_step": svd_ms / step_ms if step_ms > 0 else None,
         "breakdown_ms_per_step": {"svd_total": svd_ms / args.steps, "svd_jacobi_kernel": jac_ms / args.steps,
-                                  "heff2_matvecs": h2_ms / args.steps, "heff1_matvecs": h1_ms / args.steps,
-                                  "rest": (step_ms - svd_ms - h2_ms - h1_ms) / args.steps},
+                                  "lanczos2_total": lz2_ms / args.steps, "heff2_matvecs": h2_ms / args.steps,
+                                  "lanczos1_total": lz1_ms / args.steps, "heff1_matvecs": h1_ms / args.steps,
+                                  "env_updates": env_ms / args.steps,
+                                  "rest": (step_ms - svd_ms - lz2_ms - lz1_ms - env_ms) / args.steps},
         "gpu_launches": launches,
         "gemm_launches": gemm_launches,
         "wall_s_timed": wall,

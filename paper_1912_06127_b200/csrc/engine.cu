@@ -141,6 +141,7 @@ struct tdvp_ctx {
   // Off by default: on the saturated bench it needs MORE sweeps (12.3) than
   // the QR-preconditioned start (8.3), the discarded half being unstructured.
   bool warm_svd = false;
+  bool lz_fused = true;  // one cooperative launch per Lanczos iteration (TDVP_LZ_FUSED=0: four passes)
   int dev = 0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -167,7 +168,7 @@ struct tdvp_ctx {
   tdvp_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<std::pair<int, int>> ev_h2, ev_h1, ev_svd;
+  std::vector<std::pair<int, int>> ev_h2, ev_h1, ev_svd, ev_lz2, ev_lz1, ev_env;
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
   // NCCL
   int rank = 0, world = 1;
@@ -358,13 +359,18 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
       if (which == 2) { h->stats.heff2_flop += mv_flop; h->stats.heff2_calls++; }
       else h->stats.heff1_flop += mv_flop;
     }
-    CK(lz_dots(h->st, h->lz, V, n, k + 1, w, n, k));
-    g_launch_count++;
-    if (k + 1 < K) {
-      CK(lz_update_dots(h->st, h->lz, V, n, k + 1, w, n));
-      CK(lz_update_norm(h->st, h->lz, V, n, k + 1, w, n, k));
-      CK(lz_next(h->st, h->lz, w, V + (long long)(k + 1) * n, n, k));
-      g_launch_count += 3;
+    if (h->lz_fused) {
+      CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0));
+      g_launch_count++;
+    } else {
+      CK(lz_dots(h->st, h->lz, V, n, k + 1, w, n, k));
+      g_launch_count++;
+      if (k + 1 < K) {
+        CK(lz_update_dots(h->st, h->lz, V, n, k + 1, w, n));
+        CK(lz_update_norm(h->st, h->lz, V, n, k + 1, w, n, k));
+        CK(lz_next(h->st, h->lz, w, V + (long long)(k + 1) * n, n, k));
+        g_launch_count += 3;
+      }
     }
   }
   CK(lz_tridiag_exp(h->st, h->lz, K, tre, tim));
@@ -397,9 +403,11 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   const double tau = full ? dt : 0.5 * dt;
   const double fl = flops_heff2(cl, cr, d, W1.Dl, W2.Dr, nnz_of(W1), nnz_of(W2));
   cplx* th2 = h->tmpB->c();
+  const int el0 = h->prm.timing ? ev_record(h) : -1;
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, 0.0, -tau,
       h->prm.krylov_k, 2, fl);
+  if (el0 >= 0) h->ev_lz2.emplace_back(el0, ev_record(h));
   // a4: truncated SVD split
   int e0 = -1;
   if (h->prm.timing) e0 = ev_record(h);
@@ -462,6 +470,7 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   }
   if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
   // a5: environments for the next update
+  const int ee0 = h->prm.timing ? ev_record(h) : -1;
   if (build & BUILD_BETA) {
     CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
     g_launch_count++;
@@ -472,6 +481,7 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
     g_launch_count++;
     env_right(h, P(g.gamma[j + 1]), h->tmpA->c(), W2, chi, cr, P(g.gamma[j]));
   }
+  if (ee0 >= 0) h->ev_env.emplace_back(ee0, ev_record(h));
 }
 
 // one-site backward update Psi_j <- exp(+i dt/2 H_eff^(1)) Psi_j
@@ -484,9 +494,11 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), n));
   g_launch_count++;
   const double fl = flops_heff1(cl, cr, d, W.Dl, W.Dr, nnz_of(W));
+  const int el0 = h->prm.timing ? ev_record(h) : -1;
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff1(h, Lenv, W, Renv, cl, cr, x, y); }, h->tmpB->c(), P(g.psi[j]), n, 0.0,
       0.5 * dt, h->prm.krylov_k, 1, fl);
+  if (el0 >= 0) h->ev_lz1.emplace_back(el0, ev_record(h));
   h->stats.n_back++;
 }
 
@@ -815,6 +827,9 @@ void finish_timing(tdvp_ctx* h) {
   h->stats.heff2_ms = sum(h->ev_h2);
   h->stats.heff1_ms = sum(h->ev_h1);
   h->stats.svd_ms = sum(h->ev_svd);
+  h->stats.lanczos2_ms = sum(h->ev_lz2);
+  h->stats.lanczos1_ms = sum(h->ev_lz1);
+  h->stats.env_ms = sum(h->ev_env);
 }
 
 void do_step(tdvp_ctx* h, double dt, int p) {
@@ -834,6 +849,9 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   h->ev_h2.clear();
   h->ev_h1.clear();
   h->ev_svd.clear();
+  h->ev_lz2.clear();
+  h->ev_lz1.clear();
+  h->ev_env.clear();
   const long long l0 = g_launch_count, g0 = g_gemm_count;
   CK(cudaEventRecord(h->ev_step0, h->st));
   const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
@@ -1057,6 +1075,7 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
     h->prm.multiplet_delta = 1e-6;
     h->prm.timing = 0;
     if (const char* ev = std::getenv("TDVP_SVD_WARM")) h->warm_svd = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("TDVP_LZ_FUSED")) h->lz_fused = std::atoi(ev) != 0;
     h->cbmax.assign(L + 1, 1);
     for (int j = 0; j <= L; ++j) {
       double a = std::pow((double)d, std::min(j, 62)), b = std::pow((double)d, std::min(L - j, 62));

@@ -64,6 +64,9 @@ cudaError_t lz_update_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, 
 cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
                            long long n, int k);
 cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k);
+// one cooperative launch for a whole Lanczos iteration after the matvec (see lanczos.cu)
+cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
+                    long long n, int k, int last);
 cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im);
 cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
                        long long n);

@@ -11,8 +11,10 @@
 //   lz_next         v_{k+1} = w / beta_k       (hard zero after breakdown)
 // then an on-device K x K symmetric tridiagonal eigen-decomposition
 // (cyclic Jacobi) for y = n0 Q exp(tau mu) Q^T e_1 and v' = V y.
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "kernels.h"
+namespace cgl = cooperative_groups;
 
 namespace {
 
@@ -329,6 +331,125 @@ __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K,
   if (on) d.y[r] = cmul(cmk(mag * cs, mag * sn), y);
 }
 
+// One Lanczos iteration after the matvec in ONE cooperative launch (replaces
+// lz_dots + lz_update_dots + lz_update_norm + lz_next): three grid-wide
+// reductions, each block reducing the per-block partials in block order (so
+// every block holds the same, deterministic sums).
+//   phase 1  c = V^H w                 alpha_k = Re c_k        (last iteration stops here)
+//   phase 2  w -= V c ;  c' = V^H w    (three-term recurrence + CGS pass 1)
+//   phase 3  w -= V c' ; ||w||^2       (CGS pass 2) -> beta_k, breakdown (AMB-5)
+//   phase 4  v_{k+1} = w / beta_k      (hard zero after breakdown)
+template <int NV>
+__global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* __restrict__ V, long long ldv, cplx* w,
+                                                      cplx* vnext, long long n, int k, int last) {
+  cgl::grid_group grid = cgl::this_grid();
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NQ = 2 * NV;
+  double* PA = d.partials;
+  double* PB = d.partials + (long long)G * 2 * (KMAX + 1);
+  __shared__ double s_red[NW][NQ];
+  __shared__ double s_tot[NQ];
+  __shared__ cplx s_c[NV];
+  const long long stride = (long long)G * TPB;
+  auto block_reduce_store = [&](double (&acc)[NQ], int nq, double* P) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (q >= nq) break;
+      const double t = warp_sum(acc[q]);
+      if (lane == 0) s_red[wid][q] = t;
+    }
+    __syncthreads();
+    if (tid < nq) {
+      double t = 0.0;
+      for (int ww = 0; ww < NW; ++ww) t += s_red[ww][tid];
+      P[(long long)blockIdx.x * nq + tid] = t;
+    }
+  };
+  auto grid_total = [&](int nq, const double* P) {
+    if (tid < nq) {
+      double t = 0.0;
+      for (int b = 0; b < G; ++b) t += __ldcg(P + (long long)b * nq + tid);
+      s_tot[tid] = t;
+    }
+    __syncthreads();
+  };
+  double acc[NQ];
+  // ---- phase 1
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
+    const cplx we = w[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const cplx p = cdotc(V[i * ldv + e], we);
+      acc[2 * i] += p.x;
+      acc[2 * i + 1] += p.y;
+    }
+  }
+  block_reduce_store(acc, NQ, PA);
+  grid.sync();
+  grid_total(NQ, PA);
+  if (tid < NV) s_c[tid] = cmk(s_tot[2 * tid], s_tot[2 * tid + 1]);
+  if (blockIdx.x == 0 && tid == 0) d.scal[k] = s_tot[2 * k];
+  __syncthreads();
+  if (last) return;
+  // ---- phase 2
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
+    cplx we = w[e];
+    cplx v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = V[i * ldv + e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], v[i]));
+    w[e] = we;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const cplx p = cdotc(v[i], we);
+      acc[2 * i] += p.x;
+      acc[2 * i + 1] += p.y;
+    }
+  }
+  block_reduce_store(acc, NQ, PB);
+  grid.sync();
+  grid_total(NQ, PB);
+  if (tid < NV) s_c[tid] = cmk(s_tot[2 * tid], s_tot[2 * tid + 1]);
+  __syncthreads();
+  // ---- phase 3
+  acc[0] = 0.0;
+  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
+    cplx we = w[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], V[i * ldv + e]));
+    w[e] = we;
+    acc[0] += cabs2(we);
+  }
+  block_reduce_store(acc, 1, PA);
+  grid.sync();
+  grid_total(1, PA);
+  // beta_k and the breakdown rule, identical in every block
+  const double b = sqrt(s_tot[0]);
+  double sc = 1.0;
+  for (int i = 0; i <= k; ++i) sc = fmax(sc, fabs(__ldcg(d.scal + i)));  // alpha_0..k (alpha_k: block 0, phase 1)
+  for (int i = 0; i < k; ++i) sc = fmax(sc, __ldcg(d.scal + KMAX + i));
+  const bool was = __ldcg(d.scal + LZ_BRK) != 0.0;
+  const bool brk = was || !(b > 1e-12 * sc);
+  __syncthreads();  // every thread read the scalars before block 0 updates them
+  if (blockIdx.x == 0 && tid == 0) {
+    if (brk) {
+      d.scal[LZ_BRK] = 1.0;
+      d.scal[KMAX + k] = 0.0;
+      if (!was) atomicAdd(d.brk_count, 1);
+    } else {
+      d.scal[KMAX + k] = b;
+    }
+  }
+  // ---- phase 4
+  const double inv = brk ? 0.0 : 1.0 / b;
+  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) vnext[e] = cscale(w[e], inv);
+}
+
 __global__ void lz_combine_kernel(const cplx* __restrict__ y, const cplx* __restrict__ V, long long ldv, int K,
                                   cplx* __restrict__ out, long long n) {
   __shared__ cplx s_y[KMAX];
@@ -371,6 +492,29 @@ cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double t
   lz_tridiag_exp_kernel<<<1, 32, 0, st>>>(d, K, tau_re, tau_im);
   return cudaGetLastError();
 }
+cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
+                    long long n, int k, int last) {
+  static int occ[KMAX + 1] = {0};
+  void* fn = nullptr;
+  switch (nv) {
+#define LZI(NVV) case NVV: fn = (void*)lz_iter_kernel<NVV>; break;
+    LZI(1) LZI(2) LZI(3) LZI(4) LZI(5) LZI(6) LZI(7) LZI(8) LZI(9) LZI(10) LZI(11) LZI(12) LZI(13) LZI(14) LZI(15)
+    LZI(16)
+#undef LZI
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e;
+  if (occ[nv] == 0) {
+    int o = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, TPB, 0)) != cudaSuccess) return e;
+    occ[nv] = std::max(1, o);
+  }
+  // partials: two buffers of G * 2 * (KMAX + 1) doubles inside d.partials (4 * SMs blocks' worth)
+  const int G = std::max(1, std::min(std::min(nblk_for(n), occ[nv] * g_num_sms), 2 * g_num_sms));
+  void* args[] = {(void*)&d, (void*)&V, (void*)&ldv, (void*)&w, (void*)&vnext, (void*)&n, (void*)&k, (void*)&last};
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(TPB), args, 0, st);
+}
+
 cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
                        long long n) {
   lz_combine_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.y, V, ldv, K, out, n);
