@@ -157,7 +157,7 @@ struct tdvp_ctx {
   std::vector<int> h_chi;
   // workspace
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
-  BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, gemm_work, partials;
+  BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, svdF, gemm_work, partials;
   BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
   BufPtr svd_sigma, svd_order, svd_off, svd_ires, svd_dres, red_res, envA, envB;
   double* h_pin = nullptr;
@@ -972,6 +972,8 @@ void alloc_workspace(tdvp_ctx* h) {
   h->tmpB = make_buf(std::max(n2, n1) * sizeof(cplx));
   h->svdY = make_buf(svd * sizeof(cplx));
   h->svdQ = make_buf(svq * sizeof(cplx));
+  const size_t nflags = (size_t)8 * h->chi_max + 64;  // 2 counters per column block, blocks >= 2 columns
+  h->svdF = make_buf(nflags * sizeof(unsigned));
   h->gemm_work = make_buf(h->work_elems * sizeof(cplx));
   h->envA = make_buf(env * sizeof(cplx));
   h->envB = make_buf(env * sizeof(cplx));
@@ -996,7 +998,8 @@ void alloc_workspace(tdvp_ctx* h) {
   h->lz = LanczosDev{h->lz_scal->d(), h->lz_coef->c(), h->lz_y->c(), h->partials->d(),
                      reinterpret_cast<unsigned*>(h->lz_counter->p), h->lz_brk->i()};
   h->sv = SvdDev{h->svdY->c(), 0, h->svd_sigma->d(), h->svd_order->i(), h->svd_off->d(), h->svd_ires->i(),
-                 h->svd_dres->d(), h->h_pin, h->h_ipin, {nullptr, nullptr}, h->svdQ->c(), (size_t)svq};
+                 h->svd_dres->d(), h->h_pin, h->h_ipin, {nullptr, nullptr}, h->svdQ->c(), (size_t)svq,
+                 reinterpret_cast<unsigned*>(h->svdF->p), nflags};
 }
 
 int fail(tdvp_ctx* h, const TdvpError& e) {

@@ -85,6 +85,8 @@ struct SvdDev {
   cudaEvent_t ev_jac[2];  // optional: recorded around the Jacobi kernel (timing)
   cplx* qrbuf;            // QR preconditioning workspace (svd_qr_work_elems), nullptr = off
   size_t qrbuf_elems;
+  unsigned* flags;        // Jacobi per-block round counters (2 per column block), nullptr = grid barriers
+  size_t flags_elems;
 };
 size_t svd_qr_work_elems(int m, int n);
 struct TruncParams {

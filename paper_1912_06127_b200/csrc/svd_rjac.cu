@@ -551,7 +551,11 @@ __device__ __forceinline__ void rj_v_round(cplx (&v)[2 * BW], const double (*P)[
 template <int BW, int RX, int NTX, int NTV, bool CLUSTER, int MODE, int G>
 __global__ void __launch_bounds__(G * NTX + NTV, 1)
     rjac2_kernel(cplx* Y, long long ldy, int mr, int vofs, int nc, int nb, int nbe, double tol, int max_sweeps,
-                 double* offbuf, int* sweeps_out, int prof) {
+                 double* offbuf, int* sweeps_out, int prof, unsigned* flags) {
+  // flags != nullptr: between rounds, point-to-point per-block counters in
+  // global memory (xflag[b] = rounds whose X update of block b is stored,
+  // vflag[b] = rounds whose V update is stored) instead of a grid barrier;
+  // one grid barrier per sweep (the convergence decision).
   // G block pairs per CTA ("pair groups" of NTX X threads each, named barrier
   // 1 + g), one set of NTV V threads serving all groups
   constexpr int PC = 2 * BW, NV = 4 * BW, NWX = NTX / 32;
@@ -582,10 +586,26 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
     }
   };
   // V warps: replay round slot sb's rotations on its V blocks
-  auto apply_v = [&](int sb) {
+  unsigned* xflag = flags;
+  unsigned* vflag = flags ? flags + nbe : nullptr;
+  const int tv = tid0 - G * NTX;  // V thread index
+  auto wait_flag = [&](const unsigned* f, unsigned need) {
+    while (*(volatile const unsigned*)f < need) __nanosleep(32);
+    __threadfence();
+  };
+  auto apply_v = [&](int sb, int Rdone) {  // Rdone = the round whose rotations are replayed
    for (int g = 0; g < G; ++g) {
-    if (!s_blk_all[g][sb][2]) continue;
     const int a = s_blk_all[g][sb][0], b = s_blk_all[g][sb][1];
+    if (a < 0) continue;  // idle group
+    if (flags) {
+      // V blocks a, b were last updated by round Rdone-1's replay
+      if (tv == 0) {
+        if (a < nb) wait_flag(vflag + a, (unsigned)Rdone);
+        if (b < nb) wait_flag(vflag + b, (unsigned)Rdone);
+      }
+      asm volatile("bar.sync 15, %0;" ::"n"(NTV) : "memory");
+    }
+    if (s_blk_all[g][sb][2]) {
     const bool full = s_blk_all[g][sb][3] != 0;
     long long off[PC];
     bool ok[PC];
@@ -606,6 +626,15 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
       for (int j = 0; j < PC; ++j)
         if (ok[j]) __stcg(Y + off[j] + r, v[j]);
     }
+    }
+    if (flags) {
+      asm volatile("bar.sync 15, %0;" ::"n"(NTV) : "memory");
+      if (tv == 0) {
+        __threadfence();
+        if (a < nb) *(volatile unsigned*)(vflag + a) = (unsigned)(Rdone + 1);
+        if (b < nb) *(volatile unsigned*)(vflag + b) = (unsigned)(Rdone + 1);
+      }
+    }
    }
   };
   mark(0);
@@ -614,11 +643,22 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
     if (blockIdx.x == 0 && tid0 == 0) offbuf[(sweep + 1) % 3] = 0.0;
     for (int round = 0; round < nbe - 1; ++round, ++R) {
       if (xthr && pair >= npairs) {
-        if (tid == 0) s_blk[R & 1][2] = 0;  // idle group (odd pair count)
+        if (tid == 0) {
+          s_blk[R & 1][0] = -1;  // idle group (odd pair count)
+          s_blk[R & 1][2] = 0;
+        }
       } else if (xthr) {
         int a, b;
         rj_rr_pair(nbe, round, pair, a, b);
         const int sb = R & 1;
+        if (flags) {
+          // blocks a, b were stored by round R-1
+          if (tid == 0) {
+            if (a < nb) wait_flag(xflag + a, (unsigned)R);
+            if (b < nb) wait_flag(xflag + b, (unsigned)R);
+          }
+          rj_bar<NTX, true>(barid);
+        }
 #pragma unroll
         for (int j = 0; j < PC; ++j) {
           const int blk = j < BW ? a : b;
@@ -693,26 +733,40 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
           s_blk[sb][2] = rot ? 1 : 0;
           s_blk[sb][3] = round == 0 ? 1 : 0;
         }
+        if (flags) {
+          rj_bar<NTX, true>(barid);  // every X store of this group issued
+          if (tid == 0) {
+            __threadfence();
+            if (a < nb) *(volatile unsigned*)(xflag + a) = (unsigned)(R + 1);
+            if (b < nb) *(volatile unsigned*)(xflag + b) = (unsigned)(R + 1);
+          }
+        }
         if (wid == 0) {
           offacc = warp_max(offacc);
           if (lane == 0 && offacc > 0.0) atomic_max_nonneg(off_cur, sqrt(offacc));
         }
         mark(2);
       } else if (R > 0) {
-        apply_v((R - 1) & 1);
+        apply_v((R - 1) & 1, R - 1);
       }
-      if (CLUSTER) {
+      if (flags) {
+        __syncthreads();  // X and V warps of this CTA: the shared parameter buffers rotate
+      } else if (CLUSTER) {
         cg::this_cluster().sync();
       } else {
         cg::this_grid().sync();
       }
       mark(3);
     }
+    if (flags) {
+      if (CLUSTER) cg::this_cluster().sync();
+      else cg::this_grid().sync();
+    }
     const double off = __ldcg(off_cur);
     if (!(off > tol)) break;
   }
   // the last round's V update
-  if (!xthr && R > 0) apply_v((R - 1) & 1);
+  if (!xthr && R > 0) apply_v((R - 1) & 1, R - 1);
   if (blockIdx.x == 0 && tid0 == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
 
@@ -867,8 +921,21 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
   void* args1[] = {(void*)&Yp,  (void*)&ldy,        (void*)&mr,  (void*)&vofs,  (void*)&nc,   (void*)&nb,
                    (void*)&nbe, (void*)&tol,        (void*)&max_sweeps,  (void*)&full_rounds,
                    (void*)&offb, (void*)&sweeps_dev, (void*)&prof, (void*)&fastp};
+  unsigned* flg = nullptr;
+  static int use_flags = -1;
+  if (use_flags < 0) {
+    // off by default: measured slower than the grid barrier (flag round trips
+    // through L2 + fences cost more than cg's barrier at 32 CTAs)
+    const char* ev = std::getenv("TDVP_RJ_FLAGS");
+    use_flags = ev ? std::atoi(ev) : 0;
+  }
+  if (kind == 2 && use_flags && d.flags != nullptr && (size_t)2 * nbe <= d.flags_elems) {
+    flg = d.flags;
+    if ((e = cudaMemsetAsync(flg, 0, (size_t)2 * nbe * sizeof(unsigned), st)) != cudaSuccess) return e;
+  }
   void* args2[] = {(void*)&Yp,  (void*)&ldy, (void*)&mr,         (void*)&vofs, (void*)&nc,         (void*)&nb,
-                   (void*)&nbe, (void*)&tol, (void*)&max_sweeps, (void*)&offb, (void*)&sweeps_dev, (void*)&prof};
+                   (void*)&nbe, (void*)&tol, (void*)&max_sweeps, (void*)&offb, (void*)&sweeps_dev, (void*)&prof,
+                   (void*)&flg};
   void** args = kind == 2 ? args2 : args1;
   if (cluster) {
     if ((e = cudaLaunchKernelExC(&cfg, v.fn, args)) != cudaSuccess) return e;
