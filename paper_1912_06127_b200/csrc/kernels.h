@@ -139,6 +139,10 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
 // C (m x nc) <- H_0 ... H_{n-1} C with qr_factor_cluster's reflectors
 cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,
                           long long ldc, int nc);
+// two independent applications in one launch
+cudaError_t qr_apply_refl2(cudaStream_t st, const cplx* A0, long long lda0, const cplx* tau0, int m0, int n0, cplx* C0,
+                           long long ldc0, int nc0, const cplx* A1, long long lda1, const cplx* tau1, int m1, int n1,
+                           cplx* C1, long long ldc1, int nc1);
 
 // svd_rjac.cu: register-resident Jacobi stage on d.Y = [X ; V]; returns
 // cudaErrorNotSupported for shapes it does not cover (svd.cu falls back).

@@ -537,14 +537,31 @@ __global__ void __launch_bounds__(NT, 1)
 // One CTA per 8 columns of C held in registers (RPT rows per thread); per
 // reflector one reduction of 16 doubles (warp reduce-scatter + one
 // __syncthreads), v_k read from L2.
+struct QrApplyJob {
+  const cplx* A;
+  long long lda;
+  const cplx* tau;
+  int m, n;
+  cplx* C;
+  long long ldc;
+  int nc;
+};
+
+// blocks [0, nb0) run job j0, blocks [nb0, ...) job j1 (two independent applications in one launch)
 template <int RPT, int NT>
-__global__ void __launch_bounds__(NT)
-    qr_apply_refl_kernel(const cplx* __restrict__ A, long long lda, const cplx* __restrict__ tau, int m, int n, cplx* C,
-                         long long ldc, int nc) {
+__global__ void __launch_bounds__(NT) qr_apply_refl_kernel(QrApplyJob j0, QrApplyJob j1, int nb0) {
   constexpr int CB = 8, NV = 2 * CB, NW = NT / 32;
   __shared__ double red[2][NW][NV];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int cb0 = blockIdx.x * CB;
+  const bool second = (int)blockIdx.x >= nb0;
+  const QrApplyJob& J = second ? j1 : j0;
+  const cplx* __restrict__ A = J.A;
+  const long long lda = J.lda;
+  const cplx* __restrict__ tau = J.tau;
+  const int m = J.m, n = J.n, nc = J.nc;
+  cplx* C = J.C;
+  const long long ldc = J.ldc;
+  const int cb0 = (second ? (int)blockIdx.x - nb0 : (int)blockIdx.x) * CB;
   cplx c[RPT][CB];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
@@ -698,10 +715,20 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
 
 cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,
                           long long ldc, int nc) {
-  const int blocks = (nc + 7) / 8;
-  if (m <= 256) qr_apply_refl_kernel<1, 256><<<blocks, 256, 0, st>>>(A, lda, tau, m, n, C, ldc, nc);
-  else if (m <= 512) qr_apply_refl_kernel<2, 256><<<blocks, 256, 0, st>>>(A, lda, tau, m, n, C, ldc, nc);
-  else if (m <= 1024) qr_apply_refl_kernel<4, 256><<<blocks, 256, 0, st>>>(A, lda, tau, m, n, C, ldc, nc);
+  return qr_apply_refl2(st, A, lda, tau, m, n, C, ldc, nc, nullptr, 0, nullptr, 0, 0, nullptr, 0, 0);
+}
+
+cudaError_t qr_apply_refl2(cudaStream_t st, const cplx* A0, long long lda0, const cplx* tau0, int m0, int n0, cplx* C0,
+                           long long ldc0, int nc0, const cplx* A1, long long lda1, const cplx* tau1, int m1, int n1,
+                           cplx* C1, long long ldc1, int nc1) {
+  const QrApplyJob j0{A0, lda0, tau0, m0, n0, C0, ldc0, nc0};
+  const QrApplyJob j1{A1, lda1, tau1, m1, n1, C1, ldc1, nc1};
+  const int nb0 = (nc0 + 7) / 8, nb1 = A1 ? (nc1 + 7) / 8 : 0;
+  const int m = std::max(m0, A1 ? m1 : 0);
+  const int blocks = nb0 + nb1;
+  if (m <= 256) qr_apply_refl_kernel<1, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
+  else if (m <= 512) qr_apply_refl_kernel<2, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
+  else if (m <= 1024) qr_apply_refl_kernel<4, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else return cudaErrorNotSupported;
   return cudaGetLastError();
 }

@@ -943,8 +943,10 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     }
   }
   if (use_qr && qr_cluster) {
-    if ((e = qr_apply_refl(st, q1p, mr, w1.tau, mr, nc, d.Y, ldy, nc)) != cudaSuccess) return e;
-    if ((e = qr_apply_refl(st, q2p, nc, w2.tau, nc, nc, d.Y + mr, ldy, nc)) != cudaSuccess) return e;
+    // Q1 onto the X columns and Q2 onto V, one launch
+    if ((e = qr_apply_refl2(st, q1p, mr, w1.tau, mr, nc, d.Y, ldy, nc, q2p, nc, w2.tau, nc, nc, d.Y + mr, ldy, nc)) !=
+        cudaSuccess)
+      return e;
   } else if (use_qr) {
     if ((e = qr_apply_q(st, w1, mr, nc, d.Y, ldy, nc)) != cudaSuccess) return e;
     if ((e = qr_apply_q(st, w2, nc, nc, d.Y + mr, ldy, nc)) != cudaSuccess) return e;
