@@ -11,6 +11,7 @@
 //   lz_next         v_{k+1} = w / beta_k       (hard zero after breakdown)
 // then an on-device K x K symmetric tridiagonal eigen-decomposition
 // (cyclic Jacobi) for y = n0 Q exp(tau mu) Q^T e_1 and v' = V y.
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "kernels.h"
@@ -510,7 +511,12 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
     occ[nv] = std::max(1, o);
   }
   // partials: two buffers of G * 2 * (KMAX + 1) doubles inside d.partials (4 * SMs blocks' worth)
-  const int G = std::max(1, std::min(std::min(nblk_for(n), occ[nv] * g_num_sms), 2 * g_num_sms));
+  static int gcap = -1;
+  if (gcap < 0) {
+    const char* ev = std::getenv("TDVP_LZ_G");
+    gcap = ev ? std::max(1, std::atoi(ev)) : 2 * g_num_sms;
+  }
+  const int G = std::max(1, std::min(std::min(nblk_for(n), occ[nv] * g_num_sms), std::min(gcap, 2 * g_num_sms)));
   void* args[] = {(void*)&d, (void*)&V, (void*)&ldv, (void*)&w, (void*)&vnext, (void*)&n, (void*)&k, (void*)&last};
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(TPB), args, 0, st);
 }
