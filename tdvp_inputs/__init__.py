@@ -140,7 +140,9 @@ def canonicalize(M) -> MPS:
         q, r = np.linalg.qr(M[j].reshape(cl * d, cr))
         k = q.shape[1]
         M[j] = q.reshape(cl, d, k)
-        M[j + 1] = np.tensordot(r, M[j + 1], axes=(1, 0))
+        # the overall scale is normalised away below; keep it O(1) so long
+        # chains at large chi do not overflow
+        M[j + 1] = np.tensordot(r / np.linalg.norm(r), M[j + 1], axes=(1, 0))
     lam = [None] * (L - 1)
     for j in range(L - 1, 0, -1):
         cl, d, cr = M[j].shape
