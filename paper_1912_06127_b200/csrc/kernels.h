@@ -136,6 +136,9 @@ cudaError_t qr_r_conjtrans(cudaStream_t st, const cplx* A, long long lda, int n,
 // tails, tau[n]; optionally [R^H ; 0] (rh_rows x n, ld ldrh) written to RH.
 cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH,
                               long long ldrh, int rh_rows);
+// the same over a cooperative grid (bands up to one CTA per SM), counter in global memory
+cudaError_t qr_factor_grid(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH, long long ldrh,
+                           int rh_rows, unsigned* gcnt);
 // C (m x nc) <- H_0 ... H_{n-1} C with qr_factor_cluster's reflectors
 cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,
                           long long ldc, int nc);

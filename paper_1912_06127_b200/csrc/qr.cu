@@ -367,11 +367,15 @@ __device__ __forceinline__ unsigned long long gtime() {
 #ifndef QR_PUB
 #define QR_PUB 4
 #endif
-template <int NT, int NB>
+// GRID = false: one thread-block cluster, counters in each CTA's shared memory
+// raised by cluster-scope release stores.  GRID = true: a cooperative grid (up
+// to one CTA per SM, for bands that do not fit one cluster), one counter in
+// global memory (`gcnt`, zero on entry) raised with a GPU-scope release.
+template <int NT, int NB, bool GRID>
 __global__ void __launch_bounds__(NT, 1)
-    qrc3_factor_kernel(cplx* A, long long lda, int m, int n, int cw, cplx* tau, cplx* RH, long long ldrh, int rh_rows) {
+    qrc3_factor_kernel(cplx* A, long long lda, int m, int n, int cw, cplx* tau, cplx* RH, long long ldrh, int rh_rows,
+                       unsigned* gcnt) {
   namespace cgq = cooperative_groups;
-  cgq::cluster_group cluster = cgq::this_cluster();
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char qc_sm[];
   cplx* Aloc = reinterpret_cast<cplx*>(qc_sm);  // cw columns x m rows (own band)
@@ -381,21 +385,31 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ unsigned s_npub;  // reflectors published to this CTA (written remotely)
   __shared__ int s_nav;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int crank = (int)cluster.block_rank(), ncta = (int)cluster.num_blocks();
+  const int crank = GRID ? (int)blockIdx.x : (int)cgq::this_cluster().block_rank();
+  const int ncta = GRID ? (int)gridDim.x : (int)cgq::this_cluster().num_blocks();
+  auto all_sync = [&]() {
+    if (GRID) cgq::this_grid().sync();
+    else cgq::this_cluster().sync();
+  };
   const int c0 = crank * cw, c1 = min(n, c0 + cw), ncl = max(0, c1 - c0);
   for (int e = tid; e < ncl * m; e += NT) {
     const int j = e / m, r = e - j * m;
     Aloc[e] = A[(long long)(c0 + j) * lda + r];
   }
   if (tid == 0) s_npub = 0u;
-  cluster.sync();  // every counter initialised before any remote release
+  all_sync();  // every counter initialised before any remote release
   if (tid == 0 && crank < 16) g_qr_prof[crank][0] = gtime();
   int nbatches = 0;
   // ---------------- phase 1: apply the earlier CTAs' reflectors 0 .. c0-1
   for (int k = 0; k < c0;) {
     if (tid == 0) {
       unsigned a;
-      while ((a = ld_acquire_cluster_local(&s_npub)) <= (unsigned)k) __nanosleep(64);
+      if (GRID) {
+        while ((a = *(volatile unsigned*)gcnt) <= (unsigned)k) __nanosleep(64);
+        __threadfence();
+      } else {
+        while ((a = ld_acquire_cluster_local(&s_npub)) <= (unsigned)k) __nanosleep(64);
+      }
       s_nav = min((int)a, min(c0, k + NB)) - k;  // batch of available reflectors
     }
     __syncthreads();
@@ -474,9 +488,17 @@ __global__ void __launch_bounds__(NT, 1)
       // publish v_k to every later CTA (release orders the warp's writes
       // above); inside the band only every QR_PUB-th reflector, the band's
       // last one always
-      if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl)
-        for (int c = crank + 1 + lane; c < ncta; c += 32)
-          st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
+      if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl) {
+        if (GRID) {
+          if (lane == 0) {
+            __threadfence();
+            *(volatile unsigned*)gcnt = (unsigned)(k + 1);
+          }
+        } else {
+          for (int c = crank + 1 + lane; c < ncta; c += 32)
+            st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
+        }
+      }
       QPH(2)
     }
     asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
@@ -529,7 +551,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (r <= c && r < n) RH[(long long)r * ldrh + c] = cconj(Aloc[(long long)j * m + r]);
     }
   }
-  cluster.sync();  // keep shared memory alive until every CTA finished its DSMEM reads
+  all_sync();  // keep shared memory alive until every CTA finished its reads
 }
 
 // C (m x nc, column-major, ld ldc) <- H_0 H_1 ... H_{n-1} C with the
@@ -665,10 +687,10 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   cudaError_t e;
   static bool attr = false;
   if (!attr) {
-    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       return e;
-    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
         cudaSuccess)
       return e;
     attr = true;
@@ -691,7 +713,8 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
         cudaSuccess)
       return e;
   }
-  e = cudaLaunchKernelEx(&cfg, qrc3_factor_kernel<256, NB>, A, lda, m, n, cw, tau, RH, ldrh, rh_rows);
+  unsigned* nog = nullptr;
+  e = cudaLaunchKernelEx(&cfg, qrc3_factor_kernel<256, NB, false>, A, lda, m, n, cw, tau, RH, ldrh, rh_rows, nog);
   static int prof = -1;
   if (prof < 0) prof = std::getenv("TDVP_QR_PROF") ? 1 : 0;
   if (prof && e == cudaSuccess) {
@@ -711,6 +734,41 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
                    z[c][3]);
   }
   return e;
+}
+
+// Grid variant: bands of cw columns on up to one CTA per SM (cooperative launch)
+cudaError_t qr_factor_grid(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH, long long ldrh,
+                           int rh_rows, unsigned* gcnt) {
+  if (m < n || n < 1 || gcnt == nullptr) return cudaErrorInvalidValue;
+  constexpr int NB = 4;
+  auto fn = qrc3_factor_kernel<256, NB, true>;
+  cudaError_t e;
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) != cudaSuccess) return e;
+    attr = true;
+  }
+  // smallest band width whose shared memory fits and whose CTAs are co-resident
+  int cw = std::max(1, (n + g_num_sms - 1) / g_num_sms);
+  const size_t per_col = (size_t)m * sizeof(cplx);
+  if (((size_t)cw * m + (size_t)NB * m + cw) * sizeof(cplx) > 200 * 1024) return cudaErrorNotSupported;
+  (void)per_col;
+  // prefer bands of 8+ columns (fewer, busier CTAs) while they fit
+  while (cw < 8 && ((size_t)(2 * cw) * m + (size_t)NB * m + 2 * cw) * sizeof(cplx) <= 200 * 1024) cw *= 2;
+  const int nct = (n + cw - 1) / cw;
+  const size_t smem = ((size_t)cw * m + (size_t)NB * m + cw) * sizeof(cplx);
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem)) != cudaSuccess) return e;
+  if (occ * g_num_sms < nct) return cudaErrorNotSupported;
+  if (RH != nullptr) {
+    if ((e = cudaMemset2DAsync(RH, (size_t)ldrh * sizeof(cplx), 0, (size_t)rh_rows * sizeof(cplx), n, st)) !=
+        cudaSuccess)
+      return e;
+  }
+  if ((e = cudaMemsetAsync(gcnt, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  void* args[] = {(void*)&A, (void*)&lda, (void*)&m, (void*)&n, (void*)&cw, (void*)&tau, (void*)&RH, (void*)&ldrh,
+                  (void*)&rh_rows, (void*)&gcnt};
+  return cudaLaunchCooperativeKernel((void*)fn, dim3(nct), dim3(256), args, smem, st);
 }
 
 cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const cplx* tau, int m, int n, cplx* C,

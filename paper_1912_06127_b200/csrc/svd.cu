@@ -818,7 +818,8 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     }
     qr_cluster = false;
     if (!qrmode) {
-      // cluster-resident QR where the column bands fit shared memory
+      // cluster-resident QR where the column bands fit shared memory, else
+      // the same look-ahead QR over a cooperative grid
       e = qr_factor_cluster(st, Q1, mr, mr, nc, w1.tau, Q2, nc, nc);
       if (e == cudaSuccess) {
         if ((e = qr_factor_cluster(st, Q2, nc, nc, nc, w2.tau, d.Y, ldy, mr)) != cudaSuccess) return e;
@@ -827,6 +828,16 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
         return e;
       } else {
         cudaGetLastError();
+        unsigned* gcnt = d.flags;  // the Jacobi's counters are free before the Jacobi runs
+        e = qr_factor_grid(st, Q1, mr, mr, nc, w1.tau, Q2, nc, nc, gcnt);
+        if (e == cudaSuccess) {
+          if ((e = qr_factor_grid(st, Q2, nc, nc, nc, w2.tau, d.Y, ldy, mr, gcnt)) != cudaSuccess) return e;
+          qr_cluster = true;
+        } else if (e != cudaErrorNotSupported) {
+          return e;
+        } else {
+          cudaGetLastError();
+        }
       }
     }
     if (!qr_cluster) {
