@@ -616,15 +616,22 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
       ok[j] = blk < nb && col < nc;
       off[j] = (long long)col * ldy + vofs;
     }
-    for (int r = tid - NTX; r < nc; r += NTV) {
-      cplx v[PC];
+    // rows streamed from L2 with the next row's load in flight (latency off the chain)
+    cplx v[PC], vn[PC];
+    int r = tid - NTX;
 #pragma unroll
-      for (int j = 0; j < PC; ++j) v[j] = ok[j] ? __ldcg(Y + off[j] + r) : cmk(0.0, 0.0);
+    for (int j = 0; j < PC; ++j) v[j] = (ok[j] && r < nc) ? __ldcg(Y + off[j] + r) : cmk(0.0, 0.0);
+    for (; r < nc; r += NTV) {
+      const int rn = r + NTV;
+#pragma unroll
+      for (int j = 0; j < PC; ++j) vn[j] = (ok[j] && rn < nc) ? __ldcg(Y + off[j] + rn) : cmk(0.0, 0.0);
       if (full) rj_v_round<BW, false>(v, Ps_all[g][sb]);
       else rj_v_round<BW, true>(v, Ps_all[g][sb]);
 #pragma unroll
-      for (int j = 0; j < PC; ++j)
+      for (int j = 0; j < PC; ++j) {
         if (ok[j]) __stcg(Y + off[j] + r, v[j]);
+        v[j] = vn[j];
+      }
     }
     }
     if (flags) {
@@ -813,6 +820,8 @@ constexpr Row kTab[] = {
     {2, 4, 1, 0, 256, 256},     // 16: as 15 with 8 V warps
     {2, 4, 4, 0, 64, 128},      // 17: X <= 256 rows, 2 X warps (4 rows each)
     {2, 4, 8, 0, 32, 128},      // 18: X <= 256 rows, 1 X warp (8 rows each)
+    {2, 4, 4, 0, 256, 128},     // 19: X <= 1024, 4 V warps
+    {2, 4, 2, 0, 256, 64},      // 20: X <= 512, 2 V warps
 };
 constexpr int kNTab = sizeof(kTab) / sizeof(kTab[0]);
 
@@ -836,7 +845,9 @@ RjVariant rj_variant(int row, bool cl) {
     case 15: return rj2_pick<4, 1, 256, 128>(cl);
     case 16: return rj2_pick<4, 1, 256, 256>(cl);
     case 17: return rj2_pick<4, 4, 64, 128>(cl);
-    default: return rj2_pick<4, 8, 32, 128>(cl);
+    case 18: return rj2_pick<4, 8, 32, 128>(cl);
+    case 19: return rj2_pick<4, 4, 256, 128>(cl);
+    default: return rj2_pick<4, 2, 256, 64>(cl);
   }
 }
 
@@ -867,7 +878,7 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
   int row = -1;
   if (forced >= 0 && forced < kNTab && rows_ok(forced, mr, nc)) row = forced;
   if (row < 0) {
-    const int prefer[] = {6, 7, 8};  // measured fastest first (microbench.py --svd, B200)
+    const int prefer[] = {6, 10, 19};  // measured fastest first (microbench.py --svd, B200)
     for (int r : prefer)
       if (rows_ok(r, mr, nc)) { row = r; break; }
   }
