@@ -356,6 +356,15 @@ __device__ __forceinline__ unsigned ld_acquire_cluster_local(const unsigned* loc
 }
 
 __device__ unsigned long long g_qr_prof[16][4];
+// 1/x for normal nonzero x: MUFU seed + two Newton steps (full double precision)
+__device__ __forceinline__ double qr_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
 __device__ unsigned long long g_qr_ph[8];
 __constant__ int qr_ph_cta = 15;
 __device__ __forceinline__ unsigned long long gtime() {
@@ -448,42 +457,42 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (tid == 0 && crank < 16) g_qr_prof[crank][1] = gtime();
   // ---------------- phase 2: factor the own band with look-ahead
+  // warp 0 carries ||A[k+1:, k]||^2 of the next pivot column from its
+  // look-ahead update, so a reflector costs one pass over its column
+  double xn2_next = 0.0;
+  if (wid == 0 && ncl > 0) {
+    for (int r = c0 + 1 + lane; r < m; r += 32) xn2_next += cabs2(Aloc[r]);
+    xn2_next = warp_sum(xn2_next);
+  }
   for (int i = 0; i < ncl; ++i) {
     const int k = c0 + i;
     cplx* col = Aloc + (long long)i * m;
-    const bool ph = (crank == qr_ph_cta && tid == 0);
-    unsigned long long pt0 = ph ? clock64() : 0ull;
-#define QPH(i) if (ph) { const unsigned long long _t = clock64(); g_qr_ph[i] += _t - pt0; pt0 = _t; }
     if (wid == 0) {
-      double xn2 = 0.0;
-      for (int r = k + 1 + lane; r < m; r += 32) xn2 += cabs2(col[r]);
-      xn2 = warp_sum(xn2);
-      if (ph && xn2 == -1.0) g_qr_ph[7]++;
-      QPH(0)
+      const double xn2 = xn2_next;
       const double ar = col[k].x, ai = col[k].y;
       cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
       double beta = ar;
       const bool refl = !(xn2 == 0.0 && ai == 0.0);
       if (refl) {
         beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
-        const double ib = 1.0 / beta;
+        const double ib = qr_rcp(beta);
         t_i = cmk((beta - ar) * ib, -ai * ib);
         const double dr = ar - beta, di = ai;
-        const double iden = 1.0 / (dr * dr + di * di);
+        const double iden = qr_rcp(dr * dr + di * di);
         scale = cmk(dr * iden, -di * iden);
-        if (ph && scale.x == -1.0) g_qr_ph[7]++;
-        QPH(1)
-        for (int r = k + 1 + lane; r < m; r += 32) col[r] = cmul(col[r], scale);
       }
-      __syncwarp();
+      // scale the tail into v_k and hand it to the consumers through L2 (not
+      // DSMEM: a producer's shared-memory port would serve every later CTA)
+      for (int r = k + 1 + lane; r < m; r += 32) {
+        const cplx v = refl ? cmul(col[r], scale) : col[r];
+        col[r] = v;
+        __stcg(A + (long long)k * lda + r, v);
+      }
       if (lane == 0) {
         col[k] = cmk(beta, 0.0);
         s_tau[i] = t_i;
         __stcg(tau + k, t_i);
       }
-      // the consumers read the reflector from L2, not through DSMEM: a
-      // producer's shared-memory port would otherwise serve every later CTA
-      for (int r = k + 1 + lane; r < m; r += 32) __stcg(A + (long long)k * lda + r, col[r]);
       __syncwarp();
       // publish v_k to every later CTA (release orders the warp's writes
       // above); inside the band only every QR_PUB-th reflector, the band's
@@ -499,17 +508,19 @@ __global__ void __launch_bounds__(NT, 1)
             st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
         }
       }
-      QPH(2)
     }
     asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
-    QPH(3)
     const cplx ct = cconj(s_tau[i]);
-    if (ct.x != 0.0 || ct.y != 0.0) {
-      // warp 0: column i+1 (the next pivot); warps 1..: columns i+2, ...
-      const int jstart = (wid == 0) ? i + 1 : i + 1 + wid;
-      const int jstep = (wid == 0) ? ncl : NW - 1;
-      for (int jl = jstart; jl < ncl; jl += jstep) {
-        cplx* aj = Aloc + (long long)jl * m;
+    if (wid == 0) xn2_next = 0.0;
+    // warp 0: column i+1 (the next pivot, also its norm below row k+1);
+    // warps 1..: columns i+2, ...
+    const int jstart = (wid == 0) ? i + 1 : i + 1 + wid;
+    const int jstep = (wid == 0) ? ncl : NW - 1;
+    for (int jl = jstart; jl < ncl; jl += jstep) {
+      cplx* aj = Aloc + (long long)jl * m;
+      const bool upd = ct.x != 0.0 || ct.y != 0.0;
+      cplx f = cmk(0.0, 0.0);
+      if (upd) {
         double dr = 0.0, di = 0.0;
         for (int r = k + lane; r < m; r += 32) {
           const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
@@ -519,18 +530,20 @@ __global__ void __launch_bounds__(NT, 1)
         }
         dr = warp_sum(dr);
         di = warp_sum(di);
-        const cplx f = cmul(ct, cmk(dr, di));
-        for (int r = k + lane; r < m; r += 32) {
-          const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
-          aj[r] = csub(aj[r], cmul(v, f));
-        }
-        if (wid == 0) {
-          if (ph && aj[m - 1].x == -1.2345) g_qr_ph[7]++;
-          break;
-        }
+        f = cmul(ct, cmk(dr, di));
+      }
+      double nx = 0.0;
+      for (int r = k + lane; r < m; r += 32) {
+        const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
+        const cplx a = upd ? csub(aj[r], cmul(v, f)) : aj[r];
+        aj[r] = a;
+        if (r > k + 1) nx += cabs2(a);
+      }
+      if (wid == 0) {
+        xn2_next = warp_sum(nx);
+        break;
       }
     }
-    QPH(4)
     // next iteration: warp 0 reads column i+1 (updated by itself); the workers'
     // updates of column i+2 are ordered before warp 0 touches it by the next
     // bar.sync 2
