@@ -106,6 +106,24 @@ int tdvp_measure_sz(tdvp_t h, double* sz /* [L] */);
 int tdvp_measure_energy(tdvp_t h, double* E);
 int tdvp_measure_norm(tdvp_t h, double* norm2 /* <psi|psi> */);
 
+/* <psi_a|psi_b> of two handles' current states (same L, d, device; local
+ * mode).  Used for the infidelity I = 1 - |<a|b>| / sqrt(<a|a><b|b>) between
+ * a serial and a segment-parallel run (PAPER.md, benchmark section: "the
+ * infidelity between the states obtained serially and in parallel").  Reads
+ * both states, modifies neither; synchronises both handles' streams.
+ * Errors: TDVP_EARG (null / mismatched handles), TDVP_ESTATE (no MPO/MPS, or the
+ * state is distributed across ranks). */
+int tdvp_overlap(tdvp_t a, tdvp_t b, double* re, double* im);
+
+/* Reorthonormalisation: re-gauge the current MPS into
+ * inverse-canonical form by an SVD sweep left->right and one right->left on
+ * the device (singular values below 1e-14 sigma_1 are dropped, the state is
+ * normalised to 1), then rebuild the environments at the next tdvp_step.  The
+ * physical state is unchanged up to that floor and the normalisation; the
+ * Lambda_j afterwards are its exact Schmidt values.  Serial; local mode only.
+ * Errors: TDVP_ESTATE (no MPO/MPS, distributed), TDVP_ENUMERIC (zero norm). */
+int tdvp_reorthonormalize(tdvp_t h);
+
 int tdvp_get_stats(tdvp_t h, tdvp_stats* s);
 /* Current bond dimensions (owner view): chi[L+1]. */
 int tdvp_get_chi(tdvp_t h, int* chi);

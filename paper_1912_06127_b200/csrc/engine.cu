@@ -1233,6 +1233,155 @@ int tdvp_measure_norm(tdvp_t h, double* n) {
   return TDVP_OK;
 }
 
+// chain tensors M_j = Psi_j diag(V_j) (j < L-1), M_{L-1} = Psi_{L-1} of a local-mode handle
+static std::vector<BufPtr> chain_tensors(tdvp_ctx* h, std::vector<int>& chi) {
+  const int L = h->L, d = h->d;
+  if (h->layout_p == 0) layout(h, 1);
+  chi.assign(L + 1, 1);
+  for (int j = 1; j < L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
+  std::vector<BufPtr> M(L);
+  for (int j = 0; j < L; ++j) {
+    Segment& g = h->segs[owner_of(h, j)];
+    const long long n = (long long)chi[j] * d * chi[j + 1];
+    M[j] = make_buf(n * sizeof(cplx));
+    if (j < L - 1) CK(scale_cols(h->st, M[j]->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)chi[j] * d, chi[j + 1]));
+    else CK(copy_cplx(h->st, M[j]->c(), P(g.psi[j]), n));
+  }
+  return M;
+}
+
+// <psi_a | psi_b> by a two-state zipper (PAPER.md Sec. benchmarks, infidelity
+// I = 1 - |<1|2>| / sqrt(<1|1><2|2>)): E_{j+1} = M1_j^H (E_j M2_j)
+int tdvp_overlap(tdvp_t a, tdvp_t b, double* re, double* im) {
+  if (!a || !b || !re || !im) return TDVP_EARG;
+  try {
+    if (a->L != b->L || a->d != b->d) throw TdvpError(TDVP_EARG, "overlap: handles differ in L or d");
+    if (!a->have_mps || !b->have_mps || !a->have_mpo || !b->have_mpo)
+      throw TdvpError(TDVP_ESTATE, "overlap: MPO and MPS must be set on both handles");
+    if (!local_mode(a) || !local_mode(b)) throw TdvpError(TDVP_ESTATE, "overlap across ranks: gather the MPS first");
+    if (a->dev != b->dev) throw TdvpError(TDVP_EARG, "overlap: handles on different devices");
+    const int L = a->L, d = a->d;
+    std::vector<int> ca, cb;
+    std::vector<BufPtr> Ma = chain_tensors(a, ca);
+    std::vector<BufPtr> Mb = chain_tensors(b, cb);
+    CK(cudaStreamSynchronize(b->st));  // b's tensors are read on a's stream
+    long long tmax = 1, emax = 1;
+    for (int j = 0; j <= L; ++j) emax = std::max(emax, (long long)ca[j] * cb[j]);
+    for (int j = 0; j < L; ++j) tmax = std::max(tmax, (long long)ca[j] * d * cb[j + 1]);
+    BufPtr E0 = make_buf(emax * sizeof(cplx)), E1 = make_buf(emax * sizeof(cplx)), T = make_buf(tmax * sizeof(cplx));
+    const cplx one = ONE;
+    CK(cudaMemcpyAsync(E0->p, &one, sizeof(cplx), cudaMemcpyHostToDevice, a->st));
+    for (int j = 0; j < L; ++j) {
+      // T[a1][(s,b2)] = sum_a2 E[a1][a2] M2[a2][(s,b2)]
+      gemm(a, OP_N, OP_N, ca[j], d * cb[j + 1], cb[j], E0->c(), cb[j], Mb[j]->c(), (long long)d * cb[j + 1], T->c(),
+           (long long)d * cb[j + 1]);
+      // E'[b1][b2] = sum_{(a1,s)} conj(M1[(a1,s)][b1]) T[(a1,s)][b2]
+      gemm(a, OP_C, OP_N, ca[j + 1], cb[j + 1], ca[j] * d, Ma[j]->c(), ca[j + 1], T->c(), cb[j + 1], E1->c(),
+           cb[j + 1]);
+      std::swap(E0, E1);
+    }
+    cplx r;
+    CK(cudaMemcpyAsync(&r, E0->p, sizeof(cplx), cudaMemcpyDeviceToHost, a->st));
+    CK(cudaStreamSynchronize(a->st));
+    *re = r.x;
+    *im = r.y;
+  } catch (const TdvpError& e) {
+    return fail(a, e);
+  }
+  return TDVP_OK;
+}
+
+// Reorthonormalisation (Fig. reorth): exact re-gauging of the
+// current chain into inverse-canonical form on the device -- an SVD sweep L->R
+// (A_j <- U, A_{j+1} <- S W^dagger A_{j+1}) and one R->L (B_j = W^dagger,
+// Lambda_{j-1} = S, A_{j-1} <- A_{j-1} U S), singular values below 1e-14
+// sigma_1 dropped, the state normalised -- then the environments are rebuilt
+// at the next step (a serial procedure, as in the paper).
+int tdvp_reorthonormalize(tdvp_t h) {
+  if (!h) return TDVP_EARG;
+  try {
+    if (!h->have_mps || !h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set");
+    if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "reorthonormalisation across ranks: gather the MPS first");
+    const int L = h->L, d = h->d;
+    std::vector<int> chi;
+    std::vector<BufPtr> A = chain_tensors(h, chi);
+    long long big = 1;
+    for (int j = 0; j < L; ++j) big = std::max(big, (long long)h->cbmax[j] * d * h->cbmax[j + 1]);
+    BufPtr pl = make_buf(big * sizeof(cplx)), pr = make_buf(big * sizeof(cplx)), tmp = make_buf(big * sizeof(cplx));
+    BufPtr lam = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
+    BufPtr vin = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
+    std::vector<std::vector<double>> hlam(L - 1);
+    const TruncParams tp{h->chi_max, 0.0, 0.0, 0.0};
+    auto svd = [&](const cplx* M, int m, int n, int& k) {
+      int r = 0, ce = 0, sw = 0;
+      double w = 0.0;
+      cudaError_t se = svd_truncate_split(h->st, h->sv, M, m, n, tp, pl->c(), pr->c(), lam->d(), vin->d(), &k, &w, &r,
+                                          &ce, &sw);
+      if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "SVD numerical failure in reorthonormalisation");
+      CK(se);
+    };
+    // L -> R: A_j = U S W^dagger  ->  A_j = U,  A_{j+1} = (S W^dagger) A_{j+1}
+    for (int j = 0; j + 1 < L; ++j) {
+      int k = 0;
+      svd(A[j]->c(), chi[j] * d, chi[j + 1], k);
+      if (k > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: reorthonormalisation rank");
+      BufPtr U = make_buf((size_t)chi[j] * d * k * sizeof(cplx));
+      CK(scale_cols(h->st, U->c(), pl->c(), vin->d(), (long long)chi[j] * d, k));
+      gemm(h, OP_N, OP_N, k, d * chi[j + 2], chi[j + 1], pr->c(), chi[j + 1], A[j + 1]->c(), (long long)d * chi[j + 2],
+           tmp->c(), (long long)d * chi[j + 2]);
+      BufPtr An = make_buf((size_t)k * d * chi[j + 2] * sizeof(cplx));
+      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)k * d * chi[j + 2]));
+      A[j] = std::move(U);
+      A[j + 1] = std::move(An);
+      chi[j + 1] = k;
+    }
+    // R -> L: A_j = U S W^dagger  ->  B_j = W^dagger, Lambda_{j-1} = S, A_{j-1} = A_{j-1} (U S)
+    for (int j = L - 1; j >= 1; --j) {
+      int k = 0;
+      svd(A[j]->c(), chi[j], d * chi[j + 1], k);
+      BufPtr B = make_buf((size_t)k * d * chi[j + 1] * sizeof(cplx));
+      CK(scale_rows(h->st, B->c(), pr->c(), vin->d(), k, (long long)d * chi[j + 1]));
+      gemm(h, OP_N, OP_N, chi[j - 1] * d, k, chi[j], A[j - 1]->c(), chi[j], pl->c(), k, tmp->c(), k);
+      BufPtr An = make_buf((size_t)chi[j - 1] * d * k * sizeof(cplx));
+      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)chi[j - 1] * d * k));
+      hlam[j - 1].resize(k);
+      CK(cudaMemcpyAsync(hlam[j - 1].data(), lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      A[j] = std::move(B);
+      A[j - 1] = std::move(An);
+      chi[j] = k;
+    }
+    // download, normalise, Psi_0 = A_0 / n, Lambda /= n, Psi_j = Lambda_{j-1} B_j
+    std::vector<std::vector<double>> hpsi(L);
+    for (int j = 0; j < L; ++j) {
+      hpsi[j].resize((size_t)chi[j] * d * chi[j + 1] * 2);
+      CK(cudaMemcpyAsync(hpsi[j].data(), A[j]->p, hpsi[j].size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    double nrm = 0.0;
+    for (double v : hpsi[0]) nrm += v * v;
+    nrm = std::sqrt(nrm);
+    if (!(nrm > 0.0) || !std::isfinite(nrm)) throw TdvpError(TDVP_ENUMERIC, "zero or non-finite norm");
+    for (double& v : hpsi[0]) v /= nrm;
+    for (auto& l : hlam)
+      for (double& v : l) v /= nrm;
+    for (int j = 1; j < L; ++j) {
+      const int cl = chi[j], rest = d * chi[j + 1];
+      for (int a = 0; a < cl; ++a)
+        for (int e = 0; e < 2 * rest; ++e) hpsi[j][(size_t)a * 2 * rest + e] *= hlam[j - 1][a];
+    }
+    h->h_psi = std::move(hpsi);
+    h->h_lam = std::move(hlam);
+    h->h_chi = chi;
+    h->envs_valid = false;
+    h->layout_p = 0;  // re-layout: upload + sequential environment build at the next call
+    h->segs.clear();
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
 int tdvp_get_stats(tdvp_t h, tdvp_stats* s) {
   if (!h || !s) return TDVP_EARG;
   int brk = 0;

@@ -57,6 +57,8 @@ _SIGS = {
     "tdvp_measure_sz": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_norm": (C.c_int, [C.c_void_p, _D]),
+    "tdvp_overlap": (C.c_int, [C.c_void_p, C.c_void_p, _D, _D]),
+    "tdvp_reorthonormalize": (C.c_int, [C.c_void_p]),
     "tdvp_get_stats": (C.c_int, [C.c_void_p, C.POINTER(tdvp_stats)]),
     "tdvp_get_chi": (C.c_int, [C.c_void_p, _I]),
     "tdvp_get_mps": (C.c_int, [C.c_void_p, _PD, _PD]),
@@ -157,6 +159,29 @@ class Tdvp:
         e = C.c_double()
         _check(lib().tdvp_measure_norm(self.h, C.byref(e)), self.h)
         return e.value
+
+    def overlap(self, other):
+        """<self|other> (tdvp_overlap)."""
+        re, im = C.c_double(), C.c_double()
+        _check(lib().tdvp_overlap(self.h, other.h, C.byref(re), C.byref(im)), self.h)
+        return complex(re.value, im.value)
+
+    def infidelity(self, other):
+        """I = 1 - |<a|b>| / sqrt(<a|a><b|b>) (PAPER.md benchmark section)."""
+        return 1.0 - abs(self.overlap(other)) / np.sqrt(self.measure_norm() * other.measure_norm())
+
+    def reorthonormalize(self):
+        """Exact re-gauging into inverse-canonical form (tdvp_reorthonormalize)."""
+        _check(lib().tdvp_reorthonormalize(self.h), self.h)
+
+    def maybe_reorthonormalize(self, tol):
+        """Reorthonormalise when the norm error |<psi|psi> - 1| exceeds tol
+        (PAPER.md:517: "if the error in the norm grows unacceptably large");
+        returns whether it did."""
+        if abs(self.measure_norm() - 1.0) > tol:
+            self.reorthonormalize()
+            return True
+        return False
 
     def stats(self):
         s = tdvp_stats()
