@@ -4,6 +4,7 @@
 // HBM-bound gather/FMA over the (chi x chi) plane, not a GEMM: one thread per
 // (outer, inner) point loops over all output channels; consecutive threads
 // walk the contiguous inner index so every load/store is coalesced.
+#include <mutex>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -54,11 +55,15 @@ cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner
   if (n_outer <= 0 || n_inner <= 0) return cudaSuccess;
   const size_t sm = (size_t)cm.nnz * (sizeof(cplx) + sizeof(long long)) + (size_t)cm.n_oc * sizeof(long long) +
                     (size_t)(cm.n_oc + 1) * sizeof(int);
-  static size_t configured = 48 * 1024;
-  if (sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(chanmix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = sm;
+  static size_t configured = 48 * 1024;  // only grows; guarded for concurrent segment lanes
+  static std::mutex mu;
+  if (sm > 48 * 1024) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (sm > configured) {
+      cudaError_t e = cudaFuncSetAttribute(chanmix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      configured = sm;
+    }
   }
   dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
   chanmix_kernel<<<grid, TPB, sm, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out, out_ch);

@@ -11,8 +11,13 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -132,9 +137,35 @@ struct Segment {
   std::vector<int> wdim;
 };
 
+// One boundary message between segment lanes (SEND_R: Psi'_{e+1}, Lambda'_e,
+// V_e, beta_{e+1}; SEND_L: Psi_s, gamma_s): the sender copies
+// into the staging buffers on its stream and records `posted`; the receiver
+// waits for it on its stream, copies out and records `consumed`, which the
+// next send on this channel waits for.  Depth 1: per half-step every channel
+// carries at most one message, and the receiver consumes it within the same
+// half (segment_program), so a blocked sender never closes a cycle.
+struct LaneMsg {
+  std::mutex m;
+  std::condition_variable cv;
+  int ready = 0;
+  int meta[2] = {0, 0};
+  cudaEvent_t posted = nullptr, consumed = nullptr;
+  bool consumed_rec = false;
+  BufPtr psi, lam, vinv, env;
+  ~LaneMsg() {
+    if (posted) cudaEventDestroy(posted);
+    if (consumed) cudaEventDestroy(consumed);
+  }
+};
+
 }  // namespace
 
 struct tdvp_ctx {
+  tdvp_ctx() : mpo(mpo_own) {}
+  // a segment lane: own stream and workspace, the parent's MPO
+  explicit tdvp_ctx(tdvp_ctx* par) : mpo(par->mpo_own), parent(par) {}
+  tdvp_ctx(const tdvp_ctx&) = delete;
+  tdvp_ctx& operator=(const tdvp_ctx&) = delete;
   int L = 0, d = 0, Dmpo = 0, chi_max = 0;
   tdvp_params prm{};
   // Jacobi warm start from the previous visit of a bond (TDVP_SVD_WARM=1: on).
@@ -146,7 +177,8 @@ struct tdvp_ctx {
   cudaStream_t st = nullptr;
   std::string err;
   std::vector<int> cbmax;  // L+1
-  std::vector<MpoSite> mpo;
+  std::vector<MpoSite> mpo_own;
+  std::vector<MpoSite>& mpo;  // lanes: the parent's sites
   MpoSite mpo_id, mpo_sz;  // D = 1 identity / S^z (measurement)
   bool have_mpo = false, have_mps = false, envs_valid = false;
   int layout_p = 0;  // segments currently laid out
@@ -174,10 +206,38 @@ struct tdvp_ctx {
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   BufPtr hdr;
+  // Segment lanes (single process, p > 1): segment q runs on lane q -- its
+  // own host thread, stream and workspace (lane 0 = this handle) -- so the p
+  // segments' sweeps run concurrently on one GPU; boundary messages go
+  // through staging buffers ordered by events (LaneMsg).  TDVP_LANES=0: the
+  // round-robin executor on one stream.
+  tdvp_ctx* parent = nullptr;
+  bool lanes_on = true;
+  std::vector<std::unique_ptr<tdvp_ctx>> lanes;  // lanes 1 .. p-1
+  std::vector<std::unique_ptr<LaneMsg>> msg_r, msg_l;  // per segment: to q+1, to q-1
+  ~tdvp_ctx();
 };
 
-long long g_launch_count = 0;
-long long g_gemm_count = 0;
+std::atomic<long long> g_launch_count{0};
+std::atomic<long long> g_gemm_count{0};
+
+tdvp_ctx::~tdvp_ctx() {
+  if (st) cudaStreamSynchronize(st);
+  lanes.clear();
+  msg_r.clear();
+  msg_l.clear();
+  segs.clear();
+  mpo_own.clear();
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (ev_step0) cudaEventDestroy(ev_step0);
+  if (ev_step1) cudaEventDestroy(ev_step1);
+  for (auto e : sv.ev_jac)
+    if (e) cudaEventDestroy(e);
+  if (h_pin) cudaFreeHost(h_pin);
+  if (h_ipin) cudaFreeHost(h_ipin);
+  if (comm && nccl().ok) nccl().CommDestroy(comm);
+  if (st) cudaStreamDestroy(st);
+}
 
 namespace {
 
@@ -664,6 +724,8 @@ void layout(tdvp_ctx* h, int p) {
     alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second);
   }
   h->layout_p = p;
+  h->msg_r.clear();
+  h->msg_l.clear();
   upload_state(h);
   build_envs(h);
   h->envs_valid = true;
@@ -814,6 +876,225 @@ void run_half(tdvp_ctx* h, int hh, double dt, const std::set<int>& merged) {
   }
 }
 
+// ------------------------------------------------------------ segment lanes
+void alloc_workspace(tdvp_ctx* h);
+
+tdvp_ctx* lane_of(tdvp_ctx* h, int q) {
+  if (q == 0) return h;
+  while ((int)h->lanes.size() < q) {
+    std::unique_ptr<tdvp_ctx> ln(new tdvp_ctx(h));
+    ln->L = h->L;
+    ln->d = h->d;
+    ln->Dmpo = h->Dmpo;
+    ln->chi_max = h->chi_max;
+    ln->cbmax = h->cbmax;
+    ln->dev = h->dev;
+    CK(cudaStreamCreateWithFlags(&ln->st, cudaStreamNonBlocking));
+    alloc_workspace(ln.get());
+    ln->lz.brk_count = h->lz_brk->i();  // one breakdown counter per handle
+    h->lanes.push_back(std::move(ln));
+  }
+  return h->lanes[q - 1].get();
+}
+
+// staging buffers for the boundary messages of the current layout
+void alloc_msgs(tdvp_ctx* h) {
+  const int p = h->layout_p, d = h->d;
+  h->msg_r.clear();
+  h->msg_l.clear();
+  h->msg_r.resize(p);
+  h->msg_l.resize(p);
+  auto mk = [&](std::unique_ptr<LaneMsg>& m, size_t psi, size_t lam, size_t env) {
+    m.reset(new LaneMsg());
+    CK(cudaEventCreateWithFlags(&m->posted, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->consumed, cudaEventDisableTiming));
+    m->psi = make_buf(psi * sizeof(cplx));
+    m->env = make_buf(env * sizeof(cplx));
+    if (lam) {
+      m->lam = make_buf(lam * sizeof(double));
+      m->vinv = make_buf(lam * sizeof(double));
+    }
+  };
+  for (int q = 0; q < p; ++q) {
+    const int s = h->bounds[q].first, e = h->bounds[q].second;
+    if (q + 1 < p) {
+      const size_t c1 = h->cbmax[e + 1], c2 = h->cbmax[e + 2];
+      mk(h->msg_r[q], c1 * d * c2, c1, c1 * h->mpo[e + 1].Dl * c1);
+    }
+    if (q > 0) {
+      const size_t c0 = h->cbmax[s], c1 = h->cbmax[s + 1];
+      mk(h->msg_l[q], c0 * d * c1, 0, c1 * h->mpo[s].Dr * c1);
+    }
+  }
+}
+
+void lane_wait(LaneMsg& m, int want, const std::atomic<bool>& abort) {
+  std::unique_lock<std::mutex> lk(m.m);
+  m.cv.wait(lk, [&] { return m.ready == want || abort.load(); });
+  if (m.ready != want) throw TdvpError(TDVP_ECUDA, "segment lane aborted");
+}
+void lane_post(LaneMsg& m, int ready, bool consumed) {
+  {
+    std::lock_guard<std::mutex> lk(m.m);
+    m.ready = ready;
+    if (consumed) m.consumed_rec = true;
+  }
+  m.cv.notify_all();
+}
+void lane_copy(tdvp_ctx* ln, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ln->st));
+}
+
+// SEND_R / RECV_L: Psi'_{e+1}, Lambda'_e, V_e, beta_{e+1}
+void lane_send_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<bool>& abort) {
+  lane_wait(m, 0, abort);
+  if (m.consumed_rec) CK(cudaStreamWaitEvent(ln->st, m.consumed, 0));
+  const int e = a.e, d = ln->d, chi = a.cb[e + 1], cr = a.cb[e + 2];
+  lane_copy(ln, m.psi->p, a.psi[e + 1]->p, (size_t)chi * d * cr * sizeof(cplx));
+  lane_copy(ln, m.lam->p, a.lam[e]->p, (size_t)chi * sizeof(double));
+  lane_copy(ln, m.vinv->p, a.vinv[e]->p, (size_t)chi * sizeof(double));
+  lane_copy(ln, m.env->p, a.beta[e + 1]->p, (size_t)chi * ln->mpo[e + 1].Dl * chi * sizeof(cplx));
+  CK(cudaEventRecord(m.posted, ln->st));
+  m.meta[0] = chi;
+  m.meta[1] = cr;
+  lane_post(m, 1, false);
+}
+void lane_recv_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool>& abort) {
+  lane_wait(m, 1, abort);
+  CK(cudaStreamWaitEvent(ln->st, m.posted, 0));
+  const int e = b.s - 1, d = ln->d, chi = m.meta[0], cr = m.meta[1];
+  b.cb[e + 1] = chi;
+  lane_copy(ln, b.psi[e + 1]->p, m.psi->p, (size_t)chi * d * cr * sizeof(cplx));
+  lane_copy(ln, b.lam[e]->p, m.lam->p, (size_t)chi * sizeof(double));
+  lane_copy(ln, b.vinv[e]->p, m.vinv->p, (size_t)chi * sizeof(double));
+  lane_copy(ln, b.beta[e + 1]->p, m.env->p, (size_t)chi * ln->mpo[e + 1].Dl * chi * sizeof(cplx));
+  CK(cudaEventRecord(m.consumed, ln->st));
+  lane_post(m, 0, true);
+}
+// SEND_L / RECV_R: Psi_s, gamma_s
+void lane_send_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool>& abort) {
+  lane_wait(m, 0, abort);
+  if (m.consumed_rec) CK(cudaStreamWaitEvent(ln->st, m.consumed, 0));
+  const int s = b.s, d = ln->d, cl = b.cb[s], cr = b.cb[s + 1];
+  lane_copy(ln, m.psi->p, b.psi[s]->p, (size_t)cl * d * cr * sizeof(cplx));
+  lane_copy(ln, m.env->p, b.gamma[s]->p, (size_t)cr * ln->mpo[s].Dr * cr * sizeof(cplx));
+  CK(cudaEventRecord(m.posted, ln->st));
+  m.meta[0] = cl;
+  m.meta[1] = cr;
+  lane_post(m, 1, false);
+}
+void lane_recv_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<bool>& abort) {
+  lane_wait(m, 1, abort);
+  CK(cudaStreamWaitEvent(ln->st, m.posted, 0));
+  const int s = a.e + 1, d = ln->d, cl = m.meta[0], cr = m.meta[1];
+  a.cb[s] = cl;
+  a.cb[s + 1] = cr;
+  lane_copy(ln, a.psi[s]->p, m.psi->p, (size_t)cl * d * cr * sizeof(cplx));
+  lane_copy(ln, a.gamma[s]->p, m.env->p, (size_t)cr * ln->mpo[s].Dr * cr * sizeof(cplx));
+  CK(cudaEventRecord(m.consumed, ln->st));
+  lane_post(m, 0, true);
+}
+
+void reset_step_stats(tdvp_ctx* h) {
+  h->stats.w_step = 0.0;
+  h->stats.trunc_active = 0;
+  h->stats.n_pair = h->stats.n_back = 0;
+  h->stats.svd_sweeps_max = 0;
+  h->stats.svd_sweeps_total = 0;
+  h->stats.svd_warm = 0;
+  h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
+  h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
+  h->stats.heff2_calls = 0;
+  h->ev_used = 0;
+  h->ev_h2.clear();
+  h->ev_h1.clear();
+  h->ev_svd.clear();
+  h->ev_lz2.clear();
+  h->ev_lz1.clear();
+  h->ev_env.clear();
+}
+
+// both half-steps of segment q on its lane (the per-rank program of the NCCL
+// executor, with lane messages in place of send/recv)
+void lane_program(tdvp_ctx* h, int q, double dt, const std::set<int>& merged, const std::atomic<bool>& abort) {
+  tdvp_ctx* ln = lane_of(h, q);
+  Segment& g = h->segs[q];
+  const int L = h->L, p = h->layout_p;
+  for (int hh = 1; hh <= 2; ++hh)
+    for (const SchedOp& op : segment_program(L, p, hh, q, h->bounds[q], merged)) {
+      if (abort.load()) throw TdvpError(TDVP_ECUDA, "segment lane aborted");
+      switch (op.kind) {
+        case OP_SEND_R: lane_send_right(ln, g, *h->msg_r[q], abort); break;
+        case OP_RECV_L: lane_recv_left(ln, g, *h->msg_r[q - 1], abort); break;
+        case OP_SEND_L: lane_send_left(ln, g, *h->msg_l[q], abort); break;
+        case OP_RECV_R: lane_recv_right(ln, g, *h->msg_l[q + 1], abort); break;
+        default: exec_compute(ln, g, op, dt);
+      }
+    }
+}
+
+// one step with p concurrent lanes; the caller recorded ev_step0 on h->st
+void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
+  const int p = h->layout_p;
+  for (int q = 1; q < p; ++q) {
+    tdvp_ctx* ln = lane_of(h, q);
+    ln->prm = h->prm;
+    ln->warm_svd = h->warm_svd;
+    ln->lz_fused = h->lz_fused;
+    reset_step_stats(ln);
+    CK(cudaStreamWaitEvent(ln->st, h->ev_step0, 0));
+  }
+  std::atomic<bool> abort{false};
+  std::vector<std::exception_ptr> errs(p);
+  auto body = [&](int q) {
+    try {
+      CK(cudaSetDevice(h->dev));
+      lane_program(h, q, dt, merged, abort);
+    } catch (...) {
+      errs[q] = std::current_exception();
+      abort.store(true);
+      for (auto* v : {&h->msg_r, &h->msg_l})
+        for (auto& m : *v)
+          if (m) {
+            std::lock_guard<std::mutex> lk(m->m);
+            m->cv.notify_all();
+          }
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(p - 1);
+  for (int q = 1; q < p; ++q) th.emplace_back(body, q);
+  body(0);
+  for (auto& t : th) t.join();
+  for (int q = 0; q < p; ++q)
+    if (errs[q]) {
+      for (int r = 1; r < p; ++r) cudaStreamSynchronize(h->lanes[r - 1]->st);
+      for (auto* v : {&h->msg_r, &h->msg_l})
+        for (auto& m : *v)
+          if (m) m->ready = 0, m->consumed_rec = false;
+      std::rethrow_exception(errs[q]);
+    }
+  for (int q = 1; q < p; ++q) {
+    tdvp_ctx* ln = h->lanes[q - 1].get();
+    const int ev = ev_record(ln);
+    CK(cudaStreamWaitEvent(h->st, ln->ev_pool[ev], 0));
+    tdvp_stats& a = h->stats;
+    const tdvp_stats& b = ln->stats;
+    a.w_step += b.w_step;
+    a.trunc_active |= b.trunc_active;
+    a.n_pair += b.n_pair;
+    a.n_back += b.n_back;
+    a.svd_sweeps_max = std::max(a.svd_sweeps_max, b.svd_sweeps_max);
+    a.svd_sweeps_total += b.svd_sweeps_total;
+    a.svd_warm += b.svd_warm;
+    a.svd_jac_ms += b.svd_jac_ms;
+    a.svd_jac_flop += b.svd_jac_flop;
+    a.heff2_flop += b.heff2_flop;
+    a.heff2_calls += b.heff2_calls;
+    a.heff1_flop += b.heff1_flop;
+  }
+}
+
 void finish_timing(tdvp_ctx* h) {
   auto sum = [&](const std::vector<std::pair<int, int>>& v) {
     double t = 0.0;
@@ -836,27 +1117,18 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step");
   if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
   if (p != h->layout_p || !h->envs_valid) layout(h, p);
-  h->stats.w_step = 0.0;
-  h->stats.trunc_active = 0;
-  h->stats.n_pair = h->stats.n_back = 0;
-  h->stats.svd_sweeps_max = 0;
-  h->stats.svd_sweeps_total = 0;
-  h->stats.svd_warm = 0;
-  h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
-  h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
-  h->stats.heff2_calls = 0;
-  h->ev_used = 0;
-  h->ev_h2.clear();
-  h->ev_h1.clear();
-  h->ev_svd.clear();
-  h->ev_lz2.clear();
-  h->ev_lz1.clear();
-  h->ev_env.clear();
+  reset_step_stats(h);
   const long long l0 = g_launch_count, g0 = g_gemm_count;
   CK(cudaEventRecord(h->ev_step0, h->st));
   const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
-  run_half(h, 1, dt, merged);
-  run_half(h, 2, dt, merged);
+  const bool lanes = local_mode(h) && p > 1 && h->lanes_on;
+  if (lanes) {
+    if ((int)h->msg_r.size() != p) alloc_msgs(h);
+    run_step_lanes(h, dt, merged);
+  } else {
+    run_half(h, 1, dt, merged);
+    run_half(h, 2, dt, merged);
+  }
   CK(cudaEventRecord(h->ev_step1, h->st));
   CK(cudaStreamSynchronize(h->st));
   float ms = 0.f;
@@ -865,7 +1137,21 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   h->stats.w_total += h->stats.w_step;
   h->stats.kernel_launches = g_launch_count - l0;
   h->stats.gemm_launches = g_gemm_count - g0;
-  if (h->prm.timing) finish_timing(h);
+  if (h->prm.timing) {
+    finish_timing(h);
+    if (lanes)
+      for (int q = 1; q < p; ++q) {
+        // summed device time over lanes (concurrent: may exceed step_ms)
+        tdvp_ctx* ln = h->lanes[q - 1].get();
+        finish_timing(ln);
+        h->stats.heff2_ms += ln->stats.heff2_ms;
+        h->stats.heff1_ms += ln->stats.heff1_ms;
+        h->stats.svd_ms += ln->stats.svd_ms;
+        h->stats.lanczos2_ms += ln->stats.lanczos2_ms;
+        h->stats.lanczos1_ms += ln->stats.lanczos1_ms;
+        h->stats.env_ms += ln->stats.env_ms;
+      }
+  }
 }
 
 // ------------------------------------------------------------ measurement
@@ -1030,12 +1316,7 @@ tdvp_ctx* scratch_ctx(int maxchi, int D) {
   static tdvp_ctx* sc = nullptr;
   static int cap = 0, capD = 0;
   if (sc && cap >= maxchi && capD >= D) return sc;
-  if (sc) {
-    if (sc->h_pin) cudaFreeHost(sc->h_pin);
-    if (sc->h_ipin) cudaFreeHost(sc->h_ipin);
-    if (sc->st) cudaStreamDestroy(sc->st);
-    delete sc;
-  }
+  delete sc;
   sc = new tdvp_ctx();
   init_device_globals();
   CK(cudaStreamCreateWithFlags(&sc->st, cudaStreamNonBlocking));
@@ -1079,6 +1360,7 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
     h->prm.timing = 0;
     if (const char* ev = std::getenv("TDVP_SVD_WARM")) h->warm_svd = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("TDVP_LZ_FUSED")) h->lz_fused = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("TDVP_LANES")) h->lanes_on = std::atoi(ev) != 0;
     h->cbmax.assign(L + 1, 1);
     for (int j = 0; j <= L; ++j) {
       double a = std::pow((double)d, std::min(j, 62)), b = std::pow((double)d, std::min(L - j, 62));
@@ -1424,22 +1706,7 @@ int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
 
 const char* tdvp_last_error(tdvp_t h) { return h ? h->err.c_str() : "null handle"; }
 
-void tdvp_destroy(tdvp_t h) {
-  if (!h) return;
-  if (h->st) cudaStreamSynchronize(h->st);
-  h->segs.clear();
-  h->mpo.clear();
-  for (auto e : h->ev_pool) cudaEventDestroy(e);
-  if (h->ev_step0) cudaEventDestroy(h->ev_step0);
-  if (h->ev_step1) cudaEventDestroy(h->ev_step1);
-  for (auto e : h->sv.ev_jac)
-    if (e) cudaEventDestroy(e);
-  if (h->h_pin) cudaFreeHost(h->h_pin);
-  if (h->h_ipin) cudaFreeHost(h->h_ipin);
-  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
-  if (h->st) cudaStreamDestroy(h->st);
-  delete h;
-}
+void tdvp_destroy(tdvp_t h) { delete h; }
 
 int tdvp_nccl_unique_id(unsigned char* id128) {
   if (!id128) return TDVP_EARG;
