@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--workload", default="c2sat", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lane-segments", type=int, default=8,
+                    help="also time p2TDVP with this many segments as concurrent lanes on one GPU (N=1; 0 = off)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -288,6 +290,23 @@ def main():
         e_ms = (time.perf_counter() - e0) / args.steps * 1e3
         e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": mps_bytes(mps),
                "d2h_bytes_per_step": int(sum(x.nbytes for x in psi) + sum(x.nbytes for x in lam))}
+    # p2TDVP on this one GPU: P segments as concurrent lanes (own thread,
+    # stream and workspace each), same workload, fresh state, same timing rules
+    lanes = None
+    if args.lane_segments > 1 and world == 1:
+        q = args.lane_segments
+        t.set_params(eps=wl["eps"], timing=False)
+        t.set_mps(wl["mps"].psi, wl["mps"].lam)
+        for _ in range(args.warmup):
+            t.step(dt, q)
+        torch.cuda.synchronize()
+        lms = []
+        for _ in range(args.steps):
+            t.step(dt, q)
+            lms.append(t.stats()["step_ms"])
+        lv = float(np.mean(lms))
+        lanes = {"segments": q, "executor": "concurrent segment lanes on one GPU (thread + stream per segment)",
+                 "ms_per_step": lv, "speedup_vs_serial": ms_per_step / lv if lv > 0 else None}
     t.close()
 
     if rank != 0:
@@ -329,6 +348,7 @@ def main():
         "wall_s_timed": wall,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "p2tdvp_one_gpu": lanes,
         "chi": wl["chi"],
     }
     if not args.no_cpu_baseline and world == 1:

@@ -892,6 +892,8 @@ tdvp_ctx* lane_of(tdvp_ctx* h, int q) {
     CK(cudaStreamCreateWithFlags(&ln->st, cudaStreamNonBlocking));
     alloc_workspace(ln.get());
     ln->lz.brk_count = h->lz_brk->i();  // one breakdown counter per handle
+    CK(cudaEventCreate(&ln->sv.ev_jac[0]));
+    CK(cudaEventCreate(&ln->sv.ev_jac[1]));
     h->lanes.push_back(std::move(ln));
   }
   return h->lanes[q - 1].get();
@@ -1036,8 +1038,10 @@ void lane_program(tdvp_ctx* h, int q, double dt, const std::set<int>& merged, co
 // one step with p concurrent lanes; the caller recorded ev_step0 on h->st
 void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
   const int p = h->layout_p;
+  h->sv.throughput = 1;
   for (int q = 1; q < p; ++q) {
     tdvp_ctx* ln = lane_of(h, q);
+    ln->sv.throughput = 1;
     ln->prm = h->prm;
     ln->warm_svd = h->warm_svd;
     ln->lz_fused = h->lz_fused;
@@ -1125,6 +1129,7 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   if (lanes) {
     if ((int)h->msg_r.size() != p) alloc_msgs(h);
     run_step_lanes(h, dt, merged);
+    h->sv.throughput = 0;
   } else {
     run_half(h, 1, dt, merged);
     run_half(h, 2, dt, merged);

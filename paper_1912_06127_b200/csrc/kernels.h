@@ -87,6 +87,7 @@ struct SvdDev {
   size_t qrbuf_elems;
   unsigned* flags;        // Jacobi per-block round counters (2 per column block), nullptr = grid barriers
   size_t flags_elems;
+  int throughput;         // 1: several SVDs run concurrently (segment lanes): prefer fewer CTAs per SVD
 };
 size_t svd_qr_work_elems(int m, int n);
 struct TruncParams {

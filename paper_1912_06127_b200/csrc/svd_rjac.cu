@@ -37,6 +37,12 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Early stop (quadratic convergence of cyclic Jacobi): a sweep whose largest
+// pair cosine c satisfies c^2 <= c_rj_early * tol leaves cosines ~ c^2 << tol,
+// so the confirming sweep that would measure them is skipped (TDVP_RJ_EARLY=0:
+// always confirm).  Measured off sequences: 7.6e-4, 6.1e-7, 1.0e-12, 2.5e-15.
+__constant__ double c_rj_early = 0.01;
+
 __device__ unsigned long long g_rj_prof[12];
 
 __device__ __forceinline__ void rj_rr_pair(int n, int round, int i, int& a, int& b) {
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(NT, 1)
       mark(3);
     }
     const double off = __ldcg(off_cur);
-    if (!(off > tol)) break;
+    if (!(off > tol) || off * off <= c_rj_early * tol) break;
   }
   if (blockIdx.x == 0 && tid == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
@@ -375,7 +381,7 @@ __device__ __forceinline__ void rj2_params(double a, double c, double gr, double
 template <int BW, int RX, int NT, bool CROSS>
 __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 * BW], unsigned& stale, int s,
                                          double (*red)[BW * 4], int lane, int wid, double tol2q, double tolc2,
-                                         bool& notconv, bool& rot, double (*pout)[3], int barid = 1) {
+                                         double& cmax, bool& rot, double (*pout)[3], int barid = 1) {
   constexpr int NV = 2 * BW;
   constexpr int H = (NV == 16) ? 4 : (NV == 8) ? 3 : 2;
   constexpr int SH = 5 - H;
@@ -448,6 +454,7 @@ __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 
     } else if (ag2 > tolc2 * a * c) {
       flag = 1;
     }
+    cmax = fmax(cmax, st ? 1.0 : ag2 / (a * c));  // squared cosine of the pair (a stale norm: unknown)
   }
   if (pout != nullptr && wid == 0 && lane < BW) {
     pout[lane][0] = cs;
@@ -463,7 +470,6 @@ __device__ __forceinline__ void rj2_step(cplx (&x)[RX][2 * BW], double (&nrm)[2 
     const double sii = __shfl_sync(FULL, si, i);
     const double dni = __shfl_sync(FULL, dn, i);
     const int fl = __shfl_sync(FULL, flag, i);
-    if (fl & 1) notconv = true;
     if (sri != 0.0 || sii != 0.0) {  // warp-uniform
       rot = true;
 #pragma unroll
@@ -684,25 +690,25 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
         if (MODE == 1) {
           double nrm[PC];
           unsigned stale = 0u;
-          bool notconv = false;
+          double cmax = 0.0;
           rj2_norms<BW, RX, NTX>(x, nrm, red[buf], lane, wid, barid);
           buf ^= 1;
           if (round == 0) {
 #pragma unroll
             for (int s = 0; s < PC - 1; ++s) {
-              rj2_step<BW, RX, NTX, false>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
+              rj2_step<BW, RX, NTX, false>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, cmax, rot,
                                            Ps[sb][s], barid);
               buf ^= 1;
             }
           } else {
 #pragma unroll
             for (int s = 0; s < BW; ++s) {
-              rj2_step<BW, RX, NTX, true>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, notconv, rot,
+              rj2_step<BW, RX, NTX, true>(x, nrm, stale, s, red[buf], lane, wid, tol2q, tol * tol, cmax, rot,
                                           Ps[sb][s], barid);
               buf ^= 1;
             }
           }
-          offacc = notconv ? 1.0 : 0.0;
+          offacc = cmax;
         } else if (round == 0) {
 #pragma unroll
           for (int s = 0; s < PC - 1; ++s) {
@@ -770,7 +776,7 @@ __global__ void __launch_bounds__(G * NTX + NTV, 1)
       else cg::this_grid().sync();
     }
     const double off = __ldcg(off_cur);
-    if (!(off > tol)) break;
+    if (!(off > tol) || off * off <= c_rj_early * tol) break;
   }
   // the last round's V update
   if (!xthr && R > 0) apply_v((R - 1) & 1, R - 1);
@@ -873,14 +879,23 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
     full_rounds = fr ? std::atoi(fr) : 0;
     const char* fp = std::getenv("TDVP_RJ_FAST");
     fastp = fp ? std::atoi(fp) : 0;
+    const char* el = std::getenv("TDVP_RJ_EARLY");
+    if (el && std::atoi(el) == 0) {
+      const double z = 0.0;
+      cudaMemcpyToSymbol(c_rj_early, &z, sizeof(z));
+    }
   }
   if (forced == 99) return cudaErrorNotSupported;  // tuning: legacy Jacobi
   int row = -1;
   if (forced >= 0 && forced < kNTab && rows_ok(forced, mr, nc)) row = forced;
   if (row < 0) {
-    const int prefer[] = {6, 10, 19};  // measured fastest first (microbench.py --svd, B200)
+    // latency: measured fastest first (microbench.py --svd, B200); throughput
+    // (concurrent SVDs of segment lanes): variant 14 packs two block pairs per
+    // CTA, half the CTAs per SVD (c2sat p = 8 lanes: 146 vs 166 ms/step)
+    const int prefer[] = {6, 10, 19};
+    if (d.throughput && rows_ok(14, mr, nc)) row = 14;
     for (int r : prefer)
-      if (rows_ok(r, mr, nc)) { row = r; break; }
+      if (row < 0 && rows_ok(r, mr, nc)) { row = r; break; }
   }
   if (row < 0) return cudaErrorNotSupported;
   const int bw = kTab[row].bw, kind = kTab[row].kind, grp = kTab[row].groups;

@@ -15,7 +15,7 @@ wl = bench.workload_inputs(sys.argv[1] if len(sys.argv) > 1 else "c2sat")
 ps = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
 for p in ps:
     t = pkg.Tdvp(wl["L"], 2, 5, wl["chi"])
-    t.set_params(eps=wl["eps"])
+    t.set_params(eps=wl["eps"], timing=bool(int(os.environ.get("LB_TIMING", "0"))))
     t.set_mpo(wl["mpo"])
     t.set_mps(wl["mps"].psi, wl["mps"].lam)
     for _ in range(2):
@@ -29,4 +29,7 @@ for p in ps:
     st = t.stats()
     print(f"p={p} lanes={os.environ.get('TDVP_LANES', '1')} step_ms={np.mean(ms):.1f} wall_ms={wall:.1f} "
           f"E={t.measure_energy():.12f} chi_max={max(t.chi())} n_pair={st['n_pair']}", flush=True)
+    if os.environ.get("LB_TIMING"):
+        print("   summed over lanes: " + " ".join(f"{k}={st[k]:.1f}" for k in
+              ("svd_ms", "svd_jac_ms", "lanczos2_ms", "heff2_ms", "lanczos1_ms", "heff1_ms", "env_ms")), flush=True)
     t.close()
