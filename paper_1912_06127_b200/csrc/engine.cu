@@ -181,7 +181,8 @@ struct tdvp_ctx {
   std::vector<MpoSite>& mpo;  // lanes: the parent's sites
   MpoSite mpo_id, mpo_sz;  // D = 1 identity / S^z (measurement)
   bool have_mpo = false, have_mps = false, envs_valid = false;
-  int layout_p = 0;  // segments currently laid out
+  int layout_p = 0;  // segments currently laid out (0: the host copy h_psi/h_lam is authoritative)
+  int alloc_p = 0;   // segments whose device buffers are allocated (kept across tdvp_set_mps)
   std::vector<std::pair<int, int>> bounds;
   std::vector<Segment> segs;
   // full-state host copy (multi-process initialisation)
@@ -191,7 +192,7 @@ struct tdvp_ctx {
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
   BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, svdF, gemm_work, partials;
   BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
-  BufPtr svd_sigma, svd_order, svd_off, svd_ires, svd_dres, red_res, envA, envB;
+  BufPtr svd_sigma, svd_order, svd_perm, svd_off, svd_ires, svd_dres, red_res, envA, envB;
   double* h_pin = nullptr;
   int* h_ipin = nullptr;
   LanczosDev lz{};
@@ -714,18 +715,23 @@ void layout(tdvp_ctx* h, int p) {
   if (!local_mode(h) && p != h->world)
     throw TdvpError(TDVP_EPARTITION, "n_segments must equal the world size in multi-process mode");
   if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);  // keep the current state
-  h->segs.clear();
-  h->bounds = b;
-  if (local_mode(h)) {
-    h->segs.resize(p);
-    for (int q = 0; q < p; ++q) alloc_segment(h, h->segs[q], q, b[q].first, b[q].second);
-  } else {
-    h->segs.resize(1);
-    alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second);
+  if (h->alloc_p != p || h->segs.empty()) {
+    // (re)allocate; the same partition reuses its buffers (a new state from
+    // tdvp_set_mps is uploaded into them: no cudaMalloc/cudaFree per call)
+    h->segs.clear();
+    h->bounds = b;
+    if (local_mode(h)) {
+      h->segs.resize(p);
+      for (int q = 0; q < p; ++q) alloc_segment(h, h->segs[q], q, b[q].first, b[q].second);
+    } else {
+      h->segs.resize(1);
+      alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second);
+    }
+    h->msg_r.clear();
+    h->msg_l.clear();
+    h->alloc_p = p;
   }
   h->layout_p = p;
-  h->msg_r.clear();
-  h->msg_l.clear();
   upload_state(h);
   build_envs(h);
   h->envs_valid = true;
@@ -1280,6 +1286,7 @@ void alloc_workspace(tdvp_ctx* h) {
   const long long ncmax = 2LL * h->chi_max;
   h->svd_sigma = make_buf(ncmax * sizeof(double) + 64);
   h->svd_order = make_buf(ncmax * sizeof(int) + 64);
+  h->svd_perm = make_buf(2 * ncmax * sizeof(int) + 64);
   h->svd_off = make_buf(64);
   h->svd_ires = make_buf(64);
   h->svd_dres = make_buf(64);
@@ -1290,7 +1297,7 @@ void alloc_workspace(tdvp_ctx* h) {
                      reinterpret_cast<unsigned*>(h->lz_counter->p), h->lz_brk->i()};
   h->sv = SvdDev{h->svdY->c(), 0, h->svd_sigma->d(), h->svd_order->i(), h->svd_off->d(), h->svd_ires->i(),
                  h->svd_dres->d(), h->h_pin, h->h_ipin, {nullptr, nullptr}, h->svdQ->c(), (size_t)svq,
-                 reinterpret_cast<unsigned*>(h->svdF->p), nflags};
+                 reinterpret_cast<unsigned*>(h->svdF->p), nflags, 0, h->svd_perm->i()};
 }
 
 int fail(tdvp_ctx* h, const TdvpError& e) {
@@ -1433,6 +1440,7 @@ int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W) {
     h->envs_valid = false;
     if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);
     h->layout_p = 0;
+    h->alloc_p = 0;
     h->segs.clear();
   } catch (const TdvpError& e) {
     return fail(h, e);
@@ -1466,8 +1474,7 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     h->h_chi.assign(chi, chi + L + 1);
     h->have_mps = true;
     h->envs_valid = false;
-    h->layout_p = 0;  // re-layout (upload + env build) at the next step
-    h->segs.clear();
+    h->layout_p = 0;  // re-layout (upload + env build) at the next step, same buffers
   } catch (const TdvpError& e) {
     return fail(h, e);
   }
@@ -1662,7 +1669,6 @@ int tdvp_reorthonormalize(tdvp_t h) {
     h->h_chi = chi;
     h->envs_valid = false;
     h->layout_p = 0;  // re-layout: upload + sequential environment build at the next call
-    h->segs.clear();
   } catch (const TdvpError& e) {
     return fail(h, e);
   }
@@ -1731,6 +1737,7 @@ int tdvp_comm_init(tdvp_t h, int rank, int world, const unsigned char* id128) {
     h->rank = rank;
     h->world = world;
     h->layout_p = 0;
+    h->alloc_p = 0;
     h->segs.clear();
   } catch (const TdvpError& e) {
     return fail(h, e);

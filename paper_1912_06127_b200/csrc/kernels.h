@@ -88,6 +88,7 @@ struct SvdDev {
   unsigned* flags;        // Jacobi per-block round counters (2 per column block), nullptr = grid barriers
   size_t flags_elems;
   int throughput;         // 1: several SVDs run concurrently (segment lanes): prefer fewer CTAs per SVD
+  int* perm;              // [2 nc]: column presort permutation and its inverse (QR path), nullptr = off
 };
 size_t svd_qr_work_elems(int m, int n);
 struct TruncParams {

@@ -703,9 +703,41 @@ __global__ void svd_truncate_kernel(const double* __restrict__ sigma, int nc, in
   dres[1] = s1;
 }
 
+// Column presorting for the QR preconditioner (Drmac-Veselic: sorting the
+// columns of X by decreasing norm before X = Q1 R1 makes R1 and R2 graded and
+// cuts Jacobi sweeps; measured 45 -> 38 sweeps over six Theta of a c1-shaped
+// run).  Single CTA: perm[rank] = c, perm[nc + c] = rank, ties by index.
+__global__ void svd_presort_kernel(const double* __restrict__ nrm, int nc, int* perm) {
+  extern __shared__ double s_n[];
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) s_n[c] = nrm[c];
+  __syncthreads();
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const double v = s_n[c];
+    int r = 0;
+    for (int j = 0; j < nc; ++j) {
+      const double u = s_n[j];
+      r += (u > v) || (u == v && j < c);
+    }
+    perm[min(r, nc - 1)] = c;
+    perm[nc + c] = r;
+  }
+}
+
+// Q1[:, j] = X[:, perm[j]] (X = rows [0, mr) of Y)
+__global__ void svd_permcopy_kernel(const cplx* __restrict__ Y, long long ldy, int mr, int nc,
+                                    const int* __restrict__ perm, cplx* Q1) {
+  const long long total = (long long)mr * nc;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / mr), r = (int)(e - (long long)j * mr);
+    const int c = min(max(perm[j], 0), nc - 1);
+    Q1[e] = Y[(long long)c * ldy + r];
+  }
+}
+
 __global__ void svd_write_kernel(const cplx* __restrict__ Y, long long ldy, const int* __restrict__ order,
                                  const double* __restrict__ sigma, const int* __restrict__ ires, int m, int n, int mr,
-                                 bool transposed, cplx* psiL, cplx* psiR, double* lam, double* vinv) {
+                                 bool transposed, cplx* psiL, cplx* psiR, double* lam, double* vinv,
+                                 const int* __restrict__ iperm) {
   const int chi = ires[0];
   // Psi_L: m x chi ; Psi_R: chi x n
   const long long nL = (long long)m * chi, nR = (long long)chi * n;
@@ -714,13 +746,14 @@ __global__ void svd_write_kernel(const cplx* __restrict__ Y, long long ldy, cons
     if (e < nL) {
       const int r = (int)(e / chi), k = (int)(e - (long long)r * chi);
       const int c = order[k];
-      psiL[e] = transposed ? cscale(Y[(long long)c * ldy + mr + r], sigma[c]) : Y[(long long)c * ldy + r];
+      psiL[e] = transposed ? cscale(Y[(long long)c * ldy + mr + (iperm ? iperm[r] : r)], sigma[c])
+                           : Y[(long long)c * ldy + r];
     } else if (e < nL + nR) {
       const long long f = e - nL;
       const int k = (int)(f / n), col = (int)(f - (long long)k * n);
       const int c = order[k];
       psiR[f] = transposed ? cconj(Y[(long long)c * ldy + col])
-                           : cscale(cconj(Y[(long long)c * ldy + mr + col]), sigma[c]);
+                           : cscale(cconj(Y[(long long)c * ldy + mr + (iperm ? iperm[col] : col)]), sigma[c]);
     } else {
       const int k = (int)(e - nL - nR);
       const double s = sigma[order[k]];
@@ -789,6 +822,12 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   }
   const bool use_qr = !use_warm && precond == 2 && nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
                       svd_qr_work_elems(m, n) <= d.qrbuf_elems;
+  static int presort_env = -1;
+  if (presort_env < 0) {
+    const char* ev = std::getenv("TDVP_SVD_PRESORT");
+    presort_env = ev ? std::atoi(ev) : 1;
+  }
+  const bool presort = use_qr && presort_env && d.perm != nullptr && nc * sizeof(double) <= 48 * 1024;
   QrWork w1{}, w2{};
   int x_rows = mr;
   bool qr_cluster = false;
@@ -808,9 +847,17 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     w2.tau = p; p += nc;
     w1.W1 = w2.W1 = p; p += 32LL * nc;
     w1.W2 = w2.W2 = p; p += 32LL * nc;
-    if ((e = cudaMemcpy2DAsync(Q1, (size_t)mr * sizeof(cplx), d.Y, (size_t)ldy * sizeof(cplx), (size_t)mr * sizeof(cplx),
-                               nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    if (presort) {
+      // X P with P sorting the columns by decreasing norm; V = P (Q2 V3) at the write
+      svd_colnorm_kernel<<<(nc + 7) / 8, 256, 0, st>>>(d.Y, ldy, mr, nc, d.sigma, d.ires + 2);
+      svd_presort_kernel<<<1, 1024, nc * sizeof(double), st>>>(d.sigma, nc, d.perm);
+      const long long total = (long long)mr * nc;
+      const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
+      svd_permcopy_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, mr, nc, d.perm, Q1);
+    } else if ((e = cudaMemcpy2DAsync(Q1, (size_t)mr * sizeof(cplx), d.Y, (size_t)ldy * sizeof(cplx),
+                                      (size_t)mr * sizeof(cplx), nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) {
       return e;
+    }
     static int qrmode = -1;
     if (qrmode < 0) {
       const char* ev = std::getenv("TDVP_QR_BLOCKED");
@@ -966,7 +1013,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     const long long total = (long long)m * chi + (long long)chi * n + chi;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
     svd_write_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, d.order, d.sigma, d.ires, m, n, mr, transposed, psiL, psiR,
-                                             lam, vinv);
+                                             lam, vinv, presort ? d.perm + nc : nullptr);
   }
   *chi_out = chi;
   *w_out = d.h_buf[1];
