@@ -317,7 +317,23 @@ def main():
             lms.append(t.stats()["step_ms"])
         lv = float(np.mean(lms))
         lanes = {"segments": q, "executor": "concurrent segment lanes on one GPU (thread + stream per segment)",
+                 "partition": "uniform (PAPER.md:470)",
                  "ms_per_step": lv, "speedup_vs_serial": ms_per_step / lv if lv > 0 else None}
+        # the same with the chi-weighted partition (tdvp_partition_balanced)
+        t.set_mps(wl["mps"].psi, wl["mps"].lam)
+        bounds = pkg.balanced_partition(L, q, t.chi())
+        t.set_partition(bounds)
+        for _ in range(args.warmup):
+            t.step(dt, q)
+        torch.cuda.synchronize()
+        bms = []
+        for _ in range(args.steps):
+            t.step(dt, q)
+            bms.append(t.stats()["step_ms"])
+        bv = float(np.mean(bms))
+        t.set_partition(None)
+        lanes["balanced"] = {"bounds": bounds, "ms_per_step": bv,
+                             "speedup_vs_serial": ms_per_step / bv if bv > 0 else None}
     t.close()
 
     if rank != 0:

@@ -150,6 +150,22 @@ int tdvp_plan(int L, int p, int h, int q, int* ops, int max_ops);
 /* Segment bounds [s, e] of segment q (SURVEY O-3). */
 int tdvp_partition(int L, int p, int* s, int* e);
 
+/* Load balancing ("load imbalance is the
+ * limiter").  tdvp_set_partition: use the explicit contiguous partition with
+ * segment q starting at site s[q] (s[0] = 0, p even, 2 <= p <= L/2, every
+ * segment >= 2 sites) whenever tdvp_step is called with
+ * n_segments = p; p = 0 restores the uniform rule.  The state is kept; the
+ * next step re-lays it out and rebuilds the environments.  In multi-process
+ * mode every rank must set the same partition.  Errors: TDVP_EARG,
+ * TDVP_EPARTITION.
+ * tdvp_partition_balanced (host only): the contiguous partition into p
+ * segments (each >= 2 sites) minimising the largest segment cost, site cost
+ * chi_j chi_{j+1} (chi_j + chi_{j+1}) from the bond dimensions chi[L+1]
+ * (e.g. tdvp_get_chi): exact dynamic programme, deterministic (smallest split
+ * index on ties).  Writes s[p], e[p]. */
+int tdvp_set_partition(tdvp_t h, int p, const int* s);
+int tdvp_partition_balanced(int L, int p, const int* chi, int* s, int* e);
+
 /* ---- kernel-level entry points (host buffers; copies inside) -------------
  * For parity tests of the individual contractions against the oracle.
  * H_eff^(2) theta: Lenv (cl, Dl, cl), W1 (Dl, d, d, Dm),

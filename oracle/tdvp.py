@@ -264,6 +264,21 @@ def plan_partition(L: int, p: int):
     return segs
 
 
+def check_partition(L: int, bounds):
+    """Validate explicit segment bounds [(s, e)]: contiguous from 0 to L-1,
+    p = 1 or p even (the direction rule of PAPER.md:470 pairs segments), every
+    segment >= 2 sites when p > 1.  Returns them as tuples."""
+    b = [(int(s), int(e)) for s, e in bounds]
+    p = len(b)
+    if p != 1 and (p % 2 != 0 or p < 2):
+        raise ValueError(f"invalid number of segments p={p}")
+    if b[0][0] != 0 or b[-1][1] != L - 1 or any(b[q + 1][0] != b[q][1] + 1 for q in range(p - 1)):
+        raise ValueError("segments must be contiguous and cover 0..L-1")
+    if p > 1 and min(e - s + 1 for s, e in b) < 2:
+        raise ValueError("segment shorter than two sites")
+    return b
+
+
 RIGHT, LEFT = "R", "L"
 
 
@@ -315,12 +330,15 @@ class Stats:
 
 
 class State:
-    def __init__(self, W, params: Params, p: int):
+    def __init__(self, W, params: Params, p: int, bounds=None):
         self.W = [np.asarray(w, dtype=np.complex128) for w in W]
         self.L = len(W)
         self.params = params
         self.p = p
-        self.bounds = plan_partition(self.L, p)
+        # explicit bounds (any contiguous partition, e.g. load-balanced) or the uniform rule O-3
+        self.bounds = plan_partition(self.L, p) if bounds is None else check_partition(self.L, bounds)
+        if len(self.bounds) != p:
+            raise ValueError("len(bounds) != p")
         self.segs = [Segment(q, s, e) for q, (s, e) in enumerate(self.bounds)]
         self.stats = Stats()
         self.trace = False
@@ -346,9 +364,10 @@ def _mps_envs(psi, lam, W):
     return beta, gamma
 
 
-def init_state(mps, W, params: Params, p: int = 1) -> State:
-    """Sequential initial environments, handed to each segment's owner (O-2)."""
-    st = State(W, params, p)
+def init_state(mps, W, params: Params, p: int = 1, bounds=None) -> State:
+    """Sequential initial environments, handed to each segment's owner (O-2).
+    `bounds`: explicit segment bounds [(s, e)] instead of the uniform rule."""
+    st = State(W, params, p, bounds)
     L = st.L
     psi = [np.asarray(x, dtype=np.complex128) for x in mps.psi]
     lam = [np.asarray(x, dtype=np.float64) for x in mps.lam]

@@ -184,6 +184,7 @@ struct tdvp_ctx {
   int layout_p = 0;  // segments currently laid out (0: the host copy h_psi/h_lam is authoritative)
   int alloc_p = 0;   // segments whose device buffers are allocated (kept across tdvp_set_mps)
   std::vector<std::pair<int, int>> bounds;
+  std::vector<std::pair<int, int>> custom;  // tdvp_set_partition: explicit bounds for n_segments = custom.size()
   std::vector<Segment> segs;
   // full-state host copy (multi-process initialisation)
   std::vector<std::vector<double>> h_psi, h_lam;
@@ -711,11 +712,12 @@ void build_envs(tdvp_ctx* h) {
 void layout(tdvp_ctx* h, int p) {
   std::vector<std::pair<int, int>> b;
   std::string err;
-  if (!plan_partition(h->L, p, b, err)) throw TdvpError(TDVP_EPARTITION, err);
+  if ((int)h->custom.size() == p && p > 1) b = h->custom;
+  else if (!plan_partition(h->L, p, b, err)) throw TdvpError(TDVP_EPARTITION, err);
   if (!local_mode(h) && p != h->world)
     throw TdvpError(TDVP_EPARTITION, "n_segments must equal the world size in multi-process mode");
   if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);  // keep the current state
-  if (h->alloc_p != p || h->segs.empty()) {
+  if (h->alloc_p != p || h->segs.empty() || h->bounds != b) {
     // (re)allocate; the same partition reuses its buffers (a new state from
     // tdvp_set_mps is uploaded into them: no cudaMalloc/cudaFree per call)
     h->segs.clear();
@@ -1760,6 +1762,71 @@ int tdvp_plan(int L, int p, int hh, int q, int* ops, int max_ops) {
     ops[4 * i + 3] = prog[i].build;
   }
   return (int)prog.size();
+}
+
+int tdvp_set_partition(tdvp_t h, int p, const int* s) {
+  if (!h) return TDVP_EARG;
+  try {
+    if (p == 0) {
+      h->custom.clear();
+    } else {
+      if (!s) throw TdvpError(TDVP_EARG, "null segment starts");
+      const int L = h->L;
+      if (p < 2 || p % 2 != 0 || p > L / 2) throw TdvpError(TDVP_EPARTITION, "p must be even, 2 <= p <= L/2");
+      if (s[0] != 0) throw TdvpError(TDVP_EPARTITION, "the first segment must start at site 0");
+      std::vector<std::pair<int, int>> b(p);
+      for (int q = 0; q < p; ++q) {
+        const int e = q + 1 < p ? s[q + 1] - 1 : L - 1;
+        if (e - s[q] + 1 < 2) throw TdvpError(TDVP_EPARTITION, "segment shorter than two sites (PAPER.md:470)");
+        b[q] = {s[q], e};
+      }
+      h->custom = b;
+    }
+    h->envs_valid = false;  // re-layout (state kept) at the next step
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_partition_balanced(int L, int p, const int* chi, int* s, int* e) {
+  if (L < 2 || !chi || !s || !e) return TDVP_EARG;
+  if (p == 1) {
+    s[0] = 0;
+    e[0] = L - 1;
+    return TDVP_OK;
+  }
+  if (p < 2 || p % 2 != 0 || p > L / 2) return TDVP_EPARTITION;
+  // site cost ~ the one-site update / half a pair update: chi_j chi_{j+1} (chi_j + chi_{j+1})
+  std::vector<double> pre(L + 1, 0.0);
+  for (int j = 0; j < L; ++j) {
+    const double a = chi[j], b = chi[j + 1];
+    if (!(a >= 1.0) || !(b >= 1.0)) return TDVP_EARG;
+    pre[j + 1] = pre[j] + a * b * (a + b);
+  }
+  // f[q][i]: min over partitions of sites [0, i) into q segments (each >= 2) of the max segment cost
+  const double INF = 1e300;
+  std::vector<std::vector<double>> f(p + 1, std::vector<double>(L + 1, INF));
+  std::vector<std::vector<int>> arg(p + 1, std::vector<int>(L + 1, -1));
+  f[0][0] = 0.0;
+  for (int q = 1; q <= p; ++q)
+    for (int i = 2 * q; i <= L - 2 * (p - q); ++i)
+      for (int k = 2 * (q - 1); k <= i - 2; ++k) {
+        if (f[q - 1][k] >= INF) continue;
+        const double v = std::max(f[q - 1][k], pre[i] - pre[k]);
+        if (v < f[q][i]) {
+          f[q][i] = v;
+          arg[q][i] = k;
+        }
+      }
+  if (f[p][L] >= INF) return TDVP_EPARTITION;
+  for (int q = p, i = L; q >= 1; --q) {
+    const int k = arg[q][i];
+    s[q - 1] = k;
+    e[q - 1] = i - 1;
+    i = k;
+  }
+  return TDVP_OK;
 }
 
 int tdvp_partition(int L, int p, int* s, int* e) {

@@ -58,6 +58,8 @@ _SIGS = {
     "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_norm": (C.c_int, [C.c_void_p, _D]),
     "tdvp_overlap": (C.c_int, [C.c_void_p, C.c_void_p, _D, _D]),
+    "tdvp_set_partition": (C.c_int, [C.c_void_p, C.c_int, _I]),
+    "tdvp_partition_balanced": (C.c_int, [C.c_int, C.c_int, _I, _I, _I]),
     "tdvp_reorthonormalize": (C.c_int, [C.c_void_p]),
     "tdvp_get_stats": (C.c_int, [C.c_void_p, C.POINTER(tdvp_stats)]),
     "tdvp_get_chi": (C.c_int, [C.c_void_p, _I]),
@@ -174,6 +176,14 @@ class Tdvp:
         """Exact re-gauging into inverse-canonical form (tdvp_reorthonormalize)."""
         _check(lib().tdvp_reorthonormalize(self.h), self.h)
 
+    def set_partition(self, bounds):
+        """Explicit segment bounds [(s, e)] for n_segments = len(bounds); None = uniform rule."""
+        if not bounds:
+            _check(lib().tdvp_set_partition(self.h, 0, None), self.h)
+            return
+        starts = (C.c_int * len(bounds))(*[int(s) for s, _ in bounds])
+        _check(lib().tdvp_set_partition(self.h, len(bounds), starts), self.h)
+
     def maybe_reorthonormalize(self, tol):
         """Reorthonormalise when the norm error |<psi|psi> - 1| exceeds tol
         (PAPER.md:517: "if the error in the norm grows unacceptably large");
@@ -204,6 +214,16 @@ class Tdvp:
 
     def comm_init(self, rank, world, uid: bytes):
         _check(lib().tdvp_comm_init(self.h, rank, world, uid), self.h)
+
+
+def balanced_partition(L, p, chi):
+    """Contiguous partition minimising the largest segment cost (tdvp_partition_balanced)."""
+    ch = (C.c_int * (L + 1))(*[int(x) for x in chi])
+    s, e = (C.c_int * p)(), (C.c_int * p)()
+    rc = lib().tdvp_partition_balanced(L, p, ch, s, e)
+    if rc != 0:
+        raise TdvpError(rc, f"tdvp_partition_balanced(L={L}, p={p})")
+    return [(s[q], e[q]) for q in range(p)]
 
 
 def nccl_unique_id() -> bytes:

@@ -4,6 +4,7 @@ No compute calls (no GPU here)."""
 import os
 import re
 
+import numpy as np
 import pytest
 
 from paper_1912_06127_b200 import tdvp as B
@@ -85,3 +86,54 @@ def test_plan_serial_is_paper_sweep():
     h2 = B.plan(L, 1, 2, 0)
     assert h2 == [(2, 4, 0, 0), (1, 3, 0, 2), (2, 3, 0, 0), (1, 2, 0, 2), (2, 2, 0, 0), (1, 1, 0, 2), (2, 1, 0, 0),
                   (1, 0, 0, 2)]
+
+
+# ----------------------------------------------- N4 load-balanced partitions
+def _brute_minmax(L, p, w):
+    """Smallest achievable max segment cost over all contiguous partitions into
+    p segments of >= 2 sites (exhaustive, small L)."""
+    import itertools
+    best = None
+    for cuts in itertools.combinations(range(2, L - 1), p - 1):
+        starts = (0,) + cuts
+        ends = cuts + (L,)
+        if any(b - a < 2 for a, b in zip(starts, ends)):
+            continue
+        v = max(sum(w[a:b]) for a, b in zip(starts, ends))
+        best = v if best is None else min(best, v)
+    return best
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("L,p", [(8, 2), (11, 4), (12, 2), (13, 4)])
+def test_balanced_partition_is_optimal(L, p, seed):
+    rng = np.random.default_rng(seed * 31 + L)
+    chi = [1] + list(rng.integers(1, 40, size=L - 1)) + [1]
+    w = [chi[j] * chi[j + 1] * (chi[j] + chi[j + 1]) for j in range(L)]
+    b = B.balanced_partition(L, p, chi)
+    assert len(b) == p and b[0][0] == 0 and b[-1][1] == L - 1
+    assert all(b[q + 1][0] == b[q][1] + 1 for q in range(p - 1))
+    assert all(e - s + 1 >= 2 for s, e in b)
+    got = max(sum(w[s:e + 1]) for s, e in b)
+    assert got == _brute_minmax(L, p, w)
+
+
+def test_balanced_partition_saturated_profile():
+    """Uniform chi: the balanced partition is the uniform one; a saturated
+    profile (small chi at the chain ends) gives the edge segments more sites."""
+    import tdvp_inputs as ti
+    L = 64
+    assert B.balanced_partition(L, 8, [1] + [16] * (L - 1) + [1])[1:-1] == B.partition(L, 8)[1:-1]
+    chi = [1] + ti.saturated_chi_profile(L, 128) + [1]
+    b = B.balanced_partition(L, 8, chi)
+    sizes = [e - s + 1 for s, e in b]
+    assert sizes[0] > 8 and sizes[-1] > 8
+    w = [chi[j] * chi[j + 1] * (chi[j] + chi[j + 1]) for j in range(L)]
+    cost = lambda bb: max(sum(w[s:e + 1]) for s, e in bb)  # noqa: E731
+    assert cost(b) <= 0.875 * cost(B.partition(L, 8))  # 7 instead of 8 full-chi sites per segment
+
+
+@pytest.mark.parametrize("L,p", [(8, 3), (8, 0), (5, 4)])
+def test_balanced_partition_rejects_invalid(L, p):
+    with pytest.raises(B.TdvpError):
+        B.balanced_partition(L, p, [1] * (L + 1))

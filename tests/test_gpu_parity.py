@@ -211,3 +211,35 @@ def test_one_body_exact_on_gpu(B):
     g = gpu_run(B, ti.neel_mps(L), ti.mpo_onsite(L, h * ti.SX), 8, 1e-12, 0.1, 10, 2)
     exact = np.array([0.5 if i % 2 == 0 else -0.5 for i in range(L)]) * np.cos(h * 1.0)
     assert np.abs(g[-1]["sz"] - exact).max() < 1e-12
+
+
+@pytest.mark.parametrize("lanes", ["1", "0"])
+def test_explicit_partition_matches_oracle(B, lanes, monkeypatch):
+    """N4: an explicit (uneven, load-balanced) partition on the GPU equals the
+    oracle run on the same partition; both executors (lanes / round-robin)."""
+    monkeypatch.setenv("TDVP_LANES", lanes)
+    L = 16
+    mps, W = ti.random_canonical_mps(L, 8, seed=4), ti.mpo_xxz_nn(L, 0.5)
+    chi = [1] + [len(x) for x in mps.lam] + [1]
+    bounds = B.balanced_partition(L, 4, chi)
+    assert bounds != B.partition(L, 4)
+    t = B.Tdvp(L, 2, 5, 8)
+    t.set_params(eps=1e-10)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    t.set_partition(bounds)
+    st = O.init_state(mps, W, O.Params(chi_max=8, eps=1e-10), 4, bounds)
+    for _ in range(3):
+        t.step(0.05, 4)
+        O.step(st, 0.05)
+        m = O.measure(st)
+        assert t.chi() == O.chi_profile(st)
+        assert np.abs(t.measure_sz() - m["sz"]).max() < 1e-6
+        assert abs(t.measure_energy() - m["energy"]) < 1e-6
+    t.set_partition(None)  # back to the uniform rule: state kept, re-laid out
+    t.step(0.05, 4)
+    psi, lam = O.global_mps(st)
+    st2 = O.init_state(ti.MPS(psi, lam), W, O.Params(chi_max=8, eps=1e-10), 4)
+    O.step(st2, 0.05)
+    assert np.abs(t.measure_sz() - O.measure(st2)["sz"]).max() < 1e-6
+    t.close()

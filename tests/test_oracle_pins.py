@@ -446,3 +446,27 @@ def test_counts_per_step(L, p):
     for _, q, j, tau in pairs:
         per_bond[j] += abs(tau)
     assert np.allclose(per_bond, 0.05)
+
+
+def test_p13b_explicit_partition_converges_to_serial():
+    """Any contiguous partition (here an uneven, load-balanced-style one) is a
+    valid p2TDVP partition: its deviation from the serial run vanishes as
+    dt -> 0 like the uniform one's (P13), and a malformed one is rejected."""
+    L, T = 12, 0.4
+    W = ti.mpo_xxz_nn(L, 0.5)
+    bounds = [(0, 4), (5, 6), (7, 8), (9, 11)]
+    devs = []
+    for dt in (0.04, 0.02, 0.01):
+        out = []
+        for pp, bb in ((1, None), (4, bounds)):
+            st = O.init_state(ti.neel_mps(L), W, O.Params(chi_max=64), pp, bb)
+            assert [(s.s, s.e) for s in st.segs] == (bb or [(0, L - 1)])
+            for _ in range(int(round(T / dt))):
+                O.step(st, dt)
+            out.append(O.measure(st)["sz"])
+        devs.append(np.abs(out[0] - out[1]).max())
+    assert devs[0] > devs[1] > devs[2]
+    assert devs[2] < 1e-9
+    for bad in ([(0, 4), (5, 11), (11, 11)], [(0, 5), (7, 11)], [(0, 0), (1, 11)], [(0, 3), (4, 7), (8, 11)]):
+        with pytest.raises(ValueError):
+            O.init_state(ti.neel_mps(L), W, O.Params(chi_max=64), len(bad), bad)
