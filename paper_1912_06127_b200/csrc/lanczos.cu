@@ -284,6 +284,9 @@ __device__ void lz_tridiag_exp_jacobi(LanczosDev d, int K, double tre, double ti
 // h = tau / s, |h| ||T - a0||_inf <= 1/2, 20 terms per substep (truncation
 // error < 1e-22); lane r holds row r, T (T - a0) x needs two neighbour
 // shuffles.  Falls back to the Jacobi eigendecomposition for ||tau (T - a0)|| > 16.
+__constant__ double c_inv_k[21] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,
+                                   1.0 / 7,   1.0 / 8,    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13,
+                                   1.0 / 14,  1.0 / 15,   1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20};
 __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
   const int r = threadIdx.x;
   const bool on = r < K;
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K,
       // u = (T - a0) t   (real T)
       cplx u = cmk(dl * t.x + bm * (r > 0 ? txm : 0.0) + bl * txp, dl * t.y + bm * (r > 0 ? tym : 0.0) + bl * typ);
       if (!on) u = cmk(0.0, 0.0);
-      const double f = 1.0 / k;
+      const double f = c_inv_k[k];  // no 200-cycle IEEE division on the dependency chain
       t = cmk((hr * u.x - hi * u.y) * f, (hr * u.y + hi * u.x) * f);
       z = cadd(z, t);
     }
