@@ -125,7 +125,7 @@ struct QrWork {
   cplx* W2;
   int kb;          // panel width = qr_kb_for(m)
 };
-int qr_kb_for(int m);  // 32 / 16 / 8 for m <= 256 / 512 / 1024, 0 = unsupported
+int qr_kb_for(int m);  // 32 / 16 / 8 / 4 for m <= 256 / 512 / 1024 / 2048, 0 = unsupported
 cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, int m, int n);
 // C (column-major m x nc, ld ldc) <- Q C with Q from qr_factor (m x n reflectors)
 cudaError_t qr_apply_q(cudaStream_t st, const QrWork& w, int m, int n, cplx* C, long long ldc, int nc);

@@ -154,7 +154,7 @@ __global__ void qr_rh_kernel(const cplx* __restrict__ A, long long lda, int n, c
 }  // namespace
 
 // panel width by the row count (the panel lives in registers)
-int qr_kb_for(int m) { return m <= 256 ? 32 : m <= 512 ? 16 : m <= 1024 ? 8 : 0; }
+int qr_kb_for(int m) { return m <= 256 ? 32 : m <= 512 ? 16 : m <= 1024 ? 8 : m <= 2048 ? 4 : 0; }
 
 cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, int m, int n) {
   const int KBm = qr_kb_for(m);
@@ -173,13 +173,16 @@ cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, 
           (ea = cudaFuncSetAttribute(qr_panel_kernel<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      128 * 1024)) != cudaSuccess ||
           (ea = cudaFuncSetAttribute(qr_panel_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     128 * 1024)) != cudaSuccess ||
+          (ea = cudaFuncSetAttribute(qr_panel_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      128 * 1024)) != cudaSuccess)
         return ea;
       attr = true;
     }
     if (KBm == 32) qr_panel_kernel<32, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
     else if (KBm == 16) qr_panel_kernel<16, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
-    else qr_panel_kernel<8, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
+    else if (KBm == 8) qr_panel_kernel<8, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
+    else qr_panel_kernel<4, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
     const int nt = n - k0 - kb;
     if (nt <= 0) continue;
     // trailing A_t = A[k0:m, k0+kb:n]; row-major view Ar_t (nt x rows, ld lda)

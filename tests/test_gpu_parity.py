@@ -120,6 +120,24 @@ def test_svd_split_matches_oracle(B, m, n, chi_max):
     assert np.abs(U.conj().T @ U - np.eye(len(S))).max() < 1e-12
 
 
+def test_svd_split_large_blocked_qr(B):
+    """mr in (1024, 2048]: blocked Householder QR preconditioner (panel width 4)
+    and the streaming Jacobi; graded spectrum down to 1e-12."""
+    rng = np.random.default_rng(17)
+    m, n, chi_max = 1500, 1100, 600
+    M = rc(rng, m, n) * np.exp(-np.linspace(0, 27, n))[None, :]
+    p = O.Params(chi_max=chi_max, eps=1e-10)
+    pl_o, S_o, pr_o, w_o, _, _ = O.svd_truncate(M.reshape(m, 1, 1, n), p)
+    pl, S, pr, w = B.svd_split(M, chi_max, eps=1e-10)
+    assert len(S) == len(S_o)
+    assert np.allclose(S, S_o, rtol=1e-10, atol=1e-14 * S_o[0])
+    U = pl / S[None, :]
+    assert np.abs(U.conj().T @ U - np.eye(len(S))).max() < 1e-11
+    rec = (pl / S[None, :]) @ pr
+    rec_o = pl_o.reshape(m, -1) @ np.diag(1 / S_o) @ pr_o.reshape(-1, n)
+    assert rel(rec, rec_o) < 1e-9
+
+
 def test_svd_degenerate_and_rank_deficient(B):
     rng = np.random.default_rng(5)
     Q1, _ = np.linalg.qr(rc(rng, 20, 20))
