@@ -75,7 +75,10 @@ __global__ void svd_init_kernel(cplx* Y, long long ldy, const cplx* __restrict__
 template <int BW>
 struct CoopCfg {
   static constexpr int PC = 2 * BW;
-  static constexpr int TRc = 1536 / PC;             // rows per staged tile (6 loads in flight per thread)
+  // rows per staged tile: BW = 8 uses the register-tiled Gram/apply (64 rows,
+  // 4 column groups x 64 row threads), else 6 loads in flight per thread
+  static constexpr int TRc = (PC == 16) ? 128 : 1536 / PC;
+  static constexpr bool TILED = (PC == 16);
   static constexpr int E = PC * PC;                // Gram entries
   static constexpr int EPT = (E + NTH - 1) / NTH;  // entries per thread
   static constexpr int S = (E >= NTH) ? 1 : NTH / E;  // row slices per entry
@@ -334,6 +337,58 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
       tile[e - (e / TRc) * TRc][e / TRc] = pre[u];
     }
   };
+  if constexpr (Cf::TILED) {
+    // register-tiled Gram: thread = (4x4 block of G, row slice of 16); per
+    // row 8 shared loads (warp-broadcast) feed 16 complex MACs, so the loop
+    // is FP64-pipe bound instead of shared-memory bound (2 loads per MAC)
+    const int blk = tid & 15, sl = tid >> 4, i0 = (blk >> 2) * 4, j0 = (blk & 3) * 4;
+    cplx g[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) g[a][b] = cmk(0, 0);
+    fetch(0, mr);
+    for (int r0 = 0; r0 < mr; r0 += TRc) {
+      stash();
+      __syncthreads();
+      if (r0 + TRc < mr) fetch(r0 + TRc, mr);
+#pragma unroll
+      for (int m = 0; m < TRc / 16; ++m) {
+        const int rr = sl + 16 * m;
+        cplx ti[4], tj[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          ti[a] = tile[rr][i0 + a];
+          tj[a] = tile[rr][j0 + a];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            g[a][b].x = fma(ti[a].x, tj[b].x, fma(ti[a].y, tj[b].y, g[a][b].x));
+            g[a][b].y = fma(ti[a].x, tj[b].y, fma(-ti[a].y, tj[b].x, g[a][b].y));
+          }
+      }
+      __syncthreads();
+    }
+    // reduce the 16 row slices: lanes l, l ^ 16 (one shuffle), then the 8 warps in order
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        g[a][b].x += __shfl_xor_sync(0xffffffffu, g[a][b].x, 16);
+        g[a][b].y += __shfl_xor_sync(0xffffffffu, g[a][b].y, 16);
+      }
+    for (int w = 0; w < NTH / 32; ++w) {
+      if (wid == w && lane < 16) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) G[i0 + a][j0 + b] = w == 0 ? g[a][b] : cadd(G[i0 + a][j0 + b], g[a][b]);
+      }
+      __syncthreads();
+    }
+  } else {
   fetch(0, mr);
   for (int r0 = 0; r0 < mr; r0 += TRc) {
     stash();
@@ -381,6 +436,7 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
       if (e < Cf::E) G[e / PC][e % PC] = acc[u];
     }
   }
+  }  // !TILED
   for (int e = tid; e < PC * PC; e += NTH) Qm[e / PC][e % PC] = cmk((e / PC) == (e % PC) ? 1.0 : 0.0, 0.0);
   __syncthreads();
 
@@ -421,6 +477,35 @@ __device__ void coop_pair(cplx* Y, long long ldy, int mr, int nc, int nb, int nb
 
   // ---- apply: Y_pair <- Y_pair Q over all mr + nc rows (next tile prefetched)
   const int rows = mr + nc;
+  if constexpr (Cf::TILED) {
+    // register-tiled: thread = (row of the tile, group of 4 output columns);
+    // per k one row load + 4 broadcast Q loads for 4 complex MACs
+    const int c0 = (tid >> 6) * 4, rr = tid & 63;
+    fetch(0, rows);
+    for (int r0 = 0; r0 < rows; r0 += TRc) {
+      stash();
+      __syncthreads();
+      if (r0 + TRc < rows) fetch(r0 + TRc, rows);
+#pragma unroll
+      for (int hh = 0; hh < TRc / 64; ++hh) {
+        const int r = rr + 64 * hh;
+        cplx o[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
+        for (int k = 0; k < ncols; ++k) {
+          const cplx a = tile[r][k];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cfma(o[q], a, Qm[k][c0 + q]);
+        }
+        if (r0 + r < rows) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q < ncols) __stcg(Y + (long long)cols[c0 + q] * ldy + r0 + r, o[q]);
+        }
+      }
+      __syncthreads();
+    }
+    PROF_MARK(3);
+    return;
+  }
   fetch(0, rows);
   for (int r0 = 0; r0 < rows; r0 += TRc) {
     stash();
@@ -477,7 +562,7 @@ __global__ void __launch_bounds__(NTH) svd_coop_kernel(cplx* Y, long long ldy, i
       }
     }
     const double off = __ldcg(off_cur);
-    if (!(off > tol)) break;
+    if (!(off > tol) || off * off <= 0.01 * tol) break;  // early stop: see svd_rjac.cu c_rj_early
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = min(sweep + 1, max_sweeps);
 }
