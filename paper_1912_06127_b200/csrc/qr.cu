@@ -701,20 +701,27 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   const size_t smem = std::max<size_t>(((size_t)cw * m + (size_t)NB * m + cw) * sizeof(cplx), 116 * 1024);
   if (smem > 200 * 1024) return cudaErrorNotSupported;
   cudaError_t e;
+  // threads per CTA: 512 gives the band's trailing-column updates one warp per
+  // column (the per-reflector critical path), TDVP_QR_NT=256 the older setting
+  static int nt_sel = -1;
+  if (nt_sel < 0) {
+    const char* ev = std::getenv("TDVP_QR_NT");
+    nt_sel = (ev && std::atoi(ev) == 256) ? 256 : 512;
+  }
+  auto fn = nt_sel == 512 ? qrc3_factor_kernel<512, NB, false> : qrc3_factor_kernel<256, NB, false>;
   static bool attr = false;
   if (!attr) {
-    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024)) != cudaSuccess)
-      return e;
-    if ((e = cudaFuncSetAttribute(qrc3_factor_kernel<256, NB, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
-        cudaSuccess)
-      return e;
+    for (auto f : {qrc3_factor_kernel<512, NB, false>, qrc3_factor_kernel<256, NB, false>}) {
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) != cudaSuccess)
+        return e;
+      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+    }
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(Cu);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(nt_sel);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -730,7 +737,7 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
       return e;
   }
   unsigned* nog = nullptr;
-  e = cudaLaunchKernelEx(&cfg, qrc3_factor_kernel<256, NB, false>, A, lda, m, n, cw, tau, RH, ldrh, rh_rows, nog);
+  e = cudaLaunchKernelEx(&cfg, fn, A, lda, m, n, cw, tau, RH, ldrh, rh_rows, nog);
   static int prof = -1;
   if (prof < 0) prof = std::getenv("TDVP_QR_PROF") ? 1 : 0;
   if (prof && e == cudaSuccess) {
