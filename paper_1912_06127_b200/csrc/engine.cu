@@ -297,10 +297,28 @@ void build_site(MpoSite& ms, int Dl, int Dr, int d, const std::vector<cplx>& W) 
     cm.oc_idx = reinterpret_cast<int4*>(b2->p);
     cm.ic_idx = reinterpret_cast<int4*>(b3->p);
     cm.coef = b4->c();
+    // distinct input channels: the gather kernel loads each once per point
+    std::vector<int4> icu;
+    std::vector<int> slot(ic.size());
+    for (size_t e = 0; e < ic.size(); ++e) {
+      size_t k = 0;
+      while (k < icu.size() && !(icu[k].x == ic[e].x && icu[k].y == ic[e].y && icu[k].z == ic[e].z)) ++k;
+      if (k == icu.size()) icu.push_back(ic[e]);
+      slot[e] = (int)k;
+    }
+    cm.n_ic = (int)icu.size();
+    BufPtr b5 = make_buf(std::max<size_t>(1, icu.size()) * sizeof(int4));
+    BufPtr b6 = make_buf(std::max<size_t>(1, slot.size()) * sizeof(int));
+    if (!icu.empty()) CK(cudaMemcpy(b5->p, icu.data(), icu.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    if (!slot.empty()) CK(cudaMemcpy(b6->p, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice));
+    cm.icu_idx = reinterpret_cast<int4*>(b5->p);
+    cm.slot = b6->i();
     ms.store.push_back(std::move(b1));
     ms.store.push_back(std::move(b2));
     ms.store.push_back(std::move(b3));
     ms.store.push_back(std::move(b4));
+    ms.store.push_back(std::move(b5));
+    ms.store.push_back(std::move(b6));
   };
   {  // cmL: out (s, w') <- in (w, t), coef W[w,s,t,w']
     std::vector<int> rp{0};

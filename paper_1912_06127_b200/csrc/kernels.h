@@ -27,6 +27,9 @@ struct ChanMix {
   int4* oc_idx = nullptr;  // device [n_oc]   (c0, c1, c2, -)
   int4* ic_idx = nullptr;  // device [nnz]    (c0, c1, c2, -)
   cplx* coef = nullptr;    // device [nnz]
+  int n_ic = 0;            // distinct input channels
+  int4* icu_idx = nullptr; // device [n_ic]  (c0, c1, c2, -)
+  int* slot = nullptr;     // device [nnz]   entry -> distinct input channel
 };
 struct Strides3 {
   long long s0, s1, s2;
