@@ -692,7 +692,12 @@ __global__ void __launch_bounds__(NT) qr_apply_refl_kernel(QrApplyJob j0, QrAppl
 cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH,
                               long long ldrh, int rh_rows) {
   if (m < n || n < 1) return cudaErrorInvalidValue;
-  const int C = std::min(16, n);
+  static int cmax = -1;
+  if (cmax < 0) {
+    const char* ev = std::getenv("TDVP_QR_C");
+    cmax = ev ? std::max(1, std::min(16, std::atoi(ev))) : 16;
+  }
+  const int C = std::min(cmax, n);
   const int cw = (n + C - 1) / C;
   const int Cu = (n + cw - 1) / cw;
   if (cw > 32) return cudaErrorNotSupported;
