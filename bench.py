@@ -42,6 +42,17 @@ WORKLOADS = {
 }
 
 
+def jac_traffic():
+    """DRAM bytes (read + write) per launch of the Jacobi kernel from the
+    committed ncu --set full capture (profiles/r1b_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1b_traffic.json")) as f:
+            t = json.load(f)["rjac2"]
+        return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def workload_inputs(name):
     import tdvp_inputs as ti
     L, Delta, chi, eps, dt, desc = WORKLOADS[name]
@@ -353,7 +364,7 @@ def main():
         # dominant kernel of the step: the Jacobi stage of the truncated SVD (FP64 SIMT, latency-bound)
         "roofline": {"kernel": "svd_rjac one-sided Jacobi (register-resident block pairs)", "bound": "alu",
                      "achieved": jac_tf, "peak": FP64_ALU_PEAK_TF, "unit": "TFLOP/s",
-                     "frac": (jac_tf / FP64_ALU_PEAK_TF) if jac_tf else None, "traffic": None,
+                     "frac": (jac_tf / FP64_ALU_PEAK_TF) if jac_tf else None, "traffic": jac_traffic(),
                      "peak_source": FP64_ALU_PEAK_SRC,
                      "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
                      "share_of_step": jac_ms / bstep_ms if bstep_ms > 0 else None,

@@ -1,6 +1,6 @@
 """Key metrics of every kernel in an `ncu --set full` report (read with ncu -i ... --page raw --csv).
 
-python tools/ncu_full_summary.py gpurun_out/x.ncu-rep
+python tools/ncu_full_summary.py gpurun_out/x.ncu-rep | gpurun_out/x_raw.csv
 """
 import csv
 import io
@@ -22,7 +22,10 @@ WANT = [
 
 
 def main(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # raw page already exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
