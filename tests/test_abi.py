@@ -137,3 +137,69 @@ def test_balanced_partition_saturated_profile():
 def test_balanced_partition_rejects_invalid(L, p):
     with pytest.raises(B.TdvpError):
         B.balanced_partition(L, p, [1] * (L + 1))
+
+
+# ------------------------------------------ segment-lane channel protocol
+SEND_R, RECV_L, SEND_L, RECV_R = 3, 4, 5, 6
+
+
+@pytest.mark.parametrize("L,p", [(8, 2), (16, 4), (16, 8), (64, 8), (65, 8), (128, 16), (40, 20)])
+def test_lane_channels_depth_one(L, p):
+    """The concurrent-lane executor (engine.cu run_step_lanes) uses depth-1
+    channels: per half-step every channel (q -> q+1 and q+1 -> q) carries at
+    most one message and the neighbour receives it in the same half."""
+    for h in (1, 2):
+        progs = [B.plan(L, p, h, q) for q in range(p)]
+        for q in range(p - 1):
+            sr = sum(op[0] == SEND_R for op in progs[q])
+            rl = sum(op[0] == RECV_L for op in progs[q + 1])
+            sl = sum(op[0] == SEND_L for op in progs[q + 1])
+            rr = sum(op[0] == RECV_R for op in progs[q])
+            assert sr == rl <= 1 and sl == rr <= 1, (h, q, sr, rl, sl, rr)
+
+
+@pytest.mark.parametrize("L,p", [(8, 2), (16, 4), (16, 8), (64, 8), (128, 16), (40, 20)])
+def test_lane_execution_is_deadlock_free(L, p):
+    """Simulate the lanes: p independent programs (half 1 then half 2, no
+    barrier between halves), a SEND blocks while its depth-1 channel is full,
+    a RECV while it is empty.  Under adversarial schedules (always advance the
+    lowest- or highest-numbered runnable lane, or a seeded random one) every
+    program completes."""
+    import random
+    progs = [B.plan(L, p, 1, q) + B.plan(L, p, 2, q) for q in range(p)]
+
+    def chan(q, op):
+        k = op[0]
+        if k == SEND_R:
+            return ("R", q)
+        if k == RECV_L:
+            return ("R", q - 1)
+        if k == SEND_L:
+            return ("L", q)
+        if k == RECV_R:
+            return ("L", q + 1)
+        return None
+
+    for policy in ("low", "high", "rand0", "rand1", "rand2"):
+        rng = random.Random(policy)
+        pc, full = [0] * p, {}
+        while True:
+            runnable = []
+            for q in range(p):
+                if pc[q] == len(progs[q]):
+                    continue
+                op = progs[q][pc[q]]
+                c = chan(q, op)
+                if c is None or (op[0] in (SEND_R, SEND_L) and not full.get(c)) or \
+                        (op[0] in (RECV_L, RECV_R) and full.get(c)):
+                    runnable.append(q)
+            if not runnable:
+                break
+            q = runnable[0] if policy == "low" else runnable[-1] if policy == "high" else rng.choice(runnable)
+            op = progs[q][pc[q]]
+            c = chan(q, op)
+            if c is not None:
+                full[c] = op[0] in (SEND_R, SEND_L)
+            pc[q] += 1
+        assert all(pc[q] == len(progs[q]) for q in range(p)), (policy, pc)
+        assert not any(full.values())
