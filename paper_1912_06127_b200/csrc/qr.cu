@@ -383,7 +383,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // raised by cluster-scope release stores.  GRID = true: a cooperative grid (up
 // to one CTA per SM, for bands that do not fit one cluster), one counter in
 // global memory (`gcnt`, zero on entry) raised with a GPU-scope release.
-template <int NT, int NB, bool GRID>
+template <int NT, int NB, bool GRID, int RPL = 0>
 __global__ void __launch_bounds__(NT, 1)
     qrc3_factor_kernel(cplx* A, long long lda, int m, int n, int cw, cplx* tau, cplx* RH, long long ldrh, int rh_rows,
                        unsigned* gcnt) {
@@ -467,6 +467,128 @@ __global__ void __launch_bounds__(NT, 1)
     for (int r = c0 + 1 + lane; r < m; r += 32) xn2_next += cabs2(Aloc[r]);
     xn2_next = warp_sum(xn2_next);
   }
+  if constexpr (RPL > 0) {
+    // m <= 32 RPL: warp 0 keeps the pivot column in registers (row r = lane +
+    // 32 t in slot t), so the reflector, the scaling and the look-ahead update
+    // of the next column run on registers with one shared-memory load of that
+    // column per reflector; the workers still read v from shared memory
+    cplx pc[RPL];
+    if (wid == 0) {
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        pc[t] = (ncl > 0 && r < m) ? Aloc[r] : cmk(0.0, 0.0);
+      }
+    }
+    for (int i = 0; i < ncl; ++i) {
+      const int k = c0 + i;
+      cplx* col = Aloc + (long long)i * m;
+      cplx vr[RPL];
+      if (wid == 0) {
+        const double xn2 = xn2_next;
+        cplx akk = cmk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+          if (t == (k >> 5)) akk = pc[t];
+        const double ar = __shfl_sync(0xffffffffu, akk.x, k & 31), ai = __shfl_sync(0xffffffffu, akk.y, k & 31);
+        cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
+        double beta = ar;
+        const bool refl = !(xn2 == 0.0 && ai == 0.0);
+        if (refl) {
+          beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+          const double ib = qr_rcp(beta);
+          t_i = cmk((beta - ar) * ib, -ai * ib);
+          const double dr = ar - beta, di = ai;
+          const double iden = qr_rcp(dr * dr + di * di);
+          scale = cmk(dr * iden, -di * iden);
+        }
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int r = lane + 32 * t;
+          if (r > k && r < m) {
+            const cplx v = refl ? cmul(pc[t], scale) : pc[t];
+            vr[t] = v;
+            col[r] = v;
+            __stcg(A + (long long)k * lda + r, v);
+          } else {
+            vr[t] = (r == k) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
+          }
+        }
+        if (lane == (k & 31)) col[k] = cmk(beta, 0.0);
+        if (lane == 0) {
+          s_tau[i] = t_i;
+          __stcg(tau + k, t_i);
+        }
+        __syncwarp();
+        if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl) {
+          if (GRID) {
+            if (lane == 0) {
+              __threadfence();
+              *(volatile unsigned*)gcnt = (unsigned)(k + 1);
+            }
+          } else {
+            for (int c = crank + 1 + lane; c < ncta; c += 32)
+              st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
+          }
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+      const cplx ct = cconj(s_tau[i]);
+      const bool upd = ct.x != 0.0 || ct.y != 0.0;
+      if (wid == 0) {
+        if (i + 1 < ncl) {
+          // look-ahead: column i+1 (rows >= k) <- H_k column i+1, kept in registers
+          const cplx* aj = Aloc + (long long)(i + 1) * m;
+          double dr = 0.0, di = 0.0;
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int r = lane + 32 * t;
+            pc[t] = (r >= k && r < m) ? aj[r] : cmk(0.0, 0.0);
+            const cplx x = cdotc(vr[t], pc[t]);
+            dr += x.x;
+            di += x.y;
+          }
+          cplx f = cmk(0.0, 0.0);
+          if (upd) {
+            dr = warp_sum(dr);
+            di = warp_sum(di);
+            f = cmul(ct, cmk(dr, di));
+          }
+          double nx = 0.0;
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int r = lane + 32 * t;
+            if (upd) pc[t] = csub(pc[t], cmul(vr[t], f));
+            if (r > k + 1 && r < m) nx += cabs2(pc[t]);
+          }
+          xn2_next = warp_sum(nx);
+#pragma unroll
+          for (int t = 0; t < RPL; ++t)
+            if (lane + 32 * t == k) Aloc[(long long)(i + 1) * m + k] = pc[t];  // R[k][i+1] is final
+        }
+      } else {
+        // workers: columns i+2, ... with reflector i (v from shared memory)
+        for (int jl = i + 1 + wid; jl < ncl; jl += NW - 1) {
+          cplx* aj = Aloc + (long long)jl * m;
+          if (!upd) continue;
+          double dr = 0.0, di = 0.0;
+          for (int r = k + lane; r < m; r += 32) {
+            const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
+            const cplx x = cdotc(v, aj[r]);
+            dr += x.x;
+            di += x.y;
+          }
+          dr = warp_sum(dr);
+          di = warp_sum(di);
+          const cplx f = cmul(ct, cmk(dr, di));
+          for (int r = k + lane; r < m; r += 32) {
+            const cplx v = (r == k) ? cmk(1.0, 0.0) : col[r];
+            aj[r] = csub(aj[r], cmul(v, f));
+          }
+        }
+      }
+    }
+  } else {
   for (int i = 0; i < ncl; ++i) {
     const int k = c0 + i;
     cplx* col = Aloc + (long long)i * m;
@@ -551,6 +673,7 @@ __global__ void __launch_bounds__(NT, 1)
     // updates of column i+2 are ordered before warp 0 touches it by the next
     // bar.sync 2
   }
+  }  // RPL == 0
   __syncthreads();
   if (tid == 0 && crank < 16) {
     g_qr_prof[crank][2] = gtime();
@@ -713,10 +836,20 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
     const char* ev = std::getenv("TDVP_QR_NT");
     nt_sel = (ev && std::atoi(ev) == 256) ? 256 : 512;
   }
-  auto fn = nt_sel == 512 ? qrc3_factor_kernel<512, NB, false> : qrc3_factor_kernel<256, NB, false>;
+  static int rpl_env = -1;
+  if (rpl_env < 0) {
+    const char* ev = std::getenv("TDVP_QR_REG");
+    rpl_env = ev ? std::atoi(ev) : 2;  // 2: 512 threads (measured fastest), 1: 256, 0: off
+  }
+  const bool reg = m <= 256 && rpl_env;
+  auto fn = reg ? (rpl_env == 2 ? qrc3_factor_kernel<512, NB, false, 8> : qrc3_factor_kernel<256, NB, false, 8>)
+                : nt_sel == 512 ? qrc3_factor_kernel<512, NB, false>
+                                : qrc3_factor_kernel<256, NB, false>;
+  const int nthreads = reg ? (rpl_env == 2 ? 512 : 256) : nt_sel;
   static bool attr = false;
   if (!attr) {
-    for (auto f : {qrc3_factor_kernel<512, NB, false>, qrc3_factor_kernel<256, NB, false>}) {
+    for (auto f : {qrc3_factor_kernel<512, NB, false, 8>, qrc3_factor_kernel<256, NB, false, 8>,
+                   qrc3_factor_kernel<512, NB, false>, qrc3_factor_kernel<256, NB, false>}) {
       if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) != cudaSuccess)
         return e;
       if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
@@ -726,7 +859,7 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(Cu);
-  cfg.blockDim = dim3(nt_sel);
+  cfg.blockDim = dim3(nthreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   at[0].id = cudaLaunchAttributeClusterDimension;
