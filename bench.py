@@ -37,6 +37,9 @@ WORKLOADS = {
               "seeded random inverse-canonical MPS at saturated chi (SURVEY C6)"),
     "c3sat": (128, 1.5, 512, 1e-10, 0.02,
               "configs[2] shapes: L=128 XXZ Delta=1.5 D=5 chi_max=512 eps=1e-10 dt=0.02, saturated chi (C6)"),
+    "c4sat": (100, 1.0, 256, 1e-12, 0.02,
+              "configs[3] shapes: L=100 long-range XXZ J(r)~1/r^2 as 9 exponentials (MPO D=29) Delta=1 "
+              "chi_max=256 eps=1e-12 dt=0.02, saturated chi (C6)"),
     "c5sat": (256, 1.0, 1024, 1e-12, 0.05,
               "configs[4] shapes: L=256 XXX D=5 chi_max=1024 eps=1e-12 dt=0.05, saturated chi (C6)"),
 }
@@ -56,7 +59,12 @@ def jac_traffic():
 def workload_inputs(name):
     import tdvp_inputs as ti
     L, Delta, chi, eps, dt, desc = WORKLOADS[name]
-    return dict(L=L, chi=chi, eps=eps, dt=dt, desc=desc, mpo=ti.mpo_xxz_nn(L, Delta),
+    if name == "c4sat":
+        a, lam, _, _ = ti.fit_expsum(100, 9, 2.0)
+        mpo = ti.mpo_xxz_expsum(L, a, lam, Delta)
+    else:
+        mpo = ti.mpo_xxz_nn(L, Delta)
+    return dict(L=L, chi=chi, eps=eps, dt=dt, desc=desc, mpo=mpo, D=max(w.shape[3] for w in mpo),
                 mps=ti.random_canonical_mps(L, chi, seed=2))
 
 
@@ -238,7 +246,7 @@ def main():
     peaks = fp64_peak_tflops() if rank == 0 else {}
 
     L = wl["L"]
-    t = pkg.Tdvp(L, 2, 5, wl["chi"])
+    t = pkg.Tdvp(L, 2, wl["D"], wl["chi"])
     t.set_params(eps=wl["eps"], timing=False)  # the timed steps run uninstrumented
     if world > 1:
         uid = [pkg.nccl_unique_id() if rank == 0 else None]
@@ -358,7 +366,7 @@ def main():
         "metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "L": L, "chi_max": wl["chi"], "D_mpo": 5,
+        "config": {"workload": args.workload, "desc": wl["desc"], "L": L, "chi_max": wl["chi"], "D_mpo": wl["D"],
                    "segments": p, "parallelism": f"p2tdvp{p}" if p > 1 else "serial",
                    "l2": "working set (envs + MPS ~ 0.2 GB) larger than L2 (126 MB)"},
         # dominant kernel of the step: the Jacobi stage of the truncated SVD (FP64 SIMT, latency-bound)
