@@ -320,6 +320,23 @@ def main():
         e_ms = (time.perf_counter() - e0) / args.steps * 1e3
         e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": mps_bytes(mps),
                "d2h_bytes_per_step": int(sum(x.nbytes for x in psi) + sum(x.nbytes for x in lam))}
+    # paper-mode Krylov (max 8 vectors, tolerance 1e-6; the
+    # stopping rule runs on the device): a timing variant of the same step
+    paper_mode = None
+    if world == 1:
+        t.set_params(eps=wl["eps"], timing=False, krylov_tol=1e-6)
+        t.set_mps(wl["mps"].psi, wl["mps"].lam)
+        for _ in range(args.warmup):
+            t.step(dt, p)
+        torch.cuda.synchronize()
+        pms = []
+        for _ in range(args.steps):
+            t.step(dt, p)
+            pms.append(t.stats()["step_ms"])
+        t.set_params(eps=wl["eps"], timing=False)
+        paper_mode = {"krylov_tol": 1e-6, "krylov_k_max": 8, "segments": p, "ms_per_step": float(np.mean(pms)),
+                      "note": "timing variant; the headline value uses fixed K = 8 (parity mode, SURVEY AMB-5)"}
+
     # p2TDVP on this one GPU: P segments as concurrent lanes (own thread,
     # stream and workspace each), same workload, fresh state, same timing rules
     lanes = None
@@ -396,6 +413,7 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
         "p2tdvp_one_gpu": lanes,
+        "paper_mode_krylov": paper_mode,
         "chi": wl["chi"],
     }
     if not args.no_cpu_baseline and world == 1:

@@ -44,7 +44,10 @@ typedef struct {
   double eps;             /* relative SV cutoff epsilon, drop sigma < eps*sigma_1; default 1e-12 */
   double w_max;           /* max discarded weight per SVD; 0 = off (default) */
   int krylov_k;           /* Krylov vectors K, 1..15 ("maximum of 8"); default 8 */
-  double krylov_tol;      /* reserved: only 0 (fixed K, parity mode, SURVEY AMB-5) is implemented */
+  double krylov_tol;      /* 0 (default): always krylov_k vectors (parity mode, SURVEY AMB-5);
+                             > 0 (paper mode, "tolerance 1e-6"): stop after iteration k
+                             once n0 beta_k |(exp(tau T_{k+1}) e1)_k| < krylov_tol, decided on
+                             the device (the oracle's rule); a timing variant */
   double multiplet_delta; /* AMB-9 multiplet guard at the chi_max cut; default 1e-6 */
   int timing;             /* 1: record CUDA events around every H_eff matvec and SVD (stats) */
 } tdvp_params;

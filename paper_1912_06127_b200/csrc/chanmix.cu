@@ -15,7 +15,8 @@ constexpr int TPB = 128;
 __global__ void __launch_bounds__(TPB) chanmix_kernel(ChanMix cm, int n_inner, const cplx* __restrict__ in,
                                                       long long so_in, long long si_in, Strides3 ich,
                                                       cplx* __restrict__ out, long long so_out, long long si_out,
-                                                      Strides3 och) {
+                                                      Strides3 och, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   // stage the (small) sparse tables in shared memory
   cplx* s_coef = reinterpret_cast<cplx*>(sm_raw);
@@ -55,7 +56,8 @@ constexpr int GMAX = 32, GCH = 16;
 __global__ void __launch_bounds__(TPB) chanmix_gather_kernel(ChanMix cm, int n_inner, const cplx* __restrict__ in,
                                                              long long so_in, long long si_in, Strides3 ich,
                                                              cplx* __restrict__ out, long long so_out, long long si_out,
-                                                             Strides3 och) {
+                                                             Strides3 och, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   cplx* s_val = reinterpret_cast<cplx*>(sm_raw);          // [n_ic][TPB]
   cplx* s_coef = s_val + (size_t)cm.n_ic * TPB;           // [nnz]
@@ -109,7 +111,7 @@ std::mutex& gmu() {
 
 cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in,
                     long long si_in, Strides3 in_ch, cplx* out, long long so_out, long long si_out,
-                    Strides3 out_ch) {
+                    Strides3 out_ch, const double* skip) {
   if (n_outer <= 0 || n_inner <= 0) return cudaSuccess;
   if (cm.n_ic > 0 && cm.n_ic <= GMAX && cm.slot != nullptr) {
     const size_t smg = (size_t)cm.n_ic * TPB * sizeof(cplx) + (size_t)cm.nnz * (sizeof(cplx) + sizeof(int)) +
@@ -127,7 +129,7 @@ cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner
     if (smg <= 100 * 1024) {
       dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
       chanmix_gather_kernel<<<grid, TPB, smg, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out,
-                                                    out_ch);
+                                                    out_ch, skip);
       return cudaGetLastError();
     }
   }
@@ -144,6 +146,6 @@ cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner
     }
   }
   dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
-  chanmix_kernel<<<grid, TPB, sm, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out, out_ch);
+  chanmix_kernel<<<grid, TPB, sm, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out, out_ch, skip);
   return cudaGetLastError();
 }

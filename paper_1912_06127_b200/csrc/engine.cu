@@ -173,6 +173,7 @@ struct tdvp_ctx {
   // the QR-preconditioned start (8.3), the discarded half being unstructured.
   bool warm_svd = false;
   bool lz_fused = true;  // one cooperative launch per Lanczos iteration (TDVP_LZ_FUSED=0: four passes)
+  const double* cur_skip = nullptr;  // inside a paper-mode Lanczos: its device "converged" flag
   int dev = 0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -263,13 +264,13 @@ int ev_record(tdvp_ctx* h) {
 void gemm(tdvp_ctx* h, int opA, int opB, int M, int N, int K, const cplx* A, long long lda, const cplx* B,
           long long ldb, cplx* C, long long ldc) {
   CK(zgemm(h->st, opA, opB, M, N, K, ONE, A, lda, B, ldb, ZERO, C, ldc, 1, 0, 0, 0, h->gemm_work->c(),
-           (size_t)h->work_elems));
+           (size_t)h->work_elems, h->cur_skip));
   g_gemm_count++;
   g_launch_count++;
 }
 void cmix(tdvp_ctx* h, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in, long long si_in,
           Strides3 ich, cplx* out, long long so_out, long long si_out, Strides3 och) {
-  CK(chanmix(h->st, cm, n_outer, n_inner, in, so_in, si_in, ich, out, so_out, si_out, och));
+  CK(chanmix(h->st, cm, n_outer, n_inner, in, so_in, si_in, ich, out, so_out, si_out, och, h->cur_skip));
   g_launch_count++;
 }
 
@@ -429,6 +430,12 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
   cplx* w = h->wvec->c();
   CK(lz_start(h->st, h->lz, x, V, n));
   g_launch_count += 2;
+  // paper mode (krylov_tol > 0): the convergence test runs on
+  // the device; once it passes, every later kernel of this exponential
+  // (matvec GEMMs and channel mixes, Lanczos iterations) returns at once
+  const double ktol = h->prm.krylov_tol;
+  const bool paper = ktol > 0.0;
+  h->cur_skip = paper ? h->lz.scal + LZ_SKIP : nullptr;
   for (int k = 0; k < K; ++k) {
     int e0 = -1;
     if (h->prm.timing && which) e0 = ev_record(h);
@@ -439,8 +446,9 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
       if (which == 2) { h->stats.heff2_flop += mv_flop; h->stats.heff2_calls++; }
       else h->stats.heff1_flop += mv_flop;
     }
-    if (h->lz_fused) {
-      CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0));
+    if (h->lz_fused || paper) {
+      CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0, ktol, tre,
+                 tim));
       g_launch_count++;
     } else {
       CK(lz_dots(h->st, h->lz, V, n, k + 1, w, n, k));
@@ -453,6 +461,7 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
       }
     }
   }
+  h->cur_skip = nullptr;
   CK(lz_tridiag_exp(h->st, h->lz, K, tre, tim));
   CK(lz_combine(h->st, h->lz, V, n, K, out, n));
   g_launch_count += 2;
@@ -1426,8 +1435,8 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
 int tdvp_set_params(tdvp_t h, const tdvp_params* p) {
   if (!h || !p) return TDVP_EARG;
   if (p->krylov_k < 1 || p->krylov_k >= KMAX || !(p->eps >= 0.0) || p->eps >= 1.0 || !(p->w_max >= 0.0) ||
-      !(p->multiplet_delta >= 0.0) || p->krylov_tol != 0.0) {
-    h->err = "invalid params (krylov_k in 1..15, 0 <= eps < 1, w_max >= 0, krylov_tol == 0)";
+      !(p->multiplet_delta >= 0.0) || !(p->krylov_tol >= 0.0) || p->krylov_tol >= 1.0) {
+    h->err = "invalid params (krylov_k in 1..15, 0 <= eps < 1, w_max >= 0, 0 <= krylov_tol < 1)";
     return TDVP_EARG;
   }
   h->prm = *p;

@@ -15,7 +15,8 @@ extern int g_num_sms;
 enum { OP_N = 0, OP_T = 1, OP_C = 2, OP_R = 3 };
 cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
                   const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch = 1, long long sA = 0,
-                  long long sB = 0, long long sC = 0, cplx* work = nullptr, size_t work_elems = 0);
+                  long long sB = 0, long long sC = 0, cplx* work = nullptr, size_t work_elems = 0,
+                  const double* skip = nullptr);
 
 // -------------------------------------------------------------- chanmix.cu
 // Sparse MPO-channel contraction:
@@ -34,8 +35,10 @@ struct ChanMix {
 struct Strides3 {
   long long s0, s1, s2;
 };
+// skip: device flag, != 0 -> the kernel returns at once (converged Lanczos, krylov_tol > 0)
 cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner, const cplx* in, long long so_in,
-                    long long si_in, Strides3 in_ch, cplx* out, long long so_out, long long si_out, Strides3 out_ch);
+                    long long si_in, Strides3 in_ch, cplx* out, long long so_out, long long si_out, Strides3 out_ch,
+                    const double* skip = nullptr);
 
 // ---------------------------------------------------------------- vec.cu
 cudaError_t scale_rows(cudaStream_t st, cplx* out, const cplx* in, const double* v, int rows, long long cols);
@@ -57,7 +60,7 @@ struct LanczosDev {
   unsigned* counter;  // last-block counter (self-resetting)
   int* brk_count;     // number of Lanczos runs that hit breakdown
 };
-enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1 };
+enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1, LZ_SKIP = 2 * KMAX + 2, LZ_KEFF = 2 * KMAX + 3 };
 int lanczos_nblk(long long n);
 cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* v0, long long n);
 cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
@@ -68,8 +71,13 @@ cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, 
                            long long n, int k);
 cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k);
 // one cooperative launch for a whole Lanczos iteration after the matvec (see lanczos.cu)
+// tol > 0 (paper mode, "convergence tolerance 1e-6"): after
+// beta_k, block 0 estimates the error n0 beta_k |(exp(tau T_{k+1}) e1)_k| and,
+// below tol, sets scal[LZ_SKIP] (every later kernel of this Lanczos returns at
+// once) and scal[LZ_KEFF] = k + 1 (the Krylov dimension used by the final exp
+// and combination)
 cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
-                    long long n, int k, int last);
+                    long long n, int k, int last, double tol = 0.0, double tau_re = 0.0, double tau_im = 0.0);
 cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im);
 cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
                        long long n);

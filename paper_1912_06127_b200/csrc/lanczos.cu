@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(TPB) lz_norm_kernel(LanczosDev d, const cplx* 
     for (int i = 0; i < 2 * KMAX; ++i) d.scal[i] = 0.0;
     d.scal[LZ_N0] = sqrt(t);
     d.scal[LZ_BRK] = 0.0;
+    d.scal[LZ_SKIP] = 0.0;
+    d.scal[LZ_KEFF] = 0.0;
     *d.counter = 0u;
   }
 }
@@ -287,14 +289,15 @@ __device__ void lz_tridiag_exp_jacobi(LanczosDev d, int K, double tre, double ti
 __constant__ double c_inv_k[21] = {0.0,       1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,
                                    1.0 / 7,   1.0 / 8,    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13,
                                    1.0 / 14,  1.0 / 15,   1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20};
-__global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
-  const int r = threadIdx.x;
+// lane r (< K) returns (n0 exp(tau T_K) e1)_r by the Taylor scheme below; ok =
+// false (warp-uniform) when |tau| ||T - a0|| > 16 (the caller falls back)
+__device__ cplx lz_taylor_e1(const LanczosDev& d, int K, double tre, double tim, double n0, bool& ok) {
+  const int r = threadIdx.x & 31;
   const bool on = r < K;
   const double al = on ? d.scal[r] : 0.0;
   const double bl = (on && r + 1 < K) ? d.scal[KMAX + r] : 0.0;  // beta_r couples r, r+1
   double bm = __shfl_up_sync(0xffffffffu, bl, 1);                 // beta_{r-1}
   if (r == 0 || !on) bm = 0.0;
-  // shift a0 = centre of the diagonal range
   double amax = on ? al : -1e300, amin = on ? al : 1e300;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -305,34 +308,41 @@ __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K,
   const double dl = on ? al - a0 : 0.0;
   double rn = on ? fabs(dl) + fabs(bl) + fabs(bm) : 0.0;
   rn = warp_max(rn);
-  const double tabs = sqrt(tre * tre + tim * tim);
-  const double b = tabs * rn;
-  if (b > 16.0) {
-    lz_tridiag_exp_jacobi(d, K, tre, tim);
-    return;
-  }
+  const double b = sqrt(tre * tre + tim * tim) * rn;
+  ok = b <= 16.0;
+  if (!ok) return cmk(0.0, 0.0);
   const int nsub = max(1, (int)ceil(2.0 * b));
   const double hr = tre / nsub, hi = tim / nsub;
-  cplx y = cmk(r == 0 ? d.scal[LZ_N0] : 0.0, 0.0);
+  cplx y = cmk(r == 0 ? n0 : 0.0, 0.0);
   for (int sub = 0; sub < nsub; ++sub) {
     cplx z = y, t = y;
     for (int k = 1; k <= 20; ++k) {
       const double txm = __shfl_up_sync(0xffffffffu, t.x, 1), tym = __shfl_up_sync(0xffffffffu, t.y, 1);
       const double txp = __shfl_down_sync(0xffffffffu, t.x, 1), typ = __shfl_down_sync(0xffffffffu, t.y, 1);
-      // u = (T - a0) t   (real T)
       cplx u = cmk(dl * t.x + bm * (r > 0 ? txm : 0.0) + bl * txp, dl * t.y + bm * (r > 0 ? tym : 0.0) + bl * typ);
       if (!on) u = cmk(0.0, 0.0);
-      const double f = c_inv_k[k];  // no 200-cycle IEEE division on the dependency chain
+      const double f = c_inv_k[k];
       t = cmk((hr * u.x - hi * u.y) * f, (hr * u.y + hi * u.x) * f);
       z = cadd(z, t);
     }
     y = z;
   }
-  // e^{tau a0}
   const double mag = exp(tre * a0);
   double sn, cs;
   sincos(tim * a0, &sn, &cs);
-  if (on) d.y[r] = cmul(cmk(mag * cs, mag * sn), y);
+  return cmul(cmk(mag * cs, mag * sn), y);
+}
+
+__global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K, double tre, double tim) {
+  // paper mode: the Krylov dimension the Lanczos converged at
+  if (d.scal[LZ_SKIP] != 0.0) K = min(K, (int)d.scal[LZ_KEFF]);
+  bool ok;
+  const cplx yv = lz_taylor_e1(d, K, tre, tim, d.scal[LZ_N0], ok);
+  if (!ok) {
+    lz_tridiag_exp_jacobi(d, K, tre, tim);
+    return;
+  }
+  if ((int)threadIdx.x < K) d.y[threadIdx.x] = yv;
 }
 
 // One Lanczos iteration after the matvec in ONE cooperative launch (replaces
@@ -345,7 +355,9 @@ __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K,
 //   phase 4  v_{k+1} = w / beta_k      (hard zero after breakdown)
 template <int NV>
 __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* __restrict__ V, long long ldv, cplx* w,
-                                                      cplx* vnext, long long n, int k, int last) {
+                                                      cplx* vnext, long long n, int k, int last, double tol,
+                                                      double tre, double tim) {
+  if (d.scal[LZ_SKIP] != 0.0) return;  // converged earlier (paper mode)
   cgl::grid_group grid = cgl::this_grid();
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NQ = 2 * NV;
@@ -449,13 +461,24 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
       d.scal[KMAX + k] = b;
     }
   }
+  // paper-mode convergence test (the oracle's rule): n0 beta_k |(exp(tau T_{k+1}) e1)_k| < tol
+  if (tol > 0.0 && blockIdx.x == 0 && wid == 0) {
+    bool ok;
+    const cplx yv = lz_taylor_e1(d, k + 1, tre, tim, __ldcg(d.scal + LZ_N0), ok);
+    const double yk = __shfl_sync(0xffffffffu, sqrt(yv.x * yv.x + yv.y * yv.y), k);
+    if (lane == 0 && ok && (brk ? 0.0 : b) * yk < tol) {
+      d.scal[LZ_KEFF] = (double)(k + 1);
+      d.scal[LZ_SKIP] = 1.0;
+    }
+  }
   // ---- phase 4
   const double inv = brk ? 0.0 : 1.0 / b;
   for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) vnext[e] = cscale(w[e], inv);
 }
 
 __global__ void lz_combine_kernel(const cplx* __restrict__ y, const cplx* __restrict__ V, long long ldv, int K,
-                                  cplx* __restrict__ out, long long n) {
+                                  cplx* __restrict__ out, long long n, const double* __restrict__ scal) {
+  if (scal[LZ_SKIP] != 0.0) K = min(K, (int)scal[LZ_KEFF]);
   __shared__ cplx s_y[KMAX];
   if (threadIdx.x < K) s_y[threadIdx.x] = y[threadIdx.x];
   __syncthreads();
@@ -497,7 +520,7 @@ cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double t
   return cudaGetLastError();
 }
 cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
-                    long long n, int k, int last) {
+                    long long n, int k, int last, double tol, double tau_re, double tau_im) {
   static int occ[KMAX + 1] = {0};
   void* fn = nullptr;
   switch (nv) {
@@ -526,12 +549,13 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
   const int G = (int)std::max<long long>(
       1, std::min<long long>(std::min<long long>(nblk_for(n), (long long)occ[nv] * g_num_sms),
                              std::min<long long>(want, 2LL * g_num_sms)));
-  void* args[] = {(void*)&d, (void*)&V, (void*)&ldv, (void*)&w, (void*)&vnext, (void*)&n, (void*)&k, (void*)&last};
+  void* args[] = {(void*)&d,    (void*)&V,   (void*)&ldv, (void*)&w,      (void*)&vnext, (void*)&n,
+                  (void*)&k,    (void*)&last, (void*)&tol, (void*)&tau_re, (void*)&tau_im};
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(TPB), args, 0, st);
 }
 
 cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
                        long long n) {
-  lz_combine_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.y, V, ldv, K, out, n);
+  lz_combine_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.y, V, ldv, K, out, n, d.scal);
   return cudaGetLastError();
 }

@@ -29,6 +29,7 @@ struct GemmArgs {
   long long ldc, sC;
   int ksplit, kchunk;
   cplx* work;  // split-K partials [batch*ksplit][M][N]
+  const double* skip;  // != 0 on device: return at once (Lanczos converged, krylov_tol > 0)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -50,6 +51,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 template <int OPA, int OPB, int BM, int BN>
 __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
+  if (g.skip != nullptr && *g.skip != 0.0) return;
   constexpr bool TA = (OPA == 1 || OPA == 2), CA = (OPA == 2 || OPA == 3);
   constexpr bool TB = (OPB == 1 || OPB == 2), CB = (OPB == 2 || OPB == 3);
   constexpr int PAT = BM + 2, PB = BN + 2;
@@ -192,7 +194,8 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
 }
 
 __global__ void splitk_reduce_kernel(int M, int N, int ksplit, int batch, const cplx* __restrict__ work, cplx alpha,
-                                     cplx beta, cplx* C, long long ldc, long long sC) {
+                                     cplx beta, cplx* C, long long ldc, long long sC, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
   const long long MN = (long long)M * N;
   const long long total = MN * batch;
   const bool use_beta = (beta.x != 0.0 || beta.y != 0.0);
@@ -266,7 +269,7 @@ int g_num_sms = 148;
 
 cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
                   const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch, long long sA,
-                  long long sB, long long sC, cplx* work, size_t work_elems) {
+                  long long sB, long long sC, cplx* work, size_t work_elems, const double* skip) {
   if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
   if (K <= 0) {
     for (int b = 0; b < batch; ++b) {
@@ -281,6 +284,7 @@ cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx a
   g.B = B; g.ldb = ldb; g.sB = sB;
   g.C = C; g.ldc = ldc; g.sC = sC;
   g.work = work;
+  g.skip = skip;
   // tile choice: 64x64 when that gives >= 2 waves of CTAs, else 32x32 (4x more CTAs)
   const long long tiles64 = (long long)((M + 63) / 64) * ((N + 63) / 64) * batch;
   const bool small = tiles64 < 2LL * g_num_sms;
@@ -305,6 +309,6 @@ cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx a
   if (e != cudaSuccess || ksplit == 1) return e;
   const long long total = (long long)M * N * batch;
   const int blocks = (int)std::min<long long>(4LL * g_num_sms, (total + 255) / 256);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ksplit, batch, work, alpha, beta, C, ldc, sC);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(M, N, ksplit, batch, work, alpha, beta, C, ldc, sC, skip);
   return cudaGetLastError();
 }

@@ -126,8 +126,8 @@ class Tdvp:
 
     __del__ = close
 
-    def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False):
-        p = tdvp_params(eps, w_max, krylov_k, 0.0, multiplet_delta, int(bool(timing)))
+    def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False, krylov_tol=0.0):
+        p = tdvp_params(eps, w_max, krylov_k, krylov_tol, multiplet_delta, int(bool(timing)))
         _check(lib().tdvp_set_params(self.h, C.byref(p)), self.h)
 
     def set_mpo(self, W):

@@ -261,3 +261,29 @@ def test_explicit_partition_matches_oracle(B, lanes, monkeypatch):
     O.step(st2, 0.05)
     assert np.abs(t.measure_sz() - O.measure(st2)["sz"]).max() < 1e-6
     t.close()
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_paper_mode_krylov_tol_matches_oracle(B, p):
+    """krylov_tol > 0 (paper mode: max 8 vectors, tolerance
+    1e-6): the device-side stopping rule equals the oracle's, so the runs agree
+    like the fixed-K runs; and they differ from fixed K = 8 by at most ~tol."""
+    L = 12
+    mps, W = ti.random_canonical_mps(L, 8, seed=3), ti.mpo_xxz_nn(L, 0.5)
+    res = {}
+    for tol in (0.0, 1e-6):
+        t = B.Tdvp(L, 2, 5, 8)
+        t.set_params(eps=1e-10, krylov_tol=tol)
+        t.set_mpo(W)
+        t.set_mps(mps.psi, mps.lam)
+        st = O.init_state(mps, W, O.Params(chi_max=8, eps=1e-10, krylov_tol=tol), p)
+        for _ in range(3):
+            t.step(0.05, p)
+            O.step(st, 0.05)
+        m = O.measure(st)
+        assert t.chi() == O.chi_profile(st)
+        assert np.abs(t.measure_sz() - m["sz"]).max() < 1e-6
+        assert abs(t.measure_energy() - m["energy"]) < 1e-6
+        res[tol] = t.measure_sz()
+        t.close()
+    assert np.abs(res[0.0] - res[1e-6]).max() < 1e-4

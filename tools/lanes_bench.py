@@ -15,7 +15,8 @@ wl = bench.workload_inputs(sys.argv[1] if len(sys.argv) > 1 else "c2sat")
 ps = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
 for p in ps:
     t = pkg.Tdvp(wl["L"], 2, 5, wl["chi"])
-    t.set_params(eps=wl["eps"], timing=bool(int(os.environ.get("LB_TIMING", "0"))))
+    t.set_params(eps=wl["eps"], timing=bool(int(os.environ.get("LB_TIMING", "0"))),
+                 krylov_tol=float(os.environ.get("LB_KTOL", "0")))
     t.set_mpo(wl["mpo"])
     t.set_mps(wl["mps"].psi, wl["mps"].lam)
     for _ in range(2):
