@@ -142,3 +142,41 @@ def test_reorthonormalize_continues_run(B):
     assert a.infidelity(b) < 1e-12
     a.close()
     b.close()
+
+
+def test_many_lanes_match_oracle(B):
+    """16 concurrent segment lanes (L = 32, 2 sites each) against the oracle on
+    the same partition; then the round-robin executor gives identical numbers."""
+    import os
+    L, p = 32, 16
+    mps, W = ti.random_canonical_mps(L, 8, seed=8), ti.mpo_xxz_nn(L, 0.5)
+    st = O.init_state(mps, W, O.Params(chi_max=8, eps=1e-10), p)
+    for _ in range(2):
+        O.step(st, 0.05)
+    m = O.measure(st)
+    out = {}
+    for lanes in ("1", "0"):
+        os.environ["TDVP_LANES"] = lanes
+        try:
+            t = handle(B, W, mps, 8, eps=1e-10)
+        finally:
+            os.environ.pop("TDVP_LANES", None)
+        for _ in range(2):
+            t.step(0.05, p)
+        assert t.chi() == O.chi_profile(st)
+        out[lanes] = t.measure_sz()
+        assert np.abs(out[lanes] - m["sz"]).max() < 1e-6
+        t.close()
+    assert np.array_equal(out["1"], out["0"])  # same kernels, same order per segment: bit-identical
+
+
+def test_maybe_reorthonormalize(B):
+    L = 10
+    W = ti.mpo_xxz_nn(L, 0.5)
+    t = handle(B, W, ti.random_canonical_mps(L, 8, seed=6), 16)
+    assert not t.maybe_reorthonormalize(1e-3)  # canonical input: norm 1
+    psi, lam = t.get_mps()
+    t.set_mps([2.0 * x if j == 3 else x for j, x in enumerate(psi)], lam)  # norm 4
+    assert t.maybe_reorthonormalize(1e-3)
+    assert abs(t.measure_norm() - 1.0) < 1e-12
+    t.close()
