@@ -945,7 +945,15 @@ cudaError_t qr_apply_refl2(cudaStream_t st, const cplx* A0, long long lda0, cons
   const int nb0 = (nc0 + 7) / 8, nb1 = A1 ? (nc1 + 7) / 8 : 0;
   const int m = std::max(m0, A1 ? m1 : 0);
   const int blocks = nb0 + nb1;
-  if (m <= 256) qr_apply_refl_kernel<1, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
+  static int small_nt = -1;
+  if (small_nt < 0) {
+    const char* ev = std::getenv("TDVP_QR_APPLY_NT");
+    small_nt = ev ? std::atoi(ev) : 128;  // measured: 128 threads (2 rows each) fastest at n = 256
+  }
+  if (m <= 128 && small_nt == 128) qr_apply_refl_kernel<1, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
+  else if (m <= 256 && small_nt == 128) qr_apply_refl_kernel<2, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
+  else if (m <= 256 && small_nt == 64) qr_apply_refl_kernel<4, 64><<<blocks, 64, 0, st>>>(j0, j1, nb0);
+  else if (m <= 256) qr_apply_refl_kernel<1, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else if (m <= 512) qr_apply_refl_kernel<2, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else if (m <= 1024) qr_apply_refl_kernel<4, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else return cudaErrorNotSupported;
