@@ -368,8 +368,25 @@ def main():
             bms.append(t.stats()["step_ms"])
         bv = float(np.mean(bms))
         t.set_partition(None)
+        # strong scaling of p2TDVP on the one GPU (uniform partition, lanes)
+        scal = []
+        for qq in (2, 4, 16):
+            if qq > L // 2:
+                continue
+            t.set_mps(wl["mps"].psi, wl["mps"].lam)
+            for _ in range(max(1, args.warmup - 1)):
+                t.step(dt, qq)
+            torch.cuda.synchronize()
+            sms = []
+            for _ in range(args.steps):
+                t.step(dt, qq)
+                sms.append(t.stats()["step_ms"])
+            scal.append({"segments": qq, "ms_per_step": float(np.mean(sms))})
+        scal.append({"segments": q, "ms_per_step": lv})
+        scal.sort(key=lambda x: x["segments"])
         lanes["balanced"] = {"bounds": bounds, "ms_per_step": bv,
                              "speedup_vs_serial": ms_per_step / bv if bv > 0 else None}
+        lanes["scaling"] = [dict(x, speedup_vs_serial=ms_per_step / x["ms_per_step"]) for x in scal]
     t.close()
 
     if rank != 0:
