@@ -121,6 +121,10 @@ struct MpoSite {
   int Dl = 1, Dr = 1;
   ChanMix cmL;  // (w,t) -> (s,w'): H1, H2 stages, env_left
   ChanMix cmR;  // (t,w') -> (w,s): env_right
+  // pair (j, j+1): (w,t1,t2) -> (s1,s2,w''), coef sum_w' W_j[w,s1,t1,w'] W_{j+1}[w',s2,t2,w''];
+  // H_eff^(2)'s two channel stages in one pass when its inputs fit the gather kernel
+  ChanMix cm12;
+  bool has12 = false;
   std::vector<BufPtr> store;
 };
 
@@ -276,6 +280,46 @@ void cmix(tdvp_ctx* h, const ChanMix& cm, int n_outer, int n_inner, const cplx* 
 
 // build CSR tables of one MPO site tensor W (Dl, d, d, Dr) (host structure pass;
 // the values are copied, not computed)
+void upload_mix(MpoSite& ms, ChanMix& cm, const std::vector<int>& rowptr, const std::vector<int4>& oc,
+                const std::vector<int4>& ic, const std::vector<cplx>& coef) {
+  cm.n_oc = (int)oc.size();
+  cm.nnz = (int)ic.size();
+  BufPtr b1 = make_buf(rowptr.size() * sizeof(int));
+  BufPtr b2 = make_buf(std::max<size_t>(1, oc.size()) * sizeof(int4));
+  BufPtr b3 = make_buf(std::max<size_t>(1, ic.size()) * sizeof(int4));
+  BufPtr b4 = make_buf(std::max<size_t>(1, coef.size()) * sizeof(cplx));
+  CK(cudaMemcpy(b1->p, rowptr.data(), rowptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (!oc.empty()) CK(cudaMemcpy(b2->p, oc.data(), oc.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!ic.empty()) CK(cudaMemcpy(b3->p, ic.data(), ic.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!coef.empty()) CK(cudaMemcpy(b4->p, coef.data(), coef.size() * sizeof(cplx), cudaMemcpyHostToDevice));
+  cm.rowptr = b1->i();
+  cm.oc_idx = reinterpret_cast<int4*>(b2->p);
+  cm.ic_idx = reinterpret_cast<int4*>(b3->p);
+  cm.coef = b4->c();
+  // distinct input channels: the gather kernel loads each once per point
+  std::vector<int4> icu;
+  std::vector<int> slot(ic.size());
+  for (size_t e = 0; e < ic.size(); ++e) {
+    size_t k = 0;
+    while (k < icu.size() && !(icu[k].x == ic[e].x && icu[k].y == ic[e].y && icu[k].z == ic[e].z)) ++k;
+    if (k == icu.size()) icu.push_back(ic[e]);
+    slot[e] = (int)k;
+  }
+  cm.n_ic = (int)icu.size();
+  BufPtr b5 = make_buf(std::max<size_t>(1, icu.size()) * sizeof(int4));
+  BufPtr b6 = make_buf(std::max<size_t>(1, slot.size()) * sizeof(int));
+  if (!icu.empty()) CK(cudaMemcpy(b5->p, icu.data(), icu.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (!slot.empty()) CK(cudaMemcpy(b6->p, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice));
+  cm.icu_idx = reinterpret_cast<int4*>(b5->p);
+  cm.slot = b6->i();
+  ms.store.push_back(std::move(b1));
+  ms.store.push_back(std::move(b2));
+  ms.store.push_back(std::move(b3));
+  ms.store.push_back(std::move(b4));
+  ms.store.push_back(std::move(b5));
+  ms.store.push_back(std::move(b6));
+}
+
 void build_site(MpoSite& ms, int Dl, int Dr, int d, const std::vector<cplx>& W) {
   ms.Dl = Dl;
   ms.Dr = Dr;
@@ -283,44 +327,7 @@ void build_site(MpoSite& ms, int Dl, int Dr, int d, const std::vector<cplx>& W) 
   auto at = [&](int w, int s, int t, int w2) { return W[(((size_t)w * d + s) * d + t) * Dr + w2]; };
   auto nz = [](cplx v) { return v.x != 0.0 || v.y != 0.0; };
   auto upload = [&](ChanMix& cm, const std::vector<int>& rowptr, const std::vector<int4>& oc,
-                    const std::vector<int4>& ic, const std::vector<cplx>& coef) {
-    cm.n_oc = (int)oc.size();
-    cm.nnz = (int)ic.size();
-    BufPtr b1 = make_buf(rowptr.size() * sizeof(int));
-    BufPtr b2 = make_buf(std::max<size_t>(1, oc.size()) * sizeof(int4));
-    BufPtr b3 = make_buf(std::max<size_t>(1, ic.size()) * sizeof(int4));
-    BufPtr b4 = make_buf(std::max<size_t>(1, coef.size()) * sizeof(cplx));
-    CK(cudaMemcpy(b1->p, rowptr.data(), rowptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (!oc.empty()) CK(cudaMemcpy(b2->p, oc.data(), oc.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    if (!ic.empty()) CK(cudaMemcpy(b3->p, ic.data(), ic.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    if (!coef.empty()) CK(cudaMemcpy(b4->p, coef.data(), coef.size() * sizeof(cplx), cudaMemcpyHostToDevice));
-    cm.rowptr = b1->i();
-    cm.oc_idx = reinterpret_cast<int4*>(b2->p);
-    cm.ic_idx = reinterpret_cast<int4*>(b3->p);
-    cm.coef = b4->c();
-    // distinct input channels: the gather kernel loads each once per point
-    std::vector<int4> icu;
-    std::vector<int> slot(ic.size());
-    for (size_t e = 0; e < ic.size(); ++e) {
-      size_t k = 0;
-      while (k < icu.size() && !(icu[k].x == ic[e].x && icu[k].y == ic[e].y && icu[k].z == ic[e].z)) ++k;
-      if (k == icu.size()) icu.push_back(ic[e]);
-      slot[e] = (int)k;
-    }
-    cm.n_ic = (int)icu.size();
-    BufPtr b5 = make_buf(std::max<size_t>(1, icu.size()) * sizeof(int4));
-    BufPtr b6 = make_buf(std::max<size_t>(1, slot.size()) * sizeof(int));
-    if (!icu.empty()) CK(cudaMemcpy(b5->p, icu.data(), icu.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    if (!slot.empty()) CK(cudaMemcpy(b6->p, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice));
-    cm.icu_idx = reinterpret_cast<int4*>(b5->p);
-    cm.slot = b6->i();
-    ms.store.push_back(std::move(b1));
-    ms.store.push_back(std::move(b2));
-    ms.store.push_back(std::move(b3));
-    ms.store.push_back(std::move(b4));
-    ms.store.push_back(std::move(b5));
-    ms.store.push_back(std::move(b6));
-  };
+                    const std::vector<int4>& ic, const std::vector<cplx>& coef) { upload_mix(ms, cm, rowptr, oc, ic, coef); };
   {  // cmL: out (s, w') <- in (w, t), coef W[w,s,t,w']
     std::vector<int> rp{0};
     std::vector<int4> oc, ic;
@@ -357,6 +364,37 @@ void build_site(MpoSite& ms, int Dl, int Dr, int d, const std::vector<cplx>& W) 
   }
 }
 
+// H_eff^(2) pair table of sites (j, j+1) (host structure pass over the two
+// MPO tensors; only used when the (w, t1, t2) inputs fit the gather kernel)
+void build_pair(MpoSite& ms, int Dl, int Dm, int Dr, int d, const std::vector<cplx>& W1,
+                const std::vector<cplx>& W2) {
+  ms.has12 = false;
+  if (Dl * d * d > 32) return;
+  auto a1 = [&](int w, int s, int t, int w2) { return W1[(((size_t)w * d + s) * d + t) * Dm + w2]; };
+  auto a2 = [&](int w, int s, int t, int w2) { return W2[(((size_t)w * d + s) * d + t) * Dr + w2]; };
+  std::vector<int> rp{0};
+  std::vector<int4> oc, ic;
+  std::vector<cplx> cf;
+  for (int s1 = 0; s1 < d; ++s1)
+    for (int s2 = 0; s2 < d; ++s2)
+      for (int w3 = 0; w3 < Dr; ++w3) {
+        oc.push_back(make_int4(s1, s2, w3, 0));
+        for (int w = 0; w < Dl; ++w)
+          for (int t1 = 0; t1 < d; ++t1)
+            for (int t2 = 0; t2 < d; ++t2) {
+              cplx v = ZERO;
+              for (int w2 = 0; w2 < Dm; ++w2) v = cadd(v, cmul(a1(w, s1, t1, w2), a2(w2, s2, t2, w3)));
+              if (v.x != 0.0 || v.y != 0.0) {
+                ic.push_back(make_int4(w, t1, t2, 0));
+                cf.push_back(v);
+              }
+            }
+        rp.push_back((int)ic.size());
+      }
+  upload_mix(ms, ms.cm12, rp, oc, ic, cf);
+  ms.has12 = ms.cm12.n_ic <= 32;
+}
+
 size_t nnz_of(const MpoSite& ms) { return (size_t)ms.cmL.nnz; }
 
 // ---------------------------------------------------------- contractions
@@ -368,6 +406,14 @@ void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, 
   cplx* T2 = h->T2->c();
   // stage 1: T1[(a,w),(t1,t2,b')] = L[(a,w),a'] x[a',(t1,t2,b')]
   gemm(h, OP_N, OP_N, cl * Dl, d * d * cr, cl, Lenv, cl, x, (long long)d * d * cr, T1, (long long)d * d * cr);
+  if (W1.has12) {
+    // stages 2+3 in one pass: T3[a][s1][s2][w''][b'] = sum W12[(w,t1,t2) -> (s1,s2,w'')] T1[a][w][t1][t2][b']
+    cmix(h, W1.cm12, cl, cr, T1, (long long)Dl * d * d * cr, 1,
+         Strides3{(long long)d * d * cr, (long long)d * cr, (long long)cr}, T2, (long long)d * d * Dr * cr, 1,
+         Strides3{(long long)d * Dr * cr, (long long)Dr * cr, (long long)cr});
+    gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+    return;
+  }
   // stage 2: T2[a][s1][w'][(t2,b')] = sum W1[w,s1,t1,w'] T1[a][w][t1][(t2,b')]
   cmix(h, W1.cmL, cl, d * cr, T1, (long long)Dl * d * d * cr, 1, Strides3{(long long)d * d * cr, (long long)d * cr, 0},
        T2, (long long)d * Dm * d * cr, 1, Strides3{(long long)Dm * d * cr, (long long)d * cr, 0});
@@ -1464,6 +1510,14 @@ int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W) {
         if (!std::isfinite(W[j][i])) throw TdvpError(TDVP_ENONFINITE, "non-finite MPO entry");
       build_site(mpo[j], D[j], D[j + 1], d, to_cplx(W[j], n));
     }
+    static int fuse = -1;
+    if (fuse < 0) {
+      const char* ev = std::getenv("TDVP_HEFF_FUSE");
+      fuse = ev ? std::atoi(ev) : 1;
+    }
+    for (int j = 0; fuse && j + 1 < L; ++j)
+      build_pair(mpo[j], D[j], D[j + 1], D[j + 2], d, to_cplx(W[j], (size_t)D[j] * d * d * D[j + 1]),
+                 to_cplx(W[j + 1], (size_t)D[j + 1] * d * d * D[j + 2]));
     h->mpo = std::move(mpo);
     h->have_mpo = true;
     h->envs_valid = false;
@@ -1894,6 +1948,7 @@ int tdvp_apply_heff2(int cl, int cr, int d, int Dl, int Dm, int Dr, const double
     MpoSite w1, w2;
     build_site(w1, Dl, Dm, d, to_cplx(W1, (size_t)Dl * d * d * Dm));
     build_site(w2, Dm, Dr, d, to_cplx(W2, (size_t)Dm * d * d * Dr));
+    build_pair(w1, Dl, Dm, Dr, d, to_cplx(W1, (size_t)Dl * d * d * Dm), to_cplx(W2, (size_t)Dm * d * d * Dr));
     BufPtr L_ = up(Lenv, (size_t)cl * Dl * cl, h->st), R_ = up(Renv, (size_t)cr * Dr * cr, h->st);
     const size_t n = (size_t)cl * d * d * cr;
     BufPtr x = up(theta, n, h->st), y = make_buf(n * sizeof(cplx));
@@ -2025,6 +2080,7 @@ int tdvp_bench_heff2(int chi, int Dl, int Dm, int Dr, const double* W1, const do
     MpoSite w1, w2;
     build_site(w1, Dl, Dm, d, to_cplx(W1, (size_t)Dl * d * d * Dm));
     build_site(w2, Dm, Dr, d, to_cplx(W2, (size_t)Dm * d * d * Dr));
+    build_pair(w1, Dl, Dm, Dr, d, to_cplx(W1, (size_t)Dl * d * d * Dm), to_cplx(W2, (size_t)Dm * d * d * Dr));
     const size_t nL = (size_t)chi * Dl * chi, nR = (size_t)chi * Dr * chi, n = (size_t)chi * d * d * chi;
     BufPtr L_ = make_buf(nL * sizeof(cplx)), R_ = make_buf(nR * sizeof(cplx)), x = make_buf(n * sizeof(cplx)),
            y = make_buf(n * sizeof(cplx));
