@@ -412,7 +412,7 @@ def main():
                      "share_of_step": jac_ms / bstep_ms if bstep_ms > 0 else None,
                      "svd_calls": n_svd, "svd_warm_started": n_warm,
                      "sweeps_per_svd": sweeps / n_svd if n_svd else None},
-        "heff2": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + 2 sparse MPO stages)", "bound": "tensor",
+        "heff2": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + one fused sparse W_j W_{j+1} channel pass)", "bound": "tensor",
                   "achieved": h2_tf, "peak": zpeak, "unit": "TFLOP/s",
                   "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,
                   "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
