@@ -1538,22 +1538,27 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     if (chi[0] != 1 || chi[L] != 1) throw TdvpError(TDVP_EARG, "MPS boundary bond dims must be 1");
     for (int j = 1; j < L; ++j)
       if (chi[j] < 1 || chi[j] > h->cbmax[j]) throw TdvpError(TDVP_EARG, "bond dim exceeds min(d^j, d^(L-j), chi_max)");
-    std::vector<std::vector<double>> psi(L), lam(L - 1);
+    // validate everything first (the handle keeps its state on error), then
+    // copy into the existing host vectors (their pages are reused: no
+    // allocation or page faults per call for the same shapes)
     for (int j = 0; j < L; ++j) {
       if (!Psi[j]) throw TdvpError(TDVP_EARG, "null Psi");
       const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
-      psi[j].assign(Psi[j], Psi[j] + n);
-      for (double v : psi[j])
-        if (!std::isfinite(v)) throw TdvpError(TDVP_ENONFINITE, "non-finite Psi entry");
+      const double* src = Psi[j];
+      bool fin = true;
+      for (size_t i = 0; i < n; ++i) fin &= std::isfinite(src[i]);
+      if (!fin) throw TdvpError(TDVP_ENONFINITE, "non-finite Psi entry");
     }
     for (int b = 0; b < L - 1; ++b) {
       if (!Lambda[b]) throw TdvpError(TDVP_EARG, "null Lambda");
-      lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
-      for (double v : lam[b])
-        if (!std::isfinite(v) || !(v > 0.0)) throw TdvpError(TDVP_ENONFINITE, "Lambda must be finite and > 0");
+      for (int i = 0; i < chi[b + 1]; ++i)
+        if (!std::isfinite(Lambda[b][i]) || !(Lambda[b][i] > 0.0))
+          throw TdvpError(TDVP_ENONFINITE, "Lambda must be finite and > 0");
     }
-    h->h_psi = std::move(psi);
-    h->h_lam = std::move(lam);
+    h->h_psi.resize(L);
+    h->h_lam.resize(L - 1);
+    for (int j = 0; j < L; ++j) h->h_psi[j].assign(Psi[j], Psi[j] + (size_t)chi[j] * d * chi[j + 1] * 2);
+    for (int b = 0; b < L - 1; ++b) h->h_lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
     h->h_chi.assign(chi, chi + L + 1);
     h->have_mps = true;
     h->envs_valid = false;
@@ -1788,6 +1793,21 @@ int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
   if (!h || !Psi) return TDVP_EARG;
   try {
     if (!h->have_mps) throw TdvpError(TDVP_ESTATE, "MPS not set");
+    if (h->layout_p != 0 && local_mode(h)) {
+      // device state authoritative: straight into the caller's buffers (no host staging copy)
+      const int L = h->L, d = h->d;
+      std::vector<int> chi(L + 1, 1);
+      for (int b = 0; b < L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];
+      for (int j = 0; j < L; ++j)
+        CK(cudaMemcpyAsync(Psi[j], h->segs[owner_of(h, j)].psi[j]->p, (size_t)chi[j] * d * chi[j + 1] * sizeof(cplx),
+                           cudaMemcpyDeviceToHost, h->st));
+      if (Lambda)
+        for (int b = 0; b < L - 1; ++b)
+          CK(cudaMemcpyAsync(Lambda[b], h->segs[owner_of(h, b)].lam[b]->p, (size_t)chi[b + 1] * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      return TDVP_OK;
+    }
     if (h->layout_p != 0) download_state(h);
     for (int j = 0; j < h->L; ++j) std::memcpy(Psi[j], h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double));
     if (Lambda)
