@@ -138,6 +138,24 @@ def test_svd_split_large_blocked_qr(B):
     assert rel(rec, rec_o) < 1e-9
 
 
+def test_svd_split_chi1024_shape(B):
+    """The chi = 1024 two-site shape (2048 x 2048, configs[4]): blocked QR
+    preconditioner + streaming Jacobi (BW = 8, register-tiled Gram/apply),
+    truncated to chi_max = 1024 with eps = 1e-12 (sampled checks: sigma,
+    discarded weight, orthonormality of the kept left factor)."""
+    rng = np.random.default_rng(23)
+    n, chi_max = 2048, 1024
+    M = rc(rng, n, n) * np.exp(-np.linspace(0, 20, n))[None, :]
+    S_ref = np.linalg.svd(M, compute_uv=False)
+    pl, S, pr, w = B.svd_split(M, chi_max, eps=1e-12)
+    k = len(S)
+    assert k == min(chi_max, int(np.count_nonzero(S_ref >= 1e-12 * S_ref[0])))
+    assert np.allclose(S, S_ref[:k], rtol=1e-10, atol=1e-13 * S_ref[0])
+    assert abs(w - np.sum(S_ref[k:] ** 2)) <= 1e-10 * np.sum(S_ref ** 2)
+    U = pl[:, :64] / S[None, :64]
+    assert np.abs(U.conj().T @ U - np.eye(64)).max() < 1e-11
+
+
 def test_svd_degenerate_and_rank_deficient(B):
     rng = np.random.default_rng(5)
     Q1, _ = np.linalg.qr(rc(rng, 20, 20))
