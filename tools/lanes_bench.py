@@ -19,6 +19,8 @@ for p in ps:
                  krylov_tol=float(os.environ.get("LB_KTOL", "0")))
     t.set_mpo(wl["mpo"])
     t.set_mps(wl["mps"].psi, wl["mps"].lam)
+    if os.environ.get("LB_BAL") and p > 1:
+        t.set_partition(pkg.balanced_partition(wl["L"], p, t.chi()))
     for _ in range(2):
         t.step(wl["dt"], p)
     ms = []
