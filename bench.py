@@ -347,14 +347,21 @@ def main():
         for _ in range(args.warmup):
             t.step(dt, q)
         torch.cuda.synchronize()
-        lms = []
+        lms, lfl = [], []
         for _ in range(args.steps):
             t.step(dt, q)
-            lms.append(t.stats()["step_ms"])
+            st_ = t.stats()
+            lms.append(st_["step_ms"])
+            lfl.append(st_["svd_jac_flop"])
         lv = float(np.mean(lms))
+        # all lanes' Jacobi work over the step time: how much of the FP64 ALU the
+        # concurrent SVDs use together (the per-launch roofline above is one SVD)
+        jagg = float(np.mean(lfl)) / (lv * 1e-3) / 1e12 if lv > 0 else None
         lanes = {"segments": q, "executor": "concurrent segment lanes on one GPU (thread + stream per segment)",
                  "partition": "uniform (PAPER.md:470)",
-                 "ms_per_step": lv, "speedup_vs_serial": ms_per_step / lv if lv > 0 else None}
+                 "ms_per_step": lv, "speedup_vs_serial": ms_per_step / lv if lv > 0 else None,
+                 "jacobi_aggregate_tflops": jagg,
+                 "jacobi_aggregate_frac_of_alu_peak": (jagg / FP64_ALU_PEAK_TF) if jagg else None}
         # the same with the chi-weighted partition (tdvp_partition_balanced)
         t.set_mps(wl["mps"].psi, wl["mps"].lam)
         bounds = pkg.balanced_partition(L, q, t.chi())
