@@ -180,3 +180,22 @@ def test_maybe_reorthonormalize(B):
     assert t.maybe_reorthonormalize(1e-3)
     assert abs(t.measure_norm() - 1.0) < 1e-12
     t.close()
+
+
+def test_set_partition_validation(B):
+    L = 16
+    t = handle(B, ti.mpo_xxz_nn(L, 0.5), ti.neel_mps(L), 8)
+    for bad in ([(0, 0), (1, 15)],                      # segment of one site
+                [(1, 7), (8, 15)],                      # does not start at 0
+                [(0, 3), (4, 9), (10, 15)],             # odd p
+                [(0, 7), (8, 8)] + [(9, 15)]):          # odd p, short segment
+        with pytest.raises(B.TdvpError) as e:
+            t.set_partition(bad)
+        assert e.value.code in (-1, -3)
+    t.set_partition([(0, 3), (4, 15)])
+    t.step(0.05, 2)   # uses the explicit partition
+    t.step(0.05, 4)   # p differs: the uniform rule
+    t.set_partition(None)
+    t.step(0.05, 2)
+    assert abs(t.measure_norm() - 1.0) < 1e-9
+    t.close()
