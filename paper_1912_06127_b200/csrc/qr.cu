@@ -508,17 +508,20 @@ __global__ void __launch_bounds__(NT, 1)
           if (r > k && r < m) {
             const cplx v = refl ? cmul(pc[t], scale) : pc[t];
             vr[t] = v;
-            col[r] = v;
-            __stcg(A + (long long)k * lda + r, v);
+            col[r] = v;  // the publisher warp copies it to global (off this warp's chain)
           } else {
             vr[t] = (r == k) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
           }
         }
         if (lane == (k & 31)) col[k] = cmk(beta, 0.0);
-        if (lane == 0) {
-          s_tau[i] = t_i;
-          __stcg(tau + k, t_i);
-        }
+        if (lane == 0) s_tau[i] = t_i;
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+      if (wid == NW - 1) {
+        // publisher warp: v_k and tau_k to global, then release them to the
+        // later CTAs (every QR_PUB-th reflector and the band's last)
+        for (int r = k + 1 + lane; r < m; r += 32) __stcg(A + (long long)k * lda + r, col[r]);
+        if (lane == 0) __stcg(tau + k, s_tau[i]);
         __syncwarp();
         if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl) {
           if (GRID) {
@@ -532,7 +535,6 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
-      asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
       const cplx ct = cconj(s_tau[i]);
       const bool upd = ct.x != 0.0 || ct.y != 0.0;
       if (wid == 0) {
@@ -566,9 +568,9 @@ __global__ void __launch_bounds__(NT, 1)
           for (int t = 0; t < RPL; ++t)
             if (lane + 32 * t == k) Aloc[(long long)(i + 1) * m + k] = pc[t];  // R[k][i+1] is final
         }
-      } else {
-        // workers: columns i+2, ... with reflector i (v from shared memory)
-        for (int jl = i + 1 + wid; jl < ncl; jl += NW - 1) {
+      } else if (wid < NW - 1) {
+        // workers (warps 1 .. NW-2): columns i+2, ... with reflector i (v from shared memory)
+        for (int jl = i + 1 + wid; jl < ncl; jl += NW - 2) {
           cplx* aj = Aloc + (long long)jl * m;
           if (!upd) continue;
           double dr = 0.0, di = 0.0;
