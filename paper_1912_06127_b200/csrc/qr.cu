@@ -377,7 +377,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 #ifndef QR_PUB
-#define QR_PUB 2
+#define QR_PUB 1
 #endif
 // GRID = false: one thread-block cluster, counters in each CTA's shared memory
 // raised by cluster-scope release stores.  GRID = true: a cooperative grid (up
