@@ -120,6 +120,24 @@ def test_svd_split_matches_oracle(B, m, n, chi_max):
     assert np.abs(U.conj().T @ U - np.eye(len(S))).max() < 1e-12
 
 
+@pytest.mark.parametrize("m,n,chi_max", [(600, 520, 300), (1024, 1024, 512), (512, 384, 384)])
+def test_svd_split_grid_qr_sizes(B, m, n, chi_max):
+    """256 < n <= 1024: the cooperative-grid look-ahead QR preconditioner and
+    the register-resident Jacobi variants for X <= 512 / 1024 rows."""
+    rng = np.random.default_rng(m + n)
+    M = rc(rng, m, n) * np.exp(-np.linspace(0, 25, n))[None, :]
+    S_ref = np.linalg.svd(M, compute_uv=False)
+    pl, S, pr, w = B.svd_split(M, chi_max, eps=1e-10)
+    k = len(S)
+    assert k == min(chi_max, int(np.count_nonzero(S_ref >= 1e-10 * S_ref[0])))
+    assert np.allclose(S, S_ref[:k], rtol=1e-10, atol=1e-13 * S_ref[0])
+    assert abs(w - np.sum(S_ref[k:] ** 2)) <= 1e-10 * np.sum(S_ref ** 2)
+    U = pl / S[None, :]
+    assert np.abs(U.conj().T @ U - np.eye(k)).max() < 1e-11
+    Wt = pr / S[:, None]
+    assert np.abs(Wt @ Wt.conj().T - np.eye(k)).max() < 1e-11
+
+
 def test_svd_split_large_blocked_qr(B):
     """mr in (1024, 2048]: blocked Householder QR preconditioner (panel width 4)
     and the streaming Jacobi; graded spectrum down to 1e-12."""
