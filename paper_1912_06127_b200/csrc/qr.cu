@@ -613,17 +613,20 @@ __global__ void __launch_bounds__(NT, 1)
       for (int r = k + 1 + lane; r < m; r += 32) {
         const cplx v = refl ? cmul(col[r], scale) : col[r];
         col[r] = v;
-        __stcg(A + (long long)k * lda + r, v);
       }
       if (lane == 0) {
         col[k] = cmk(beta, 0.0);
         s_tau[i] = t_i;
-        __stcg(tau + k, t_i);
       }
       __syncwarp();
-      // publish v_k to every later CTA (release orders the warp's writes
-      // above); inside the band only every QR_PUB-th reflector, the band's
-      // last one always
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
+    const cplx ct = cconj(s_tau[i]);
+    if (wid == NW - 1) {
+      // publisher warp: v_k and tau_k to global, then release them (off warp 0's chain)
+      for (int r = k + 1 + lane; r < m; r += 32) __stcg(A + (long long)k * lda + r, col[r]);
+      if (lane == 0) __stcg(tau + k, s_tau[i]);
+      __syncwarp();
       if (((i + 1) % QR_PUB) == 0 || i + 1 == ncl) {
         if (GRID) {
           if (lane == 0) {
@@ -635,14 +638,13 @@ __global__ void __launch_bounds__(NT, 1)
             st_release_cluster_rank(&s_npub, (unsigned)c, (unsigned)(k + 1));
         }
       }
+      continue;
     }
-    asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");
-    const cplx ct = cconj(s_tau[i]);
     if (wid == 0) xn2_next = 0.0;
     // warp 0: column i+1 (the next pivot, also its norm below row k+1);
-    // warps 1..: columns i+2, ...
+    // warps 1 .. NW-2: columns i+2, ...
     const int jstart = (wid == 0) ? i + 1 : i + 1 + wid;
-    const int jstep = (wid == 0) ? ncl : NW - 1;
+    const int jstep = (wid == 0) ? ncl : NW - 2;
     for (int jl = jstart; jl < ncl; jl += jstep) {
       cplx* aj = Aloc + (long long)jl * m;
       const bool upd = ct.x != 0.0 || ct.y != 0.0;
