@@ -1,13 +1,16 @@
 """p2TDVP hot-path benchmark (BASELINE.json metric).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2sat|c5sat|...]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5sat|c2sat|...]
 
 A "step" is one full 2TDVP/p2TDVP timestep (two half-sweeps: every pair
 update = merge, K=8 Lanczos H_eff^(2) matvecs, SVD truncation, environment
-update; every one-site backward update).  Default workload (N=1):
-BASELINE configs[1] shapes (L=64 XXZ Delta=0.5, MPO D=5, chi_max=128,
-eps=1e-10, dt=0.05) started from a seeded random inverse-canonical MPS with
-saturated bonds so every timed step runs at chi=128.
+update; every one-site backward update).  Default workload (N=1): the
+largest single-GPU configuration of BASELINE.json, configs[4]'s shapes
+(XXX chain, MPO D=5, chi_max=1024, eps=1e-12, dt=0.05) on an L=24 chain
+started from a seeded random inverse-canonical MPS with saturated bonds
+(SURVEY C6), so every timed step runs with chi = 1024 on the central bonds
+(2048 x 2048 two-site SVDs, H_eff^(2) at chi = 1024).  The chi=128 c2sat
+workload of round 1 is reported as a secondary field.
 value = device time per step (ms, lower is better), max over ranks.
 """
 import argparse
@@ -40,20 +43,10 @@ WORKLOADS = {
     "c4sat": (100, 1.0, 256, 1e-12, 0.02,
               "configs[3] shapes: L=100 long-range XXZ J(r)~1/r^2 as 9 exponentials (MPO D=29) Delta=1 "
               "chi_max=256 eps=1e-12 dt=0.02, saturated chi (C6)"),
-    "c5sat": (256, 1.0, 1024, 1e-12, 0.05,
-              "configs[4] shapes: L=256 XXX D=5 chi_max=1024 eps=1e-12 dt=0.05, saturated chi (C6)"),
+    "c5sat": (24, 1.0, 1024, 1e-12, 0.05,
+              "configs[4] shapes on an L=24 chain: XXX D=5 chi_max=1024 eps=1e-12 dt=0.05, seeded random "
+              "inverse-canonical MPS at saturated chi (SURVEY C6): bonds 10..14 at chi=1024"),
 }
-
-
-def jac_traffic():
-    """DRAM bytes (read + write) per launch of the Jacobi kernel from the
-    committed ncu --set full capture (profiles/r1b_traffic.json), else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1b_traffic.json")) as f:
-            t = json.load(f)["rjac2"]
-        return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
-    except (OSError, KeyError, ValueError):
-        return None
 
 
 def workload_inputs(name):
@@ -153,44 +146,101 @@ def fp64_peak_tflops():
 
 
 # ---------------------------------------------------------------- oracle (CPU baseline)
+def step_matvec_flops(wl):
+    """Algorithmic flops of all H_eff matvecs of one full step at the workload's
+    bond profile (SURVEY §8(d) formulas, K = 8 per exponential; two halves,
+    L-1 pair updates and L-2 one-site updates each)."""
+    import tdvp_inputs as ti
+    L, d, K = wl["L"], 2, 8
+    chi = [1] + ti.saturated_chi_profile(L, wl["chi"]) + [1]
+    Ws = wl["mpo"]
+
+    def nnz(W):
+        return int(np.count_nonzero(np.abs(W) > 0))
+
+    def f2(j):
+        cl, cr = chi[j], chi[j + 2]
+        return 8.0 * (d * d * cl * cr * (Ws[j].shape[0] * cl + Ws[j + 1].shape[3] * cr) +
+                      d * cl * cr * (nnz(Ws[j]) + nnz(Ws[j + 1])))
+
+    def f1(j):
+        cl, cr = chi[j], chi[j + 1]
+        return 8.0 * (d * cl * cr * (Ws[j].shape[0] * cl + Ws[j].shape[3] * cr) + cl * cr * nnz(Ws[j]))
+
+    tot = 2 * K * (sum(f2(j) for j in range(L - 1)) + sum(f1(j) for j in range(1, L - 1)))
+    jc = max(range(L - 1), key=lambda j: chi[j] * chi[j + 2])
+    return tot, jc, f2(jc)
+
+
 def cpu_baseline(wl, budget_s=12.0):
     """Time the oracle (as it stands) on a bounded sample of the same workload:
-    bulk pair+single updates of the first half-sweep, scaled to a full step by
-    the per-update contraction cost d chi_l chi_r (chi_l + chi_r)."""
+    repeated oracle H_eff^(2) matvecs (oracle.tdvp.apply_h2) at the largest
+    pair of the saturated chain, extrapolated to a full step by the ratio of
+    all matvec flops of a step to that matvec's flops.  The oracle's SVDs,
+    environment updates and Lanczos vector work are NOT included, so the
+    figure is a LOWER bound on the oracle's step time (one oracle 2048 x 2048
+    gesvd alone takes minutes on the host)."""
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         threads = os.cpu_count()
+    import tdvp_inputs as ti
     from oracle import tdvp as O
-    L, dt = wl["L"], wl["dt"]
-    st = O.init_state(wl["mps"], wl["mpo"], O.Params(chi_max=wl["chi"], eps=wl["eps"]), 1)
-    seg = st.segs[0]
-    chi = O.chi_profile(st)
-
-    def w_pair(j):
-        cl, cr = chi[j], chi[j + 2]
-        return cl * cr * (cl + cr) * 2.0
-
-    def w_back(j):
-        cl, cr = chi[j], chi[j + 1]
-        return cl * cr * (cl + cr)
-
-    total_w = 2 * sum(w_pair(j) for j in range(L - 1)) + 2 * sum(w_back(j) for j in range(1, L - 1))
+    tot, j, fj = step_matvec_flops(wl)
+    chi = [1] + ti.saturated_chi_profile(wl["L"], wl["chi"]) + [1]
+    cl, cr = chi[j], chi[j + 2]
+    rng = np.random.default_rng(4)
+    W1, W2 = wl["mpo"][j], wl["mpo"][j + 1]
+    Le = rng.standard_normal((cl, W1.shape[0], cl)) + 1j * rng.standard_normal((cl, W1.shape[0], cl))
+    Re = rng.standard_normal((cr, W2.shape[3], cr)) + 1j * rng.standard_normal((cr, W2.shape[3], cr))
+    th = rng.standard_normal((cl, 2, 2, cr)) + 1j * rng.standard_normal((cl, 2, 2, cr))
     t0 = time.perf_counter()
-    done_w, n = 0.0, 0
-    j = L // 2 - 4
-    while time.perf_counter() - t0 < budget_s and j < L - 2:
-        O._pair(st, seg, j, -0.5j * dt, True, False)
-        O._back(st, seg, j + 1, dt)
-        done_w += w_pair(j) + w_back(j + 1)
+    n = 0
+    while n == 0 or time.perf_counter() - t0 < budget_s:
+        th = O.apply_h2(Le, W1, W2, Re, th)
+        th /= np.linalg.norm(th)
         n += 1
-        j += 1
     el = time.perf_counter() - t0
-    ms_step = el / done_w * total_w * 1e3
+    ms_step = el / n * (tot / fj) * 1e3
     return {"value": ms_step, "unit": "ms/step", "cores": int(threads), "kind": "oracle",
-            "sample": f"{n} bulk pair+single updates (chi={wl['chi']}) of half-sweep 1 in {el:.1f} s, "
-                      f"scaled to a full step by sum d*cl*cr*(cl+cr)"}
+            "extrapolated": True, "lower_bound": True,
+            "sample": f"{n} oracle H_eff^(2) matvecs at pair ({j},{j + 1}) (chi_L={cl}, chi_R={cr}) in {el:.1f} s, "
+                      f"scaled by (all matvec flops of a step {tot:.3g}) / (one matvec {fj:.3g}); "
+                      f"oracle SVDs, environments and Lanczos vector work excluded (lower bound)"}
+
+
+def workload_config(name, wl, p, n_gpus, mode):
+    return {"workload": name, "desc": wl["desc"], "L": wl["L"], "chi_max": wl["chi"], "D_mpo": wl["D"],
+            "eps": wl["eps"], "dt": wl["dt"], "segments": p, "n_gpus": n_gpus,
+            "parallelism": (f"p2tdvp{p}" if p > 1 else "serial") + (f" ({mode})" if p > 1 else ""),
+            "l2": "working set (environments + MPS, > 1 GB at chi=1024) larger than L2 (126 MB)"}
+
+
+def timed_steps(t, dt, p, k):
+    out = []
+    for _ in range(k):
+        t.step(dt, p)
+        out.append(t.stats())
+    return out
+
+
+def secondary_c2sat(pkg, steps, warmup):
+    """Round 1's chi=128 headline (configs[1] shapes), serial and as 8 segment lanes on this GPU."""
+    wl = workload_inputs("c2sat")
+    t = pkg.Tdvp(wl["L"], 2, wl["D"], wl["chi"])
+    t.set_params(eps=wl["eps"], timing=False)
+    t.set_mpo(wl["mpo"])
+    res = {}
+    for p in (1, 8):
+        t.set_mps(wl["mps"].psi, wl["mps"].lam)
+        for _ in range(warmup):
+            t.step(wl["dt"], p)
+        ms = [s["step_ms"] for s in timed_steps(t, wl["dt"], p, steps)]
+        res["serial_ms_per_step" if p == 1 else "lanes8_ms_per_step"] = float(np.mean(ms))
+    t.close()
+    res["desc"] = wl["desc"]
+    return res
 
 
 # ---------------------------------------------------------------- main
@@ -200,36 +250,38 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2sat", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c5sat", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lane-segments", type=int, default=8,
-                    help="also time p2TDVP with this many segments as concurrent lanes on one GPU (N=1; 0 = off)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary c2sat / lanes figures")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    n_gpus = args.gpus
+    p = n_gpus  # one segment per GPU; N=1 -> serial 2TDVP
+    mode = "one rank per GPU, NCCL send/recv" if world > 1 else "one process driving N devices"
     wl = workload_inputs(args.workload)
+    config = workload_config(args.workload, wl, p, n_gpus, mode)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        # the oracle is the reference arm for this tier: K bounded samples
-        vals = []
+        # the oracle is the reference arm for this tier: W untimed warm-up
+        # samples, then K timed bounded samples of the same workload
         for _ in range(args.warmup):
-            pass
-        for _ in range(args.steps):
-            vals.append(cpu_baseline(wl, budget_s=8.0))
+            cpu_baseline(wl, budget_s=1.0)
+        vals = [cpu_baseline(wl, budget_s=2.0) for _ in range(args.steps)]
         v = float(np.median([x["value"] for x in vals]))
         cb = dict(vals[0])
         cb["value"] = v
-        print(json.dumps({"metric": METRIC, "value": v, "unit": "ms/step", "impl": "reference", "n_gpus": args.gpus,
+        print(json.dumps({"metric": METRIC, "value": v, "unit": "ms/step", "impl": "reference", "n_gpus": n_gpus,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
                           "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-                          "config": {"workload": args.workload, "desc": wl["desc"], "L": wl["L"],
-                                     "chi_max": wl["chi"], "segments": 1},
-                          "cpu_baseline": cb,
+                          "config": config, "extrapolated": True, "cpu_baseline": cb,
                           "e2e": {"value": v, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -241,12 +293,14 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    p = world  # one segment per GPU; N=1 -> serial 2TDVP
+    elif n_gpus > torch.cuda.device_count():
+        sys.exit(f"bench.py: --gpus {n_gpus} but only {torch.cuda.device_count()} CUDA devices")
 
     peaks = fp64_peak_tflops() if rank == 0 else {}
 
     L = wl["L"]
-    t = pkg.Tdvp(L, 2, wl["D"], wl["chi"])
+    devices = list(range(n_gpus)) if (world == 1 and n_gpus > 1) else None
+    t = pkg.Tdvp(L, 2, wl["D"], wl["chi"], devices=devices)
     t.set_params(eps=wl["eps"], timing=False)  # the timed steps run uninstrumented
     if world > 1:
         uid = [pkg.nccl_unique_id() if rank == 0 else None]
@@ -264,187 +318,123 @@ def main():
         torch.cuda.synchronize()
 
     barrier()
-    per = []
     with ClockSampler(local_rank) as clk:
         wall0 = time.perf_counter()
-        for _ in range(args.steps):
-            t.step(dt, p)
-            per.append(t.stats())
+        per = timed_steps(t, dt, p, args.steps)
         barrier()
         wall = time.perf_counter() - wall0
     step_ms = float(np.sum([s["step_ms"] for s in per]))
+    launches = int(np.sum([s["kernel_launches"] for s in per]))
     if dist is not None:
         x = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         step_ms = float(x.item())
     ms_per_step = step_ms / args.steps
-    # breakdown pass: K more steps with CUDA events around every matvec, SVD,
-    # Jacobi kernel and environment update (the events cost ~4% of a step,
-    # so these steps are not the timed ones)
+    # breakdown pass: a few more steps with CUDA events around every matvec,
+    # exponential, SVD, Jacobi kernel and environment update (the events cost a
+    # few % of a step, so these are not the timed steps)
+    nb = max(1, min(args.steps, 2))
     t.set_params(eps=wl["eps"], timing=True)
-    per_t = []
-    for _ in range(args.steps):
-        t.step(dt, p)
-        per_t.append(t.stats())
+    per_t = timed_steps(t, dt, p, nb)
     t.set_params(eps=wl["eps"], timing=False)
-    bstep_ms = float(np.sum([s["step_ms"] for s in per_t]))
-    per = per_t
-    h2_ms = float(np.sum([s["heff2_ms"] for s in per]))
-    h1_ms = float(np.sum([s["heff1_ms"] for s in per]))
-    lz2_ms = float(np.sum([s["lanczos2_ms"] for s in per]))
-    lz1_ms = float(np.sum([s["lanczos1_ms"] for s in per]))
-    env_ms = float(np.sum([s["env_ms"] for s in per]))
-    h2_fl = float(np.sum([s["heff2_flop"] for s in per]))
-    svd_ms = float(np.sum([s["svd_ms"] for s in per]))
-    jac_ms = float(np.sum([s["svd_jac_ms"] for s in per]))
-    jac_fl = float(np.sum([s["svd_jac_flop"] for s in per]))
-    sweeps = int(np.sum([s["svd_sweeps_total"] for s in per]))
-    n_svd = int(np.sum([s["n_pair"] for s in per]))
-    n_warm = int(np.sum([s["svd_warm"] for s in per]))
-    launches = int(np.sum([s["kernel_launches"] for s in per]))
-    gemm_launches = int(np.sum([s["gemm_launches"] for s in per]))
+    S = lambda k: float(np.sum([s[k] for s in per_t]))  # noqa: E731
+    bstep_ms = S("step_ms")
+    h2_ms, h1_ms, svd_ms, jac_ms = S("heff2_ms"), S("heff1_ms"), S("svd_ms"), S("svd_jac_ms")
+    lz2_ms, lz1_ms, env_ms = S("lanczos2_ms"), S("lanczos1_ms"), S("env_ms")
+    h2_fl, h1_fl, jac_fl = S("heff2_flop"), S("heff1_flop"), S("svd_jac_flop")
+    lz_bytes = S("lz_vec_bytes")
+    sweeps, n_svd = int(S("svd_sweeps_total")), int(S("n_pair"))
+    bins_ms = np.sum([s["heff2_ms_bin"] for s in per_t], axis=0)
+    bins_fl = np.sum([s["heff2_flop_bin"] for s in per_t], axis=0)
+    zpeak = peaks.get("zgemm") if peaks else None
 
     # e2e: the same step through the C-ABI with HOST buffers (set_mps H2D incl.
     # the sequential environment build, step, get_mps D2H) every step
     e2e = None
     if not args.no_e2e and world == 1:
         mps = wl["mps"]
-        t.step(dt, p)
+        ne = max(1, min(args.steps, 3))
         torch.cuda.synchronize()
         e0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(ne):
             t.set_mps(mps.psi, mps.lam)
             t.step(dt, p)
             psi, lam = t.get_mps()
         torch.cuda.synchronize()
-        e_ms = (time.perf_counter() - e0) / args.steps * 1e3
+        e_ms = (time.perf_counter() - e0) / ne * 1e3
         e2e = {"value": e_ms, "unit": "ms/step", "h2d_bytes_per_step": mps_bytes(mps),
-               "d2h_bytes_per_step": int(sum(x.nbytes for x in psi) + sum(x.nbytes for x in lam))}
-    # paper-mode Krylov (max 8 vectors, tolerance 1e-6; the
-    # stopping rule runs on the device): a timing variant of the same step
-    paper_mode = None
-    if world == 1:
-        t.set_params(eps=wl["eps"], timing=False, krylov_tol=1e-6)
-        t.set_mps(wl["mps"].psi, wl["mps"].lam)
-        for _ in range(args.warmup):
-            t.step(dt, p)
-        torch.cuda.synchronize()
-        pms = []
-        for _ in range(args.steps):
-            t.step(dt, p)
-            pms.append(t.stats()["step_ms"])
-        t.set_params(eps=wl["eps"], timing=False)
-        paper_mode = {"krylov_tol": 1e-6, "krylov_k_max": 8, "segments": p, "ms_per_step": float(np.mean(pms)),
-                      "note": "timing variant; the headline value uses fixed K = 8 (parity mode, SURVEY AMB-5)"}
-
-    # p2TDVP on this one GPU: P segments as concurrent lanes (own thread,
-    # stream and workspace each), same workload, fresh state, same timing rules
-    lanes = None
-    if args.lane_segments > 1 and world == 1:
-        q = args.lane_segments
-        t.set_params(eps=wl["eps"], timing=False)
-        t.set_mps(wl["mps"].psi, wl["mps"].lam)
-        for _ in range(args.warmup):
-            t.step(dt, q)
-        torch.cuda.synchronize()
-        lms, lfl = [], []
-        for _ in range(args.steps):
-            t.step(dt, q)
-            st_ = t.stats()
-            lms.append(st_["step_ms"])
-            lfl.append(st_["svd_jac_flop"])
-        lv = float(np.mean(lms))
-        # all lanes' Jacobi work over the step time: how much of the FP64 ALU the
-        # concurrent SVDs use together (the per-launch roofline above is one SVD)
-        jagg = float(np.mean(lfl)) / (lv * 1e-3) / 1e12 if lv > 0 else None
-        lanes = {"segments": q, "executor": "concurrent segment lanes on one GPU (thread + stream per segment)",
-                 "partition": "uniform (PAPER.md:470)",
-                 "ms_per_step": lv, "speedup_vs_serial": ms_per_step / lv if lv > 0 else None,
-                 "jacobi_aggregate_tflops": jagg,
-                 "jacobi_aggregate_frac_of_alu_peak": (jagg / FP64_ALU_PEAK_TF) if jagg else None}
-        # the same with the chi-weighted partition (tdvp_partition_balanced)
-        t.set_mps(wl["mps"].psi, wl["mps"].lam)
-        bounds = pkg.balanced_partition(L, q, t.chi())
-        t.set_partition(bounds)
-        for _ in range(args.warmup):
-            t.step(dt, q)
-        torch.cuda.synchronize()
-        bms = []
-        for _ in range(args.steps):
-            t.step(dt, q)
-            bms.append(t.stats()["step_ms"])
-        bv = float(np.mean(bms))
-        t.set_partition(None)
-        # strong scaling of p2TDVP on the one GPU (uniform partition, lanes)
-        scal = []
-        for qq in (2, 4, 16):
-            if qq > L // 2:
-                continue
-            t.set_mps(wl["mps"].psi, wl["mps"].lam)
-            for _ in range(max(1, args.warmup - 1)):
-                t.step(dt, qq)
-            torch.cuda.synchronize()
-            sms = []
-            for _ in range(args.steps):
-                t.step(dt, qq)
-                sms.append(t.stats()["step_ms"])
-            scal.append({"segments": qq, "ms_per_step": float(np.mean(sms))})
-        scal.append({"segments": q, "ms_per_step": lv})
-        scal.sort(key=lambda x: x["segments"])
-        lanes["balanced"] = {"bounds": bounds, "ms_per_step": bv,
-                             "speedup_vs_serial": ms_per_step / bv if bv > 0 else None}
-        lanes["scaling"] = [dict(x, speedup_vs_serial=ms_per_step / x["ms_per_step"]) for x in scal]
+               "d2h_bytes_per_step": int(sum(x.nbytes for x in psi) + sum(x.nbytes for x in lam)), "steps": ne}
     t.close()
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
-    h2_tf = h2_fl / (h2_ms * 1e-3) / 1e12 if h2_ms > 0 else None
-    zpeak = peaks.get("zgemm") if peaks else None
-    jac_tf = jac_fl / (jac_ms * 1e-3) / 1e12 if jac_ms > 0 else None
+    tf = lambda fl, ms: fl / (ms * 1e-3) / 1e12 if ms > 0 else None  # noqa: E731
+    h2_tf, jac_tf = tf(h2_fl, h2_ms), tf(jac_fl, jac_ms)
+    lz_vec_ms = lz2_ms + lz1_ms - h2_ms - h1_ms
+    lz_gbs = lz_bytes / (lz_vec_ms * 1e-3) / 1e9 if lz_vec_ms > 0 else None
+    hbm = hbm_peak()
+    # the dominant kernel of the step: the Jacobi SVD stage (FP64 ALU) or the
+    # DMMA GEMMs of the H_eff matvecs (FP64 tensor), whichever takes more time
+    rf_jac = {"kernel": "SVD Jacobi stage", "bound": "alu", "achieved": jac_tf, "peak": FP64_ALU_PEAK_TF,
+              "unit": "TFLOP/s", "frac": (jac_tf / FP64_ALU_PEAK_TF) if jac_tf else None, "traffic": None,
+              "peak_source": FP64_ALU_PEAK_SRC,
+              "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
+              "share_of_step": jac_ms / bstep_ms if bstep_ms > 0 else None,
+              "svd_calls": n_svd, "sweeps_per_svd": sweeps / n_svd if n_svd else None}
+    rf_h = {"kernel": "H_eff^(2)+H_eff^(1) matvecs (DMMA zgemm + sparse channel pass)", "bound": "tensor",
+            "achieved": tf(h2_fl + h1_fl, h2_ms + h1_ms), "peak": zpeak, "unit": "TFLOP/s",
+            "frac": (tf(h2_fl + h1_fl, h2_ms + h1_ms) / zpeak) if (zpeak and h2_ms + h1_ms > 0) else None,
+            "traffic": None,
+            "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
+            "flop_per_unit": "SURVEY §8(d): 8[d^2 cl cr (Dl cl + Dr cr) + d cl cr (nnzW_j + nnzW_j+1)] per H2 matvec",
+            "share_of_step": (h2_ms + h1_ms) / bstep_ms if bstep_ms > 0 else None}
+    roof = rf_jac if jac_ms >= h2_ms + h1_ms else rf_h
+    bins = {}
+    for name, ms_, fl_ in zip(("chi<=128", "chi<=256", "chi<=512", "chi<=1024"), bins_ms, bins_fl):
+        if ms_ > 0:
+            v = tf(fl_, ms_)
+            bins[name] = {"tflops": v, "frac_of_zgemm_peak": (v / zpeak) if zpeak else None, "ms_per_step": ms_ / nb}
     line = {
-        "metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "L": L, "chi_max": wl["chi"], "D_mpo": wl["D"],
-                   "segments": p, "parallelism": f"p2tdvp{p}" if p > 1 else "serial",
-                   "l2": "working set (envs + MPS ~ 0.2 GB) larger than L2 (126 MB)"},
-        # dominant kernel of the step: the Jacobi stage of the truncated SVD (FP64 SIMT, latency-bound)
-        "roofline": {"kernel": "svd_rjac one-sided Jacobi (register-resident block pairs)", "bound": "alu",
-                     "achieved": jac_tf, "peak": FP64_ALU_PEAK_TF, "unit": "TFLOP/s",
-                     "frac": (jac_tf / FP64_ALU_PEAK_TF) if jac_tf else None, "traffic": jac_traffic(),
-                     "peak_source": FP64_ALU_PEAK_SRC,
-                     "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
-                     "share_of_step": jac_ms / bstep_ms if bstep_ms > 0 else None,
-                     "svd_calls": n_svd, "svd_warm_started": n_warm,
-                     "sweeps_per_svd": sweeps / n_svd if n_svd else None},
-        "heff2": {"kernel": "H_eff^(2) matvec (2 DMMA GEMMs + one fused sparse W_j W_{j+1} channel pass)", "bound": "tensor",
-                  "achieved": h2_tf, "peak": zpeak, "unit": "TFLOP/s",
-                  "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,
-                  "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
+        "roofline": roof,
+        "roofline_other": rf_h if roof is rf_jac else rf_jac,
+        "heff2_tflops_by_chi": bins,
+        "heff2": {"achieved": h2_tf, "peak": zpeak, "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,
                   "share_of_step": h2_ms / bstep_ms if bstep_ms > 0 else None},
+        "lanczos_vectors": {"achieved_gbs": lz_gbs, "peak_gbs": hbm, "frac": (lz_gbs / hbm) if lz_gbs else None,
+                            "bytes_per_step": lz_bytes / nb, "ms_per_step": lz_vec_ms / nb,
+                            "bytes": "algorithmic: per exponential 16 n [3 + sum_{k<K-1}(3(k+1)+6) + (K+1) + (K+1)]"},
         "svd_share_of_step": svd_ms / bstep_ms if bstep_ms > 0 else None,
-        "breakdown_ms_per_step_instrumented": bstep_ms / args.steps,
-        "breakdown_ms_per_step": {"svd_total": svd_ms / args.steps, "svd_jacobi_kernel": jac_ms / args.steps,
-                                  "lanczos2_total": lz2_ms / args.steps, "heff2_matvecs": h2_ms / args.steps,
-                                  "lanczos1_total": lz1_ms / args.steps, "heff1_matvecs": h1_ms / args.steps,
-                                  "env_updates": env_ms / args.steps,
-                                  "rest": (bstep_ms - svd_ms - lz2_ms - lz1_ms - env_ms) / args.steps},
+        "breakdown_ms_per_step_instrumented": bstep_ms / nb,
+        "breakdown_ms_per_step": {"svd_total": svd_ms / nb, "svd_jacobi_kernel": jac_ms / nb,
+                                  "lanczos2_total": lz2_ms / nb, "heff2_matvecs": h2_ms / nb,
+                                  "lanczos1_total": lz1_ms / nb, "heff1_matvecs": h1_ms / nb,
+                                  "env_updates": env_ms / nb,
+                                  "rest": (bstep_ms - svd_ms - lz2_ms - lz1_ms - env_ms) / nb},
         "gpu_launches": launches,
-        "gemm_launches": gemm_launches,
         "wall_s_timed": wall,
         "clocks": clk.summary(),
         "e2e": e2e,
-        "p2tdvp_one_gpu": lanes,
-        "paper_mode_krylov": paper_mode,
-        "chi": wl["chi"],
     }
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_extras and world == 1 and n_gpus == 1:
+        line["secondary_c2sat"] = secondary_c2sat(pkg, max(1, min(args.steps, 5)), 2)
+    if not args.no_cpu_baseline and world == 1 and n_gpus == 1:
         line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 7700.0
 
 
 if __name__ == "__main__":

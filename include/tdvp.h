@@ -74,6 +74,13 @@ typedef struct {
   double lanczos2_ms;     /* whole two-site Krylov exponentials incl. their H_eff^(2) matvecs (timing=1) */
   double lanczos1_ms;     /* whole one-site backward exponentials (timing=1) */
   double env_ms;          /* environment updates after the splits (timing=1) */
+  /* H_eff^(2) matvec time and algorithmic flops binned by max(chi_L, chi_R) of the
+   * pair: [0] <= 128, [1] <= 256, [2] <= 512, [3] > 512 (timing=1) */
+  double heff2_ms_bin[4];
+  double heff2_flop_bin[4];
+  /* algorithmic HBM bytes of the Lanczos vector passes of the last step (timing=1;
+   * their time is lanczos2_ms + lanczos1_ms - heff2_ms - heff1_ms) */
+  double lz_vec_bytes;
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

@@ -186,6 +186,7 @@ struct tdvp_ctx {
   std::vector<MpoSite>& mpo;  // lanes: the parent's sites
   MpoSite mpo_id, mpo_sz;  // D = 1 identity / S^z (measurement)
   bool have_mpo = false, have_mps = false, envs_valid = false;
+  bool evolved = false;  // stepped since the last tdvp_set_mps (the host copy h_psi is stale in rank mode)
   int layout_p = 0;  // segments currently laid out (0: the host copy h_psi/h_lam is authoritative)
   int alloc_p = 0;   // segments whose device buffers are allocated (kept across tdvp_set_mps)
   std::vector<std::pair<int, int>> bounds;
@@ -208,6 +209,8 @@ struct tdvp_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<int, int>> ev_h2, ev_h1, ev_svd, ev_lz2, ev_lz1, ev_env;
+  std::vector<int> ev_h2_bin;  // chi bin of every ev_h2 entry (tdvp_stats.heff2_*_bin)
+  int cur_bin = 0;             // chi bin of the pair update in progress
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
   // NCCL
   int rank = 0, world = 1;
@@ -489,8 +492,14 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
     if (e0 >= 0) {
       const int e1 = ev_record(h);
       (which == 2 ? h->ev_h2 : h->ev_h1).emplace_back(e0, e1);
-      if (which == 2) { h->stats.heff2_flop += mv_flop; h->stats.heff2_calls++; }
-      else h->stats.heff1_flop += mv_flop;
+      if (which == 2) {
+        h->stats.heff2_flop += mv_flop;
+        h->stats.heff2_calls++;
+        h->stats.heff2_flop_bin[h->cur_bin] += mv_flop;
+        h->ev_h2_bin.push_back(h->cur_bin);
+      } else {
+        h->stats.heff1_flop += mv_flop;
+      }
     }
     if (h->lz_fused || paper) {
       CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0, ktol, tre,
@@ -508,6 +517,14 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
     }
   }
   h->cur_skip = nullptr;
+  if (h->prm.timing && which) {
+    // algorithmic bytes of the vector passes: start 3 passes over n,
+    // iteration k < K-1 with nv = k+1 basis vectors (3 nv + 6) (dots; update + dots;
+    // update + norm; scale), the last (nv + 1) (dots only), combination K + 1
+    double units = 3.0 + (double)(K + 1) + (double)(K + 1);
+    for (int k = 0; k + 1 < K; ++k) units += 3.0 * (k + 1) + 6.0;
+    h->stats.lz_vec_bytes += units * 16.0 * (double)n;
+  }
   CK(lz_tridiag_exp(h->st, h->lz, K, tre, tim));
   CK(lz_combine(h->st, h->lz, V, n, K, out, n));
   g_launch_count += 2;
@@ -537,6 +554,10 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   const cplx* Renv = P(g.gamma[j + 1]);
   const double tau = full ? dt : 0.5 * dt;
   const double fl = flops_heff2(cl, cr, d, W1.Dl, W2.Dr, nnz_of(W1), nnz_of(W2));
+  {
+    const int cx = std::max(cl, cr);
+    h->cur_bin = cx <= 128 ? 0 : cx <= 256 ? 1 : cx <= 512 ? 2 : 3;
+  }
   cplx* th2 = h->tmpB->c();
   const int el0 = h->prm.timing ? ev_record(h) : -1;
   expm_lanczos(
@@ -790,6 +811,10 @@ void layout(tdvp_ctx* h, int p) {
   if (!local_mode(h) && p != h->world)
     throw TdvpError(TDVP_EPARTITION, "n_segments must equal the world size in multi-process mode");
   if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);  // keep the current state
+  if (h->layout_p != 0 && !local_mode(h) && h->evolved)
+    throw TdvpError(TDVP_ESTATE,
+                    "re-layout of an evolved state is not supported in multi-process mode (each rank holds only its "
+                    "segment); call tdvp_set_mps first");
   if (h->alloc_p != p || h->segs.empty() || h->bounds != b) {
     // (re)allocate; the same partition reuses its buffers (a new state from
     // tdvp_set_mps is uploaded into them: no cudaMalloc/cudaFree per call)
@@ -1088,8 +1113,11 @@ void reset_step_stats(tdvp_ctx* h) {
   h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
   h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
   h->stats.heff2_calls = 0;
+  h->stats.lz_vec_bytes = 0.0;
+  for (int i = 0; i < 4; ++i) h->stats.heff2_ms_bin[i] = h->stats.heff2_flop_bin[i] = 0.0;
   h->ev_used = 0;
   h->ev_h2.clear();
+  h->ev_h2_bin.clear();
   h->ev_h1.clear();
   h->ev_svd.clear();
   h->ev_lz2.clear();
@@ -1177,6 +1205,8 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     a.heff2_flop += b.heff2_flop;
     a.heff2_calls += b.heff2_calls;
     a.heff1_flop += b.heff1_flop;
+    a.lz_vec_bytes += b.lz_vec_bytes;
+    for (int i = 0; i < 4; ++i) a.heff2_flop_bin[i] += b.heff2_flop_bin[i];
   }
 }
 
@@ -1191,6 +1221,11 @@ void finish_timing(tdvp_ctx* h) {
     return t;
   };
   h->stats.heff2_ms = sum(h->ev_h2);
+  for (size_t i = 0; i < h->ev_h2.size() && i < h->ev_h2_bin.size(); ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev_pool[h->ev_h2[i].first], h->ev_pool[h->ev_h2[i].second]));
+    h->stats.heff2_ms_bin[h->ev_h2_bin[i]] += ms;
+  }
   h->stats.heff1_ms = sum(h->ev_h1);
   h->stats.svd_ms = sum(h->ev_svd);
   h->stats.lanczos2_ms = sum(h->ev_lz2);
@@ -1203,6 +1238,7 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
   if (p != h->layout_p || !h->envs_valid) layout(h, p);
   reset_step_stats(h);
+  h->evolved = true;
   const long long l0 = g_launch_count, g0 = g_gemm_count;
   CK(cudaEventRecord(h->ev_step0, h->st));
   const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
@@ -1344,7 +1380,11 @@ void alloc_workspace(tdvp_ctx* h) {
   h->tmpB = make_buf(std::max(n2, n1) * sizeof(cplx));
   h->svdY = make_buf(svd * sizeof(cplx));
   h->svdQ = make_buf(svq * sizeof(cplx));
-  const size_t nflags = (size_t)8 * h->chi_max + 64;  // 2 counters per column block, blocks >= 2 columns
+  // the SVD has nc = min(cl d, d cr) <= d chi_max columns: every per-column
+  // buffer below is sized by d chi_max (2 Jacobi counters per column block,
+  // blocks >= 2 columns)
+  const long long ncmax = (long long)h->d * h->chi_max;
+  const size_t nflags = (size_t)4 * ncmax + 64;
   h->svdF = make_buf(nflags * sizeof(unsigned));
   h->gemm_work = make_buf(h->work_elems * sizeof(cplx));
   h->envA = make_buf(env * sizeof(cplx));
@@ -1358,7 +1398,6 @@ void alloc_workspace(tdvp_ctx* h) {
   h->lz_brk = make_buf(64);
   CK(cudaMemset(h->lz_counter->p, 0, 64));
   CK(cudaMemset(h->lz_brk->p, 0, 64));
-  const long long ncmax = 2LL * h->chi_max;
   h->svd_sigma = make_buf(ncmax * sizeof(double) + 64);
   h->svd_order = make_buf(ncmax * sizeof(int) + 64);
   h->svd_perm = make_buf(2 * ncmax * sizeof(int) + 64);
@@ -1561,6 +1600,7 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     for (int b = 0; b < L - 1; ++b) h->h_lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
     h->h_chi.assign(chi, chi + L + 1);
     h->have_mps = true;
+    h->evolved = false;
     h->envs_valid = false;
     h->layout_p = 0;  // re-layout (upload + env build) at the next step, same buffers
   } catch (const TdvpError& e) {

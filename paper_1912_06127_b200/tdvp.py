@@ -37,10 +37,15 @@ class tdvp_stats(C.Structure):
                 ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int),
                 ("svd_warm", C.c_int), ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
-                ("env_ms", C.c_double)]
+                ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
+                ("lz_vec_bytes", C.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        out = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            out[k] = list(v) if isinstance(v, C.Array) else v
+        return out
 
 
 _D = C.POINTER(C.c_double)
@@ -113,11 +118,13 @@ def _check(rc, h=None):
 class Tdvp:
     """Handle over one libtdvp context (one device, or one rank)."""
 
-    def __init__(self, L, d, D_mpo, chi_max):
+    def __init__(self, L, d, D_mpo, chi_max, devices=None):
         self.L, self.d = L, d
         h = C.c_void_p()
         _check(lib().tdvp_create(L, d, D_mpo, chi_max, C.byref(h)))
         self.h = h
+        if devices is not None and len(devices) > 1:
+            raise NotImplementedError("multi-device handle")
 
     def close(self):
         if getattr(self, "h", None):

@@ -1,15 +1,23 @@
 """GPU-vs-oracle parity on BASELINE.json's configs at their full sizes, in
 the launch configuration bench.py uses (one handle, the config's segment
 count), same seeded inputs and partition.  Observables after every few steps:
-1e-9 absolute while no truncation is active, 1e-6 once it is.  The chi
-profile must match except for isolated eps-threshold flips (|dchi| = 1 at a
-bond where a singular value sits within rounding of eps*sigma_1), which are
-counted and bounded."""
+1e-9 absolute while no truncation is active, 1e-6 once it is (north_star).
+
+Bond spectra (gauge invariant) are compared value by value over the common
+prefix.  Where the two chi differ, every value kept by one side only must be
+an eps-threshold or multiplet-guard flip (readings R-F, R-9b): it
+lies within the cut's uncertainty band of eps*sigma_1, or continues the
+multiplet at the last common value.  The band is derived from the measured
+GPU-oracle difference of the common spectrum at that bond (4x its max, floor
+1e-13 sigma_1 = the SVDs' own rounding at n <= 2048), not from the observable
+tolerance.  Flip counts are returned and bounded per config."""
 import numpy as np
 import pytest
 
 import tdvp_inputs as ti
 from oracle import tdvp as O
+
+from _parity import check_spectra
 
 pytestmark = pytest.mark.gpu
 
@@ -30,7 +38,7 @@ def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
     t.set_mpo(W)
     t.set_mps(mps.psi, mps.lam)
     st = O.init_state(mps, W, O.Params(chi_max=chi_max, eps=eps), p)
-    flips, trunc, worst = 0, False, 0.0
+    flips, trunc, worst, max_dchi = 0, False, 0.0, 0
     for n in range(steps):
         t.step(dt, p)
         O.step(st, dt)
@@ -44,24 +52,16 @@ def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
         err = max(np.abs(sz - m["sz"]).max(), abs(E - m["energy"]), abs(nrm - m["norm"]))
         worst = max(worst, err)
         assert err < tol, (n + 1, err, tol)
-        # bond spectra (gauge invariant): the common prefix agrees; values kept
-        # by only one side are eps-threshold flips or sit at the parity level
         _, glam = t.get_mps()
         _, olam = O.global_mps(st)
         for a, b in zip(glam, olam):
-            k = min(len(a), len(b))
-            assert np.abs(a[:k] - b[:k]).max() <= tol * b[0], (len(a), len(b))
-            extra = np.concatenate([a[k:], b[k:]])
-            # a chi difference is an eps-threshold flip (reading R-F):
-            # every value kept by one side only is at most max(10 eps, tol)
-            # sigma_1, i.e. at the cut or at the parity tolerance of the state
-            # (GPU and oracle states differ at ~1e-11 after a few steps, which
-            # moves values of that size across the cut)
-            assert extra.size == 0 or extra.max() <= max(10 * eps, tol) * b[0], (extra.max() / b[0], tol)
+            dchi = check_spectra(a, b, eps, tol)
+            max_dchi = max(max_dchi, dchi)
         flips += sum(1 for x, y in zip(chi, ochi) if x != y)
     s = t.stats()
     t.close()
-    return dict(flips=flips, trunc=trunc, worst=worst, stats=s, chi=ochi)
+    print(f"parity: worst {worst:.3g} flips {flips} max|dchi| {max_dchi} trunc {trunc}")
+    return dict(flips=flips, trunc=trunc, worst=worst, stats=s, chi=ochi, max_dchi=max_dchi)
 
 
 def test_config2_serial_full(B):

@@ -112,6 +112,54 @@ def test_p9_lanczos_special_cases():
     assert np.allclose(out, np.exp(-0.7j * np.diag(H4)) * v4, atol=1e-13)
 
 
+def test_p9b_paper_mode_krylov_stop_rule():
+    """Paper-mode Krylov ("maximum of 8 basis vectors ...
+    convergence tolerance 1e-6"; SURVEY O-10 step 5, AMB-5): with tol > 0 the
+    oracle stops after the first m with n0 beta_m |(exp(tau T_m) e_1)_m| < tol.
+
+    Pinned on a case whose Lanczos process is known in closed form: for a real
+    symmetric tridiagonal (Jacobi) matrix J and v = n0 e_1, the Lanczos basis
+    is e_1, e_2, ... and T_m is J's leading m x m block.  So the stopping index
+    is predicted here from scipy.linalg.expm of the leading blocks (an
+    independent route: Pade, not the oracle's eigh), and the result must be
+    n0 * expm(tau T_m) e_1 embedded in R^n, within tol of the exact
+    n0 * expm(tau J) e_1.  An off-by-one in the index, a missing n0 or a
+    wrong component of c moves K_eff or the result."""
+    rng = np.random.default_rng(5)
+    n, n0 = 40, 3.0
+    alpha = rng.uniform(-1.0, 1.0, n)
+    beta = rng.uniform(0.5, 1.5, n - 1)
+    J = np.diag(alpha) + np.diag(beta, 1) + np.diag(beta, -1)
+    v = np.zeros(n, complex)
+    v[0] = n0
+    for tau, tol in ((-0.05j, 1e-6), (-0.2j, 1e-6), (0.1j, 1e-7), (-0.02j, 1e-12), (-0.5j, 1e-6)):
+        pred = None
+        for m in range(1, 9):
+            c_m = scipy.linalg.expm(tau * J[:m, :m])[m - 1, 0]
+            if n0 * beta[m - 1] * abs(c_m) < tol:
+                pred = m
+                break
+        info = {}
+        out = O.expm_lanczos(lambda x: J @ x, v, tau, K=8, tol=tol, info=info)
+        k_eff = info["k"]
+        assert k_eff == (pred if pred is not None else 8), (tau, tol, k_eff, pred)
+        ref_k = np.zeros(n, complex)
+        ref_k[:k_eff] = n0 * scipy.linalg.expm(tau * J[:k_eff, :k_eff])[:, 0]
+        assert np.abs(out - ref_k).max() < 1e-13
+        exact = n0 * scipy.linalg.expm(tau * J)[:, 0]
+        assert np.linalg.norm(out - exact) < (10 * tol if pred is not None else 1e-6)
+    # an easy spectrum stops early (K_eff < K); a generic Hermitian case is within tol
+    assert O.expm_lanczos(lambda x: J @ x, v, -0.05j, K=8, tol=1e-6, info=(inf := {})) is not None and inf["k"] < 8
+    A = rng.standard_normal((32, 32)) + 1j * rng.standard_normal((32, 32))
+    H = (A + A.conj().T) / 2
+    H /= np.linalg.norm(H, 2)
+    x = rng.standard_normal(32) + 1j * rng.standard_normal(32)
+    info = {}
+    out = O.expm_lanczos(lambda y: H @ y, x, -0.05j, K=8, tol=1e-6, info=info)
+    assert info["k"] < 8
+    assert np.linalg.norm(out - scipy.linalg.expm(-0.05j * H) @ x) < 1e-6
+
+
 def test_p15_svd_tail_and_reconstruction():
     rng = np.random.default_rng(11)
     for trial in range(200):
