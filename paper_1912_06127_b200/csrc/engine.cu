@@ -199,7 +199,7 @@ struct tdvp_ctx {
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
   BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, svdF, gemm_work, partials;
   BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
-  BufPtr svd_sigma, svd_order, svd_perm, svd_off, svd_ires, svd_dres, red_res, envA, envB;
+  BufPtr svd_sigma, svd_order, svd_perm, svd_bj, svd_off, svd_ires, svd_dres, red_res, envA, envB;
   double* h_pin = nullptr;
   int* h_ipin = nullptr;
   LanczosDev lz{};
@@ -599,9 +599,10 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
     wst.store = g.wbasis[j]->c();
     wst.store_ok = &store_ok;
   }
+  double jac_flop = 0.0;
   cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
                                       g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps,
-                                      h->prm.timing ? &jac_ms : nullptr, warm ? &wst : nullptr);
+                                      h->prm.timing ? &jac_ms : nullptr, warm ? &wst : nullptr, &jac_flop);
   if (warm) {
     g.wside[j] = store_ok ? (dir > 0 ? 'L' : 'R') : 0;
     g.wdim[j] = n2;
@@ -622,7 +623,9 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   {
     const double mr = std::max(cl * d, d * cr), nc = std::min(cl * d, d * cr);
     h->stats.svd_jac_ms += jac_ms;
-    h->stats.svd_jac_flop += (double)sweeps * nc * (nc - 1) / 2 * (16.0 * mr + 24.0 * (mr + nc));
+    // block-Jacobi (DMMA) path: the flops it executed; SIMT paths: the scalar count per sweep
+    h->stats.svd_jac_flop += jac_flop > 0.0 ? jac_flop
+                                            : (double)sweeps * nc * (nc - 1) / 2 * (16.0 * mr + 24.0 * (mr + nc));
   }
   if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
   // a5: environments for the next update
@@ -1401,6 +1404,7 @@ void alloc_workspace(tdvp_ctx* h) {
   h->svd_sigma = make_buf(ncmax * sizeof(double) + 64);
   h->svd_order = make_buf(ncmax * sizeof(int) + 64);
   h->svd_perm = make_buf(2 * ncmax * sizeof(int) + 64);
+  h->svd_bj = make_buf(svd_bjac_work_elems(g_num_sms) * sizeof(cplx));
   h->svd_off = make_buf(64);
   h->svd_ires = make_buf(64);
   h->svd_dres = make_buf(64);
@@ -1411,7 +1415,8 @@ void alloc_workspace(tdvp_ctx* h) {
                      reinterpret_cast<unsigned*>(h->lz_counter->p), h->lz_brk->i()};
   h->sv = SvdDev{h->svdY->c(), 0, h->svd_sigma->d(), h->svd_order->i(), h->svd_off->d(), h->svd_ires->i(),
                  h->svd_dres->d(), h->h_pin, h->h_ipin, {nullptr, nullptr}, h->svdQ->c(), (size_t)svq,
-                 reinterpret_cast<unsigned*>(h->svdF->p), nflags, 0, h->svd_perm->i()};
+                 reinterpret_cast<unsigned*>(h->svdF->p), nflags, 0, h->svd_perm->i(), h->svd_bj->c(),
+                 svd_bjac_work_elems(g_num_sms)};
 }
 
 int fail(tdvp_ctx* h, const TdvpError& e) {

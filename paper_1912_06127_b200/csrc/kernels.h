@@ -100,6 +100,8 @@ struct SvdDev {
   size_t flags_elems;
   int throughput;         // 1: several SVDs run concurrently (segment lanes): prefer fewer CTAs per SVD
   int* perm;              // [2 nc]: column presort permutation and its inverse (QR path), nullptr = off
+  cplx* bjwork;           // block-Jacobi partial Gram matrices (svd_bjac_work_elems), nullptr = off
+  size_t bjwork_elems;
 };
 size_t svd_qr_work_elems(int m, int n);
 struct TruncParams {
@@ -120,10 +122,14 @@ struct SvdWarm {
 // Full SVD by blocked one-sided Jacobi, then truncation (SURVEY O-7) and the split
 // Psi_L = U S, Lambda = S, V = 1/S, Psi_R = S W^dagger.  theta is m x n row-major.
 // Returns chi via *chi_out (host), discarded weight via *w_out (host).
+// *jac_flop_out (optional): algorithmic flops of the Jacobi stage as executed
+// (block-Jacobi DMMA path; 0 for the SIMT paths, whose count the caller derives
+// from the sweeps)
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out = nullptr, const SvdWarm* warm = nullptr);
+                               float* jac_ms_out = nullptr, const SvdWarm* warm = nullptr,
+                               double* jac_flop_out = nullptr);
 size_t svd_work_elems(int m, int n);
 // ------------------------------------------------------------------ qr.cu
 // Blocked Householder QR workspace (column-major A, m x n, m >= n).
@@ -135,8 +141,10 @@ struct QrWork {
   cplx* W1;        // [max(n, nc) * kb]
   cplx* W2;
   int kb;          // panel width = qr_kb_for(m)
+  cplx* gw;        // split-K workspace of the V^H C products (nullptr: no split)
+  size_t gw_elems;
 };
-int qr_kb_for(int m);  // 32 / 16 / 8 / 4 for m <= 256 / 512 / 1024 / 2048, 0 = unsupported
+int qr_kb_for(int m);  // panel width 32 (one CTA for <= 256 rows, a cluster beyond), 0 = unsupported
 cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, int m, int n);
 // C (column-major m x nc, ld ldc) <- Q C with Q from qr_factor (m x n reflectors)
 cudaError_t qr_apply_q(cudaStream_t st, const QrWork& w, int m, int n, cplx* C, long long ldc, int nc);
@@ -159,6 +167,19 @@ cudaError_t qr_apply_refl(cudaStream_t st, const cplx* A, long long lda, const c
 cudaError_t qr_apply_refl2(cudaStream_t st, const cplx* A0, long long lda0, const cplx* tau0, int m0, int n0, cplx* C0,
                            long long ldc0, int nc0, const cplx* A1, long long lda1, const cplx* tau1, int m1, int n1,
                            cplx* C1, long long ldc1, int nc1);
+
+// svd_bjac.cu: block one-sided Jacobi on the DMMA pipe (blocks of 16 columns,
+// pairs spread over S CTAs by rows, one cooperative launch).  X rows [0, xr),
+// V rows [vofs, vofs + nc) of d.Y.  *flop_dev += executed DMMA flops.
+size_t svd_bjac_work_elems(int sms);
+cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int nc, long long ldy, double tol,
+                         int* sweeps_dev, double* flop_dev);
+
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device,
+// once per (device, kernel), thread-safe (lanes and handles on several devices).
+cudaError_t set_smem_attr(const void* fn, int bytes);
+// Allow non-portable cluster sizes (up to 16 CTAs) for a kernel, once per device.
+cudaError_t set_cluster_nonportable(const void* fn);
 
 // svd_rjac.cu: register-resident Jacobi stage on d.Y = [X ; V]; returns
 // cudaErrorNotSupported for shapes it does not cover (svd.cu falls back).

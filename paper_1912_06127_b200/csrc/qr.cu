@@ -138,6 +138,161 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_kernel(cplx* A, long long lda,
   }
 }
 
+// Panel [k0, k0+kb) of column-major A (rows k0..m-1, kb <= 32) factored by ONE
+// thread-block cluster of C CTAs: CTA c holds rows [c*rc, (c+1)*rc) of the
+// panel in its shared memory.  Per reflector i two cluster barriers: (1) the
+// partial norms of column i below the pivot (and the pivot alpha from its
+// owner) are summed by every CTA in rank order through DSMEM -> identical
+// zlarfg (beta, tau, 1/(alpha-beta)) everywhere; (2) the partial dots
+// w_j = v_i^H a_j (j > i) and z_j = v_j^H v_i (j < i, for T) are summed the
+// same way, then every CTA updates its rows of a_j -= conj(tau) v_i w_j.
+// Output as qr_panel_kernel (R / reflector tails in A, explicit rows Vc, tau, T).
+constexpr int QPW = 32;   // max panel width
+constexpr int QPNT = 256;
+__global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long lda, int m, int k0, int kb, int rc,
+                                                               cplx* tau, cplx* Vc, long long ldv, cplx* T) {
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cluster = cgx::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int crank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char qr_sm[];
+  cplx* P = reinterpret_cast<cplx*>(qr_sm);  // [kb][rc] column j at P + j*rc
+  __shared__ double s_nrm[2];                 // partial |x|^2 below the pivot; [1] unused
+  __shared__ cplx s_alpha;                    // pivot value (owner CTA)
+  __shared__ cplx s_w[QPW];                   // partial dots of this CTA
+  __shared__ cplx s_wt[QPW];                  // summed dots
+  __shared__ cplx s_z[QPW][QPW + 1];          // (CTA 0) z[j][i] = v_j^H v_i
+  __shared__ cplx s_tau[QPW];
+  __shared__ cplx s_T[QPW][QPW + 1];
+  __shared__ double s_red[8];
+  __shared__ cplx s_scale;
+  __shared__ int s_refl;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rows = m - k0;
+  const int r0 = crank * rc;                       // first panel row of this CTA
+  const int nr = max(0, min(rc, rows - r0));       // rows held
+  for (int e = tid; e < kb * rc; e += QPNT) {
+    const int j = e / rc, r = e - j * rc;
+    P[j * rc + r] = (r < nr) ? A[(long long)(k0 + j) * lda + k0 + r0 + r] : cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int i = 0; i < kb; ++i) {
+    const int pr = i;  // pivot row within the panel
+    cplx* vi = P + i * rc;
+    // ---- (1) partial norm of column i below the pivot
+    {
+      double x = 0.0;
+      for (int r = tid; r < nr; r += QPNT)
+        if (r0 + r > pr) x += cabs2(vi[r]);
+      x = warp_sum(x);
+      if (lane == 0) s_red[wid] = x;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < QPNT / 32; ++w) t += s_red[w];
+        s_nrm[0] = t;
+        if (pr >= r0 && pr < r0 + nr) s_alpha = vi[pr - r0];
+      }
+    }
+    cluster.sync();
+    if (tid == 0) {
+      double xn2 = 0.0;
+      for (int c = 0; c < C; ++c) xn2 += *cluster.map_shared_rank(&s_nrm[0], c);
+      const int owner = pr / rc;
+      const cplx al = *cluster.map_shared_rank(&s_alpha, owner);
+      const double ar = al.x, ai = al.y;
+      cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
+      double beta = ar;
+      const bool refl = !(xn2 == 0.0 && ai == 0.0);
+      if (refl) {
+        beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        t_i = cmk((beta - ar) / beta, -ai / beta);
+        const double dr = ar - beta, di = ai;
+        const double den = dr * dr + di * di;
+        scale = cmk(dr / den, -di / den);  // 1 / (alpha - beta)
+      }
+      s_tau[i] = t_i;
+      s_scale = scale;
+      s_refl = refl;
+      if (pr >= r0 && pr < r0 + nr) vi[pr - r0] = cmk(beta, 0.0);  // R_pp; v_p = 1 implicitly
+    }
+    __syncthreads();
+    if (s_refl) {
+      const cplx sc = s_scale;
+      for (int r = tid; r < nr; r += QPNT)
+        if (r0 + r > pr) vi[r] = cmul(vi[r], sc);
+    }
+    __syncthreads();
+    // ---- (2) partial dots: w_j = v_i^H a_j (j > i), z_j = v_j^H v_i (j < i)
+    for (int j = wid; j < kb; j += QPNT / 32) {
+      if (j == i) continue;
+      const cplx* aj = P + j * rc;
+      double dr = 0.0, di = 0.0;
+      for (int r = lane; r < nr; r += 32) {
+        const int g = r0 + r;
+        if (g < pr) continue;
+        const cplx v = (g == pr) ? cmk(1.0, 0.0) : vi[r];
+        const cplx x = (j > i) ? cdotc(v, aj[r]) : cdotc((g == j) ? cmk(1.0, 0.0) : aj[r], v);
+        dr += x.x;
+        di += x.y;
+      }
+      dr = warp_sum(dr);
+      di = warp_sum(di);
+      if (lane == 0) s_w[j] = cmk(dr, di);
+    }
+    __syncthreads();
+    cluster.sync();
+    if (tid < kb && tid != i) {
+      cplx t = cmk(0.0, 0.0);
+      for (int c = 0; c < C; ++c) t = cadd(t, *cluster.map_shared_rank(&s_w[tid], c));
+      s_wt[tid] = t;
+      if (crank == 0 && tid < i) s_z[tid][i] = t;
+    }
+    __syncthreads();
+    const cplx ct = cconj(s_tau[i]);
+    for (int j = wid; j < kb; j += QPNT / 32) {
+      if (j <= i) continue;
+      cplx* aj = P + j * rc;
+      const cplx f = cmul(ct, s_wt[j]);
+      for (int r = lane; r < nr; r += 32) {
+        const int g = r0 + r;
+        if (g < pr) continue;
+        const cplx v = (g == pr) ? cmk(1.0, 0.0) : vi[r];
+        aj[r] = csub(aj[r], cmul(v, f));
+      }
+    }
+    __syncthreads();
+  }
+  // ---- T (zlarft forward/columnwise) on CTA 0
+  if (crank == 0 && tid == 0) {
+    for (int i = 0; i < kb; ++i) {
+      s_T[i][i] = s_tau[i];
+      for (int r = 0; r < i; ++r) {
+        cplx acc = cmk(0.0, 0.0);
+        for (int c = r; c < i; ++c) acc = cadd(acc, cmul(s_T[r][c], s_z[c][i]));
+        s_T[r][i] = cmul(cmk(-s_tau[i].x, -s_tau[i].y), acc);
+      }
+      for (int r = i + 1; r < kb; ++r) s_T[r][i] = cmk(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+  if (crank == 0) {
+    for (int e = tid; e < QPW * QPW; e += QPNT)
+      T[e] = (e / QPW < kb && e % QPW < kb) ? s_T[e / QPW][e % QPW] : cmk(0.0, 0.0);
+    for (int e = tid; e < kb; e += QPNT) tau[k0 + e] = s_tau[e];
+  }
+  for (int e = tid; e < kb * rc; e += QPNT) {
+    const int j = e / rc, r = e - j * rc;
+    if (r >= nr) continue;
+    const int g = r0 + r;
+    const cplx a = P[j * rc + r];
+    A[(long long)(k0 + j) * lda + k0 + g] = a;
+    const cplx v = (g < j) ? cmk(0.0, 0.0) : (g == j) ? cmk(1.0, 0.0) : a;
+    Vc[(long long)(k0 + j) * ldv + k0 + g] = v;
+  }
+  cluster.sync();  // shared memory stays alive until every CTA finished its DSMEM reads
+}
+
 // R^H (n x n, lower) from the upper triangle of column-major QR output A (ld lda)
 // into column-major X (ld ldx); rows [n, rows_total) of X zeroed.
 __global__ void qr_rh_kernel(const cplx* __restrict__ A, long long lda, int n, cplx* X, long long ldx, int rows_total) {
@@ -154,7 +309,7 @@ __global__ void qr_rh_kernel(const cplx* __restrict__ A, long long lda, int n, c
 }  // namespace
 
 // panel width by the row count (the panel lives in registers)
-int qr_kb_for(int m) { return m <= 256 ? 32 : m <= 512 ? 16 : m <= 1024 ? 8 : m <= 2048 ? 4 : 0; }
+int qr_kb_for(int m) { return m <= 4096 ? 32 : 0; }
 
 cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, int m, int n) {
   const int KBm = qr_kb_for(m);
@@ -164,33 +319,46 @@ cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, 
     const int kb = std::min(KBm, n - k0);
     const int rows = m - k0;
     cplx* T = w.T + (long long)p * KBm * KBm;
-    const size_t smem = (size_t)rows * kb * sizeof(cplx);
-    static bool attr = false;
-    if (!attr) {  // panels need <= 128 KB (rows * kb * 16 B)
-      cudaError_t ea;
-      if ((ea = cudaFuncSetAttribute(qr_panel_kernel<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     128 * 1024)) != cudaSuccess ||
-          (ea = cudaFuncSetAttribute(qr_panel_kernel<16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     128 * 1024)) != cudaSuccess ||
-          (ea = cudaFuncSetAttribute(qr_panel_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     128 * 1024)) != cudaSuccess ||
-          (ea = cudaFuncSetAttribute(qr_panel_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     128 * 1024)) != cudaSuccess)
-        return ea;
-      attr = true;
+    cudaError_t e;
+    if (rows <= 256) {
+      const size_t smem = (size_t)rows * kb * sizeof(cplx);
+      if ((e = set_smem_attr(reinterpret_cast<const void*>(qr_panel_kernel<32, 256>), 128 * 1024)) != cudaSuccess)
+        return e;
+      qr_panel_kernel<32, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
+    } else {
+      // cluster panel: C CTAs of rc rows each (rc * kb * 16 B of shared memory)
+      const int C = rows <= 512 ? 4 : rows <= 1024 ? 8 : 16;
+      const int rc = (rows + C - 1) / C;
+      const size_t smem = (size_t)rc * kb * sizeof(cplx);
+      if ((e = set_smem_attr(reinterpret_cast<const void*>(qr_panel_cl_kernel), (int)std::max<size_t>(smem, 48 * 1024))) !=
+          cudaSuccess)
+        return e;
+      if ((e = set_cluster_nonportable(reinterpret_cast<const void*>(qr_panel_cl_kernel))) != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(QPNT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if ((e = cudaLaunchKernelEx(&cfg, qr_panel_cl_kernel, A, lda, m, k0, kb, rc, w.tau, w.Vc, w.ldv, T)) !=
+          cudaSuccess)
+        return e;
     }
-    if (KBm == 32) qr_panel_kernel<32, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
-    else if (KBm == 16) qr_panel_kernel<16, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
-    else if (KBm == 8) qr_panel_kernel<8, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
-    else qr_panel_kernel<4, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
     const int nt = n - k0 - kb;
     if (nt <= 0) continue;
     // trailing A_t = A[k0:m, k0+kb:n]; row-major view Ar_t (nt x rows, ld lda)
     cplx* Art = A + (long long)(k0 + kb) * lda + k0;
     const cplx* Vp = w.Vc + (long long)k0 * w.ldv + k0;  // kb x rows, ld ldv
-    cudaError_t e;
-    // Wt = Ar_t Vc^H                     (nt x kb)
-    if ((e = zgemm(st, OP_N, OP_C, nt, kb, rows, one, Art, lda, Vp, w.ldv, zero, w.W1, kb)) != cudaSuccess) return e;
+    // Wt = Ar_t Vc^H                     (nt x kb; K = rows: split-K into w.gw)
+    if ((e = zgemm(st, OP_N, OP_C, nt, kb, rows, one, Art, lda, Vp, w.ldv, zero, w.W1, kb, 1, 0, 0, 0, w.gw,
+                   w.gw_elems)) != cudaSuccess)
+      return e;
     // Wt2 = Wt conj(T)                   (= (T^H W)^T)
     if ((e = zgemm(st, OP_N, OP_R, nt, kb, kb, one, w.W1, kb, T, KBm, zero, w.W2, kb)) != cudaSuccess) return e;
     // Ar_t -= Wt2 Vc
@@ -210,7 +378,9 @@ cudaError_t qr_apply_q(cudaStream_t st, const QrWork& w, int m, int n, cplx* C, 
     cplx* Crt = C + k0;  // row-major view of column-major C: nc x rows, ld ldc
     cudaError_t e;
     // Wt = Cr_t Vc^H ; Wt2 = Wt T^T (= (T W)^T) ; Cr_t -= Wt2 Vc
-    if ((e = zgemm(st, OP_N, OP_C, nc, kb, rows, one, Crt, ldc, Vp, w.ldv, zero, w.W1, kb)) != cudaSuccess) return e;
+    if ((e = zgemm(st, OP_N, OP_C, nc, kb, rows, one, Crt, ldc, Vp, w.ldv, zero, w.W1, kb, 1, 0, 0, 0, w.gw,
+                   w.gw_elems)) != cudaSuccess)
+      return e;
     if ((e = zgemm(st, OP_N, OP_T, nc, kb, kb, one, w.W1, kb, T, KBm, zero, w.W2, kb)) != cudaSuccess) return e;
     if ((e = zgemm(st, OP_N, OP_N, nc, rows, kb, mone, w.W2, kb, Vp, w.ldv, one, Crt, ldc)) != cudaSuccess) return e;
   }

@@ -853,7 +853,8 @@ __global__ void svd_write_kernel(const cplx* __restrict__ Y, long long ldy, cons
 size_t svd_qr_work_elems(int m, int n) {
   const long long mr = std::max(m, n), nc = std::min(m, n);
   // Q1 (mr x nc) + Vc1 (nc x mr) + Q2, Vc2 (nc x nc) + T1, T2 + tau1, tau2 + W1, W2 (nc x 32)
-  return (size_t)(2 * mr * nc + 2 * nc * nc + 2 * 32 * (nc + 32) + 2 * nc + 2 * 32 * nc + 64);
+  // + split-K partials of the V^H C products (16 x nc x 32)
+  return (size_t)(2 * mr * nc + 2 * nc * nc + 2 * 32 * (nc + 32) + 2 * nc + 2 * 32 * nc + 16 * 32 * nc + 64);
 }
 
 size_t svd_work_elems(int m, int n) {
@@ -875,7 +876,7 @@ __global__ void svd_store_kernel(const cplx* __restrict__ Y, long long ldy, cons
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out, const SvdWarm* warm) {
+                               float* jac_ms_out, const SvdWarm* warm, double* jac_flop_out) {
   // warm start only for square matrices (orientation forced by the caller)
   if (warm != nullptr && m != n) warm = nullptr;
   const bool transposed = warm ? warm->orient == 1 : m < n;
@@ -932,6 +933,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     w2.tau = p; p += nc;
     w1.W1 = w2.W1 = p; p += 32LL * nc;
     w1.W2 = w2.W2 = p; p += 32LL * nc;
+    w1.gw = w2.gw = p; w1.gw_elems = w2.gw_elems = (size_t)16 * 32 * nc; p += 16LL * 32 * nc;
     if (presort) {
       // X P with P sorting the columns by decreasing norm; V = P (Q2 V3) at the write
       svd_colnorm_kernel<<<(nc + 7) / 8, 256, 0, st>>>(d.Y, ldy, mr, nc, d.sigma, d.ires + 2);
@@ -986,7 +988,20 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   int sweeps = 0;
   const bool tj = jac_ms_out != nullptr && d.ev_jac[0] != nullptr;
   if (tj && (e = cudaEventRecord(d.ev_jac[0], st)) != cudaSuccess) return e;
-  if (nc >= 2 && (e = svd_rjac_run(st, d, x_rows, mr, nc, ldy, tol, d.ires + 4)) != cudaErrorNotSupported) {
+  static int bj_min = -1;
+  if (bj_min < 0) {
+    const char* ev = std::getenv("TDVP_SVD_BJ_MIN");
+    bj_min = ev ? std::atoi(ev) : 384;
+  }
+  if ((e = cudaMemsetAsync(d.dres + 2, 0, sizeof(double), st)) != cudaSuccess) return e;
+  bool bj = false;
+  if (nc >= bj_min && (e = svd_bjac_run(st, d, x_rows, mr, nc, ldy, tol, d.ires + 4, d.dres + 2)) !=
+                          cudaErrorNotSupported) {
+    // block Jacobi on the DMMA pipe (svd_bjac.cu)
+    if (e != cudaSuccess) return e;
+    sweeps = -1;
+    bj = true;
+  } else if (nc >= 2 && (e = svd_rjac_run(st, d, x_rows, mr, nc, ldy, tol, d.ires + 4)) != cudaErrorNotSupported) {
     // register-resident Jacobi (svd_rjac.cu)
     if (e != cudaSuccess) return e;
     sweeps = -1;
@@ -1065,7 +1080,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   svd_colnorm_kernel<<<(nc + 7) / 8, 256, 0, st>>>(d.Y, ldy, mr, nc, d.sigma, d.ires + 2);
   svd_truncate_kernel<<<1, 1024, (2 * nc + 1) * sizeof(double), st>>>(d.sigma, nc, d.order, tp, d.ires, d.dres);
   if ((e = cudaMemcpyAsync(d.h_ibuf, d.ires, 8 * sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyAsync(d.h_buf + 1, d.dres, 2 * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(d.h_buf + 1, d.dres, 3 * sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   if (d.h_ibuf[2] != 0 || !std::isfinite(d.h_buf[1]) || !(d.h_buf[2] > 0.0)) return cudaErrorUnknown;
   const int chi = d.h_ibuf[0];
@@ -1105,5 +1120,6 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   *r_out = d.h_ibuf[3];
   *chi_eps_out = d.h_ibuf[1];
   *sweeps_out = sweeps;
+  if (jac_flop_out) *jac_flop_out = bj ? d.h_buf[3] : 0.0;
   return cudaGetLastError();
 }

@@ -1,0 +1,594 @@
+// Block one-sided (Hestenes) Jacobi on the FP64 tensor pipe (DMMA) for the
+// truncated SVD of the two-site matrix (Fig. 6; SURVEY §8(a) a4,
+// K2 "block rotations on DMMA").
+//
+// Operates on d.Y = [X ; V] (column-major, ld = ldy): X = rows [0, xr) (after
+// the QR preconditioner X = R2^H, xr = nc), V = rows [vofs, vofs + nc).  The
+// columns are cut into blocks of BB = 16; a sweep is a round-robin tournament
+// over the blocks (nbe - 1 rounds of nbe / 2 disjoint block pairs).  For one
+// block pair (PC = 32 columns) a round
+//   1. forms the PC x PC Gram matrix G = X_p^H X_p on the DMMA pipe (the
+//      upper-triangular 8 x 8 tiles; one complex MAC = 4 real DMMA.8x8x4),
+//      split over the S CTAs of the pair by rows (deterministic reduction:
+//      warps in a fixed tree, CTAs in index order through global memory);
+//   2. measures the pair's largest scaled coupling c = |g_ij| / sqrt(g_ii g_jj)
+//      (the one-sided convergence test, relative, so tiny columns count);
+//   3. if c > tol / 4: diagonalises G by cyclic two-sided Jacobi rotations in
+//      shared memory (each of the 256 threads updates one 2 x 2 block of G per
+//      round), accumulating the unitary Q (every S CTA of the pair does this
+//      redundantly on the identical G, so no broadcast is needed), and
+//   4. applies [X_p ; V_p] <- [X_p ; V_p] Q on the DMMA pipe over its rows.
+// The inner solve only has to produce a unitary Q that orthogonalises the
+// pair well; the result's accuracy is set by the outer test, computed from
+// the actual columns every round (one-sided Jacobi's relative accuracy).
+// Rounds are ordered by point-to-point flags per (block, row slice) -- a pair
+// starts as soon as its two blocks finished the previous round on its rows --
+// and sweeps by a grid barrier; the sweep loop stops with the rule
+// of svd_rjac.cu (c <= tol, or c^2 <= 0.01 tol: the next sweep would rotate
+// nothing).  All sweeps run in ONE cooperative launch.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+__device__ unsigned long long g_bj_prof[8];  // CTA 0 cycles per phase (TDVP_SVD_PROF)
+
+namespace {
+
+constexpr int BB = 16;        // columns per block
+constexpr int PC = 2 * BB;    // columns per block pair
+constexpr int NTB = 256;      // threads per CTA (8 warps)
+constexpr int GP = PC + 1;    // padded row length of the shared PC x PC matrices
+constexpr int NUT = 10;       // upper-triangular 8 x 8 tiles of a 32 x 32 Gram matrix
+
+struct BjArgs {
+  cplx* Y;
+  long long ldy;
+  int xr, vofs, nc, nb, nbe;
+  int S, P;  // CTAs per pair, pairs per round
+  double tol;
+  int max_sweeps;
+  cplx* part;      // [2][P][S][PC * PC] partial Gram matrices (double-buffered by round parity)
+  unsigned* pcnt;  // [P] monotonic pair counters
+  unsigned* gbar;  // [1] monotonic grid-barrier counter (end of every sweep)
+  unsigned* done;  // [nbe][S] rounds completed on row slice s of block b (monotonic)
+  double* offb;    // [3] per-sweep max scaled coupling
+  int* sweeps_out;
+  double* flop_out;  // algorithmic DMMA flops executed (Gram + apply)
+  int prof;
+  int inner_max;  // inner Jacobi sweeps per block pair and round (at most)
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void rr_pair(int n, int round, int i, int& a, int& b) {
+  // circle method on n (even) players: player n-1 fixed
+  const int m = n - 1;
+  if (i == 0) {
+    a = n - 1;
+    b = round % m;
+  } else {
+    a = (round + i) % m;
+    b = (round - i + m) % m;
+  }
+  if (a > b) { const int t = a; a = b; b = t; }
+}
+
+// upper-triangular tile index t -> (ti, tj), ti <= tj, of the 4 x 4 tile grid
+__device__ __forceinline__ void ut_tile(int t, int& ti, int& tj) {
+  constexpr int TI[NUT] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3};
+  constexpr int TJ[NUT] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
+  ti = TI[t];
+  tj = TJ[t];
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct Smem {
+  cplx red[4][PC * GP];  // warp-tree reduction of the Gram tiles
+  cplx G[PC][GP];
+  cplx Q[PC][GP];
+  double cs[PC / 2];
+  cplx sn[PC / 2];
+  int rp[PC / 2], rq[PC / 2];
+  int col[PC];       // global column of pair column i (-1: absent)
+  double offw[8];
+  int any;
+};
+
+__global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int pair = blockIdx.x / a.S, s = blockIdx.x - pair * a.S;
+  const unsigned G_ = gridDim.x;
+  cplx* __restrict__ Y = a.Y;
+  const long long ldy = a.ldy;
+  const double tol = a.tol, tol4 = 0.25 * tol;
+  // this CTA's row ranges (multiples of 8) of X and of V
+  auto split = [&](int n, int& r0, int& r1) {
+    const int chunks = (n + 7) / 8;
+    const int c0 = (int)((long long)chunks * s / a.S), c1 = (int)((long long)chunks * (s + 1) / a.S);
+    r0 = c0 * 8;
+    r1 = min(n, c1 * 8);
+  };
+  int xr0, xr1, vr0, vr1;
+  split(a.xr, xr0, xr1);
+  split(a.nc, vr0, vr1);
+  unsigned long long round_g = 0;  // rounds completed (all sweeps), for the monotonic counters
+  const bool prof = a.prof && blockIdx.x == 0 && tid == 0;
+  unsigned long long pt = clock64();
+  auto mark = [&](int i) {
+    if (prof) {
+      const unsigned long long t = clock64();
+      g_bj_prof[i] += t - pt;
+      pt = t;
+    }
+  };
+  double flops = 0.0;
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    double* off_cur = a.offb + (sweep % 3);
+    if (blockIdx.x == 0 && tid == 0) a.offb[(sweep + 1) % 3] = 0.0;
+    for (int round = 0; round < a.nbe - 1; ++round, ++round_g) {
+      int bI, bJ;
+      rr_pair(a.nbe, round, pair, bI, bJ);
+      // point-to-point dependencies instead of a grid barrier: slice s of
+      // blocks I and J must have finished the previous round (their slice s
+      // rows are only ever read and written by the slice-s CTA of their pair)
+      if (tid == 0) {
+        const unsigned need = (unsigned)round_g;
+        for (const int blk : {bI, bJ}) {
+          const unsigned* f = a.done + (long long)blk * a.S + s;
+          while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if ((int)(v - need) >= 0) break;
+            __nanosleep(20);
+          }
+        }
+      }
+      if (tid < PC) {
+        const int blk = tid < BB ? bI : bJ;
+        const int c = blk * BB + (tid & (BB - 1));
+        sm.col[tid] = (blk < a.nb && c < a.nc) ? c : -1;
+      }
+      __syncthreads();
+      // ---- 1. partial Gram over rows [xr0, xr1) of X: warp w takes 4-row steps w, w+8, ...
+      // 3M products: conj(a) b = (P1 + P2) + i (P3 - P1 + P2) with P1 = ar br,
+      // P2 = ai bi, P3 = (ar - ai)(br + bi): three real DMMAs per complex MAC
+      double g1[NUT][2], g2[NUT][2], g3[NUT][2];
+#pragma unroll
+      for (int t = 0; t < NUT; ++t) g1[t][0] = g1[t][1] = g2[t][0] = g2[t][1] = g3[t][0] = g3[t][1] = 0.0;
+      {
+        int cc[4];
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) cc[cb] = sm.col[cb * 8 + (lane >> 2)];
+        const int nsteps = (xr1 - xr0 + 3) / 4;
+        constexpr int U = 2;  // steps in flight per warp
+        for (int st0 = wid; st0 < nsteps; st0 += 8 * U) {
+          cplx x[U][4];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int r = xr0 + (st0 + 8 * u) * 4 + (lane & 3);
+            const bool rv = (st0 + 8 * u) < nsteps && r < xr1;
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+              x[u][cb] = (rv && cc[cb] >= 0) ? __ldcg(Y + (long long)cc[cb] * ldy + r) : cmk(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            double xs[4], xd[4];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {
+              xs[cb] = x[u][cb].x + x[u][cb].y;
+              xd[cb] = x[u][cb].x - x[u][cb].y;
+            }
+#pragma unroll
+            for (int t = 0; t < NUT; ++t) {
+              int ti, tj;
+              ut_tile(t, ti, tj);
+              // G[i][j] += conj(x_ki) x_kj : A from x[ti] (row-major 8x4), B from x[tj] (col-major 4x8)
+              dmma(g1[t][0], g1[t][1], x[u][ti].x, x[u][tj].x);
+              dmma(g2[t][0], g2[t][1], x[u][ti].y, x[u][tj].y);
+              dmma(g3[t][0], g3[t][1], xd[ti], xs[tj]);
+            }
+          }
+        }
+      }
+      double gR[NUT][2], gI[NUT][2];
+#pragma unroll
+      for (int t = 0; t < NUT; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          gR[t][h] = g1[t][h] + g2[t][h];
+          gI[t][h] = g3[t][h] - g1[t][h] + g2[t][h];
+        }
+      mark(0);
+      // warp tree (fixed order): 4-7 -> 0-3, 2-3 -> 0-1, 1 -> 0
+      auto tile_store = [&](cplx* dst) {
+#pragma unroll
+        for (int t = 0; t < NUT; ++t) {
+          int ti, tj;
+          ut_tile(t, ti, tj);
+          const int r = ti * 8 + (lane >> 2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) dst[r * GP + tj * 8 + 2 * (lane & 3) + h] = cmk(gR[t][h], gI[t][h]);
+        }
+      };
+      auto tile_add = [&](const cplx* src) {
+#pragma unroll
+        for (int t = 0; t < NUT; ++t) {
+          int ti, tj;
+          ut_tile(t, ti, tj);
+          const int r = ti * 8 + (lane >> 2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const cplx v = src[r * GP + tj * 8 + 2 * (lane & 3) + h];
+            gR[t][h] += v.x;
+            gI[t][h] += v.y;
+          }
+        }
+      };
+      if (wid >= 4) tile_store(sm.red[wid - 4]);
+      __syncthreads();
+      if (wid < 4) tile_add(sm.red[wid]);
+      __syncthreads();
+      if (wid == 2 || wid == 3) tile_store(sm.red[wid - 2]);
+      __syncthreads();
+      if (wid < 2) tile_add(sm.red[wid]);
+      __syncthreads();
+      if (wid == 1) tile_store(sm.red[0]);
+      __syncthreads();
+      if (wid == 0) {
+        tile_add(sm.red[0]);
+        // this CTA's partial -> global slot (upper tiles only)
+        cplx* dst = a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + s) * (PC * PC);
+#pragma unroll
+        for (int t = 0; t < NUT; ++t) {
+          int ti, tj;
+          ut_tile(t, ti, tj);
+          const int r = ti * 8 + (lane >> 2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) __stcg(dst + r * PC + tj * 8 + 2 * (lane & 3) + h, cmk(gR[t][h], gI[t][h]));
+        }
+      }
+      // pair barrier: all S partials of this pair written
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(a.pcnt + pair, 1u);
+        const unsigned target = (unsigned)((round_g + 1) * (unsigned long long)a.S);
+        while (true) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.pcnt + pair) : "memory");
+          if ((int)(v - target) >= 0) break;
+          __nanosleep(20);
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      // ---- sum the S partials in index order -> G (Hermitian, both triangles)
+      for (int e = tid; e < PC * PC; e += NTB) {
+        const int i = e / PC, j = e - i * PC;
+        if (i <= j) {
+          cplx v = cmk(0.0, 0.0);
+          for (int q = 0; q < a.S; ++q)
+            v = cadd(v, __ldcg(a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + q) * (PC * PC) + e));
+          if (i == j) v.y = 0.0;
+          sm.G[i][j] = v;
+          sm.G[j][i] = cconj(v);
+        }
+      }
+      __syncthreads();
+      // ---- 2. largest scaled coupling of the pair (one-sided convergence test)
+      {
+        double m = 0.0;
+        for (int e = tid; e < PC * PC; e += NTB) {
+          const int i = e / PC, j = e - i * PC;
+          if (i < j) {
+            const double gi = sm.G[i][i].x, gj = sm.G[j][j].x;
+            if (gi > 0.0 && gj > 0.0) m = fmax(m, cabs2(sm.G[i][j]) / (gi * gj));
+          }
+        }
+        m = warp_max(m);
+        if (lane == 0) sm.offw[wid] = m;
+      }
+      __syncthreads();
+      double c2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) c2 = fmax(c2, sm.offw[w]);
+      const double cpair = sqrt(c2);
+      mark(1);
+      if (s == 0 && tid == 0) {
+        atomic_max_nonneg(off_cur, cpair);
+        flops += 8.0 * (double)a.xr * PC * PC * (double)NUT / 16.0;
+      }
+      if (cpair > tol4) {
+        // ---- 3. two-sided cyclic Jacobi on G (shared memory), Q accumulated
+        for (int e = tid; e < PC * PC; e += NTB) {
+          const int i = e / PC, j = e - i * PC;
+          sm.Q[i][j] = cmk(i == j ? 1.0 : 0.0, 0.0);
+        }
+        const double tol2q = tol4 * tol4;
+        // absolute noise floor of the updated G entries: the first inner sweep
+        // works on the freshly computed G (accurate relative to the column
+        // norms), later sweeps on G after rotations, whose entries carry
+        // rounding ~ u max_i g_ii; below that floor a rotation only chases noise
+        double gmax = 0.0;
+        for (int i = 0; i < PC; ++i) gmax = fmax(gmax, sm.G[i][i].x);
+        const double floor2 = (64.0 * DBL_EPSILON * gmax) * (64.0 * DBL_EPSILON * gmax);
+        // Round of 16 disjoint rotations: threads 0..15 compute the rotation
+        // parameters (rsqrt only) into shared memory; then every thread
+        // updates one 2 x 2 block of the upper triangle of G (row pair ra <=
+        // column pair rb; the lower triangle is its mirror) and the Q entries
+        // of rows 2 ra, 2 ra + 1 in column pair rb.
+        const int ra = tid >> 4, rb = tid & 15;
+        for (int isw = 0; isw < a.inner_max; ++isw) {
+          if (tid == 0) sm.any = 0;
+          if (tid < 8) sm.offw[tid] = 0.0;
+          __syncthreads();
+          double smax = 0.0;
+          for (int rd = 0; rd < PC - 1; ++rd) {
+            if (tid < PC / 2) {
+              int p, q;
+              rr_pair(PC, rd, tid, p, q);
+              double cs = 1.0;
+              cplx sn = cmk(0.0, 0.0);
+              const double ga = sm.G[p][p].x, gc = sm.G[q][q].x;
+              const cplx g = sm.G[p][q];
+              const double ag2 = cabs2(g);
+              const double gg = ga * gc;
+              if (ga > 0.0 && gc > 0.0 && ag2 > 1e-300) {
+                smax = fmax(smax, ag2 / gg);
+                if (ag2 > tol2q * gg && (isw == 0 || ag2 > floor2)) {
+                  // zero g = x_p^H x_q by x_p' = cs x_p - conj(sn) x_q, x_q' = sn x_p + cs x_q:
+                  // cos^2 = (1 + |w| / D) / 2, sn = sgn(w) g / (D cs), D = sqrt(w^2 + 4 |g|^2)
+                  const double w = gc - ga;
+                  const double rD = rsqrt(fma(w, w, 4.0 * ag2));
+                  const double qq = 0.5 * fma(fabs(w), rD, 1.0);
+                  const double rcs = rsqrt(qq);
+                  cs = qq * rcs;
+                  const double f = copysign(rD * rcs, w);
+                  sn = cmk(f * g.x, f * g.y);
+                  sm.any = 1;
+                }
+              }
+              sm.rp[tid] = p;
+              sm.rq[tid] = q;
+              sm.cs[tid] = cs;
+              sm.sn[tid] = sn;
+            }
+            __syncthreads();
+            {
+              const int p1 = sm.rp[ra], q1 = sm.rq[ra], p2 = sm.rp[rb], q2 = sm.rq[rb];
+              const double ca = sm.cs[ra], cb = sm.cs[rb];
+              const cplx sa = sm.sn[ra], sb = sm.sn[rb];
+              if (ra <= rb) {
+                const cplx b00 = sm.G[p1][p2], b01 = sm.G[p1][q2], b10 = sm.G[q1][p2], b11 = sm.G[q1][q2];
+                // B <- J_a^H B J_b ; rows: p' = ca p - sa q, q' = conj(sa) p + ca q
+                const cplx r00 = csub(cscale(b00, ca), cmul(sa, b10));
+                const cplx r01 = csub(cscale(b01, ca), cmul(sa, b11));
+                const cplx r10 = cadd(cmul(cconj(sa), b00), cscale(b10, ca));
+                const cplx r11 = cadd(cmul(cconj(sa), b01), cscale(b11, ca));
+                // columns: p' = cb p - conj(sb) q ; q' = sb p + cb q
+                cplx n00 = csub(cscale(r00, cb), cmul(cconj(sb), r01));
+                cplx n01 = cadd(cmul(sb, r00), cscale(r01, cb));
+                cplx n10 = csub(cscale(r10, cb), cmul(cconj(sb), r11));
+                cplx n11 = cadd(cmul(sb, r10), cscale(r11, cb));
+                if (ra == rb) {
+                  if (sa.x != 0.0 || sa.y != 0.0) n01 = n10 = cmk(0.0, 0.0);
+                  n00.y = n11.y = 0.0;
+                  n10 = cconj(n01);
+                }
+                sm.G[p1][p2] = n00;
+                sm.G[p1][q2] = n01;
+                sm.G[q1][p2] = n10;
+                sm.G[q1][q2] = n11;
+                if (ra != rb) {  // mirror: G[b][a] = G[a][b]^H
+                  sm.G[p2][p1] = cconj(n00);
+                  sm.G[q2][p1] = cconj(n01);
+                  sm.G[p2][q1] = cconj(n10);
+                  sm.G[q2][q1] = cconj(n11);
+                }
+              }
+              // Q <- Q J_b on rows 2 ra, 2 ra + 1
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int row = 2 * ra + h;
+                const cplx qp = sm.Q[row][p2], qq = sm.Q[row][q2];
+                sm.Q[row][p2] = csub(cscale(qp, cb), cmul(cconj(sb), qq));
+                sm.Q[row][q2] = cadd(cmul(sb, qp), cscale(qq, cb));
+              }
+            }
+            __syncthreads();
+          }
+          // stop after a sweep without rotations, or when the largest coupling
+          // of the sweep was so small that the next sweep's are below tol / 4
+          if (tid < PC / 2) atomic_max_nonneg(&sm.offw[0], smax);
+          __syncthreads();
+          const double sw = sm.offw[0];
+          const int any = sm.any;
+          __syncthreads();
+          if (prof) g_bj_prof[6]++;
+          if (!any || sw * sw <= 0.01 * tol2q) break;
+        }
+        if (prof) g_bj_prof[7]++;
+        mark(2);
+        // ---- 4. [X_p ; V_p] <- [X_p ; V_p] Q on the DMMA pipe, this CTA's rows
+        if (s == 0 && tid == 0) flops += 8.0 * (double)(a.xr + a.nc) * PC * PC;
+        // 3M products: a q = (P1 - P2) + i (P3 - P1 - P2) with P1 = ar qr,
+        // P2 = ai qi, P3 = (ar + ai)(qr + qi)
+        double bqr[8][4], bqi[8][4], bqs[8][4];  // B fragments of Q: [k-step][j-tile]
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt) {
+            const cplx q = sm.Q[ks * 4 + (lane & 3)][jt * 8 + (lane >> 2)];
+            bqr[ks][jt] = q.x;
+            bqi[ks][jt] = q.y;
+            bqs[ks][jt] = q.x + q.y;
+          }
+        int cc[8], cs_[4][2];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) cc[ks] = sm.col[ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) cs_[jt][h] = sm.col[jt * 8 + 2 * (lane & 3) + h];
+        for (int part = 0; part < 2; ++part) {
+          const int rb0 = part == 0 ? xr0 : a.vofs + vr0;
+          const int rb1 = part == 0 ? xr1 : a.vofs + vr1;
+          for (int r0 = rb0 + wid * 8; r0 < rb1; r0 += 64) {
+            const int r = r0 + (lane >> 2);
+            const bool rv = r < rb1;
+            cplx av[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              av[ks] = (rv && cc[ks] >= 0) ? __ldcg(Y + (long long)cc[ks] * ldy + r) : cmk(0.0, 0.0);
+            double c1[4][2], c2[4][2], c3[4][2];
+#pragma unroll
+            for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const double as = av[ks].x + av[ks].y;
+#pragma unroll
+              for (int jt = 0; jt < 4; ++jt) {
+                dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
+                dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
+                dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
+              }
+            }
+            double cR[4][2], cI[4][2];
+#pragma unroll
+            for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                cR[jt][h] = c1[jt][h] - c2[jt][h];
+                cI[jt][h] = c3[jt][h] - c1[jt][h] - c2[jt][h];
+              }
+            const int ro = r0 + (lane >> 2);
+            if (ro < rb1) {
+#pragma unroll
+              for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  if (cs_[jt][h] >= 0) __stcg(Y + (long long)cs_[jt][h] * ldy + ro, cmk(cR[jt][h], cI[jt][h]));
+            }
+          }
+        }
+      }
+      mark(3);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        const unsigned v = (unsigned)(round_g + 1);
+        for (const int blk : {bI, bJ}) {
+          unsigned* f = a.done + (long long)blk * a.S + s;
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+        }
+      }
+    }
+    grid_barrier(a.gbar, (unsigned)((sweep + 1) * (unsigned long long)G_));
+    mark(4);
+    const double off = __ldcg(off_cur);
+    if (!(off > tol) || off * off <= 0.01 * tol) break;
+  }
+  if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = min(sweep + 1, a.max_sweeps);
+  if (s == 0 && tid == 0 && flops > 0.0) atomicAdd(a.flop_out, flops);
+}
+
+}  // namespace
+
+size_t svd_bjac_work_elems(int sms) { return (size_t)2 * sms * PC * PC + 64; }
+
+// Jacobi stage on d.Y = [X ; V]: X rows [0, xr), V rows [vofs, vofs + nc).
+// cudaErrorNotSupported when the shape or the workspace does not fit.
+cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int nc, long long ldy, double tol,
+                         int* sweeps_dev, double* flop_dev) {
+  if (d.bjwork == nullptr || d.flags == nullptr || nc < PC) return cudaErrorNotSupported;
+  const int nb = (nc + BB - 1) / BB;
+  const int nbe = nb + (nb & 1);
+  const int P = nbe / 2;
+  int S = std::max(1, std::min(16, g_num_sms / P));
+  const size_t smem = sizeof(Smem);
+  cudaError_t e;
+  if ((e = set_smem_attr(reinterpret_cast<const void*>(bjac_kernel), (int)smem)) != cudaSuccess) return e;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bjac_kernel, NTB, smem)) != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorNotSupported;
+  while (S > 1 && P * S > occ * g_num_sms) --S;
+  if (P * S > occ * g_num_sms) return cudaErrorNotSupported;
+  const size_t nfl = (size_t)P + 1 + (size_t)nbe * S;
+  if ((size_t)2 * P * S * PC * PC > d.bjwork_elems || nfl > d.flags_elems) return cudaErrorNotSupported;
+  unsigned* pcnt = d.flags;
+  unsigned* gbar = d.flags + P;
+  unsigned* done = d.flags + P + 1;
+  if ((e = cudaMemsetAsync(d.flags, 0, nfl * sizeof(unsigned), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
+  BjArgs a;
+  a.Y = d.Y;
+  a.ldy = ldy;
+  a.xr = xr;
+  a.vofs = vofs;
+  a.nc = nc;
+  a.nb = nb;
+  a.nbe = nbe;
+  a.S = S;
+  a.P = P;
+  a.tol = tol;
+  a.max_sweeps = 60;
+  a.part = d.bjwork;
+  a.pcnt = pcnt;
+  a.gbar = gbar;
+  a.done = done;
+  a.offb = d.offmax;
+  a.sweeps_out = sweeps_dev;
+  a.flop_out = flop_dev;
+  static int prof = -1;
+  if (prof < 0) prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;
+  a.prof = prof;
+  static int inner_max = -1;
+  if (inner_max < 0) {
+    const char* ev = std::getenv("TDVP_BJ_INNER");
+    inner_max = ev ? std::max(1, std::atoi(ev)) : 1;
+  }
+  a.inner_max = inner_max;
+  if (prof) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbolAsync(g_bj_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  }
+  void* args[] = {(void*)&a};
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bjac_kernel), dim3(P * S), dim3(NTB), args, smem, st);
+  if (e == cudaSuccess && prof) {
+    unsigned long long z[8];
+    cudaMemcpyFromSymbolAsync(z, g_bj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::fprintf(stderr,
+                 "bjac prof xr=%d nc=%d P=%d S=%d cycles: gram %llu pairsum %llu inner %llu apply %llu gridbar %llu | "
+                 "inner sweeps %llu in %llu rounds\n",
+                 xr, nc, P, S, z[0], z[1], z[2], z[3], z[4], z[6], z[7]);
+  }
+  return e;
+}

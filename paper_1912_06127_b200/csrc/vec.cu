@@ -3,6 +3,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace {
 
 inline int grid_for(long long n, int tpb = 256) {
@@ -117,4 +121,33 @@ cudaError_t any_nonfinite(cudaStream_t st, const cplx* x, long long n, int* flag
   if (n <= 0) return cudaSuccess;
   nonfinite_kernel<<<grid_for(n), 256, 0, st>>>(x, n, flag);
   return cudaGetLastError();
+}
+
+cudaError_t set_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, fn);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
+
+cudaError_t set_cluster_nonportable(const void* fn) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, fn);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) done[key] = 1;
+  return e;
 }
