@@ -988,10 +988,14 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   int sweeps = 0;
   const bool tj = jac_ms_out != nullptr && d.ev_jac[0] != nullptr;
   if (tj && (e = cudaEventRecord(d.ev_jac[0], st)) != cudaSuccess) return e;
+  // block Jacobi on DMMA (svd_bjac.cu) beyond 1024 columns (chi = 1024 two-site
+  // matrices: 290 vs 674 ms at n = 2048); up to 1024 the register-resident
+  // rjac is as fast (microbench.py --svd: 15.6 vs 17.1 ms at 512, 50.5 vs 53.3
+  // at 1024).  TDVP_SVD_BJ_MIN lowers the threshold (parity tests run both).
   static int bj_min = -1;
   if (bj_min < 0) {
     const char* ev = std::getenv("TDVP_SVD_BJ_MIN");
-    bj_min = ev ? std::atoi(ev) : 384;
+    bj_min = ev ? std::atoi(ev) : 1025;
   }
   if ((e = cudaMemsetAsync(d.dres + 2, 0, sizeof(double), st)) != cudaSuccess) return e;
   bool bj = false;

@@ -531,14 +531,15 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   const int nb = (nc + BB - 1) / BB;
   const int nbe = nb + (nb & 1);
   const int P = nbe / 2;
-  int S = std::max(1, std::min(16, g_num_sms / P));
+  const void* fn = reinterpret_cast<const void*>(bjac_kernel);
   const size_t smem = sizeof(Smem);
   cudaError_t e;
-  if ((e = set_smem_attr(reinterpret_cast<const void*>(bjac_kernel), (int)smem)) != cudaSuccess) return e;
+  if ((e = set_smem_attr(fn, (int)smem)) != cudaSuccess) return e;
   int occ = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bjac_kernel, NTB, smem)) != cudaSuccess) return e;
   if (occ < 1) return cudaErrorNotSupported;
-  while (S > 1 && P * S > occ * g_num_sms) --S;
+  // S CTAs per pair (row slices) so that the grid fills the SMs once
+  const int S = std::max(1, std::min(16, occ * g_num_sms / P));
   if (P * S > occ * g_num_sms) return cudaErrorNotSupported;
   const size_t nfl = (size_t)P + 1 + (size_t)nbe * S;
   if ((size_t)2 * P * S * PC * PC > d.bjwork_elems || nfl > d.flags_elems) return cudaErrorNotSupported;
@@ -569,18 +570,13 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   static int prof = -1;
   if (prof < 0) prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;
   a.prof = prof;
-  static int inner_max = -1;
-  if (inner_max < 0) {
-    const char* ev = std::getenv("TDVP_BJ_INNER");
-    inner_max = ev ? std::max(1, std::atoi(ev)) : 1;
-  }
-  a.inner_max = inner_max;
+  a.inner_max = 1;  // one inner sweep per round (measured fastest: the outer sweep count does not grow)
   if (prof) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbolAsync(g_bj_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
   void* args[] = {(void*)&a};
-  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bjac_kernel), dim3(P * S), dim3(NTB), args, smem, st);
+  e = cudaLaunchCooperativeKernel(fn, dim3(P * S), dim3(NTB), args, smem, st);
   if (e == cudaSuccess && prof) {
     unsigned long long z[8];
     cudaMemcpyFromSymbolAsync(z, g_bj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);

@@ -323,3 +323,16 @@ def test_paper_mode_krylov_tol_matches_oracle(B, p):
         res[tol] = t.measure_sz()
         t.close()
     assert np.abs(res[0.0] - res[1e-6]).max() < 1e-4
+
+
+def test_svd_block_jacobi_forced_small(B):
+    """The DMMA block-Jacobi SVD path (svd_bjac.cu, default only beyond 1024
+    columns) forced down to 32 columns (TDVP_SVD_BJ_MIN, read once per process,
+    hence a subprocess): every SVD parity test above on ragged small shapes."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TDVP_SVD_BJ_MIN="32")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "svd and not forced",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
