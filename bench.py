@@ -254,6 +254,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary c2sat / lanes figures")
+    ap.add_argument("--dist", default="lead", choices=["lead", "nccl"],
+                    help="under torchrun (WORLD_SIZE = N): 'lead' = rank 0 drives all N devices through one "
+                         "multi-device handle (peer copies over NVLink; the other ranks only join the barriers), "
+                         "'nccl' = one segment per rank, boundary messages by NCCL send/recv")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -263,7 +267,9 @@ def main():
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     n_gpus = args.gpus
     p = n_gpus  # one segment per GPU; N=1 -> serial 2TDVP
-    mode = "one rank per GPU, NCCL send/recv" if world > 1 else "one process driving N devices"
+    nccl_ranks = world > 1 and args.dist == "nccl"
+    mode = ("one rank per GPU, NCCL send/recv" if nccl_ranks else
+            "one process driving N devices (segment lanes, cudaMemcpyPeerAsync over NVLink)")
     wl = workload_inputs(args.workload)
     config = workload_config(args.workload, wl, p, n_gpus, mode)
 
@@ -293,16 +299,25 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    elif n_gpus > torch.cuda.device_count():
+    if n_gpus > torch.cuda.device_count():
         sys.exit(f"bench.py: --gpus {n_gpus} but only {torch.cuda.device_count()} CUDA devices")
+    if world > 1 and not nccl_ranks and rank != 0:
+        # lead mode: rank 0 drives every device; this rank joins the barriers around
+        # the timed region and the max-over-ranks reduction, then exits
+        dist.barrier()
+        dist.barrier()
+        x = torch.tensor([0.0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+        return
 
     peaks = fp64_peak_tflops() if rank == 0 else {}
 
     L = wl["L"]
-    devices = list(range(n_gpus)) if (world == 1 and n_gpus > 1) else None
+    devices = list(range(n_gpus)) if (not nccl_ranks and n_gpus > 1) else None
     t = pkg.Tdvp(L, 2, wl["D"], wl["chi"], devices=devices)
     t.set_params(eps=wl["eps"], timing=False)  # the timed steps run uninstrumented
-    if world > 1:
+    if nccl_ranks:
         uid = [pkg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         t.comm_init(rank, world, uid[0])
@@ -351,7 +366,7 @@ def main():
     # e2e: the same step through the C-ABI with HOST buffers (set_mps H2D incl.
     # the sequential environment build, step, get_mps D2H) every step
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and (world == 1 or not nccl_ranks):
         mps = wl["mps"]
         ne = max(1, min(args.steps, 3))
         torch.cuda.synchronize()

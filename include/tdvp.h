@@ -50,6 +50,18 @@ typedef struct {
                              the device (the oracle's rule); a timing variant */
   double multiplet_delta; /* AMB-9 multiplet guard at the chi_max cut; default 1e-6 */
   int timing;             /* 1: record CUDA events around every H_eff matvec and SVD (stats) */
+  /* Multi-GPU in ONE process (SURVEY §8(b) "one process drives devices 0..p-1";
+   * PAPER.md:470 one segment per processor): n_devices > 1 spreads the p segments
+   * of tdvp_step(h, dt, p) over device_ids[0..n_devices-1] (segment q on
+   * device_ids[q * n_devices / p]); each segment runs on its own host thread and
+   * stream, boundary messages travel as cudaMemcpyPeerAsync
+   * (NVLink P2P; peer access is enabled where supported); measurements and
+   * tdvp_get_mps gather onto device_ids[0].  device_ids[0] must be the device the
+   * handle was created on; ids may repeat (several segments per device).  The
+   * array is copied.  n_devices <= 1: all segments on the handle's device.
+   * tdvp_get_params returns the handle's copy. */
+  int n_devices;
+  const int* device_ids;
 } tdvp_params;
 
 typedef struct {
@@ -124,6 +136,10 @@ int tdvp_measure_norm(tdvp_t h, double* norm2 /* <psi|psi> */);
  * Errors: TDVP_EARG (null / mismatched handles), TDVP_ESTATE (no MPO/MPS, or the
  * state is distributed across ranks). */
 int tdvp_overlap(tdvp_t a, tdvp_t b, double* re, double* im);
+/* I = 1 - |<a|b>| / sqrt(<a|a><b|b>) (PAPER.md benchmark section "the infidelity
+ * between the states obtained serially and in parallel"), computed by the
+ * library from tdvp_overlap and the two norms.  Errors as tdvp_overlap. */
+int tdvp_infidelity(tdvp_t a, tdvp_t b, double* infidelity);
 
 /* Reorthonormalisation: re-gauge the current MPS into
  * inverse-canonical form by an SVD sweep left->right and one right->left on

@@ -116,16 +116,8 @@ cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner
   if (cm.n_ic > 0 && cm.n_ic <= GMAX && cm.slot != nullptr) {
     const size_t smg = (size_t)cm.n_ic * TPB * sizeof(cplx) + (size_t)cm.nnz * (sizeof(cplx) + sizeof(int)) +
                        (size_t)(cm.n_ic + cm.n_oc) * sizeof(long long) + (size_t)(cm.n_oc + 1) * sizeof(int);
-    static bool gattr = false;
-    if (!gattr) {
-      std::lock_guard<std::mutex> lk(gmu());
-      if (!gattr) {
-        cudaError_t e = cudaFuncSetAttribute(chanmix_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             100 * 1024);
-        if (e != cudaSuccess) return e;
-        gattr = true;
-      }
-    }
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(chanmix_gather_kernel), 100 * 1024);
+    if (e != cudaSuccess) return e;
     if (smg <= 100 * 1024) {
       dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
       chanmix_gather_kernel<<<grid, TPB, smg, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out,
@@ -135,15 +127,9 @@ cudaError_t chanmix(cudaStream_t st, const ChanMix& cm, int n_outer, int n_inner
   }
   const size_t sm = (size_t)cm.nnz * (sizeof(cplx) + sizeof(long long)) + (size_t)cm.n_oc * sizeof(long long) +
                     (size_t)(cm.n_oc + 1) * sizeof(int);
-  static size_t configured = 48 * 1024;  // only grows; guarded for concurrent segment lanes
-  static std::mutex mu;
   if (sm > 48 * 1024) {
-    std::lock_guard<std::mutex> lk(mu);
-    if (sm > configured) {
-      cudaError_t e = cudaFuncSetAttribute(chanmix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) return e;
-      configured = sm;
-    }
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(chanmix_kernel), (int)sm);
+    if (e != cudaSuccess) return e;
   }
   dim3 grid((n_inner + TPB - 1) / TPB, n_outer);
   chanmix_kernel<<<grid, TPB, sm, st>>>(cm, n_inner, in, so_in, si_in, in_ch, out, so_out, si_out, out_ch, skip);

@@ -110,6 +110,26 @@ struct DevBuf {
   int* i() const { return reinterpret_cast<int*>(p); }
 };
 using BufPtr = std::unique_ptr<DevBuf>;
+
+// RAII: make `dev` current for the scope (multi-device handles allocate and
+// launch per segment device), restore the previous device afterwards
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+// device-to-device copy on `st` (a stream of the current device); across
+// devices by cudaMemcpyPeerAsync (NVLink P2P when peer access is enabled)
+inline void d2d(void* dst, int ddev, const void* src, int sdev, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  if (ddev == sdev) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  else CK(cudaMemcpyPeerAsync(dst, ddev, src, sdev, bytes, st));
+}
 BufPtr make_buf(size_t bytes) {
   BufPtr b(new DevBuf());
   b->alloc(bytes);
@@ -131,6 +151,7 @@ struct MpoSite {
 // Segment: everything one process owns
 struct Segment {
   int q = 0, s = 0, e = 0;
+  int dev = 0;          // device holding this segment's tensors (multi-device handles)
   std::vector<int> cb;  // bond dims, L+1 (own view)
   std::vector<BufPtr> psi, beta, gamma;  // per site (null if not held)
   std::vector<BufPtr> lam, vinv;         // per bond
@@ -153,6 +174,7 @@ struct LaneMsg {
   std::condition_variable cv;
   int ready = 0;
   int meta[2] = {0, 0};
+  int sdev = 0, rdev = 0;  // sender / receiver device (staging lives on rdev)
   cudaEvent_t posted = nullptr, consumed = nullptr;
   bool consumed_rec = false;
   BufPtr psi, lam, vinv, env;
@@ -167,7 +189,7 @@ struct LaneMsg {
 struct tdvp_ctx {
   tdvp_ctx() : mpo(mpo_own) {}
   // a segment lane: own stream and workspace, the parent's MPO
-  explicit tdvp_ctx(tdvp_ctx* par) : mpo(par->mpo_own), parent(par) {}
+  explicit tdvp_ctx(tdvp_ctx* par, bool own_mpo = false) : mpo(own_mpo ? mpo_own : par->mpo_own), parent(par) {}
   tdvp_ctx(const tdvp_ctx&) = delete;
   tdvp_ctx& operator=(const tdvp_ctx&) = delete;
   int L = 0, d = 0, Dmpo = 0, chi_max = 0;
@@ -179,6 +201,12 @@ struct tdvp_ctx {
   bool lz_fused = true;  // one cooperative launch per Lanczos iteration (TDVP_LZ_FUSED=0: four passes)
   const double* cur_skip = nullptr;  // inside a paper-mode Lanczos: its device "converged" flag
   int dev = 0;
+  // devices of a multi-device handle (tdvp_params.n_devices / device_ids):
+  // segment q of a p-segment step lives on devs[q * n / p]; devs[0] = dev
+  std::vector<int> devs;
+  bool multi_dev = false;
+  std::vector<int> h_D;                       // MPO bond dims (host copy, per-device MPO tables)
+  std::vector<std::vector<cplx>> h_W;         // MPO tensors (host copy)
   cudaStream_t st = nullptr;
   std::string err;
   std::vector<int> cbmax;  // L+1
@@ -199,6 +227,7 @@ struct tdvp_ctx {
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
   BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, svdF, gemm_work, partials;
   BufPtr lz_scal, lz_coef, lz_y, lz_counter, lz_brk;
+  BufPtr lz_brk_own;  // a multi-device lane's breakdown counter (on its device)
   BufPtr svd_sigma, svd_order, svd_perm, svd_bj, svd_off, svd_ires, svd_dres, red_res, envA, envB;
   double* h_pin = nullptr;
   int* h_ipin = nullptr;
@@ -232,6 +261,9 @@ std::atomic<long long> g_launch_count{0};
 std::atomic<long long> g_gemm_count{0};
 
 tdvp_ctx::~tdvp_ctx() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != dev) cudaSetDevice(dev);  // this context's stream, events and buffers live on `dev`
   if (st) cudaStreamSynchronize(st);
   lanes.clear();
   msg_r.clear();
@@ -247,6 +279,7 @@ tdvp_ctx::~tdvp_ctx() {
   if (h_ipin) cudaFreeHost(h_ipin);
   if (comm && nccl().ok) nccl().CommDestroy(comm);
   if (st) cudaStreamDestroy(st);
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
 }
 
 namespace {
@@ -662,8 +695,10 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
 }
 
 // ------------------------------------------------------------ layout / init
-void alloc_segment(tdvp_ctx* h, Segment& g, int q, int s, int e) {
+void alloc_segment(tdvp_ctx* h, Segment& g, int q, int s, int e, int dev) {
   const int L = h->L, d = h->d;
+  DeviceGuard dg(dev);
+  g.dev = dev;
   g.q = q;
   g.s = s;
   g.e = e;
@@ -706,23 +741,37 @@ int owner_of(tdvp_ctx* h, int j) {
 }
 bool local_mode(tdvp_ctx* h) { return h->world == 1; }
 
+// device of segment q in a p-segment layout: contiguous groups of segments per
+// device (neighbouring segments share a device when p > n_devices)
+int seg_device(tdvp_ctx* h, int q, int p) {
+  if (!h->multi_dev || h->devs.empty()) return h->dev;
+  const int n = (int)h->devs.size();
+  return h->devs[std::min(n - 1, (int)((long long)q * n / p))];
+}
+
+tdvp_ctx* lane_of(tdvp_ctx* h, int q);
+
 // upload the full host MPS copy into the current layout
 void upload_state(tdvp_ctx* h) {
   const int L = h->L;
   for (auto& g : h->segs) {
+    // the segment's own device and a stream of it (its lane's, when on another device)
+    DeviceGuard dg(g.dev);
+    cudaStream_t st = g.dev == h->dev ? h->st : lane_of(h, g.q)->st;
     std::fill(g.wside.begin(), g.wside.end(), 0);  // new state: no warm-start bases
     g.cb = h->h_chi;
     const int hi = std::min(g.e + 1, L - 1);
     for (int j = g.s; j <= hi; ++j)
       CK(cudaMemcpyAsync(g.psi[j]->p, h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double), cudaMemcpyHostToDevice,
-                         h->st));
+                         st));
     for (int b = std::max(g.s - 1, 0); b <= std::min(g.e, L - 2); ++b) {
       CK(cudaMemcpyAsync(g.lam[b]->p, h->h_lam[b].data(), h->h_lam[b].size() * sizeof(double),
-                         cudaMemcpyHostToDevice, h->st));
+                         cudaMemcpyHostToDevice, st));
       const int n = (int)h->h_lam[b].size();
-      recip_kernel<<<(n + 255) / 256, 256, 0, h->st>>>(g.lam[b]->d(), g.vinv[b]->d(), n);
+      recip_kernel<<<(n + 255) / 256, 256, 0, st>>>(g.lam[b]->d(), g.vinv[b]->d(), n);
       CK(cudaGetLastError());
     }
+    CK(cudaStreamSynchronize(st));
   }
   CK(cudaStreamSynchronize(h->st));
 }
@@ -734,18 +783,20 @@ void download_state(tdvp_ctx* h) {
   std::vector<int> chi(L + 1, 1);
   for (int b = 0; b < L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];  // left owner owns bond b
   h->h_chi = chi;
+  CK(cudaStreamSynchronize(h->st));  // every lane's work was joined into h->st by the step
   for (int j = 0; j < L; ++j) {
     Segment& g = h->segs[owner_of(h, j)];
     const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
     h->h_psi[j].resize(n);
-    CK(cudaMemcpyAsync(h->h_psi[j].data(), g.psi[j]->p, n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    DeviceGuard dg(g.dev);
+    CK(cudaMemcpy(h->h_psi[j].data(), g.psi[j]->p, n * sizeof(double), cudaMemcpyDeviceToHost));
   }
   for (int b = 0; b < L - 1; ++b) {
     Segment& g = h->segs[owner_of(h, b)];
     h->h_lam[b].resize(chi[b + 1]);
-    CK(cudaMemcpyAsync(h->h_lam[b].data(), g.lam[b]->p, chi[b + 1] * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    DeviceGuard dg(g.dev);
+    CK(cudaMemcpy(h->h_lam[b].data(), g.lam[b]->p, chi[b + 1] * sizeof(double), cudaMemcpyDeviceToHost));
   }
-  CK(cudaStreamSynchronize(h->st));
 }
 
 // Sequential initial environments (O-2) from the host
@@ -777,7 +828,7 @@ void build_envs(tdvp_ctx* h) {
   auto store = [&](bool left, int j, const cplx* src, long long n) {
     for (auto& g : h->segs) {
       const BufPtr& b = left ? g.beta[j] : g.gamma[j];
-      if (b) CK(cudaMemcpyAsync(b->p, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, h->st));
+      if (b) d2d(b->p, g.dev, src, h->dev, n * sizeof(cplx), h->st);
     }
   };
   store(true, 0, cur, 1);
@@ -825,10 +876,10 @@ void layout(tdvp_ctx* h, int p) {
     h->bounds = b;
     if (local_mode(h)) {
       h->segs.resize(p);
-      for (int q = 0; q < p; ++q) alloc_segment(h, h->segs[q], q, b[q].first, b[q].second);
+      for (int q = 0; q < p; ++q) alloc_segment(h, h->segs[q], q, b[q].first, b[q].second, seg_device(h, q, p));
     } else {
       h->segs.resize(1);
-      alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second);
+      alloc_segment(h, h->segs[0], h->rank, b[h->rank].first, b[h->rank].second, h->dev);
     }
     h->msg_r.clear();
     h->msg_l.clear();
@@ -988,19 +1039,44 @@ void run_half(tdvp_ctx* h, int hh, double dt, const std::set<int>& merged) {
 // ------------------------------------------------------------ segment lanes
 void alloc_workspace(tdvp_ctx* h);
 
+void build_mpo_tables(std::vector<MpoSite>& mpo, int L, int d, const std::vector<int>& D,
+                      const std::vector<std::vector<cplx>>& W);
+
+// lane q (1..p-1): own host thread, stream and workspace, on the device of
+// segment q.  In a multi-device handle every lane also holds its own copy of
+// the MPO tables (device pointers) on its device; a lane whose device no
+// longer matches the layout is rebuilt.
 tdvp_ctx* lane_of(tdvp_ctx* h, int q) {
   if (q == 0) return h;
+  const int p = std::max(h->layout_p, q + 1);
+  const int want = seg_device(h, q, p);
+  if ((int)h->lanes.size() >= q && h->lanes[q - 1]->dev != want) {
+    CK(cudaStreamSynchronize(h->lanes[q - 1]->st));
+    h->lanes.resize(q - 1);  // rebuild this lane and the later ones
+  }
   while ((int)h->lanes.size() < q) {
-    std::unique_ptr<tdvp_ctx> ln(new tdvp_ctx(h));
+    const int lq = (int)h->lanes.size() + 1;
+    const int ldev = seg_device(h, lq, p);
+    DeviceGuard dg(ldev);
+    std::unique_ptr<tdvp_ctx> ln(new tdvp_ctx(h, h->multi_dev));
     ln->L = h->L;
     ln->d = h->d;
     ln->Dmpo = h->Dmpo;
     ln->chi_max = h->chi_max;
     ln->cbmax = h->cbmax;
-    ln->dev = h->dev;
+    ln->dev = ldev;
     CK(cudaStreamCreateWithFlags(&ln->st, cudaStreamNonBlocking));
     alloc_workspace(ln.get());
-    ln->lz.brk_count = h->lz_brk->i();  // one breakdown counter per handle
+    if (h->multi_dev) {
+      CK(cudaMalloc(&ln->lz.brk_count, 64));
+      ln->lz_brk_own.reset(new DevBuf());
+      ln->lz_brk_own->p = ln->lz.brk_count;
+      ln->lz_brk_own->bytes = 64;
+      CK(cudaMemset(ln->lz.brk_count, 0, 64));
+      if (h->have_mpo) build_mpo_tables(ln->mpo_own, h->L, h->d, h->h_D, h->h_W);
+    } else {
+      ln->lz.brk_count = h->lz_brk->i();  // one breakdown counter per handle
+    }
     CK(cudaEventCreate(&ln->sv.ev_jac[0]));
     CK(cudaEventCreate(&ln->sv.ev_jac[1]));
     h->lanes.push_back(std::move(ln));
@@ -1015,9 +1091,18 @@ void alloc_msgs(tdvp_ctx* h) {
   h->msg_l.clear();
   h->msg_r.resize(p);
   h->msg_l.resize(p);
-  auto mk = [&](std::unique_ptr<LaneMsg>& m, size_t psi, size_t lam, size_t env) {
+  // staging buffers on the RECEIVER's device (the sender's copy crosses
+  // NVLink); `posted` recorded by the sender's stream, `consumed` by the
+  // receiver's, each created on its recording device
+  auto mk = [&](std::unique_ptr<LaneMsg>& m, int sdev, int rdev, size_t psi, size_t lam, size_t env) {
     m.reset(new LaneMsg());
-    CK(cudaEventCreateWithFlags(&m->posted, cudaEventDisableTiming));
+    m->sdev = sdev;
+    m->rdev = rdev;
+    {
+      DeviceGuard dg(sdev);
+      CK(cudaEventCreateWithFlags(&m->posted, cudaEventDisableTiming));
+    }
+    DeviceGuard dg(rdev);
     CK(cudaEventCreateWithFlags(&m->consumed, cudaEventDisableTiming));
     m->psi = make_buf(psi * sizeof(cplx));
     m->env = make_buf(env * sizeof(cplx));
@@ -1030,11 +1115,11 @@ void alloc_msgs(tdvp_ctx* h) {
     const int s = h->bounds[q].first, e = h->bounds[q].second;
     if (q + 1 < p) {
       const size_t c1 = h->cbmax[e + 1], c2 = h->cbmax[e + 2];
-      mk(h->msg_r[q], c1 * d * c2, c1, c1 * h->mpo[e + 1].Dl * c1);
+      mk(h->msg_r[q], h->segs[q].dev, h->segs[q + 1].dev, c1 * d * c2, c1, c1 * h->mpo[e + 1].Dl * c1);
     }
     if (q > 0) {
       const size_t c0 = h->cbmax[s], c1 = h->cbmax[s + 1];
-      mk(h->msg_l[q], c0 * d * c1, 0, c1 * h->mpo[s].Dr * c1);
+      mk(h->msg_l[q], h->segs[q].dev, h->segs[q - 1].dev, c0 * d * c1, 0, c1 * h->mpo[s].Dr * c1);
     }
   }
 }
@@ -1061,10 +1146,10 @@ void lane_send_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<boo
   lane_wait(m, 0, abort);
   if (m.consumed_rec) CK(cudaStreamWaitEvent(ln->st, m.consumed, 0));
   const int e = a.e, d = ln->d, chi = a.cb[e + 1], cr = a.cb[e + 2];
-  lane_copy(ln, m.psi->p, a.psi[e + 1]->p, (size_t)chi * d * cr * sizeof(cplx));
-  lane_copy(ln, m.lam->p, a.lam[e]->p, (size_t)chi * sizeof(double));
-  lane_copy(ln, m.vinv->p, a.vinv[e]->p, (size_t)chi * sizeof(double));
-  lane_copy(ln, m.env->p, a.beta[e + 1]->p, (size_t)chi * ln->mpo[e + 1].Dl * chi * sizeof(cplx));
+  d2d(m.psi->p, m.rdev, a.psi[e + 1]->p, m.sdev, (size_t)chi * d * cr * sizeof(cplx), ln->st);
+  d2d(m.lam->p, m.rdev, a.lam[e]->p, m.sdev, (size_t)chi * sizeof(double), ln->st);
+  d2d(m.vinv->p, m.rdev, a.vinv[e]->p, m.sdev, (size_t)chi * sizeof(double), ln->st);
+  d2d(m.env->p, m.rdev, a.beta[e + 1]->p, m.sdev, (size_t)chi * ln->mpo[e + 1].Dl * chi * sizeof(cplx), ln->st);
   CK(cudaEventRecord(m.posted, ln->st));
   m.meta[0] = chi;
   m.meta[1] = cr;
@@ -1087,8 +1172,8 @@ void lane_send_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool
   lane_wait(m, 0, abort);
   if (m.consumed_rec) CK(cudaStreamWaitEvent(ln->st, m.consumed, 0));
   const int s = b.s, d = ln->d, cl = b.cb[s], cr = b.cb[s + 1];
-  lane_copy(ln, m.psi->p, b.psi[s]->p, (size_t)cl * d * cr * sizeof(cplx));
-  lane_copy(ln, m.env->p, b.gamma[s]->p, (size_t)cr * ln->mpo[s].Dr * cr * sizeof(cplx));
+  d2d(m.psi->p, m.rdev, b.psi[s]->p, m.sdev, (size_t)cl * d * cr * sizeof(cplx), ln->st);
+  d2d(m.env->p, m.rdev, b.gamma[s]->p, m.sdev, (size_t)cr * ln->mpo[s].Dr * cr * sizeof(cplx), ln->st);
   CK(cudaEventRecord(m.posted, ln->st));
   m.meta[0] = cl;
   m.meta[1] = cr;
@@ -1164,7 +1249,7 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
   std::vector<std::exception_ptr> errs(p);
   auto body = [&](int q) {
     try {
-      CK(cudaSetDevice(h->dev));
+      CK(cudaSetDevice(q == 0 ? h->dev : lane_of(h, q)->dev));
       lane_program(h, q, dt, merged, abort);
     } catch (...) {
       errs[q] = std::current_exception();
@@ -1192,7 +1277,11 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     }
   for (int q = 1; q < p; ++q) {
     tdvp_ctx* ln = h->lanes[q - 1].get();
-    const int ev = ev_record(ln);
+    int ev;
+    {
+      DeviceGuard dg(ln->dev);
+      ev = ev_record(ln);
+    }
     CK(cudaStreamWaitEvent(h->st, ln->ev_pool[ev], 0));
     tdvp_stats& a = h->stats;
     const tdvp_stats& b = ln->stats;
@@ -1245,7 +1334,7 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   const long long l0 = g_launch_count, g0 = g_gemm_count;
   CK(cudaEventRecord(h->ev_step0, h->st));
   const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
-  const bool lanes = local_mode(h) && p > 1 && h->lanes_on;
+  const bool lanes = local_mode(h) && p > 1 && (h->lanes_on || h->multi_dev);
   if (lanes) {
     if ((int)h->msg_r.size() != p) alloc_msgs(h);
     run_step_lanes(h, dt, merged);
@@ -1349,6 +1438,16 @@ void measure(tdvp_ctx* h, bool want_sz, bool want_E, MeasureOut& out) {
     CK(cudaStreamSynchronize(h->st));
     out.energy = e.x / out.norm;
   }
+}
+
+// CSR tables of every MPO site and the pair tables W_j W_{j+1} (H_eff^(2)'s
+// fused channel pass) on the current device
+void build_mpo_tables(std::vector<MpoSite>& mpo, int L, int d, const std::vector<int>& D,
+                      const std::vector<std::vector<cplx>>& W) {
+  mpo.clear();
+  mpo.resize(L);
+  for (int j = 0; j < L; ++j) build_site(mpo[j], D[j], D[j + 1], d, W[j]);
+  for (int j = 0; j + 1 < L; ++j) build_pair(mpo[j], D[j], D[j + 1], D[j + 2], d, W[j], W[j + 1]);
 }
 
 // ------------------------------------------------------------ workspace
@@ -1489,6 +1588,9 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
     h->prm.krylov_tol = 0.0;
     h->prm.multiplet_delta = 1e-6;
     h->prm.timing = 0;
+    h->devs = {h->dev};
+    h->prm.n_devices = 1;
+    h->prm.device_ids = h->devs.data();
     if (const char* ev = std::getenv("TDVP_SVD_WARM")) h->warm_svd = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("TDVP_LZ_FUSED")) h->lz_fused = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("TDVP_LANES")) h->lanes_on = std::atoi(ev) != 0;
@@ -1529,7 +1631,51 @@ int tdvp_set_params(tdvp_t h, const tdvp_params* p) {
     h->err = "invalid params (krylov_k in 1..15, 0 <= eps < 1, w_max >= 0, 0 <= krylov_tol < 1)";
     return TDVP_EARG;
   }
+  try {
+    std::vector<int> devs;
+    if (p->n_devices > 1) {
+      if (!p->device_ids) throw TdvpError(TDVP_EARG, "n_devices > 1 needs device_ids");
+      int ndev = 0;
+      CK(cudaGetDeviceCount(&ndev));
+      for (int i = 0; i < p->n_devices; ++i) {
+        const int dv = p->device_ids[i];
+        if (dv < 0 || dv >= ndev) throw TdvpError(TDVP_EARG, "device id out of range");
+        devs.push_back(dv);
+      }
+      if (devs[0] != h->dev)
+        throw TdvpError(TDVP_EARG, "device_ids[0] must be the device the handle was created on");
+      if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "a multi-device handle cannot also be a rank of a group");
+    }
+    const bool multi = devs.size() > 1;
+    if (multi != h->multi_dev || (multi && devs != h->devs)) {
+      // new device map: keep the state, re-lay it out at the next step
+      if (h->layout_p != 0 && h->have_mps) download_state(h);
+      h->layout_p = 0;
+      h->alloc_p = 0;
+      h->segs.clear();
+      h->msg_r.clear();
+      h->msg_l.clear();
+      h->lanes.clear();
+      h->multi_dev = multi;
+      h->devs = multi ? devs : std::vector<int>{h->dev};
+      if (multi)
+        for (int a : h->devs)
+          for (int b : h->devs)
+            if (a != b) {
+              int ok = 0;
+              if (cudaDeviceCanAccessPeer(&ok, a, b) == cudaSuccess && ok) {
+                DeviceGuard dg(a);
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+                if (pe != cudaSuccess) cudaGetLastError();  // already enabled: fine
+              }
+            }
+    }
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
   h->prm = *p;
+  h->prm.n_devices = (int)h->devs.size();
+  h->prm.device_ids = h->devs.data();
   return TDVP_OK;
 }
 
@@ -1546,23 +1692,20 @@ int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W) {
     if (D[0] != 1 || D[L] != 1) throw TdvpError(TDVP_EARG, "MPO boundary bond dims must be 1");
     for (int j = 0; j <= L; ++j)
       if (D[j] < 1 || D[j] > h->Dmpo) throw TdvpError(TDVP_EARG, "MPO bond dim out of range");
-    std::vector<MpoSite> mpo(L);
+    std::vector<std::vector<cplx>> hw(L);
     for (int j = 0; j < L; ++j) {
       if (!W[j]) throw TdvpError(TDVP_EARG, "null MPO tensor");
       const size_t n = (size_t)D[j] * d * d * D[j + 1];
       for (size_t i = 0; i < 2 * n; ++i)
         if (!std::isfinite(W[j][i])) throw TdvpError(TDVP_ENONFINITE, "non-finite MPO entry");
-      build_site(mpo[j], D[j], D[j + 1], d, to_cplx(W[j], n));
+      hw[j] = to_cplx(W[j], n);
     }
-    static int fuse = -1;
-    if (fuse < 0) {
-      const char* ev = std::getenv("TDVP_HEFF_FUSE");
-      fuse = ev ? std::atoi(ev) : 1;
-    }
-    for (int j = 0; fuse && j + 1 < L; ++j)
-      build_pair(mpo[j], D[j], D[j + 1], D[j + 2], d, to_cplx(W[j], (size_t)D[j] * d * d * D[j + 1]),
-                 to_cplx(W[j + 1], (size_t)D[j + 1] * d * d * D[j + 2]));
+    std::vector<MpoSite> mpo;
+    h->h_D.assign(D, D + L + 1);
+    build_mpo_tables(mpo, L, d, h->h_D, hw);
+    h->h_W = std::move(hw);
     h->mpo = std::move(mpo);
+    h->lanes.clear();  // lanes of a multi-device handle hold per-device copies of the tables
     h->have_mpo = true;
     h->envs_valid = false;
     if (h->layout_p != 0 && h->have_mps && local_mode(h)) download_state(h);
@@ -1667,12 +1810,19 @@ static std::vector<BufPtr> chain_tensors(tdvp_ctx* h, std::vector<int>& chi) {
   chi.assign(L + 1, 1);
   for (int j = 1; j < L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
   std::vector<BufPtr> M(L);
+  CK(cudaStreamSynchronize(h->st));
+  BufPtr tv = make_buf((size_t)h->chi_max * sizeof(double) + 64);
   for (int j = 0; j < L; ++j) {
     Segment& g = h->segs[owner_of(h, j)];
     const long long n = (long long)chi[j] * d * chi[j + 1];
     M[j] = make_buf(n * sizeof(cplx));
-    if (j < L - 1) CK(scale_cols(h->st, M[j]->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)chi[j] * d, chi[j + 1]));
-    else CK(copy_cplx(h->st, M[j]->c(), P(g.psi[j]), n));
+    // a multi-device handle gathers the chain onto the lead device (NVLink peer copies)
+    d2d(M[j]->p, h->dev, g.psi[j]->p, g.dev, (size_t)n * sizeof(cplx), h->st);
+    if (j < L - 1) {
+      d2d(tv->p, h->dev, g.vinv[j]->p, g.dev, (size_t)chi[j + 1] * sizeof(double), h->st);
+      CK(scale_cols(h->st, M[j]->c(), M[j]->c(), tv->d(), (long long)chi[j] * d, chi[j + 1]));
+      CK(cudaStreamSynchronize(h->st));  // tv is reused
+    }
   }
   return M;
 }
@@ -1712,6 +1862,24 @@ int tdvp_overlap(tdvp_t a, tdvp_t b, double* re, double* im) {
     CK(cudaStreamSynchronize(a->st));
     *re = r.x;
     *im = r.y;
+  } catch (const TdvpError& e) {
+    return fail(a, e);
+  }
+  return TDVP_OK;
+}
+
+// infidelity I = 1 - |<a|b>| / sqrt(<a|a><b|b>) between two handles' states
+// (PAPER.md benchmark section: serial vs parallel)
+int tdvp_infidelity(tdvp_t a, tdvp_t b, double* inf) {
+  if (!a || !b || !inf) return TDVP_EARG;
+  double re = 0.0, im = 0.0;
+  int rc = tdvp_overlap(a, b, &re, &im);
+  if (rc != TDVP_OK) return rc;
+  try {
+    MeasureOut ma, mb;
+    measure(a, false, false, ma);
+    measure(b, false, false, mb);
+    *inf = 1.0 - std::hypot(re, im) / std::sqrt(ma.norm * mb.norm);
   } catch (const TdvpError& e) {
     return fail(a, e);
   }
@@ -1843,14 +2011,18 @@ int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
       const int L = h->L, d = h->d;
       std::vector<int> chi(L + 1, 1);
       for (int b = 0; b < L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];
-      for (int j = 0; j < L; ++j)
-        CK(cudaMemcpyAsync(Psi[j], h->segs[owner_of(h, j)].psi[j]->p, (size_t)chi[j] * d * chi[j + 1] * sizeof(cplx),
-                           cudaMemcpyDeviceToHost, h->st));
-      if (Lambda)
-        for (int b = 0; b < L - 1; ++b)
-          CK(cudaMemcpyAsync(Lambda[b], h->segs[owner_of(h, b)].lam[b]->p, (size_t)chi[b + 1] * sizeof(double),
-                             cudaMemcpyDeviceToHost, h->st));
       CK(cudaStreamSynchronize(h->st));
+      for (int j = 0; j < L; ++j) {
+        const Segment& g = h->segs[owner_of(h, j)];
+        DeviceGuard dg(g.dev);
+        CK(cudaMemcpy(Psi[j], g.psi[j]->p, (size_t)chi[j] * d * chi[j + 1] * sizeof(cplx), cudaMemcpyDeviceToHost));
+      }
+      if (Lambda)
+        for (int b = 0; b < L - 1; ++b) {
+          const Segment& g = h->segs[owner_of(h, b)];
+          DeviceGuard dg(g.dev);
+          CK(cudaMemcpy(Lambda[b], g.lam[b]->p, (size_t)chi[b + 1] * sizeof(double), cudaMemcpyDeviceToHost));
+        }
       return TDVP_OK;
     }
     if (h->layout_p != 0) download_state(h);

@@ -1020,16 +1020,8 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
                 : nt_sel == 512 ? qrc3_factor_kernel<512, NB, false>
                                 : qrc3_factor_kernel<256, NB, false>;
   const int nthreads = reg ? (rpl_env == 2 ? 512 : 256) : nt_sel;
-  static bool attr = false;
-  if (!attr) {
-    for (auto f : {qrc3_factor_kernel<512, NB, false, 8>, qrc3_factor_kernel<256, NB, false, 8>,
-                   qrc3_factor_kernel<512, NB, false>, qrc3_factor_kernel<256, NB, false>}) {
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) != cudaSuccess)
-        return e;
-      if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
-    }
-    attr = true;
-  }
+  if ((e = set_smem_attr(reinterpret_cast<const void*>(fn), 200 * 1024)) != cudaSuccess) return e;
+  if ((e = set_cluster_nonportable(reinterpret_cast<const void*>(fn))) != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(Cu);
@@ -1078,11 +1070,7 @@ cudaError_t qr_factor_grid(cudaStream_t st, cplx* A, long long lda, int m, int n
   constexpr int NB = 4;
   auto fn = qrc3_factor_kernel<256, NB, true>;
   cudaError_t e;
-  static bool attr = false;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) != cudaSuccess) return e;
-    attr = true;
-  }
+  if ((e = set_smem_attr(reinterpret_cast<const void*>(fn), 200 * 1024)) != cudaSuccess) return e;
   // smallest band width whose shared memory fits and whose CTAs are co-resident
   int cw = std::max(1, (n + g_num_sms - 1) / g_num_sms);
   const size_t per_col = (size_t)m * sizeof(cplx);

@@ -1049,13 +1049,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
       fn = bw == 4 ? (void*)svd_coop_smem_kernel<4> : (void*)svd_coop_smem_kernel<8>;
       nth = 256;
       dsm = (size_t)rows * 2 * bw * sizeof(cplx);
-      static size_t configured[2] = {0, 0};
-      size_t& cf = configured[bw == 4 ? 0 : 1];
-      if (dsm > cf) {
-        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024)) != cudaSuccess)
-          return e;
-        cf = 210 * 1024;
-      }
+      if ((e = set_smem_attr(fn, 210 * 1024)) != cudaSuccess) return e;
     } else {
       fn = bw == 4 ? (void*)svd_coop_kernel<4> : (void*)svd_coop_kernel<8>;
       nth = NTH;

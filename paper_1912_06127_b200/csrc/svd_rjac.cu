@@ -919,11 +919,7 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
   cfg.numAttrs = 1;
   if (cluster) {
     v = rj_variant(row, true);
-    static bool attr_set[kNTab] = {false};
-    if (!attr_set[row]) {
-      if ((e = cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
-      attr_set[row] = true;
-    }
+    if ((e = set_cluster_nonportable(v.fn)) != cudaSuccess) return e;
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, v.fn, &cfg) != cudaSuccess || ncl < 1) {
       cudaGetLastError();

@@ -129,12 +129,27 @@ cudaError_t set_smem_attr(const void* fn, int bytes) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  // lock-free fast path: a small per-thread cache of (device, kernel) -> bytes already opted in
+  struct Ent { int dev; const void* fn; int bytes; };
+  static thread_local Ent cache[32];
+  static thread_local int ncache = 0;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].fn == fn && cache[i].dev == dev && cache[i].bytes >= bytes) return cudaSuccess;
   std::lock_guard<std::mutex> lk(mu);
+  auto remember = [&](int b) {
+    if (ncache < 32) cache[ncache++] = Ent{dev, fn, b};
+  };
   auto key = std::make_pair(dev, fn);
   auto it = done.find(key);
-  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  if (it != done.end() && it->second >= bytes) {
+    remember(it->second);
+    return cudaSuccess;
+  }
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done[key] = bytes;
+  if (e == cudaSuccess) {
+    done[key] = bytes;
+    remember(bytes);
+  }
   return e;
 }
 

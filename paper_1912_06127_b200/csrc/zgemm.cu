@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <atomic>
+
 namespace {
 
 constexpr int BK = 8, STAGES = 4, NT = 128;
@@ -231,13 +233,16 @@ constexpr size_t smem_bytes() {
 
 template <int OPA, int OPB, int BM, int BN>
 cudaError_t launch_t(const GemmArgs& g, dim3 grid, cudaStream_t st) {
-  static bool configured = false;
+  // opt-in once per device (lock-free fast path: one bit per device)
+  static std::atomic<unsigned long long> dev_mask{0};
   constexpr size_t sm = smem_bytes<OPA, OPB, BM, BN>();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<OPA, OPB, BM, BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(dev_mask.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(zgemm_dmma_kernel<OPA, OPB, BM, BN>), (int)sm);
     if (e != cudaSuccess) return e;
-    configured = true;
+    dev_mask.fetch_or(bit, std::memory_order_acq_rel);
   }
   zgemm_dmma_kernel<OPA, OPB, BM, BN><<<grid, NT, sm, st>>>(g);
   return cudaGetLastError();

@@ -18,6 +18,19 @@ TDVP_ERRORS = {-1: "bad argument", -2: "non-finite input", -3: "invalid partitio
                -5: "numerical failure", -6: "call order"}
 
 
+def _check_cuda(dev):
+    """Make `dev` the current CUDA device of this thread (the handle is created
+    on the current device) through the CUDA runtime libtdvp links."""
+    lib()  # libtdvp first: the CUDA runtime it links is the one resolved below
+    rt = C.CDLL("libcudart.so.12") if _cudart[0] is None else _cudart[0]
+    _cudart[0] = rt
+    if rt.cudaSetDevice(int(dev)) != 0:
+        raise TdvpError(-4, f"cudaSetDevice({dev}) failed")
+
+
+_cudart = [None]
+
+
 class TdvpError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libtdvp error {code} ({TDVP_ERRORS.get(code, '?')}): {msg}")
@@ -26,7 +39,8 @@ class TdvpError(RuntimeError):
 
 class tdvp_params(C.Structure):
     _fields_ = [("eps", C.c_double), ("w_max", C.c_double), ("krylov_k", C.c_int), ("krylov_tol", C.c_double),
-                ("multiplet_delta", C.c_double), ("timing", C.c_int)]
+                ("multiplet_delta", C.c_double), ("timing", C.c_int), ("n_devices", C.c_int),
+                ("device_ids", C.POINTER(C.c_int))]
 
 
 class tdvp_stats(C.Structure):
@@ -63,6 +77,7 @@ _SIGS = {
     "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_norm": (C.c_int, [C.c_void_p, _D]),
     "tdvp_overlap": (C.c_int, [C.c_void_p, C.c_void_p, _D, _D]),
+    "tdvp_infidelity": (C.c_int, [C.c_void_p, C.c_void_p, _D]),
     "tdvp_set_partition": (C.c_int, [C.c_void_p, C.c_int, _I]),
     "tdvp_partition_balanced": (C.c_int, [C.c_int, C.c_int, _I, _I, _I]),
     "tdvp_reorthonormalize": (C.c_int, [C.c_void_p]),
@@ -119,12 +134,17 @@ class Tdvp:
     """Handle over one libtdvp context (one device, or one rank)."""
 
     def __init__(self, L, d, D_mpo, chi_max, devices=None):
+        """devices: CUDA device ids for a multi-device handle (tdvp_params.n_devices /
+        device_ids; the handle is created on devices[0], segment q of a p-segment
+        step runs on devices[q * len(devices) // p])."""
         self.L, self.d = L, d
+        self.devices = [int(x) for x in devices] if devices else []
         h = C.c_void_p()
+        if self.devices:
+            _check_cuda(self.devices[0])
         _check(lib().tdvp_create(L, d, D_mpo, chi_max, C.byref(h)))
         self.h = h
-        if devices is not None and len(devices) > 1:
-            raise NotImplementedError("multi-device handle")
+        self.set_params()
 
     def close(self):
         if getattr(self, "h", None):
@@ -134,7 +154,10 @@ class Tdvp:
     __del__ = close
 
     def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False, krylov_tol=0.0):
-        p = tdvp_params(eps, w_max, krylov_k, krylov_tol, multiplet_delta, int(bool(timing)))
+        nd = len(self.devices)
+        ids = (C.c_int * max(1, nd))(*(self.devices or [0]))
+        p = tdvp_params(eps, w_max, krylov_k, krylov_tol, multiplet_delta, int(bool(timing)), nd if nd > 1 else 1,
+                        ids)
         _check(lib().tdvp_set_params(self.h, C.byref(p)), self.h)
 
     def set_mpo(self, W):
@@ -176,8 +199,10 @@ class Tdvp:
         return complex(re.value, im.value)
 
     def infidelity(self, other):
-        """I = 1 - |<a|b>| / sqrt(<a|a><b|b>) (PAPER.md benchmark section)."""
-        return 1.0 - abs(self.overlap(other)) / np.sqrt(self.measure_norm() * other.measure_norm())
+        """I = 1 - |<a|b>| / sqrt(<a|a><b|b>) (PAPER.md benchmark section; tdvp_infidelity)."""
+        out = C.c_double()
+        _check(lib().tdvp_infidelity(self.h, other.h, C.byref(out)), self.h)
+        return out.value
 
     def reorthonormalize(self):
         """Exact re-gauging into inverse-canonical form (tdvp_reorthonormalize)."""

@@ -1,0 +1,115 @@
+"""GPU: one handle driving several devices (tdvp_params.n_devices / device_ids,
+SURVEY §8(b) "one process drives devices 0..p-1", §8(e); PAPER.md:470 one
+segment per processor, :484 boundary messages) against the oracle run with the
+same segment partition.
+
+This round's GPU box has ONE B200, so the multi-device code path is exercised
+with repeated device ids ([0, 0], [0, 0, 0, 0]): every segment gets its own
+lane context with its own copy of the MPO tables, staging buffers live on the
+receiver's device and cross via cudaMemcpyPeerAsync, measurements and get_mps
+gather onto device_ids[0] -- the same code that runs with distinct ids.  The
+distinct-device test runs when a node has >= 2 GPUs.
+"""
+import numpy as np
+import pytest
+
+import tdvp_inputs as ti
+from oracle import tdvp as O
+
+from _parity import check_spectra
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1912_06127_b200 as pkg
+    return pkg
+
+
+def run(B, devices, mps, W, chi_max, eps, dt, steps, p):
+    D = max(max(w.shape[0], w.shape[3]) for w in W)
+    t = B.Tdvp(len(W), 2, D, chi_max, devices=devices)
+    t.set_params(eps=eps)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    st = O.init_state(mps, W, O.Params(chi_max=chi_max, eps=eps), p)
+    trunc = False
+    for _ in range(steps):
+        t.step(dt, p)
+        O.step(st, dt)
+        trunc = trunc or st.stats.trunc_active
+    m = O.measure(st)
+    tol = 1e-6 if trunc else 1e-9
+    err = max(np.abs(t.measure_sz() - m["sz"]).max(), abs(t.measure_energy() - m["energy"]),
+              abs(t.measure_norm() - m["norm"]))
+    assert err < tol, (devices, p, err)
+    _, glam = t.get_mps()
+    _, olam = O.global_mps(st)
+    for a, b in zip(glam, olam):
+        check_spectra(a, b, eps, tol)
+    assert t.chi() == O.chi_profile(st) or trunc
+    return t, st
+
+
+@pytest.mark.parametrize("ndev,p", [(2, 2), (2, 4), (4, 4), (2, 8)])
+def test_multidevice_neel_untruncated(B, ndev, p):
+    L = 16
+    t, _ = run(B, [0] * ndev, ti.neel_mps(L), ti.mpo_xxz_nn(L, 0.7), 64, 1e-12, 0.05, 4, p)
+    t.close()
+
+
+def test_multidevice_truncated_and_overlap(B):
+    """Saturated random state, chi_max binding, p = 4 over 2 device slots; the
+    overlap of the multi-device handle with a single-device run of the same
+    protocol is 1 to rounding (same partition, same arithmetic)."""
+    L = 16
+    mps = ti.random_canonical_mps(L, 24, seed=7)
+    W = ti.mpo_xxz_nn(L, 1.0)
+    t, _ = run(B, [0, 0], mps, W, 24, 1e-10, 0.05, 2, 4)
+    s = B.Tdvp(L, 2, 5, 24)
+    s.set_params(eps=1e-10)
+    s.set_mpo(W)
+    s.set_mps(mps.psi, mps.lam)
+    for _ in range(2):
+        s.step(0.05, 4)
+    assert abs(t.infidelity(s)) < 1e-12
+    t.close()
+    s.close()
+
+
+def test_multidevice_relayout_keeps_state(B):
+    """Changing the segment count (and so the device map) mid-run keeps the state."""
+    L = 12
+    W = ti.mpo_xxz_nn(L, 0.5)
+    mps = ti.neel_mps(L)
+    t = B.Tdvp(L, 2, 5, 64, devices=[0, 0])
+    t.set_params(eps=1e-12)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    st = O.init_state(mps, W, O.Params(chi_max=64, eps=1e-12), 2)
+    for _ in range(2):
+        t.step(0.05, 2)
+        O.step(st, 0.05)
+    psi, lam = O.global_mps(st)
+    st4 = O.init_state(ti.MPS(psi, lam), W, O.Params(chi_max=64, eps=1e-12), 4)
+    for _ in range(2):
+        t.step(0.05, 4)
+        O.step(st4, 0.05)
+    m = O.measure(st4)
+    assert np.abs(t.measure_sz() - m["sz"]).max() < 1e-9
+    t.close()
+
+
+def test_multidevice_distinct_gpus(B):
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    L = 16
+    for p in (2, 4):
+        t, _ = run(B, list(range(min(n, p))), ti.neel_mps(L), ti.mpo_xxz_nn(L, 0.7), 64, 1e-12, 0.05, 3, p)
+        t.close()
