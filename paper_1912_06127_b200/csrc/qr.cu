@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
   __shared__ double s_red[8];
   __shared__ cplx s_scale;
   __shared__ int s_refl;
+  __shared__ double s_pn[16];       // partial norms of all CTAs
+  __shared__ cplx s_al;
+  __shared__ cplx s_pw[QPW][16];    // partial dots of all CTAs
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int rows = m - k0;
   const int r0 = crank * rc;                       // first panel row of this CTA
@@ -195,11 +198,14 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
       }
     }
     cluster.sync();
+    // the C partial norms fetched in parallel (one DSMEM round trip), summed in rank order
+    if (tid < C) s_pn[tid] = *cluster.map_shared_rank(&s_nrm[0], tid);
+    if (tid == 32) s_al = *cluster.map_shared_rank(&s_alpha, pr / rc);
+    __syncthreads();
     if (tid == 0) {
       double xn2 = 0.0;
-      for (int c = 0; c < C; ++c) xn2 += *cluster.map_shared_rank(&s_nrm[0], c);
-      const int owner = pr / rc;
-      const cplx al = *cluster.map_shared_rank(&s_alpha, owner);
+      for (int c = 0; c < C; ++c) xn2 += s_pn[c];
+      const cplx al = s_al;
       const double ar = al.x, ai = al.y;
       cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
       double beta = ar;
@@ -242,9 +248,15 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
     }
     __syncthreads();
     cluster.sync();
+    // kb x C partial dots fetched in parallel, then summed per column in rank order
+    for (int e = tid; e < kb * C; e += QPNT) {
+      const int j = e / C, c = e - j * C;
+      if (j != i) s_pw[j][c] = *cluster.map_shared_rank(&s_w[j], c);
+    }
+    __syncthreads();
     if (tid < kb && tid != i) {
       cplx t = cmk(0.0, 0.0);
-      for (int c = 0; c < C; ++c) t = cadd(t, *cluster.map_shared_rank(&s_w[tid], c));
+      for (int c = 0; c < C; ++c) t = cadd(t, s_pw[tid][c]);
       s_wt[tid] = t;
       if (crank == 0 && tid < i) s_z[tid][i] = t;
     }
@@ -327,7 +339,7 @@ cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, 
       qr_panel_kernel<32, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
     } else {
       // cluster panel: C CTAs of rc rows each (rc * kb * 16 B of shared memory)
-      const int C = rows <= 512 ? 4 : rows <= 1024 ? 8 : 16;
+      const int C = rows <= 1024 ? 4 : rows <= 2048 ? 8 : 16;
       const int rc = (rows + C - 1) / C;
       const size_t smem = (size_t)rc * kb * sizeof(cplx);
       if ((e = set_smem_attr(reinterpret_cast<const void*>(qr_panel_cl_kernel), (int)std::max<size_t>(smem, 48 * 1024))) !=
