@@ -62,6 +62,14 @@ typedef struct {
    * tdvp_get_params returns the handle's copy. */
   int n_devices;
   const int* device_ids;
+  /* Dynamic load balancing ("dynamic load balancer",
+   * :237 load imbalance limits the scaling): 0 = off (default); in (0, 1):
+   * before every tdvp_step with n_segments = p > 1 the chi-weighted min-max
+   * partition (tdvp_partition_balanced of the current bond dimensions) replaces
+   * the current one when its largest segment cost is below (1 - rebalance) x
+   * the current partition's.  The state is kept; the environments are rebuilt
+   * (the sequential section).  Single-process handles only. */
+  double rebalance;
 } tdvp_params;
 
 typedef struct {
@@ -93,6 +101,7 @@ typedef struct {
   /* algorithmic HBM bytes of the Lanczos vector passes of the last step (timing=1;
    * their time is lanczos2_ms + lanczos1_ms - heff2_ms - heff1_ms) */
   double lz_vec_bytes;
+  int rebalances;         /* cumulative dynamic re-partitionings (tdvp_params.rebalance) */
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension
@@ -191,6 +200,9 @@ int tdvp_partition(int L, int p, int* s, int* e);
  * index on ties).  Writes s[p], e[p]. */
 int tdvp_set_partition(tdvp_t h, int p, const int* s);
 int tdvp_partition_balanced(int L, int p, const int* chi, int* s, int* e);
+/* The partition the handle's segments currently use: *p segments, segment q
+ * = sites [s[q], e[q]] (caller arrays of >= *p entries; NULL s/e: count only). */
+int tdvp_get_partition(tdvp_t h, int* p, int* s, int* e);
 
 /* ---- kernel-level entry points (host buffers; copies inside) -------------
  * For parity tests of the individual contractions against the oracle.

@@ -1325,9 +1325,40 @@ void finish_timing(tdvp_ctx* h) {
   h->stats.env_ms = sum(h->ev_env);
 }
 
+int balanced_partition(int L, int p, const int* chi, int* s, int* e, double* best);
+double partition_cost(int L, const int* chi, const std::vector<std::pair<int, int>>& bounds);
+void reorthonormalize(tdvp_ctx* h);
+
 void do_step(tdvp_ctx* h, double dt, int p) {
   if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step");
   if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
+  // dynamic load balancing ("dynamic load balancer"):
+  // before the step, re-partition when the chi-weighted optimum beats the
+  // current partition's largest segment cost by the relative margin
+  // prm.rebalance (state kept; the environments are rebuilt, a serial section)
+  if (h->prm.rebalance > 0.0 && p > 1 && local_mode(h) && h->layout_p == p && h->envs_valid) {
+    std::vector<int> chi(h->L + 1, 1), ss(p), ee(p);
+    for (int b = 0; b < h->L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];
+    double best = 0.0;
+    if (balanced_partition(h->L, p, chi.data(), ss.data(), ee.data(), &best) == TDVP_OK) {
+      const double cur = partition_cost(h->L, chi.data(), h->bounds);
+      if (best < (1.0 - h->prm.rebalance) * cur) {
+        std::vector<std::pair<int, int>> nb(p);
+        for (int q = 0; q < p; ++q) nb[q] = {ss[q], ee[q]};
+        if (nb != h->bounds) {
+          // Moving a boundary turns a gauge-broken boundary bond (both sides
+          // evolved independently) into an interior bond whose
+          // next merge Psi_b V_b Psi_{b+1} would amplify the mismatch by
+          // V = 1/Lambda: re-gauge the state exactly first
+          // (reorthonormalisation), then lay it out anew.
+          reorthonormalize(h);
+          h->custom = nb;
+          h->envs_valid = false;
+          h->stats.rebalances++;
+        }
+      }
+    }
+  }
   if (p != h->layout_p || !h->envs_valid) layout(h, p);
   reset_step_stats(h);
   h->evolved = true;
@@ -1518,6 +1549,167 @@ void alloc_workspace(tdvp_ctx* h) {
                  svd_bjac_work_elems(g_num_sms)};
 }
 
+// chi-weighted min-max contiguous partition:
+// exact DP, smallest split index on ties; *best = its largest segment cost
+int balanced_partition(int L, int p, const int* chi, int* s, int* e, double* best) {
+  if (p == 1) {
+    s[0] = 0;
+    e[0] = L - 1;
+    return TDVP_OK;
+  }
+  if (p < 2 || p % 2 != 0 || p > L / 2) return TDVP_EPARTITION;
+  // site cost ~ the one-site update / half a pair update: chi_j chi_{j+1} (chi_j + chi_{j+1})
+  std::vector<double> pre(L + 1, 0.0);
+  for (int j = 0; j < L; ++j) {
+    const double a = chi[j], b = chi[j + 1];
+    if (!(a >= 1.0) || !(b >= 1.0)) return TDVP_EARG;
+    pre[j + 1] = pre[j] + a * b * (a + b);
+  }
+  // f[q][i]: min over partitions of sites [0, i) into q segments (each >= 2) of the max segment cost
+  const double INF = 1e300;
+  std::vector<std::vector<double>> f(p + 1, std::vector<double>(L + 1, INF));
+  std::vector<std::vector<int>> arg(p + 1, std::vector<int>(L + 1, -1));
+  f[0][0] = 0.0;
+  for (int q = 1; q <= p; ++q)
+    for (int i = 2 * q; i <= L - 2 * (p - q); ++i)
+      for (int k = 2 * (q - 1); k <= i - 2; ++k) {
+        if (f[q - 1][k] >= INF) continue;
+        const double v = std::max(f[q - 1][k], pre[i] - pre[k]);
+        if (v < f[q][i]) {
+          f[q][i] = v;
+          arg[q][i] = k;
+        }
+      }
+  if (f[p][L] >= INF) return TDVP_EPARTITION;
+  if (best) *best = f[p][L];
+  for (int q = p, i = L; q >= 1; --q) {
+    const int k = arg[q][i];
+    s[q - 1] = k;
+    e[q - 1] = i - 1;
+    i = k;
+  }
+  return TDVP_OK;
+}
+
+// largest segment cost of the contiguous partition `bounds` (site cost as above)
+double partition_cost(int L, const int* chi, const std::vector<std::pair<int, int>>& bounds) {
+  double worst = 0.0;
+  for (const auto& sg : bounds) {
+    double c = 0.0;
+    for (int j = sg.first; j <= sg.second && j < L; ++j) {
+      const double a = chi[j], b = chi[j + 1];
+      c += a * b * (a + b);
+    }
+    worst = std::max(worst, c);
+  }
+  return worst;
+}
+
+// chain tensors M_j = Psi_j diag(V_j) (j < L-1), M_{L-1} = Psi_{L-1} of a local-mode handle
+std::vector<BufPtr> chain_tensors(tdvp_ctx* h, std::vector<int>& chi) {
+  const int L = h->L, d = h->d;
+  if (h->layout_p == 0) layout(h, 1);
+  chi.assign(L + 1, 1);
+  for (int j = 1; j < L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
+  std::vector<BufPtr> M(L);
+  CK(cudaStreamSynchronize(h->st));
+  BufPtr tv = make_buf((size_t)h->chi_max * sizeof(double) + 64);
+  for (int j = 0; j < L; ++j) {
+    Segment& g = h->segs[owner_of(h, j)];
+    const long long n = (long long)chi[j] * d * chi[j + 1];
+    M[j] = make_buf(n * sizeof(cplx));
+    // a multi-device handle gathers the chain onto the lead device (NVLink peer copies)
+    d2d(M[j]->p, h->dev, g.psi[j]->p, g.dev, (size_t)n * sizeof(cplx), h->st);
+    if (j < L - 1) {
+      d2d(tv->p, h->dev, g.vinv[j]->p, g.dev, (size_t)chi[j + 1] * sizeof(double), h->st);
+      CK(scale_cols(h->st, M[j]->c(), M[j]->c(), tv->d(), (long long)chi[j] * d, chi[j + 1]));
+      CK(cudaStreamSynchronize(h->st));  // tv is reused
+    }
+  }
+  return M;
+}
+
+void reorthonormalize(tdvp_ctx* h) {
+  {
+    if (!h->have_mps || !h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set");
+    if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "reorthonormalisation across ranks: gather the MPS first");
+    const int L = h->L, d = h->d;
+    std::vector<int> chi;
+    std::vector<BufPtr> A = chain_tensors(h, chi);
+    long long big = 1;
+    for (int j = 0; j < L; ++j) big = std::max(big, (long long)h->cbmax[j] * d * h->cbmax[j + 1]);
+    BufPtr pl = make_buf(big * sizeof(cplx)), pr = make_buf(big * sizeof(cplx)), tmp = make_buf(big * sizeof(cplx));
+    BufPtr lam = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
+    BufPtr vin = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
+    std::vector<std::vector<double>> hlam(L - 1);
+    const TruncParams tp{h->chi_max, 0.0, 0.0, 0.0};
+    auto svd = [&](const cplx* M, int m, int n, int& k) {
+      int r = 0, ce = 0, sw = 0;
+      double w = 0.0;
+      cudaError_t se = svd_truncate_split(h->st, h->sv, M, m, n, tp, pl->c(), pr->c(), lam->d(), vin->d(), &k, &w, &r,
+                                          &ce, &sw);
+      if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "SVD numerical failure in reorthonormalisation");
+      CK(se);
+    };
+    // L -> R: A_j = U S W^dagger  ->  A_j = U,  A_{j+1} = (S W^dagger) A_{j+1}
+    for (int j = 0; j + 1 < L; ++j) {
+      int k = 0;
+      svd(A[j]->c(), chi[j] * d, chi[j + 1], k);
+      if (k > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: reorthonormalisation rank");
+      BufPtr U = make_buf((size_t)chi[j] * d * k * sizeof(cplx));
+      CK(scale_cols(h->st, U->c(), pl->c(), vin->d(), (long long)chi[j] * d, k));
+      gemm(h, OP_N, OP_N, k, d * chi[j + 2], chi[j + 1], pr->c(), chi[j + 1], A[j + 1]->c(), (long long)d * chi[j + 2],
+           tmp->c(), (long long)d * chi[j + 2]);
+      BufPtr An = make_buf((size_t)k * d * chi[j + 2] * sizeof(cplx));
+      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)k * d * chi[j + 2]));
+      A[j] = std::move(U);
+      A[j + 1] = std::move(An);
+      chi[j + 1] = k;
+    }
+    // R -> L: A_j = U S W^dagger  ->  B_j = W^dagger, Lambda_{j-1} = S, A_{j-1} = A_{j-1} (U S)
+    for (int j = L - 1; j >= 1; --j) {
+      int k = 0;
+      svd(A[j]->c(), chi[j], d * chi[j + 1], k);
+      BufPtr B = make_buf((size_t)k * d * chi[j + 1] * sizeof(cplx));
+      CK(scale_rows(h->st, B->c(), pr->c(), vin->d(), k, (long long)d * chi[j + 1]));
+      gemm(h, OP_N, OP_N, chi[j - 1] * d, k, chi[j], A[j - 1]->c(), chi[j], pl->c(), k, tmp->c(), k);
+      BufPtr An = make_buf((size_t)chi[j - 1] * d * k * sizeof(cplx));
+      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)chi[j - 1] * d * k));
+      hlam[j - 1].resize(k);
+      CK(cudaMemcpyAsync(hlam[j - 1].data(), lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      A[j] = std::move(B);
+      A[j - 1] = std::move(An);
+      chi[j] = k;
+    }
+    // download, normalise, Psi_0 = A_0 / n, Lambda /= n, Psi_j = Lambda_{j-1} B_j
+    std::vector<std::vector<double>> hpsi(L);
+    for (int j = 0; j < L; ++j) {
+      hpsi[j].resize((size_t)chi[j] * d * chi[j + 1] * 2);
+      CK(cudaMemcpyAsync(hpsi[j].data(), A[j]->p, hpsi[j].size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    double nrm = 0.0;
+    for (double v : hpsi[0]) nrm += v * v;
+    nrm = std::sqrt(nrm);
+    if (!(nrm > 0.0) || !std::isfinite(nrm)) throw TdvpError(TDVP_ENUMERIC, "zero or non-finite norm");
+    for (double& v : hpsi[0]) v /= nrm;
+    for (auto& l : hlam)
+      for (double& v : l) v /= nrm;
+    for (int j = 1; j < L; ++j) {
+      const int cl = chi[j], rest = d * chi[j + 1];
+      for (int a = 0; a < cl; ++a)
+        for (int e = 0; e < 2 * rest; ++e) hpsi[j][(size_t)a * 2 * rest + e] *= hlam[j - 1][a];
+    }
+    h->h_psi = std::move(hpsi);
+    h->h_lam = std::move(hlam);
+    h->h_chi = chi;
+    h->envs_valid = false;
+    h->layout_p = 0;  // re-layout: upload + sequential environment build at the next call
+  }
+}
+
+
 int fail(tdvp_ctx* h, const TdvpError& e) {
   if (h) h->err = e.what();
   return e.code;
@@ -1627,7 +1819,8 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
 int tdvp_set_params(tdvp_t h, const tdvp_params* p) {
   if (!h || !p) return TDVP_EARG;
   if (p->krylov_k < 1 || p->krylov_k >= KMAX || !(p->eps >= 0.0) || p->eps >= 1.0 || !(p->w_max >= 0.0) ||
-      !(p->multiplet_delta >= 0.0) || !(p->krylov_tol >= 0.0) || p->krylov_tol >= 1.0) {
+      !(p->multiplet_delta >= 0.0) || !(p->krylov_tol >= 0.0) || p->krylov_tol >= 1.0 || !(p->rebalance >= 0.0) ||
+      p->rebalance >= 1.0) {
     h->err = "invalid params (krylov_k in 1..15, 0 <= eps < 1, w_max >= 0, 0 <= krylov_tol < 1)";
     return TDVP_EARG;
   }
@@ -1803,29 +1996,6 @@ int tdvp_measure_norm(tdvp_t h, double* n) {
   return TDVP_OK;
 }
 
-// chain tensors M_j = Psi_j diag(V_j) (j < L-1), M_{L-1} = Psi_{L-1} of a local-mode handle
-static std::vector<BufPtr> chain_tensors(tdvp_ctx* h, std::vector<int>& chi) {
-  const int L = h->L, d = h->d;
-  if (h->layout_p == 0) layout(h, 1);
-  chi.assign(L + 1, 1);
-  for (int j = 1; j < L; ++j) chi[j] = h->segs[owner_of(h, j - 1)].cb[j];
-  std::vector<BufPtr> M(L);
-  CK(cudaStreamSynchronize(h->st));
-  BufPtr tv = make_buf((size_t)h->chi_max * sizeof(double) + 64);
-  for (int j = 0; j < L; ++j) {
-    Segment& g = h->segs[owner_of(h, j)];
-    const long long n = (long long)chi[j] * d * chi[j + 1];
-    M[j] = make_buf(n * sizeof(cplx));
-    // a multi-device handle gathers the chain onto the lead device (NVLink peer copies)
-    d2d(M[j]->p, h->dev, g.psi[j]->p, g.dev, (size_t)n * sizeof(cplx), h->st);
-    if (j < L - 1) {
-      d2d(tv->p, h->dev, g.vinv[j]->p, g.dev, (size_t)chi[j + 1] * sizeof(double), h->st);
-      CK(scale_cols(h->st, M[j]->c(), M[j]->c(), tv->d(), (long long)chi[j] * d, chi[j + 1]));
-      CK(cudaStreamSynchronize(h->st));  // tv is reused
-    }
-  }
-  return M;
-}
 
 // <psi_a | psi_b> by a two-state zipper (PAPER.md Sec. benchmarks, infidelity
 // I = 1 - |<1|2>| / sqrt(<1|1><2|2>)): E_{j+1} = M1_j^H (E_j M2_j)
@@ -1895,81 +2065,7 @@ int tdvp_infidelity(tdvp_t a, tdvp_t b, double* inf) {
 int tdvp_reorthonormalize(tdvp_t h) {
   if (!h) return TDVP_EARG;
   try {
-    if (!h->have_mps || !h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set");
-    if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "reorthonormalisation across ranks: gather the MPS first");
-    const int L = h->L, d = h->d;
-    std::vector<int> chi;
-    std::vector<BufPtr> A = chain_tensors(h, chi);
-    long long big = 1;
-    for (int j = 0; j < L; ++j) big = std::max(big, (long long)h->cbmax[j] * d * h->cbmax[j + 1]);
-    BufPtr pl = make_buf(big * sizeof(cplx)), pr = make_buf(big * sizeof(cplx)), tmp = make_buf(big * sizeof(cplx));
-    BufPtr lam = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
-    BufPtr vin = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
-    std::vector<std::vector<double>> hlam(L - 1);
-    const TruncParams tp{h->chi_max, 0.0, 0.0, 0.0};
-    auto svd = [&](const cplx* M, int m, int n, int& k) {
-      int r = 0, ce = 0, sw = 0;
-      double w = 0.0;
-      cudaError_t se = svd_truncate_split(h->st, h->sv, M, m, n, tp, pl->c(), pr->c(), lam->d(), vin->d(), &k, &w, &r,
-                                          &ce, &sw);
-      if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "SVD numerical failure in reorthonormalisation");
-      CK(se);
-    };
-    // L -> R: A_j = U S W^dagger  ->  A_j = U,  A_{j+1} = (S W^dagger) A_{j+1}
-    for (int j = 0; j + 1 < L; ++j) {
-      int k = 0;
-      svd(A[j]->c(), chi[j] * d, chi[j + 1], k);
-      if (k > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: reorthonormalisation rank");
-      BufPtr U = make_buf((size_t)chi[j] * d * k * sizeof(cplx));
-      CK(scale_cols(h->st, U->c(), pl->c(), vin->d(), (long long)chi[j] * d, k));
-      gemm(h, OP_N, OP_N, k, d * chi[j + 2], chi[j + 1], pr->c(), chi[j + 1], A[j + 1]->c(), (long long)d * chi[j + 2],
-           tmp->c(), (long long)d * chi[j + 2]);
-      BufPtr An = make_buf((size_t)k * d * chi[j + 2] * sizeof(cplx));
-      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)k * d * chi[j + 2]));
-      A[j] = std::move(U);
-      A[j + 1] = std::move(An);
-      chi[j + 1] = k;
-    }
-    // R -> L: A_j = U S W^dagger  ->  B_j = W^dagger, Lambda_{j-1} = S, A_{j-1} = A_{j-1} (U S)
-    for (int j = L - 1; j >= 1; --j) {
-      int k = 0;
-      svd(A[j]->c(), chi[j], d * chi[j + 1], k);
-      BufPtr B = make_buf((size_t)k * d * chi[j + 1] * sizeof(cplx));
-      CK(scale_rows(h->st, B->c(), pr->c(), vin->d(), k, (long long)d * chi[j + 1]));
-      gemm(h, OP_N, OP_N, chi[j - 1] * d, k, chi[j], A[j - 1]->c(), chi[j], pl->c(), k, tmp->c(), k);
-      BufPtr An = make_buf((size_t)chi[j - 1] * d * k * sizeof(cplx));
-      CK(copy_cplx(h->st, An->c(), tmp->c(), (long long)chi[j - 1] * d * k));
-      hlam[j - 1].resize(k);
-      CK(cudaMemcpyAsync(hlam[j - 1].data(), lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-      CK(cudaStreamSynchronize(h->st));
-      A[j] = std::move(B);
-      A[j - 1] = std::move(An);
-      chi[j] = k;
-    }
-    // download, normalise, Psi_0 = A_0 / n, Lambda /= n, Psi_j = Lambda_{j-1} B_j
-    std::vector<std::vector<double>> hpsi(L);
-    for (int j = 0; j < L; ++j) {
-      hpsi[j].resize((size_t)chi[j] * d * chi[j + 1] * 2);
-      CK(cudaMemcpyAsync(hpsi[j].data(), A[j]->p, hpsi[j].size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    }
-    CK(cudaStreamSynchronize(h->st));
-    double nrm = 0.0;
-    for (double v : hpsi[0]) nrm += v * v;
-    nrm = std::sqrt(nrm);
-    if (!(nrm > 0.0) || !std::isfinite(nrm)) throw TdvpError(TDVP_ENUMERIC, "zero or non-finite norm");
-    for (double& v : hpsi[0]) v /= nrm;
-    for (auto& l : hlam)
-      for (double& v : l) v /= nrm;
-    for (int j = 1; j < L; ++j) {
-      const int cl = chi[j], rest = d * chi[j + 1];
-      for (int a = 0; a < cl; ++a)
-        for (int e = 0; e < 2 * rest; ++e) hpsi[j][(size_t)a * 2 * rest + e] *= hlam[j - 1][a];
-    }
-    h->h_psi = std::move(hpsi);
-    h->h_lam = std::move(hlam);
-    h->h_chi = chi;
-    h->envs_valid = false;
-    h->layout_p = 0;  // re-layout: upload + sequential environment build at the next call
+    reorthonormalize(h);
   } catch (const TdvpError& e) {
     return fail(h, e);
   }
@@ -2109,41 +2205,17 @@ int tdvp_set_partition(tdvp_t h, int p, const int* s) {
 
 int tdvp_partition_balanced(int L, int p, const int* chi, int* s, int* e) {
   if (L < 2 || !chi || !s || !e) return TDVP_EARG;
-  if (p == 1) {
-    s[0] = 0;
-    e[0] = L - 1;
-    return TDVP_OK;
-  }
-  if (p < 2 || p % 2 != 0 || p > L / 2) return TDVP_EPARTITION;
-  // site cost ~ the one-site update / half a pair update: chi_j chi_{j+1} (chi_j + chi_{j+1})
-  std::vector<double> pre(L + 1, 0.0);
-  for (int j = 0; j < L; ++j) {
-    const double a = chi[j], b = chi[j + 1];
-    if (!(a >= 1.0) || !(b >= 1.0)) return TDVP_EARG;
-    pre[j + 1] = pre[j] + a * b * (a + b);
-  }
-  // f[q][i]: min over partitions of sites [0, i) into q segments (each >= 2) of the max segment cost
-  const double INF = 1e300;
-  std::vector<std::vector<double>> f(p + 1, std::vector<double>(L + 1, INF));
-  std::vector<std::vector<int>> arg(p + 1, std::vector<int>(L + 1, -1));
-  f[0][0] = 0.0;
-  for (int q = 1; q <= p; ++q)
-    for (int i = 2 * q; i <= L - 2 * (p - q); ++i)
-      for (int k = 2 * (q - 1); k <= i - 2; ++k) {
-        if (f[q - 1][k] >= INF) continue;
-        const double v = std::max(f[q - 1][k], pre[i] - pre[k]);
-        if (v < f[q][i]) {
-          f[q][i] = v;
-          arg[q][i] = k;
-        }
-      }
-  if (f[p][L] >= INF) return TDVP_EPARTITION;
-  for (int q = p, i = L; q >= 1; --q) {
-    const int k = arg[q][i];
-    s[q - 1] = k;
-    e[q - 1] = i - 1;
-    i = k;
-  }
+  return balanced_partition(L, p, chi, s, e, nullptr);
+}
+
+int tdvp_get_partition(tdvp_t h, int* p, int* s, int* e) {
+  if (!h || !p) return TDVP_EARG;
+  *p = (int)h->bounds.size();
+  if (s && e)
+    for (size_t q = 0; q < h->bounds.size(); ++q) {
+      s[q] = h->bounds[q].first;
+      e[q] = h->bounds[q].second;
+    }
   return TDVP_OK;
 }
 

@@ -40,7 +40,7 @@ class TdvpError(RuntimeError):
 class tdvp_params(C.Structure):
     _fields_ = [("eps", C.c_double), ("w_max", C.c_double), ("krylov_k", C.c_int), ("krylov_tol", C.c_double),
                 ("multiplet_delta", C.c_double), ("timing", C.c_int), ("n_devices", C.c_int),
-                ("device_ids", C.POINTER(C.c_int))]
+                ("device_ids", C.POINTER(C.c_int)), ("rebalance", C.c_double)]
 
 
 class tdvp_stats(C.Structure):
@@ -52,7 +52,7 @@ class tdvp_stats(C.Structure):
                 ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int),
                 ("svd_warm", C.c_int), ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
                 ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
-                ("lz_vec_bytes", C.c_double)]
+                ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int)]
 
     def as_dict(self):
         out = {}
@@ -90,6 +90,7 @@ _SIGS = {
     "tdvp_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
     "tdvp_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, C.c_int]),
     "tdvp_partition": (C.c_int, [C.c_int, C.c_int, _I, _I]),
+    "tdvp_get_partition": (C.c_int, [C.c_void_p, _I, _I, _I]),
     "tdvp_apply_heff2": (C.c_int, [C.c_int] * 6 + [_D] * 6),
     "tdvp_apply_heff1": (C.c_int, [C.c_int] * 5 + [_D] * 5),
     "tdvp_env_left": (C.c_int, [C.c_int] * 5 + [_D] * 4),
@@ -153,11 +154,12 @@ class Tdvp:
 
     __del__ = close
 
-    def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False, krylov_tol=0.0):
+    def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False, krylov_tol=0.0,
+                   rebalance=0.0):
         nd = len(self.devices)
         ids = (C.c_int * max(1, nd))(*(self.devices or [0]))
         p = tdvp_params(eps, w_max, krylov_k, krylov_tol, multiplet_delta, int(bool(timing)), nd if nd > 1 else 1,
-                        ids)
+                        ids, float(rebalance))
         _check(lib().tdvp_set_params(self.h, C.byref(p)), self.h)
 
     def set_mpo(self, W):
@@ -215,6 +217,14 @@ class Tdvp:
             return
         starts = (C.c_int * len(bounds))(*[int(s) for s, _ in bounds])
         _check(lib().tdvp_set_partition(self.h, len(bounds), starts), self.h)
+
+    def partition(self):
+        """The segment bounds [(s, e)] the handle currently uses (tdvp_get_partition)."""
+        n = C.c_int()
+        _check(lib().tdvp_get_partition(self.h, C.byref(n), None, None), self.h)
+        ss, ee = (C.c_int * max(1, n.value))(), (C.c_int * max(1, n.value))()
+        _check(lib().tdvp_get_partition(self.h, C.byref(n), ss, ee), self.h)
+        return [(ss[q], ee[q]) for q in range(n.value)]
 
     def maybe_reorthonormalize(self, tol):
         """Reorthonormalise when the norm error |<psi|psi> - 1| exceeds tol

@@ -113,3 +113,43 @@ def test_multidevice_distinct_gpus(B):
     for p in (2, 4):
         t, _ = run(B, list(range(min(n, p))), ti.neel_mps(L), ti.mpo_xxz_nn(L, 0.7), 64, 1e-12, 0.05, 3, p)
         t.close()
+
+
+def test_dynamic_rebalance_matches_oracle(B):
+    """SURVEY N4 / PAPER.md:245: with tdvp_params.rebalance the library moves
+    the segment bounds toward the chi-weighted optimum as chi grows in the
+    middle of a Neel quench (re-gauging the state first); the oracle, re-gauged
+    and re-laid out with the same partition sequence, gives the same
+    observables.  (Without the re-gauging both blow up: a moved boundary's
+    gauge-broken bond is merged with V = 1/Lambda.)"""
+    L, p, dt = 32, 4, 0.05
+    W = ti.mpo_xxz_nn(L, 0.5)
+    mps = ti.neel_mps(L)
+    t = B.Tdvp(L, 2, 5, 64)
+    t.set_params(eps=1e-12, rebalance=0.05)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    prm = O.Params(chi_max=64, eps=1e-12)
+    st = O.init_state(mps, W, prm, p)
+    bounds, seen = None, []
+    trunc = False
+    for _ in range(8):
+        t.step(dt, p)
+        nb = t.partition()
+        if bounds is not None and nb != bounds:
+            # the library re-gauges before moving a boundary (reorthonormalisation,
+            # PAPER.md:513-519): the exact re-gauging of the same chain here
+            psi, lam = O.global_mps(st)
+            st = O.init_state(ti.canonicalize(O._chain_tensors(psi, lam)), W, prm, p, bounds=nb)
+        elif bounds is None and nb != O.plan_partition(L, p):
+            st = O.init_state(mps, W, prm, p, bounds=nb)
+        bounds = nb
+        seen.append(nb)
+        O.step(st, dt)
+        trunc = trunc or st.stats.trunc_active
+    assert t.stats()["rebalances"] >= 1 and len({tuple(b) for b in seen}) >= 2, seen
+    m = O.measure(st)
+    tol = 1e-6 if trunc else 1e-9
+    assert np.abs(t.measure_sz() - m["sz"]).max() < tol
+    assert abs(t.measure_energy() - m["energy"]) < tol
+    t.close()
