@@ -159,6 +159,21 @@ int tdvp_infidelity(tdvp_t a, tdvp_t b, double* infidelity);
  * Errors: TDVP_ESTATE (no MPO/MPS, distributed), TDVP_ENUMERIC (zero norm). */
 int tdvp_reorthonormalize(tdvp_t h);
 
+/* Two-site DMRG ground-state sweeps on the handle's MPO, starting from its
+ * current MPS (every quench
+ * starts from a DMRG ground state).  A sweep = pairs j = 0..L-2 left->right,
+ * then j = L-3..0 right->left; each pair update merges Theta,
+ * replaces it by the lowest eigenvector of H_eff^(2) from
+ * `restarts` restarted Lanczos runs of tdvp_params.krylov_k vectors, and splits
+ * it with the same truncated SVD as tdvp_step.
+ * energies[s] (optional, n_sweeps entries) = the Ritz value of the last update
+ * of sweep s.  The final state is re-gauged into exactly inverse-canonical
+ * form (as tdvp_reorthonormalize; "important to ensure the
+ * initial state is orthonormal") and stays in the handle: set another MPO with
+ * tdvp_set_mpo and call tdvp_step for a quench.  Serial, one device.
+ * Errors: TDVP_EARG, TDVP_ESTATE (no MPO/MPS, multi-rank), TDVP_ENUMERIC. */
+int tdvp_dmrg(tdvp_t h, int n_sweeps, int restarts, double* energies);
+
 int tdvp_get_stats(tdvp_t h, tdvp_stats* s);
 /* Current bond dimensions (owner view): chi[L+1]. */
 int tdvp_get_chi(tdvp_t h, int* chi);

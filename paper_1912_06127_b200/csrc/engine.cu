@@ -676,6 +676,72 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   if (ee0 >= 0) h->ev_env.emplace_back(ee0, ev_record(h));
 }
 
+// ----------------------------------------------------------- two-site DMRG
+// (SURVEY N3; PAPER.md:100 ARPACK with 8 Krylov vectors, :122, :130, :178 the
+// ground states every quench starts from).  Lowest eigenvector of H_eff^(2)
+// by restarted Lanczos on the device: `restarts` times, the K-vector basis of
+// the fused Lanczos iterations from the current vector, the lowest eigenpair
+// of the tridiagonal (one thread, Jacobi; y_0 >= 0), x <- V y.  Reading
+// R-DMRG in DESIGN.md; the oracle is oracle/dmrg.py.
+void ground_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& matvec, const cplx* x, cplx* out,
+                    long long n, int K, int restarts) {
+  cplx* V = h->krylov->c();
+  cplx* w = h->wvec->c();
+  const cplx* cur = x;
+  for (int r = 0; r < restarts; ++r) {
+    CK(lz_start(h->st, h->lz, cur, V, n));
+    g_launch_count += 2;
+    for (int k = 0; k < K; ++k) {
+      matvec(V + (long long)k * n, w);
+      CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0));
+      g_launch_count++;
+    }
+    CK(lz_tridiag_ground(h->st, h->lz, K));
+    CK(lz_combine(h->st, h->lz, V, n, K, out, n));
+    g_launch_count += 2;
+    cur = out;
+  }
+}
+
+// DMRG pair update of (j, j+1): merge, ground state of H_eff^(2), the same
+// truncated SVD split as the TDVP pair update, environments `build`
+void dmrg_pair(tdvp_ctx* h, Segment& g, int j, int build, int restarts) {
+  const int d = h->d;
+  const int cl = g.cb[j], cm = g.cb[j + 1], cr = g.cb[j + 2];
+  const MpoSite& W1 = h->mpo[j];
+  const MpoSite& W2 = h->mpo[j + 1];
+  cplx* th = h->theta->c();
+  CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), cm, (long long)d * cr));
+  gemm(h, OP_N, OP_N, cl * d, d * cr, cm, P(g.psi[j]), cm, h->tmpA->c(), (long long)d * cr, th, (long long)d * cr);
+  const long long n = (long long)cl * d * d * cr;
+  const cplx* Lenv = P(g.beta[j]);
+  const cplx* Renv = P(g.gamma[j + 1]);
+  cplx* th2 = h->tmpB->c();
+  ground_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, h->prm.krylov_k,
+      restarts);
+  TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
+  int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
+  double w = 0.0;
+  cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
+                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps);
+  if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
+  CK(se);
+  if (chi > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: chi exceeds allocation");
+  g.cb[j + 1] = chi;
+  h->stats.w_step += w;
+  h->stats.n_pair++;
+  if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
+  if (build & BUILD_BETA) {
+    CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
+    env_left(h, P(g.beta[j]), h->tmpA->c(), W1, cl, chi, P(g.beta[j + 1]));
+  }
+  if (build & BUILD_GAMMA) {
+    CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), chi, (long long)d * cr));
+    env_right(h, P(g.gamma[j + 1]), h->tmpA->c(), W2, chi, cr, P(g.gamma[j]));
+  }
+}
+
 // one-site backward update Psi_j <- exp(+i dt/2 H_eff^(1)) Psi_j
 void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   const int d = h->d, cl = g.cb[j], cr = g.cb[j + 1];
@@ -2066,6 +2132,35 @@ int tdvp_reorthonormalize(tdvp_t h) {
   if (!h) return TDVP_EARG;
   try {
     reorthonormalize(h);
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_dmrg(tdvp_t h, int n_sweeps, int restarts, double* energies) {
+  if (!h || n_sweeps < 0 || restarts < 1) return TDVP_EARG;
+  try {
+    if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_dmrg");
+    if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "tdvp_dmrg runs on a single-process handle");
+    const int L = h->L;
+    if (h->layout_p != 1 || !h->envs_valid) layout(h, 1);
+    Segment& g = h->segs[0];
+    reset_step_stats(h);
+    for (int sw = 0; sw < n_sweeps; ++sw) {
+      for (int j = 0; j + 1 < L; ++j) dmrg_pair(h, g, j, BUILD_BETA | (j == L - 2 ? BUILD_GAMMA : 0), restarts);
+      for (int j = L - 3; j >= 0; --j) dmrg_pair(h, g, j, BUILD_GAMMA | (j == 0 ? BUILD_BETA : 0), restarts);
+      double e = 0.0;
+      CK(cudaMemcpyAsync(&e, h->lz.scal + LZ_E0, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      if (energies) energies[sw] = e;
+    }
+    // a DMRG state is a valid factorisation but not exactly inverse-canonical
+    // (each Lambda_j dates from the last update of bond j, the state changed
+    // since); 2TDVP needs exactly inverse-canonical input, so
+    // re-gauge it (reorthonormalisation)
+    if (n_sweeps > 0) reorthonormalize(h);
+    h->evolved = true;
   } catch (const TdvpError& e) {
     return fail(h, e);
   }

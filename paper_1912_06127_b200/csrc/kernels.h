@@ -60,7 +60,7 @@ struct LanczosDev {
   unsigned* counter;  // last-block counter (self-resetting)
   int* brk_count;     // number of Lanczos runs that hit breakdown
 };
-enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1, LZ_SKIP = 2 * KMAX + 2, LZ_KEFF = 2 * KMAX + 3 };
+enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1, LZ_SKIP = 2 * KMAX + 2, LZ_KEFF = 2 * KMAX + 3, LZ_E0 = 2 * KMAX + 4 };
 int lanczos_nblk(long long n);
 cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* v0, long long n);
 cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
@@ -79,6 +79,11 @@ cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* v
 cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
                     long long n, int k, int last, double tol = 0.0, double tau_re = 0.0, double tau_im = 0.0);
 cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im);
+// ground state of the K x K Lanczos tridiagonal (two-site DMRG):
+// restricted to the Krylov dimension before a breakdown, the lowest eigenpair
+// (mu_0, y) by cyclic Jacobi; y normalised with y_0 >= 0 into d.y (zeros beyond),
+// mu_0 into scal[LZ_E0]
+cudaError_t lz_tridiag_ground(cudaStream_t st, const LanczosDev& d, int K);
 cudaError_t lz_combine(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int K, cplx* out,
                        long long n);
 

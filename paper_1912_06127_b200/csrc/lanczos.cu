@@ -476,6 +476,68 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
   for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) vnext[e] = cscale(w[e], inv);
 }
 
+// Lowest eigenpair of the symmetric tridiagonal T = tridiag(alpha, beta) (one
+// thread; K <= KMAX): K_eff = the Krylov dimension before a breakdown (the
+// first zero beta; later vectors are zero), cyclic Jacobi on the K_eff x K_eff
+// block until the off-diagonal mass is below 1e-30 of the Frobenius mass.
+__global__ void lz_tridiag_ground_kernel(LanczosDev d, int K) {
+  if (threadIdx.x != 0) return;
+  double A[KMAX][KMAX], Q[KMAX][KMAX];
+  int m = K;
+  for (int k = 0; k + 1 < K; ++k)
+    if (d.scal[KMAX + k] == 0.0) {
+      m = k + 1;
+      break;
+    }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      A[i][j] = i == j ? d.scal[i] : (j == i + 1 ? d.scal[KMAX + i] : (i == j + 1 ? d.scal[KMAX + j] : 0.0));
+      Q[i][j] = i == j ? 1.0 : 0.0;
+    }
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        tot += A[i][j] * A[i][j];
+        if (i != j) off += A[i][j] * A[i][j];
+      }
+    if (!(off > 1e-30 * tot)) break;
+    for (int p = 0; p < m - 1; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = A[p][q];
+        if (apq == 0.0) continue;
+        // symmetric Schur rotation zeroing A[p][q]
+        const double th = (A[q][q] - A[p][p]) / (2.0 * apq);
+        const double t = copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < m; ++k) {
+          const double akp = A[k][p], akq = A[k][q];
+          A[k][p] = c * akp - s * akq;
+          A[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = c * apk - s * aqk;
+          A[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double qkp = Q[k][p], qkq = Q[k][q];
+          Q[k][p] = c * qkp - s * qkq;
+          Q[k][q] = s * qkp + c * qkq;
+        }
+      }
+  }
+  int imin = 0;
+  for (int i = 1; i < m; ++i)
+    if (A[i][i] < A[imin][imin]) imin = i;
+  double nrm = 0.0;
+  for (int i = 0; i < m; ++i) nrm += Q[i][imin] * Q[i][imin];
+  nrm = sqrt(nrm);
+  const double sg = Q[0][imin] < 0.0 ? -1.0 : 1.0;
+  for (int i = 0; i < KMAX; ++i) d.y[i] = cmk(i < m ? sg * Q[i][imin] / nrm : 0.0, 0.0);
+  d.scal[LZ_E0] = A[imin][imin];
+}
+
 __global__ void lz_combine_kernel(const cplx* __restrict__ y, const cplx* __restrict__ V, long long ldv, int K,
                                   cplx* __restrict__ out, long long n, const double* __restrict__ scal) {
   if (scal[LZ_SKIP] != 0.0) K = min(K, (int)scal[LZ_KEFF]);
@@ -517,6 +579,11 @@ cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* v
 cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im) {
   if (K > KMAX) return cudaErrorInvalidValue;
   lz_tridiag_exp_kernel<<<1, 32, 0, st>>>(d, K, tau_re, tau_im);
+  return cudaGetLastError();
+}
+cudaError_t lz_tridiag_ground(cudaStream_t st, const LanczosDev& d, int K) {
+  if (K > KMAX) return cudaErrorInvalidValue;
+  lz_tridiag_ground_kernel<<<1, 32, 0, st>>>(d, K);
   return cudaGetLastError();
 }
 cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,

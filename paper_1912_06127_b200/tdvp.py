@@ -91,6 +91,7 @@ _SIGS = {
     "tdvp_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, C.c_int]),
     "tdvp_partition": (C.c_int, [C.c_int, C.c_int, _I, _I]),
     "tdvp_get_partition": (C.c_int, [C.c_void_p, _I, _I, _I]),
+    "tdvp_dmrg": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _D]),
     "tdvp_apply_heff2": (C.c_int, [C.c_int] * 6 + [_D] * 6),
     "tdvp_apply_heff1": (C.c_int, [C.c_int] * 5 + [_D] * 5),
     "tdvp_env_left": (C.c_int, [C.c_int] * 5 + [_D] * 4),
@@ -217,6 +218,12 @@ class Tdvp:
             return
         starts = (C.c_int * len(bounds))(*[int(s) for s, _ in bounds])
         _check(lib().tdvp_set_partition(self.h, len(bounds), starts), self.h)
+
+    def dmrg(self, n_sweeps, restarts=4):
+        """Two-site DMRG sweeps (tdvp_dmrg); returns the energy after every sweep."""
+        out = np.zeros(max(1, n_sweeps))
+        _check(lib().tdvp_dmrg(self.h, int(n_sweeps), int(restarts), out.ctypes.data_as(_D)), self.h)
+        return out[:n_sweeps]
 
     def partition(self):
         """The segment bounds [(s, e)] the handle currently uses (tdvp_get_partition)."""
