@@ -90,7 +90,6 @@ typedef struct {
   double svd_jac_ms;      /* summed device time of the Jacobi kernel of every SVD (timing=1) */
   double svd_jac_flop;    /* its algorithmic real flops: sweeps * nc(nc-1)/2 * (16 mr + 24 (mr + nc)) */
   int svd_sweeps_total;   /* Jacobi sweeps summed over the SVDs of the last step */
-  int svd_warm;           /* SVDs of the last step warm-started from the previous visit of their bond */
   double lanczos2_ms;     /* whole two-site Krylov exponentials incl. their H_eff^(2) matvecs (timing=1) */
   double lanczos1_ms;     /* whole one-site backward exponentials (timing=1) */
   double env_ms;          /* environment updates after the splits (timing=1) */

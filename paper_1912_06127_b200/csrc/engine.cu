@@ -155,11 +155,6 @@ struct Segment {
   std::vector<int> cb;  // bond dims, L+1 (own view)
   std::vector<BufPtr> psi, beta, gamma;  // per site (null if not held)
   std::vector<BufPtr> lam, vinv;         // per bond
-  // Jacobi warm start per bond: a unitary basis of one side of the last SVD
-  // (side 'L' = left factor U of Theta, 'R' = right factor W), its dimension
-  std::vector<BufPtr> wbasis;
-  std::vector<char> wside;
-  std::vector<int> wdim;
 };
 
 // One boundary message between segment lanes (SEND_R: Psi'_{e+1}, Lambda'_e,
@@ -194,11 +189,6 @@ struct tdvp_ctx {
   tdvp_ctx& operator=(const tdvp_ctx&) = delete;
   int L = 0, d = 0, Dmpo = 0, chi_max = 0;
   tdvp_params prm{};
-  // Jacobi warm start from the previous visit of a bond (TDVP_SVD_WARM=1: on).
-  // Off by default: on the saturated bench it needs MORE sweeps (12.3) than
-  // the QR-preconditioned start (8.3), the discarded half being unstructured.
-  bool warm_svd = false;
-  bool lz_fused = true;  // one cooperative launch per Lanczos iteration (TDVP_LZ_FUSED=0: four passes)
   const double* cur_skip = nullptr;  // inside a paper-mode Lanczos: its device "converged" flag
   int dev = 0;
   // devices of a multi-device handle (tdvp_params.n_devices / device_ids):
@@ -534,20 +524,8 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
         h->stats.heff1_flop += mv_flop;
       }
     }
-    if (h->lz_fused || paper) {
-      CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0, ktol, tre,
-                 tim));
-      g_launch_count++;
-    } else {
-      CK(lz_dots(h->st, h->lz, V, n, k + 1, w, n, k));
-      g_launch_count++;
-      if (k + 1 < K) {
-        CK(lz_update_dots(h->st, h->lz, V, n, k + 1, w, n));
-        CK(lz_update_norm(h->st, h->lz, V, n, k + 1, w, n, k));
-        CK(lz_next(h->st, h->lz, w, V + (long long)(k + 1) * n, n, k));
-        g_launch_count += 3;
-      }
-    }
+    CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0, ktol, tre, tim));
+    g_launch_count++;
   }
   h->cur_skip = nullptr;
   if (h->prm.timing && which) {
@@ -604,45 +582,10 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
   double w = 0.0;
   float jac_ms = 0.f;
-  // Warm start (square Theta, interior pairs of a sweep): sweeping right, the
-  // right basis (s2, b_{j+1}) of bond j is the one the last left sweep's SVD of
-  // this bond produced (nothing between touches bond j+1), and sweeping left
-  // the left basis (a_{j-1}, s1) is; each SVD keeps the basis the next visit
-  // from the other direction needs.  Any unitary start gives the exact SVD;
-  // a stale one only costs sweeps.
-  const int m2 = cl * d, n2 = d * cr;
-  const int dir = full ? 0 : (build == BUILD_BETA ? 1 : build == BUILD_GAMMA ? -1 : 0);
-  SvdWarm wst{};
-  int store_ok = 0;
-  const bool warm = h->warm_svd && dir != 0 && m2 == n2;
-  if (warm) {
-    if ((int)g.wbasis.size() < h->L) {
-      g.wbasis.resize(h->L);
-      g.wside.assign(h->L, 0);
-      g.wdim.assign(h->L, 0);
-    }
-    if (!g.wbasis[j] || g.wdim[j] < n2) {
-      g.wbasis[j] = make_buf((size_t)n2 * n2 * sizeof(cplx));
-      g.wside[j] = 0;
-      g.wdim[j] = n2;
-    }
-    wst.orient = dir > 0 ? 0 : 1;
-    const char need = dir > 0 ? 'R' : 'L';
-    wst.pre = (g.wside[j] == need && g.wdim[j] == n2) ? g.wbasis[j]->c() : nullptr;
-    wst.store = g.wbasis[j]->c();
-    wst.store_ok = &store_ok;
-  }
   double jac_flop = 0.0;
   cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
                                       g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps,
-                                      h->prm.timing ? &jac_ms : nullptr, warm ? &wst : nullptr, &jac_flop);
-  if (warm) {
-    g.wside[j] = store_ok ? (dir > 0 ? 'L' : 'R') : 0;
-    g.wdim[j] = n2;
-    if (wst.pre) h->stats.svd_warm++;
-  } else if (j < (int)g.wside.size()) {
-    g.wside[j] = 0;
-  }
+                                      h->prm.timing ? &jac_ms : nullptr, &jac_flop);
   if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
   CK(se);
   g_launch_count += 5;
@@ -774,9 +717,6 @@ void alloc_segment(tdvp_ctx* h, Segment& g, int q, int s, int e, int dev) {
   g.gamma.clear();
   g.lam.clear();
   g.vinv.clear();
-  g.wbasis.clear();
-  g.wside.clear();
-  g.wdim.clear();
   g.psi.resize(L);
   g.beta.resize(L);
   g.gamma.resize(L);
@@ -824,7 +764,6 @@ void upload_state(tdvp_ctx* h) {
     // the segment's own device and a stream of it (its lane's, when on another device)
     DeviceGuard dg(g.dev);
     cudaStream_t st = g.dev == h->dev ? h->st : lane_of(h, g.q)->st;
-    std::fill(g.wside.begin(), g.wside.end(), 0);  // new state: no warm-start bases
     g.cb = h->h_chi;
     const int hi = std::min(g.e + 1, L - 1);
     for (int j = g.s; j <= hi; ++j)
@@ -1263,7 +1202,6 @@ void reset_step_stats(tdvp_ctx* h) {
   h->stats.n_pair = h->stats.n_back = 0;
   h->stats.svd_sweeps_max = 0;
   h->stats.svd_sweeps_total = 0;
-  h->stats.svd_warm = 0;
   h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
   h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
   h->stats.heff2_calls = 0;
@@ -1306,8 +1244,6 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     tdvp_ctx* ln = lane_of(h, q);
     ln->sv.throughput = 1;
     ln->prm = h->prm;
-    ln->warm_svd = h->warm_svd;
-    ln->lz_fused = h->lz_fused;
     reset_step_stats(ln);
     CK(cudaStreamWaitEvent(ln->st, h->ev_step0, 0));
   }
@@ -1357,7 +1293,6 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     a.n_back += b.n_back;
     a.svd_sweeps_max = std::max(a.svd_sweeps_max, b.svd_sweeps_max);
     a.svd_sweeps_total += b.svd_sweeps_total;
-    a.svd_warm += b.svd_warm;
     a.svd_jac_ms += b.svd_jac_ms;
     a.svd_jac_flop += b.svd_jac_flop;
     a.heff2_flop += b.heff2_flop;
@@ -1849,8 +1784,6 @@ int tdvp_create(int L, int d, int D_mpo, int chi_max, tdvp_t* out) {
     h->devs = {h->dev};
     h->prm.n_devices = 1;
     h->prm.device_ids = h->devs.data();
-    if (const char* ev = std::getenv("TDVP_SVD_WARM")) h->warm_svd = std::atoi(ev) != 0;
-    if (const char* ev = std::getenv("TDVP_LZ_FUSED")) h->lz_fused = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("TDVP_LANES")) h->lanes_on = std::atoi(ev) != 0;
     h->cbmax.assign(L + 1, 1);
     for (int j = 0; j <= L; ++j) {

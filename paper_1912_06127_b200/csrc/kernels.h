@@ -63,13 +63,6 @@ struct LanczosDev {
 enum { LZ_N0 = 2 * KMAX, LZ_BRK = 2 * KMAX + 1, LZ_SKIP = 2 * KMAX + 2, LZ_KEFF = 2 * KMAX + 3, LZ_E0 = 2 * KMAX + 4 };
 int lanczos_nblk(long long n);
 cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* v0, long long n);
-cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
-                    long long n, int k);
-cudaError_t lz_update_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
-                           long long n);
-cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
-                           long long n, int k);
-cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k);
 // one cooperative launch for a whole Lanczos iteration after the matvec (see lanczos.cu)
 // tol > 0 (paper mode, "convergence tolerance 1e-6"): after
 // beta_k, block 0 estimates the error n0 beta_k |(exp(tau T_{k+1}) e1)_k| and,
@@ -113,17 +106,6 @@ struct TruncParams {
   int chi_max;
   double eps, w_max, delta;
 };
-// Warm start of the Jacobi SVD from the previous visit of the same bond
-// (square matrices): X = Theta (orient 0) or Theta^H (orient 1); `pre` (nc x nc,
-// column-major, unitary to the Jacobi tolerance) is a basis of X's column
-// space from the previous SVD, X0 = X pre and V0 = pre; `store` receives this
-// SVD's left factor of X (columns X_c / sigma_c) when every sigma_c > 0.
-struct SvdWarm {
-  int orient;
-  const cplx* pre;
-  cplx* store;
-  int* store_ok;
-};
 // Full SVD by blocked one-sided Jacobi, then truncation (SURVEY O-7) and the split
 // Psi_L = U S, Lambda = S, V = 1/S, Psi_R = S W^dagger.  theta is m x n row-major.
 // Returns chi via *chi_out (host), discarded weight via *w_out (host).
@@ -133,8 +115,7 @@ struct SvdWarm {
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out = nullptr, const SvdWarm* warm = nullptr,
-                               double* jac_flop_out = nullptr);
+                               float* jac_ms_out = nullptr, double* jac_flop_out = nullptr);
 size_t svd_work_elems(int m, int n);
 // ------------------------------------------------------------------ qr.cu
 // Blocked Householder QR workspace (column-major A, m x n, m >= n).

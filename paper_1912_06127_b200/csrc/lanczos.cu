@@ -5,10 +5,11 @@
 // Krylov coefficients live in device memory.  Each vector pass is a single
 // HBM-bound kernel with a deterministic two-level reduction (per-block
 // partials, the last block to finish reduces them in block order):
-//   lz_dots         c = V^H w                  (alpha_k = Re c_k)
-//   lz_update_dots  w -= V c ;   c' = V^H w    (3-term recurrence + CGS pass 1, fused)
-//   lz_update_norm  w -= V c' ;  ||w||^2       (CGS pass 2; beta_k, breakdown)
-//   lz_next         v_{k+1} = w / beta_k       (hard zero after breakdown)
+//   c = V^H w                  (alpha_k = Re c_k)
+//   w -= V c ;   c' = V^H w    (3-term recurrence + CGS pass 1, fused)
+//   w -= V c' ;  ||w||^2       (CGS pass 2; beta_k, breakdown)
+//   v_{k+1} = w / beta_k       (hard zero after breakdown)
+// all four in ONE cooperative launch per iteration (lz_iter_kernel).
 // then an on-device K x K symmetric tridiagonal eigen-decomposition
 // (cyclic Jacobi) for y = n0 Q exp(tau mu) Q^T e_1 and v' = V y.
 #include <cstdlib>
@@ -25,108 +26,6 @@ constexpr int NW = TPB / 32;
 int nblk_for(long long n) {
   long long b = (n + TPB - 1) / TPB;
   return (int)std::max<long long>(1, std::min<long long>(b, 2LL * g_num_sms));
-}
-
-enum { M_DOTS = 0, M_UPD_DOTS = 1, M_UPD_NORM = 2 };
-
-template <int NV, int MODE>
-__global__ void __launch_bounds__(TPB) lz_pass_kernel(LanczosDev d, const cplx* __restrict__ V, long long ldv,
-                                                      cplx* w, long long n, int k) {
-  constexpr int NQ = (MODE == M_UPD_NORM) ? 1 : NV;  // number of complex quantities reduced
-  __shared__ cplx s_c[NV];
-  __shared__ double s_red[NW][2 * NQ];
-  __shared__ bool s_last;
-  if (MODE != M_DOTS) {
-    if (threadIdx.x < NV) s_c[threadIdx.x] = d.coef[(MODE == M_UPD_DOTS ? 0 : (KMAX + 1)) + threadIdx.x];
-    __syncthreads();
-  }
-  double acc[2 * NQ];
-#pragma unroll
-  for (int q = 0; q < 2 * NQ; ++q) acc[q] = 0.0;
-
-  for (long long e = blockIdx.x * (long long)TPB + threadIdx.x; e < n; e += (long long)gridDim.x * TPB) {
-    cplx we = w[e];
-    cplx v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = V[i * ldv + e];
-    if (MODE != M_DOTS) {
-#pragma unroll
-      for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], v[i]));
-      w[e] = we;
-    }
-    if (MODE == M_UPD_NORM) {
-      acc[0] += cabs2(we);
-    } else {
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const cplx p = cdotc(v[i], we);
-        acc[2 * i] += p.x;
-        acc[2 * i + 1] += p.y;
-      }
-    }
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < 2 * NQ; ++q) {
-    const double t = warp_sum(acc[q]);
-    if (lane == 0) s_red[wid][q] = t;
-  }
-  __syncthreads();
-  if (threadIdx.x < 2 * NQ) {
-    double t = 0.0;
-    for (int ww = 0; ww < NW; ++ww) t += s_red[ww][threadIdx.x];
-    d.partials[(long long)blockIdx.x * (2 * NQ) + threadIdx.x] = t;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(d.counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  __shared__ double s_tot[2 * NQ];
-  if (threadIdx.x < 2 * NQ) {
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)d.partials)[(long long)b * (2 * NQ) + threadIdx.x];
-    s_tot[threadIdx.x] = t;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *d.counter = 0u;
-    if (MODE == M_DOTS) {
-      for (int i = 0; i < NV; ++i) d.coef[i] = cmk(s_tot[2 * i], s_tot[2 * i + 1]);
-      d.scal[k] = s_tot[2 * k];  // alpha_k = Re <v_k, H v_k>
-    } else if (MODE == M_UPD_DOTS) {
-      for (int i = 0; i < NV; ++i) d.coef[KMAX + 1 + i] = cmk(s_tot[2 * i], s_tot[2 * i + 1]);
-    } else {
-      const double b = sqrt(s_tot[0]);
-      double s = 1.0;
-      for (int i = 0; i <= k; ++i) s = fmax(s, fabs(d.scal[i]));
-      for (int i = 0; i < k; ++i) s = fmax(s, d.scal[KMAX + i]);
-      const bool was = d.scal[LZ_BRK] != 0.0;
-      if (was || !(b > 1e-12 * s)) {
-        d.scal[LZ_BRK] = 1.0;
-        d.scal[KMAX + k] = 0.0;
-        if (!was) atomicAdd(d.brk_count, 1);
-      } else {
-        d.scal[KMAX + k] = b;
-      }
-    }
-  }
-}
-
-template <int MODE>
-cudaError_t pass_dispatch(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
-                          long long n, int k) {
-  const int nb = nblk_for(n);
-#define LZ_CASE(NVV) \
-  case NVV: lz_pass_kernel<NVV, MODE><<<nb, TPB, 0, st>>>(d, V, ldv, w, n, k); break;
-  switch (nv) {
-    LZ_CASE(1) LZ_CASE(2) LZ_CASE(3) LZ_CASE(4) LZ_CASE(5) LZ_CASE(6) LZ_CASE(7) LZ_CASE(8)
-    LZ_CASE(9) LZ_CASE(10) LZ_CASE(11) LZ_CASE(12) LZ_CASE(13) LZ_CASE(14) LZ_CASE(15) LZ_CASE(16)
-    default: return cudaErrorInvalidValue;
-  }
-#undef LZ_CASE
-  return cudaGetLastError();
 }
 
 // n0 = ||x||, reset scalars
@@ -346,7 +245,7 @@ __global__ void __launch_bounds__(32) lz_tridiag_exp_kernel(LanczosDev d, int K,
 }
 
 // One Lanczos iteration after the matvec in ONE cooperative launch (replaces
-// lz_dots + lz_update_dots + lz_update_norm + lz_next): three grid-wide
+// four separate passes): three grid-wide
 // reductions, each block reducing the per-block partials in block order (so
 // every block holds the same, deterministic sums).
 //   phase 1  c = V^H w                 alpha_k = Re c_k        (last iteration stops here)
@@ -560,22 +459,6 @@ cudaError_t lz_start(cudaStream_t st, const LanczosDev& d, const cplx* x, cplx* 
   lz_scale_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.scal, LZ_N0, false, x, v0, n);
   return cudaGetLastError();
 }
-cudaError_t lz_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, const cplx* w,
-                    long long n, int k) {
-  return pass_dispatch<M_DOTS>(st, d, V, ldv, nv, const_cast<cplx*>(w), n, k);
-}
-cudaError_t lz_update_dots(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
-                           long long n) {
-  return pass_dispatch<M_UPD_DOTS>(st, d, V, ldv, nv, w, n, 0);
-}
-cudaError_t lz_update_norm(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w,
-                           long long n, int k) {
-  return pass_dispatch<M_UPD_NORM>(st, d, V, ldv, nv, w, n, k);
-}
-cudaError_t lz_next(cudaStream_t st, const LanczosDev& d, const cplx* w, cplx* vnext, long long n, int k) {
-  lz_scale_kernel<<<nblk_for(n) * 2, TPB, 0, st>>>(d.scal, KMAX + k, true, w, vnext, n);
-  return cudaGetLastError();
-}
 cudaError_t lz_tridiag_exp(cudaStream_t st, const LanczosDev& d, int K, double tau_re, double tau_im) {
   if (K > KMAX) return cudaErrorInvalidValue;
   lz_tridiag_exp_kernel<<<1, 32, 0, st>>>(d, K, tau_re, tau_im);
@@ -604,15 +487,10 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
     occ[nv] = std::max(1, o);
   }
   // partials: two buffers of G * 2 * (KMAX + 1) doubles inside d.partials (4 * SMs blocks' worth)
-  static int gcap = -1;
-  if (gcap < 0) {
-    const char* ev = std::getenv("TDVP_LZ_G");
-    gcap = ev ? std::max(1, std::atoi(ev)) : 0;
-  }
   // grid-wide barriers get cheaper with fewer blocks: 64 blocks for small
   // vectors (measured: the non-matvec Lanczos time at chi = 128 drops by a
   // third against 296 blocks), more once a vector exceeds 16K elements/block
-  const long long want = gcap > 0 ? gcap : std::max<long long>(64, n / 16384);
+  const long long want = std::max<long long>(64, n / 16384);
   const int G = (int)std::max<long long>(
       1, std::min<long long>(std::min<long long>(nblk_for(n), (long long)occ[nv] * g_num_sms),
                              std::min<long long>(want, 2LL * g_num_sms)));

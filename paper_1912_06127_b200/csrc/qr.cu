@@ -1001,12 +1001,7 @@ __global__ void __launch_bounds__(NT) qr_apply_refl_kernel(QrApplyJob j0, QrAppl
 cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, int n, cplx* tau, cplx* RH,
                               long long ldrh, int rh_rows) {
   if (m < n || n < 1) return cudaErrorInvalidValue;
-  static int cmax = -1;
-  if (cmax < 0) {
-    const char* ev = std::getenv("TDVP_QR_C");
-    cmax = ev ? std::max(1, std::min(16, std::atoi(ev))) : 16;
-  }
-  const int C = std::min(cmax, n);
+  const int C = std::min(16, n);
   const int cw = (n + C - 1) / C;
   const int Cu = (n + cw - 1) / cw;
   if (cw > 32) return cudaErrorNotSupported;
@@ -1015,23 +1010,11 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   const size_t smem = std::max<size_t>(((size_t)cw * m + (size_t)NB * m + cw) * sizeof(cplx), 116 * 1024);
   if (smem > 200 * 1024) return cudaErrorNotSupported;
   cudaError_t e;
-  // threads per CTA: 512 gives the band's trailing-column updates one warp per
-  // column (the per-reflector critical path), TDVP_QR_NT=256 the older setting
-  static int nt_sel = -1;
-  if (nt_sel < 0) {
-    const char* ev = std::getenv("TDVP_QR_NT");
-    nt_sel = (ev && std::atoi(ev) == 256) ? 256 : 512;
-  }
-  static int rpl_env = -1;
-  if (rpl_env < 0) {
-    const char* ev = std::getenv("TDVP_QR_REG");
-    rpl_env = ev ? std::atoi(ev) : 2;  // 2: 512 threads (measured fastest), 1: 256, 0: off
-  }
-  const bool reg = m <= 256 && rpl_env;
-  auto fn = reg ? (rpl_env == 2 ? qrc3_factor_kernel<512, NB, false, 8> : qrc3_factor_kernel<256, NB, false, 8>)
-                : nt_sel == 512 ? qrc3_factor_kernel<512, NB, false>
-                                : qrc3_factor_kernel<256, NB, false>;
-  const int nthreads = reg ? (rpl_env == 2 ? 512 : 256) : nt_sel;
+  // 512 threads: one warp per trailing column of a band (the per-reflector
+  // critical path); m <= 256: the pivot column in registers (measured fastest)
+  const bool reg = m <= 256;
+  auto fn = reg ? qrc3_factor_kernel<512, NB, false, 8> : qrc3_factor_kernel<512, NB, false>;
+  const int nthreads = 512;
   if ((e = set_smem_attr(reinterpret_cast<const void*>(fn), 200 * 1024)) != cudaSuccess) return e;
   if ((e = set_cluster_nonportable(reinterpret_cast<const void*>(fn))) != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1119,15 +1102,9 @@ cudaError_t qr_apply_refl2(cudaStream_t st, const cplx* A0, long long lda0, cons
   const int nb0 = (nc0 + 7) / 8, nb1 = A1 ? (nc1 + 7) / 8 : 0;
   const int m = std::max(m0, A1 ? m1 : 0);
   const int blocks = nb0 + nb1;
-  static int small_nt = -1;
-  if (small_nt < 0) {
-    const char* ev = std::getenv("TDVP_QR_APPLY_NT");
-    small_nt = ev ? std::atoi(ev) : 128;  // measured: 128 threads (2 rows each) fastest at n = 256
-  }
-  if (m <= 128 && small_nt == 128) qr_apply_refl_kernel<1, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
-  else if (m <= 256 && small_nt == 128) qr_apply_refl_kernel<2, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
-  else if (m <= 256 && small_nt == 64) qr_apply_refl_kernel<4, 64><<<blocks, 64, 0, st>>>(j0, j1, nb0);
-  else if (m <= 256) qr_apply_refl_kernel<1, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
+  // measured: 128 threads (1-2 rows each) fastest up to 256 rows
+  if (m <= 128) qr_apply_refl_kernel<1, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
+  else if (m <= 256) qr_apply_refl_kernel<2, 128><<<blocks, 128, 0, st>>>(j0, j1, nb0);
   else if (m <= 512) qr_apply_refl_kernel<2, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else if (m <= 1024) qr_apply_refl_kernel<4, 256><<<blocks, 256, 0, st>>>(j0, j1, nb0);
   else return cudaErrorNotSupported;

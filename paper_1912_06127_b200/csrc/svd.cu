@@ -862,38 +862,15 @@ size_t svd_work_elems(int m, int n) {
   return (size_t)(mr + nc) * nc;
 }
 
-// store[c][r] = X[r][c] / sigma_c (column-major nc x nc): the left factor of X, whose
-// columns are orthonormal to the Jacobi tolerance (relative orthogonality)
-__global__ void svd_store_kernel(const cplx* __restrict__ Y, long long ldy, const double* __restrict__ sigma, int nr,
-                                 int nc, cplx* store) {
-  const long long total = (long long)nr * nc;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(e / nr), r = (int)(e - (long long)c * nr);
-    store[e] = cscale(Y[(long long)c * ldy + r], 1.0 / sigma[c]);
-  }
-}
-
 cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* theta, int m, int n,
                                const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv,
                                int* chi_out, double* w_out, int* r_out, int* chi_eps_out, int* sweeps_out,
-                               float* jac_ms_out, const SvdWarm* warm, double* jac_flop_out) {
-  // warm start only for square matrices (orientation forced by the caller)
-  if (warm != nullptr && m != n) warm = nullptr;
-  const bool transposed = warm ? warm->orient == 1 : m < n;
+                               float* jac_ms_out, double* jac_flop_out) {
+  const bool transposed = m < n;
   const int mr = std::max(m, n), nc = std::min(m, n);
   const long long ldy = (long long)mr + nc;
   cudaError_t e;
-  const bool use_warm = warm != nullptr && warm->pre != nullptr;
-  if (use_warm) {
-    // X0 = X P (X = Theta or Theta^H), V0 = P: the previous visit's basis of X's column space
-    const cplx one = cmk(1.0, 0.0), zero = cmk(0.0, 0.0);
-    if ((e = zgemm(st, OP_N, transposed ? OP_R : OP_T, nc, mr, nc, one, warm->pre, nc, theta, n, zero, d.Y, ldy)) !=
-        cudaSuccess)
-      return e;
-    if ((e = cudaMemcpy2DAsync(d.Y + mr, (size_t)ldy * sizeof(cplx), warm->pre, (size_t)nc * sizeof(cplx),
-                               (size_t)nc * sizeof(cplx), nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-      return e;
-  } else {
+  {
     const long long total = ldy * nc;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 8LL * g_num_sms));
     svd_init_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, theta, m, n, mr, nc, transposed);
@@ -901,19 +878,9 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   // QR preconditioning (Drmac-Veselic): X = Q1 R1, R1^H = Q2 R2, Jacobi on
   // X3 = R2^H (nc x nc) with V accumulated; then X = (Q1 U3) S (Q2 V)^H, i.e.
   // Q1 is applied to the converged X3 columns and Q2 to V before the split.
-  static int precond = -1;
-  if (precond < 0) {
-    const char* ev = std::getenv("TDVP_SVD_PRECOND");
-    precond = ev ? std::atoi(ev) : 2;
-  }
-  const bool use_qr = !use_warm && precond == 2 && nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
+  const bool use_qr = nc >= 2 && d.qrbuf != nullptr && qr_kb_for(mr) > 0 && qr_kb_for(nc) > 0 &&
                       svd_qr_work_elems(m, n) <= d.qrbuf_elems;
-  static int presort_env = -1;
-  if (presort_env < 0) {
-    const char* ev = std::getenv("TDVP_SVD_PRESORT");
-    presort_env = ev ? std::atoi(ev) : 1;
-  }
-  const bool presort = use_qr && presort_env && d.perm != nullptr && nc * sizeof(double) <= 48 * 1024;
+  const bool presort = use_qr && d.perm != nullptr && nc * sizeof(double) <= 48 * 1024;
   QrWork w1{}, w2{};
   int x_rows = mr;
   bool qr_cluster = false;
@@ -945,13 +912,8 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
                                       (size_t)mr * sizeof(cplx), nc, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) {
       return e;
     }
-    static int qrmode = -1;
-    if (qrmode < 0) {
-      const char* ev = std::getenv("TDVP_QR_BLOCKED");
-      qrmode = ev ? std::atoi(ev) : 0;
-    }
     qr_cluster = false;
-    if (!qrmode) {
+    {
       // cluster-resident QR where the column bands fit shared memory, else
       // the same look-ahead QR over a cooperative grid
       e = qr_factor_cluster(st, Q1, mr, mr, nc, w1.tau, Q2, nc, nc);
@@ -1011,22 +973,12 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     sweeps = -1;
   } else if (nc >= 2) {
     cudaGetLastError();
-    static int forced = -1;
-    if (forced < 0) {
-      const char* ev = std::getenv("TDVP_SVD_BW");
-      forced = ev ? std::atoi(ev) : 0;
-    }
-    // shared-memory-resident block pairs when the columns fit (<= 200 KB), else Gram variant
+    // fallback for shapes neither svd_bjac nor svd_rjac take: shared-memory-
+    // resident block pairs when the columns fit (<= 200 KB), else the Gram variant
     const long long rows = (long long)mr + nc;
     int bw;
     bool smem_path;
-    if (forced == 104 || forced == 108) {
-      bw = forced - 100;
-      smem_path = true;
-    } else if (forced > 0) {
-      bw = forced == 8 ? 8 : 4;
-      smem_path = false;
-    } else if (rows * 8 * 16 <= 200 * 1024) {
+    if (rows * 8 * 16 <= 200 * 1024) {
       // measured on B200 (microbench.py --svd, profiles/r1_microbench.md): the
       // shared-memory block-pair variant with b = 4 is fastest where it fits
       bw = 4;
@@ -1087,16 +1039,6 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     float ms = 0.f;
     if ((e = cudaEventElapsedTime(&ms, d.ev_jac[0], d.ev_jac[1])) != cudaSuccess) return e;
     *jac_ms_out = ms;
-  }
-  if (warm != nullptr && warm->store != nullptr) {
-    // keep this SVD's left factor of X for the next visit of the bond (all columns nonzero)
-    *warm->store_ok = 0;
-    if (d.h_ibuf[5] == nc) {
-      const long long total = (long long)mr * nc;
-      const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 4LL * g_num_sms));
-      svd_store_kernel<<<blocks, 256, 0, st>>>(d.Y, ldy, d.sigma, mr, nc, warm->store);
-      *warm->store_ok = 1;
-    }
   }
   if (use_qr && qr_cluster) {
     // Q1 onto the X columns and Q2 onto V, one launch

@@ -869,26 +869,14 @@ bool rows_ok(int row, int mr, int nc) {
 // cudaErrorNotSupported when no register-resident variant fits the shape.
 cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int nc, long long ldy, double tol,
                          int* sweeps_dev) {
-  static int forced = -2, prof = 0, full_rounds = 0, fastp = 0;
-  if (forced == -2) {
-    const char* ev = std::getenv("TDVP_RJ_VARIANT");
-    forced = ev ? std::atoi(ev) : -1;
-    const char* pe = std::getenv("TDVP_SVD_PROF");
+  static int prof = -1;
+  if (prof < 0) {
+    const char* pe = std::getenv("TDVP_SVD_PROF");  // per-phase cycle counts on stderr (diagnostics only)
     prof = pe ? std::max(1, std::atoi(pe)) : 0;
-    const char* fr = std::getenv("TDVP_RJ_FULL");
-    full_rounds = fr ? std::atoi(fr) : 0;
-    const char* fp = std::getenv("TDVP_RJ_FAST");
-    fastp = fp ? std::atoi(fp) : 0;
-    const char* el = std::getenv("TDVP_RJ_EARLY");
-    if (el && std::atoi(el) == 0) {
-      const double z = 0.0;
-      cudaMemcpyToSymbol(c_rj_early, &z, sizeof(z));
-    }
   }
-  if (forced == 99) return cudaErrorNotSupported;  // tuning: legacy Jacobi
+  constexpr int full_rounds = 0, fastp = 0;
   int row = -1;
-  if (forced >= 0 && forced < kNTab && rows_ok(forced, mr, nc)) row = forced;
-  if (row < 0) {
+  {
     // latency: measured fastest first (microbench.py --svd, B200); throughput
     // (concurrent SVDs of segment lanes): variant 14 packs two block pairs per
     // CTA, half the CTAs per SVD (c2sat p = 8 lanes: 146 vs 166 ms/step)
@@ -904,7 +892,7 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
   const int nbe = std::max(2, nb + (nb & 1));
   const int P = (nbe / 2 + grp - 1) / grp;  // CTAs
   cudaError_t e;
-  bool cluster = P <= 16 && std::getenv("TDVP_RJ_GRID") == nullptr;
+  bool cluster = P <= 16;
   RjVariant v{};
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -944,13 +932,9 @@ cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int
                    (void*)&nbe, (void*)&tol,        (void*)&max_sweeps,  (void*)&full_rounds,
                    (void*)&offb, (void*)&sweeps_dev, (void*)&prof, (void*)&fastp};
   unsigned* flg = nullptr;
-  static int use_flags = -1;
-  if (use_flags < 0) {
-    // off by default: measured slower than the grid barrier (flag round trips
-    // through L2 + fences cost more than cg's barrier at 32 CTAs)
-    const char* ev = std::getenv("TDVP_RJ_FLAGS");
-    use_flags = ev ? std::atoi(ev) : 0;
-  }
+  // point-to-point round flags: measured slower than the grid barrier (flag
+  // round trips through L2 + fences cost more than cg's barrier at 32 CTAs)
+  constexpr int use_flags = 0;
   if (kind == 2 && use_flags && d.flags != nullptr && (size_t)2 * nbe <= d.flags_elems) {
     flg = d.flags;
     if ((e = cudaMemsetAsync(flg, 0, (size_t)2 * nbe * sizeof(unsigned), st)) != cudaSuccess) return e;

@@ -50,7 +50,7 @@ class tdvp_stats(C.Structure):
                 ("heff2_calls", C.c_int), ("heff1_ms", C.c_double), ("heff1_flop", C.c_double),
                 ("svd_ms", C.c_double), ("gemm_launches", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int),
-                ("svd_warm", C.c_int), ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
+                ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
                 ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
                 ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int)]
 
