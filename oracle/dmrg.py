@@ -75,7 +75,12 @@ def _pair_ground(st: State, seg, j: int, restarts: int, build_beta: bool, build_
     L_, R_ = seg.beta[j], seg.gamma[j + 1]
     W1, W2 = st.W[j], st.W[j + 1]
     th2, e0 = lanczos_ground(lambda x: apply_h2(L_, W1, W2, R_, x), th, p.krylov_k, restarts)
-    psi_l, S, psi_r, w, r, chi_eps = svd_truncate(th2, p)
+    if p.u1:
+        from .u1 import svd_truncate_u1
+        psi_l, S, psi_r, w, r, chi_eps, qm = svd_truncate_u1(th2, seg.qb[j], seg.qb[j + 2], p)
+        seg.qb[j + 1] = qm
+    else:
+        psi_l, S, psi_r, w, r, chi_eps = svd_truncate(th2, p)
     seg.psi[j], seg.lam[j], seg.psi[j + 1] = psi_l, S, psi_r
     st.stats.w_step += w
     st.stats.n_pair += 1

@@ -36,6 +36,7 @@ class Params:
     krylov_k: int = 8           # max Krylov vectors
     krylov_tol: float = 0.0     # 0 = always K vectors (parity mode, AMB-5)
     multiplet_delta: float = 1e-6  # AMB-9 multiplet guard
+    u1: bool = False            # S^z-conserving block-sparse SVD (oracle/u1.py)
 
 
 # ----------------------------------------------------------------------------
@@ -315,6 +316,7 @@ class Segment:
     def __init__(self, q, s, e):
         self.q, self.s, self.e = q, s, e
         self.psi, self.lam, self.beta, self.gamma = {}, {}, {}, {}
+        self.qb = {}  # U(1) mode: bond charges by bond position k (bond left of site k)
 
 
 @dataclass
@@ -377,7 +379,13 @@ def init_state(mps, W, params: Params, p: int = 1, bounds=None) -> State:
         if np.any(l <= 0) or not np.all(np.isfinite(l)):
             raise ValueError("Lambda must be finite and > 0")
     beta, gamma = _mps_envs(psi, lam, st.W)
+    qb = None
+    if params.u1:
+        from .u1 import infer_charges
+        qb = infer_charges(psi)
     for seg in st.segs:
+        if qb is not None:
+            seg.qb = {k: qb[k].copy() for k in range(L + 1)}
         hi = min(seg.e + 1, L - 1)
         for j in range(seg.s, hi + 1):
             seg.psi[j] = psi[j].copy()
@@ -408,7 +416,12 @@ def _pair(st: State, seg: Segment, j: int, tau: complex, build_beta: bool, build
     th2 = expm_lanczos(lambda x: apply_h2(L_, W1, W2, R_, x), th, tau,
                        p.krylov_k, p.krylov_tol, info)
     st.stats.krylov_breakdowns += int(info.get("breakdown", False))
-    psi_l, S, psi_r, w, r, chi_eps = svd_truncate(th2, p)
+    if p.u1:
+        from .u1 import svd_truncate_u1
+        psi_l, S, psi_r, w, r, chi_eps, qm = svd_truncate_u1(th2, seg.qb[j], seg.qb[j + 2], p)
+        seg.qb[j + 1] = qm
+    else:
+        psi_l, S, psi_r, w, r, chi_eps = svd_truncate(th2, p)
     seg.psi[j], seg.lam[j], seg.psi[j + 1] = psi_l, S, psi_r
     st.stats.w_step += w
     st.stats.n_svd += 1
@@ -467,6 +480,8 @@ def _half(st: State, dt: float, h: int, merged: set):
                 b.psi[e + 1] = a.psi[e + 1].copy()
                 b.lam[e] = a.lam[e].copy()
                 b.beta[e + 1] = a.beta[e + 1].copy()
+                if st.params.u1:
+                    b.qb[e + 1] = a.qb[e + 1].copy()
 
     # ---- sweep phase
     for seg in st.segs:
@@ -505,6 +520,8 @@ def _half(st: State, dt: float, h: int, merged: set):
             # right sends Psi_s, gamma_s to left
             a.psi[s] = b.psi[s].copy()
             a.gamma[s] = b.gamma[s].copy()
+            if st.params.u1:
+                a.qb[s + 1] = b.qb[s + 1].copy()
             tau = tau_f if h == 1 else tau_h
             _pair(st, a, e, tau, True, True)
             if tau == tau_f:
@@ -513,6 +530,8 @@ def _half(st: State, dt: float, h: int, merged: set):
             b.psi[s] = a.psi[s].copy()
             b.lam[e] = a.lam[e].copy()
             b.beta[s] = a.beta[s].copy()
+            if st.params.u1:
+                b.qb[e + 1] = a.qb[e + 1].copy()
     return new_merged
 
 

@@ -306,3 +306,125 @@ def config(name: str):
 
 def random_complex(shape, rng):
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+# ----------------------------------------------------------------------------
+# U(1) (S^z_tot-conserving) synthetic inputs: a random MPS
+# of definite total S^z whose bond indices carry charges q = 2 S^z of the
+# sites to their left, Psi_j[a, s, b] = 0 unless q_b = q_a + c(s) with
+# c(up) = +1, c(down) = -1.  Input preparation only.
+# ----------------------------------------------------------------------------
+
+U1_CS = (1, -1)
+
+
+def _u1_bond_charges(L: int, chi: int, total: int = 0):
+    """Charge multiplicities of a saturated charge-definite bond profile: bond
+    position k (left of site k) gets the charges q of k spins that the L - k
+    spins to its right can complete to `total`, each with multiplicity at
+    most min(#left states, #right states) of that charge, the bond dimension
+    min(2^k, 2^(L-k), chi) spread over the charges in proportion to those
+    counts (largest first)."""
+    out = []
+    for k in range(L + 1):
+        cap = {}
+        for nup in range(k + 1):
+            q = 2 * nup - k
+            rq = total - q  # charge the right part must carry
+            if (L - k + rq) % 2 or abs(rq) > L - k:
+                continue
+            cap[q] = min(math.comb(k, nup), math.comb(L - k, (L - k + rq) // 2))
+        target = min(2 ** min(k, 62), 2 ** min(L - k, 62), chi, sum(cap.values()))
+        tot = sum(cap.values())
+        mult = {q: min(c, int(target * c / tot)) for q, c in cap.items()}
+        left = target - sum(mult.values())
+        for q in sorted(cap, key=lambda x: (-cap[x], x)):
+            if left <= 0:
+                break
+            add = min(left, cap[q] - mult[q])
+            mult[q] += add
+            left -= add
+        out.append(np.array(sorted(q for q, m in mult.items() for _ in range(m)), dtype=np.int64))
+    return out
+
+
+def random_u1_mps(L: int, chi: int, seed: int = 2, total: int = 0) -> MPS:
+    """Random inverse-canonical MPS of definite total charge (2 S^z_tot = total)
+    with a saturated charge-resolved bond profile; seeded complex-normal
+    entries on the allowed blocks, re-gauged by canonicalize_u1."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    q = _u1_bond_charges(L, chi, total)
+    M = []
+    for j in range(L):
+        t = np.zeros((len(q[j]), D_PHYS, len(q[j + 1])), dtype=np.complex128)
+        for s in range(D_PHYS):
+            mask = (q[j][:, None] + U1_CS[s]) == q[j + 1][None, :]
+            t[:, s, :] = np.where(mask, random_complex(mask.shape, rng), 0.0)
+        M.append(t)
+    return canonicalize_u1(M, q)
+
+
+def canonicalize_u1(M, q) -> MPS:
+    """canonicalize() done sector by sector, so that every tensor keeps exact
+    zeros outside its charge blocks (the block structure is what the U(1)
+    path of both oracle and library infer the charges from).  Bond indices
+    are ordered by descending Schmidt value."""
+    M = [np.asarray(m, dtype=np.complex128).copy() for m in M]
+    q = [np.asarray(x, dtype=np.int64).copy() for x in q]
+    L = len(M)
+    # QR sweep L -> R, per sector of the right bond
+    for j in range(L - 1):
+        cl, d, cr = M[j].shape
+        A = M[j].reshape(cl * d, cr)
+        rq = (q[j][:, None] + np.array(U1_CS[:d])[None, :]).reshape(-1)
+        Qs, Rs, newq = [], [], []
+        for Q in sorted(set(q[j + 1].tolist())):
+            rows, cols = np.nonzero(rq == Q)[0], np.nonzero(q[j + 1] == Q)[0]
+            qq, rr = np.linalg.qr(A[np.ix_(rows, cols)])
+            Qs.append((rows, qq))
+            Rs.append((cols, rr))
+            newq += [Q] * qq.shape[1]
+        k = len(newq)
+        An = np.zeros((cl * d, k), dtype=np.complex128)
+        R = np.zeros((k, cr), dtype=np.complex128)
+        off = 0
+        for (rows, qq), (cols, rr) in zip(Qs, Rs):
+            An[rows, off:off + qq.shape[1]] = qq
+            R[off:off + rr.shape[0], cols] = rr
+            off += qq.shape[1]
+        M[j] = An.reshape(cl, d, k)
+        M[j + 1] = np.tensordot(R / np.linalg.norm(R), M[j + 1], axes=(1, 0))
+        q[j + 1] = np.array(newq, dtype=np.int64)
+    # SVD sweep R -> L, per sector of the left bond
+    lam = [None] * (L - 1)
+    for j in range(L - 1, 0, -1):
+        cl, d, cr = M[j].shape
+        A = M[j].reshape(cl, d * cr)
+        cq = (q[j + 1][None, :] - np.array(U1_CS[:d])[:, None]).reshape(-1)
+        trip = []
+        for Q in sorted(set(q[j].tolist())):
+            rows, cols = np.nonzero(q[j] == Q)[0], np.nonzero(cq == Q)[0]
+            u, s, vh = np.linalg.svd(A[np.ix_(rows, cols)], full_matrices=False)
+            for kk in range(len(s)):
+                trip.append((s[kk], Q, rows, u[:, kk], cols, vh[kk]))
+        trip.sort(key=lambda t: (-t[0], t[1]))
+        smax = trip[0][0]
+        trip = [t for t in trip if t[0] > 1e-14 * smax]
+        k = len(trip)
+        U = np.zeros((cl, k), dtype=np.complex128)
+        B = np.zeros((k, d * cr), dtype=np.complex128)
+        s_ = np.zeros(k)
+        for kk, (s, Q, rows, u, cols, vh) in enumerate(trip):
+            U[rows, kk] = u
+            B[kk, cols] = vh
+            s_[kk] = s
+        M[j] = B.reshape(k, d, cr)
+        M[j - 1] = np.tensordot(M[j - 1], U * s_[None, :], axes=(2, 0))
+        lam[j - 1] = s_
+        q[j] = np.array([t[1] for t in trip], dtype=np.int64)
+    nrm = np.linalg.norm(M[0])
+    psi = [M[0] / nrm]
+    lam = [l / nrm for l in lam]
+    for j in range(1, L):
+        psi.append(lam[j - 1][:, None, None] * M[j])
+    return MPS(psi, lam)
