@@ -70,6 +70,16 @@ typedef struct {
    * the current partition's.  The state is kept; the environments are rebuilt
    * (the sequential section).  Single-process handles only. */
   double rebalance;
+  /* U(1) block-sparse splits ("symmetric
+   * block-sparse tensors"): 0 = off (default); 1 = the MPO conserves S^z_tot and
+   * the MPS has definite S^z_tot (d = 2).  Bond charges (2 S^z of the left part)
+   * are inferred from the MPS's nonzero pattern at the next layout (TDVP_EARG if
+   * it is not charge-definite) and tracked through every split and boundary
+   * message; every SVD (tdvp_step, tdvp_dmrg, tdvp_reorthonormalize) then runs
+   * sector by sector with the truncation rule applied to the union of all
+   * sectors' singular values (identical kept spectrum to the dense split), and
+   * every tensor keeps exact zeros outside its charge blocks.  Single-process. */
+  int u1;
 } tdvp_params;
 
 typedef struct {

@@ -21,6 +21,9 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <limits>
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -155,6 +158,10 @@ struct Segment {
   std::vector<int> cb;  // bond dims, L+1 (own view)
   std::vector<BufPtr> psi, beta, gamma;  // per site (null if not held)
   std::vector<BufPtr> lam, vinv;         // per bond
+  // U(1) mode (tdvp_params.u1): charges 2 S^z of the left part for every index
+  // of bond position k (bond left of site k), k = 0..L; kept for the bonds
+  // this segment's updates touch (host side: chi is host-known anyway)
+  std::vector<std::vector<int>> qb;
 };
 
 // One boundary message between segment lanes (SEND_R: Psi'_{e+1}, Lambda'_e,
@@ -173,6 +180,7 @@ struct LaneMsg {
   cudaEvent_t posted = nullptr, consumed = nullptr;
   bool consumed_rec = false;
   BufPtr psi, lam, vinv, env;
+  std::vector<int> q;  // U(1) mode: charges of the bond the message updates
   ~LaneMsg() {
     if (posted) cudaEventDestroy(posted);
     if (consumed) cudaEventDestroy(consumed);
@@ -213,6 +221,8 @@ struct tdvp_ctx {
   // full-state host copy (multi-process initialisation)
   std::vector<std::vector<double>> h_psi, h_lam;
   std::vector<int> h_chi;
+  std::vector<std::vector<int>> h_q;  // U(1) mode: bond charges of the host copy (positions 0..L)
+  BufPtr u1_idx, u1_lam, u1_vinv;     // U(1) split: sector index lists, per-sector spectra
   // workspace
   long long n2max = 0, n1max = 0, scratch = 0, svdmax = 0, work_elems = 0;
   BufPtr theta, krylov, wvec, T1, T2, tmpA, tmpB, svdY, svdQ, svdF, gemm_work, partials;
@@ -548,6 +558,248 @@ void require_held(const Segment& g, int j) {
   if (!g.psi[j] || !g.beta[j] || !g.gamma[j]) throw TdvpError(TDVP_ECUDA, "internal: site not held by segment");
 }
 
+// ------------------------------------------------------------ U(1) split
+// (PAPER.md:643-651 symmetric block-sparse tensors).  With an
+// S^z-conserving MPO and a state of definite S^z every bond index carries a
+// charge q = 2 S^z of the sites to its left; the matrix to split is block
+// diagonal in the charge of the new bond (rows and columns carry it), so its
+// SVD is the union of the sector SVDs.  Each sector is gathered and split by
+// the dense path (svd_truncate_split, untruncated), the truncation rule O-7
+// (incl. AMB-9 / R-9b) is applied on the host to the union of all sectors'
+// singular values in descending order, exactly as the dense kernel does, and
+// the kept columns / rows are scattered into Psi_L / Psi_R, which keep exact
+// zeros outside their blocks.  Oracle: oracle/u1.py.
+constexpr int U1_C[2] = {1, -1};  // 2 S^z of the basis states (0 = up, 1 = down)
+
+__global__ void u1_gather_kernel(const cplx* __restrict__ M, long long ldm, const int* __restrict__ rows,
+                                 const int* __restrict__ cols, int mq, int nq, cplx* out) {
+  const long long total = (long long)mq * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / nq), k = (int)(e - (long long)i * nq);
+    out[e] = M[(long long)rows[i] * ldm + cols[k]];
+  }
+}
+// dst[rows[i]][kmap[k]] = src[i][k] (kmap[k] < 0: dropped), src mq x kq, dst ld ldd
+__global__ void u1_scatter_cols_kernel(const cplx* __restrict__ src, int mq, int kq, const int* __restrict__ rows,
+                                       const int* __restrict__ kmap, cplx* dst, long long ldd) {
+  const long long total = (long long)mq * kq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / kq), k = (int)(e - (long long)i * kq);
+    const int c = kmap[k];
+    if (c >= 0) dst[(long long)rows[i] * ldd + c] = src[e];
+  }
+}
+// dst[kmap[k]][cols[i]] = src[k][i], src kq x nq, dst ld ldd
+__global__ void u1_scatter_rows_kernel(const cplx* __restrict__ src, int kq, int nq, const int* __restrict__ cols,
+                                       const int* __restrict__ kmap, cplx* dst, long long ldd) {
+  const long long total = (long long)kq * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e / nq), i = (int)(e - (long long)k * nq);
+    const int c = kmap[k];
+    if (c >= 0) dst[(long long)c * ldd + cols[i]] = src[e];
+  }
+}
+
+// bond charges of the host MPS copy from its nonzero pattern (q[0] = {0});
+// TDVP_EARG if an index is reachable with two charges or none
+std::vector<std::vector<int>> infer_charges(const tdvp_ctx* h) {
+  const int L = h->L, d = h->d;
+  std::vector<std::vector<int>> q(L + 1);
+  q[0] = {0};
+  const int UNSET = std::numeric_limits<int>::min();
+  for (int j = 0; j < L; ++j) {
+    const int cl = h->h_chi[j], cr = h->h_chi[j + 1];
+    const std::vector<double>& t = h->h_psi[j];
+    q[j + 1].assign(cr, UNSET);
+    for (int a = 0; a < cl; ++a)
+      for (int s = 0; s < d; ++s)
+        for (int b = 0; b < cr; ++b) {
+          const size_t e = (((size_t)a * d + s) * cr + b) * 2;
+          if (t[e] == 0.0 && t[e + 1] == 0.0) continue;
+          const int v = q[j][a] + U1_C[s];
+          if (q[j + 1][b] == UNSET) q[j + 1][b] = v;
+          else if (q[j + 1][b] != v)
+            throw TdvpError(TDVP_EARG, "u1: the MPS is not of definite charge (bond " + std::to_string(j + 1) + ")");
+        }
+    for (int b = 0; b < cr; ++b)
+      if (q[j + 1][b] == UNSET) throw TdvpError(TDVP_EARG, "u1: a bond index with no nonzero entry");
+  }
+  return q;
+}
+
+int owner_of(tdvp_ctx* h, int j);
+// the bond charges of the current (laid-out) state, owner view
+std::vector<std::vector<int>> assemble_charges(tdvp_ctx* h) {
+  const int L = h->L;
+  std::vector<std::vector<int>> q(L + 1);
+  q[0] = {0};
+  for (int k = 1; k < L; ++k) q[k] = h->segs[owner_of(h, k - 1)].qb[k];
+  q[L] = h->segs[owner_of(h, L - 1)].qb[L];
+  return q;
+}
+
+inline int u1_grid(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 4LL * g_num_sms)); }
+
+// Split the m x n row-major matrix M (device) with row charges rq and column
+// charges cq: Psi_L (m x chi), Psi_R (chi x n), Lambda / V (chi), q_mid (chi).
+void u1_svd_split(tdvp_ctx* h, const cplx* M, int m, int n, const std::vector<int>& rq, const std::vector<int>& cq,
+                  const TruncParams& tp, cplx* psiL, cplx* psiR, double* lam, double* vinv, int& chi, double& w,
+                  int& r, int& chi_eps, std::vector<int>& q_mid, int& sweeps_sum) {
+  std::map<int, std::pair<std::vector<int>, std::vector<int>>> sec;
+  for (int i = 0; i < m; ++i) sec[rq[i]].first.push_back(i);
+  for (int k = 0; k < n; ++k) sec[cq[k]].second.push_back(k);
+  struct Sector {
+    int Q, mq, nq, kq = 0, idx_off = 0;
+    long long offL = 0, offR = 0;
+    std::vector<double> sig;
+  };
+  std::vector<Sector> ss;
+  std::vector<int> idx;  // rows then cols of every sector
+  for (auto& kv : sec) {
+    if (kv.second.first.empty() || kv.second.second.empty()) continue;
+    Sector t;
+    t.Q = kv.first;
+    t.mq = (int)kv.second.first.size();
+    t.nq = (int)kv.second.second.size();
+    t.idx_off = (int)idx.size();
+    idx.insert(idx.end(), kv.second.first.begin(), kv.second.first.end());
+    idx.insert(idx.end(), kv.second.second.begin(), kv.second.second.end());
+    ss.push_back(std::move(t));
+  }
+  if (ss.empty()) throw TdvpError(TDVP_ENUMERIC, "U(1) split: no charge sector carries weight");
+  if (idx.size() * sizeof(int) > h->u1_idx->bytes / 2) throw TdvpError(TDVP_ECUDA, "internal: U(1) index buffer");
+  int* didx = h->u1_idx->i();
+  CK(cudaMemcpyAsync(didx, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice, h->st));
+  const TruncParams full{std::max(m, n), 0.0, 0.0, 0.0};
+  cplx* stL = h->T1->c();
+  cplx* stR = h->T2->c();
+  long long offL = 0, offR = 0;
+  sweeps_sum = 0;
+  for (auto& t : ss) {
+    CK(cudaStreamSynchronize(h->st));  // idx upload / previous host reads done
+    u1_gather_kernel<<<u1_grid((long long)t.mq * t.nq), 256, 0, h->st>>>(M, n, didx + t.idx_off,
+                                                                         didx + t.idx_off + t.mq, t.mq, t.nq,
+                                                                         h->tmpA->c());
+    CK(cudaGetLastError());
+    int k = 0, rr = 0, ce = 0, sw = 0;
+    double ww = 0.0;
+    t.offL = offL;
+    t.offR = offR;
+    cudaError_t se = svd_truncate_split(h->st, h->sv, h->tmpA->c(), t.mq, t.nq, full, stL + offL, stR + offR,
+                                        h->u1_lam->d(), h->u1_vinv->d(), &k, &ww, &rr, &ce, &sw);
+    if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in a U(1) sector");
+    CK(se);
+    sweeps_sum += std::max(sw, 0);
+    t.kq = k;
+    t.sig.resize(k);
+    CK(cudaMemcpyAsync(t.sig.data(), h->u1_lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    offL += (long long)t.mq * k;
+    offR += (long long)k * t.nq;
+  }
+  // global order: descending sigma, ties by sector charge then index (oracle/u1.py)
+  struct Ent { double s; int sec, k; };
+  std::vector<Ent> all;
+  for (int si = 0; si < (int)ss.size(); ++si)
+    for (int k = 0; k < ss[si].kq; ++k) all.push_back(Ent{ss[si].sig[k], si, k});
+  std::stable_sort(all.begin(), all.end(), [&](const Ent& a, const Ent& b) {
+    if (a.s != b.s) return a.s > b.s;
+    if (ss[a.sec].Q != ss[b.sec].Q) return ss[a.sec].Q < ss[b.sec].Q;
+    return a.k < b.k;
+  });
+  r = (int)all.size();
+  const double s1 = all[0].s;
+  if (!(s1 > 0.0) || !std::isfinite(s1)) throw TdvpError(TDVP_ENUMERIC, "U(1) split: zero or non-finite spectrum");
+  // the truncation rule O-7 with AMB-9 / R-9b (as svd_truncate_kernel)
+  const double eps = tp.eps > 0.0 ? tp.eps : 1e-14;
+  int nz = 0;
+  chi_eps = 0;
+  for (auto& e : all) {
+    chi_eps += (e.s >= eps * s1);
+    nz += (e.s > 0.0);
+  }
+  int chi_w = nz;
+  if (tp.w_max > 0.0) {
+    std::vector<double> tail(r + 1, 0.0);
+    for (int k = r - 1; k >= 0; --k) tail[k] = tail[k + 1] + all[k].s * all[k].s;
+    for (int c = 0; c <= r; ++c)
+      if (tail[c] <= tp.w_max) { chi_w = c; break; }
+    chi_w = std::max(chi_w, 1);
+  }
+  chi = std::max(1, std::min(std::min(chi_eps, chi_w), tp.chi_max));
+  while (chi > 1 && chi < r && all[chi - 1].s - all[chi].s <= tp.delta * all[chi - 1].s + 1e-13 * s1) --chi;
+  w = 0.0;
+  for (int k = chi; k < r; ++k) w += all[k].s * all[k].s;
+  // scatter the kept triplets; lam / V / charges in the global order
+  CK(cudaMemsetAsync(psiL, 0, (size_t)m * chi * sizeof(cplx), h->st));
+  CK(cudaMemsetAsync(psiR, 0, (size_t)chi * n * sizeof(cplx), h->st));
+  std::vector<int> kmap(offL > 0 ? 0 : 0);
+  std::vector<std::vector<int>> km(ss.size());
+  for (int si = 0; si < (int)ss.size(); ++si) km[si].assign(ss[si].kq, -1);
+  std::vector<double> hl(chi), hv(chi);
+  q_mid.assign(chi, 0);
+  for (int c = 0; c < chi; ++c) {
+    km[all[c].sec][all[c].k] = c;
+    hl[c] = all[c].s;
+    hv[c] = 1.0 / all[c].s;
+    q_mid[c] = ss[all[c].sec].Q;
+  }
+  std::vector<int> kflat;
+  std::vector<int> koff(ss.size());
+  for (int si = 0; si < (int)ss.size(); ++si) {
+    koff[si] = (int)kflat.size();
+    kflat.insert(kflat.end(), km[si].begin(), km[si].end());
+  }
+  int* dk = didx + (h->u1_idx->bytes / 2) / sizeof(int);  // second half of the index buffer
+  CK(cudaMemcpyAsync(dk, kflat.data(), std::max<size_t>(1, kflat.size()) * sizeof(int), cudaMemcpyHostToDevice, h->st));
+  for (int si = 0; si < (int)ss.size(); ++si) {
+    const Sector& t = ss[si];
+    if (t.kq == 0) continue;
+    u1_scatter_cols_kernel<<<u1_grid((long long)t.mq * t.kq), 256, 0, h->st>>>(stL + t.offL, t.mq, t.kq,
+                                                                               didx + t.idx_off, dk + koff[si], psiL,
+                                                                               chi);
+    u1_scatter_rows_kernel<<<u1_grid((long long)t.kq * t.nq), 256, 0, h->st>>>(stR + t.offR, t.kq, t.nq,
+                                                                               didx + t.idx_off + t.mq,
+                                                                               dk + koff[si], psiR, n);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(lam, hl.data(), chi * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(vinv, hv.data(), chi * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
+}
+
+// row / column charges of the two-site matrix of pair (j, j+1): rows (a, s1),
+// columns (s2, b) (AMB-17)
+void u1_pair_charges(const Segment& g, int j, int d, std::vector<int>& rq, std::vector<int>& cq) {
+  const std::vector<int>& qa = g.qb[j];
+  const std::vector<int>& qc = g.qb[j + 2];
+  const int cl = g.cb[j], cr = g.cb[j + 2];
+  if ((int)qa.size() != cl || (int)qc.size() != cr) throw TdvpError(TDVP_ECUDA, "internal: U(1) charges out of date");
+  rq.resize((size_t)cl * d);
+  cq.resize((size_t)d * cr);
+  for (int a = 0; a < cl; ++a)
+    for (int s = 0; s < d; ++s) rq[(size_t)a * d + s] = qa[a] + U1_C[s];
+  for (int s = 0; s < d; ++s)
+    for (int b = 0; b < cr; ++b) cq[(size_t)s * cr + b] = qc[b] - U1_C[s];
+}
+
+// the split of a two-site update: dense or sector-wise (U(1))
+cudaError_t split_theta(tdvp_ctx* h, Segment& g, int j, const cplx* th2, int cl, int cr, const TruncParams& tp,
+                        int& chi, double& w, int& r, int& chi_eps, int& sweeps, float* jac_ms, double* jac_flop) {
+  const int d = h->d;
+  if (!h->prm.u1)
+    return svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]), g.lam[j]->d(),
+                              g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps, jac_ms, jac_flop);
+  std::vector<int> rq, cq, qm;
+  u1_pair_charges(g, j, d, rq, cq);
+  u1_svd_split(h, th2, cl * d, d * cr, rq, cq, tp, P(g.psi[j]), P(g.psi[j + 1]), g.lam[j]->d(), g.vinv[j]->d(), chi, w,
+               r, chi_eps, qm, sweeps);
+  g.qb[j + 1] = qm;
+  if (jac_flop) *jac_flop = 0.0;
+  if (jac_ms) *jac_ms = 0.f;
+  return cudaSuccess;
+}
+
 // two-site forward update of (j, j+1) (SURVEY O-6)
 void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build) {
   const int d = h->d;
@@ -583,9 +835,8 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   double w = 0.0;
   float jac_ms = 0.f;
   double jac_flop = 0.0;
-  cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
-                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps,
-                                      h->prm.timing ? &jac_ms : nullptr, &jac_flop);
+  cudaError_t se = split_theta(h, g, j, th2, cl, cr, tp, chi, w, r, chi_eps, sweeps, h->prm.timing ? &jac_ms : nullptr,
+                               &jac_flop);
   if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
   CK(se);
   g_launch_count += 5;
@@ -666,8 +917,7 @@ void dmrg_pair(tdvp_ctx* h, Segment& g, int j, int build, int restarts) {
   TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
   int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
   double w = 0.0;
-  cudaError_t se = svd_truncate_split(h->st, h->sv, th2, cl * d, d * cr, tp, P(g.psi[j]), P(g.psi[j + 1]),
-                                      g.lam[j]->d(), g.vinv[j]->d(), &chi, &w, &r, &chi_eps, &sweeps);
+  cudaError_t se = split_theta(h, g, j, th2, cl, cr, tp, chi, w, r, chi_eps, sweeps, nullptr, nullptr);
   if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(j));
   CK(se);
   if (chi > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: chi exceeds allocation");
@@ -765,6 +1015,12 @@ void upload_state(tdvp_ctx* h) {
     DeviceGuard dg(g.dev);
     cudaStream_t st = g.dev == h->dev ? h->st : lane_of(h, g.q)->st;
     g.cb = h->h_chi;
+    if (h->prm.u1) {
+      if ((int)h->h_q.size() != L + 1) h->h_q = infer_charges(h);
+      g.qb = h->h_q;
+    } else {
+      g.qb.clear();
+    }
     const int hi = std::min(g.e + 1, L - 1);
     for (int j = g.s; j <= hi; ++j)
       CK(cudaMemcpyAsync(g.psi[j]->p, h->h_psi[j].data(), h->h_psi[j].size() * sizeof(double), cudaMemcpyHostToDevice,
@@ -789,6 +1045,7 @@ void download_state(tdvp_ctx* h) {
   for (int b = 0; b < L - 1; ++b) chi[b + 1] = h->segs[owner_of(h, b)].cb[b + 1];  // left owner owns bond b
   h->h_chi = chi;
   CK(cudaStreamSynchronize(h->st));  // every lane's work was joined into h->st by the step
+  if (h->prm.u1 && !h->segs.empty() && !h->segs[0].qb.empty()) h->h_q = assemble_charges(h);
   for (int j = 0; j < L; ++j) {
     Segment& g = h->segs[owner_of(h, j)];
     const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
@@ -907,6 +1164,7 @@ void send_right_local(tdvp_ctx* h, Segment& a, Segment& b) {
   const int e = a.e, d = h->d;
   const int chi = a.cb[e + 1], cr = a.cb[e + 2];
   b.cb[e + 1] = chi;
+  if (h->prm.u1) b.qb[e + 1] = a.qb[e + 1];
   copy_buf(h, b.psi[e + 1], a.psi[e + 1], (size_t)chi * d * cr * sizeof(cplx));
   copy_buf(h, b.lam[e], a.lam[e], (size_t)chi * sizeof(double));
   copy_buf(h, b.vinv[e], a.vinv[e], (size_t)chi * sizeof(double));
@@ -918,6 +1176,7 @@ void send_left_local(tdvp_ctx* h, Segment& b, Segment& a) {
   const int cl = b.cb[s], cr = b.cb[s + 1];
   a.cb[s + 1] = cr;
   a.cb[s] = cl;
+  if (h->prm.u1) a.qb[s + 1] = b.qb[s + 1];
   copy_buf(h, a.psi[s], b.psi[s], (size_t)cl * d * cr * sizeof(cplx));
   copy_buf(h, a.gamma[s], b.gamma[s], (size_t)cr * h->mpo[s].Dr * cr * sizeof(cplx));
 }
@@ -1158,6 +1417,7 @@ void lane_send_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<boo
   CK(cudaEventRecord(m.posted, ln->st));
   m.meta[0] = chi;
   m.meta[1] = cr;
+  if (ln->prm.u1) m.q = a.qb[e + 1];
   lane_post(m, 1, false);
 }
 void lane_recv_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool>& abort) {
@@ -1165,6 +1425,7 @@ void lane_recv_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool
   CK(cudaStreamWaitEvent(ln->st, m.posted, 0));
   const int e = b.s - 1, d = ln->d, chi = m.meta[0], cr = m.meta[1];
   b.cb[e + 1] = chi;
+  if (ln->prm.u1) b.qb[e + 1] = m.q;
   lane_copy(ln, b.psi[e + 1]->p, m.psi->p, (size_t)chi * d * cr * sizeof(cplx));
   lane_copy(ln, b.lam[e]->p, m.lam->p, (size_t)chi * sizeof(double));
   lane_copy(ln, b.vinv[e]->p, m.vinv->p, (size_t)chi * sizeof(double));
@@ -1182,6 +1443,7 @@ void lane_send_left(tdvp_ctx* ln, Segment& b, LaneMsg& m, const std::atomic<bool
   CK(cudaEventRecord(m.posted, ln->st));
   m.meta[0] = cl;
   m.meta[1] = cr;
+  if (ln->prm.u1) m.q = b.qb[s + 1];
   lane_post(m, 1, false);
 }
 void lane_recv_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<bool>& abort) {
@@ -1190,6 +1452,7 @@ void lane_recv_right(tdvp_ctx* ln, Segment& a, LaneMsg& m, const std::atomic<boo
   const int s = a.e + 1, d = ln->d, cl = m.meta[0], cr = m.meta[1];
   a.cb[s] = cl;
   a.cb[s + 1] = cr;
+  if (ln->prm.u1) a.qb[s + 1] = m.q;
   lane_copy(ln, a.psi[s]->p, m.psi->p, (size_t)cl * d * cr * sizeof(cplx));
   lane_copy(ln, a.gamma[s]->p, m.env->p, (size_t)cr * ln->mpo[s].Dr * cr * sizeof(cplx));
   CK(cudaEventRecord(m.consumed, ln->st));
@@ -1333,6 +1596,7 @@ void reorthonormalize(tdvp_ctx* h);
 void do_step(tdvp_ctx* h, double dt, int p) {
   if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step");
   if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
+  if (h->prm.u1 && !local_mode(h)) throw TdvpError(TDVP_EARG, "u1 is not supported across ranks (use one process)");
   // dynamic load balancing ("dynamic load balancer"):
   // before the step, re-partition when the chi-weighted optimum beats the
   // current partition's largest segment cost by the relative margin
@@ -1536,6 +1800,9 @@ void alloc_workspace(tdvp_ctx* h) {
   h->svd_order = make_buf(ncmax * sizeof(int) + 64);
   h->svd_perm = make_buf(2 * ncmax * sizeof(int) + 64);
   h->svd_bj = make_buf(svd_bjac_work_elems(g_num_sms) * sizeof(cplx));
+  h->u1_idx = make_buf((size_t)2 * (4 * ncmax + 64) * sizeof(int));
+  h->u1_lam = make_buf(ncmax * sizeof(double) + 64);
+  h->u1_vinv = make_buf(ncmax * sizeof(double) + 64);
   h->svd_off = make_buf(64);
   h->svd_ires = make_buf(64);
   h->svd_dres = make_buf(64);
@@ -1644,18 +1911,34 @@ void reorthonormalize(tdvp_ctx* h) {
     BufPtr vin = make_buf((size_t)(2 * h->chi_max + 8) * sizeof(double));
     std::vector<std::vector<double>> hlam(L - 1);
     const TruncParams tp{h->chi_max, 0.0, 0.0, 0.0};
-    auto svd = [&](const cplx* M, int m, int n, int& k) {
+    std::vector<std::vector<int>> q;
+    if (h->prm.u1) q = assemble_charges(h);
+    // U(1) mode: rq / cq are the row / column charges, the kept vectors' charges come back in qm
+    auto svd = [&](const cplx* M, int m, int n, int& k, const std::vector<int>* rq, const std::vector<int>* cq,
+                   std::vector<int>* qm) {
       int r = 0, ce = 0, sw = 0;
       double w = 0.0;
+      if (h->prm.u1) {
+        u1_svd_split(h, M, m, n, *rq, *cq, tp, pl->c(), pr->c(), lam->d(), vin->d(), k, w, r, ce, *qm, sw);
+        return;
+      }
       cudaError_t se = svd_truncate_split(h->st, h->sv, M, m, n, tp, pl->c(), pr->c(), lam->d(), vin->d(), &k, &w, &r,
                                           &ce, &sw);
       if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "SVD numerical failure in reorthonormalisation");
       CK(se);
     };
+    std::vector<int> rq, cq, qm;
     // L -> R: A_j = U S W^dagger  ->  A_j = U,  A_{j+1} = (S W^dagger) A_{j+1}
     for (int j = 0; j + 1 < L; ++j) {
       int k = 0;
-      svd(A[j]->c(), chi[j] * d, chi[j + 1], k);
+      if (h->prm.u1) {
+        rq.resize((size_t)chi[j] * d);
+        for (int a = 0; a < chi[j]; ++a)
+          for (int s2 = 0; s2 < d; ++s2) rq[(size_t)a * d + s2] = q[j][a] + U1_C[s2];
+        cq = q[j + 1];
+      }
+      svd(A[j]->c(), chi[j] * d, chi[j + 1], k, &rq, &cq, &qm);
+      if (h->prm.u1) q[j + 1] = qm;
       if (k > h->cbmax[j + 1]) throw TdvpError(TDVP_ECUDA, "internal: reorthonormalisation rank");
       BufPtr U = make_buf((size_t)chi[j] * d * k * sizeof(cplx));
       CK(scale_cols(h->st, U->c(), pl->c(), vin->d(), (long long)chi[j] * d, k));
@@ -1670,7 +1953,14 @@ void reorthonormalize(tdvp_ctx* h) {
     // R -> L: A_j = U S W^dagger  ->  B_j = W^dagger, Lambda_{j-1} = S, A_{j-1} = A_{j-1} (U S)
     for (int j = L - 1; j >= 1; --j) {
       int k = 0;
-      svd(A[j]->c(), chi[j], d * chi[j + 1], k);
+      if (h->prm.u1) {
+        rq = q[j];
+        cq.resize((size_t)d * chi[j + 1]);
+        for (int s2 = 0; s2 < d; ++s2)
+          for (int b = 0; b < chi[j + 1]; ++b) cq[(size_t)s2 * chi[j + 1] + b] = q[j + 1][b] - U1_C[s2];
+      }
+      svd(A[j]->c(), chi[j], d * chi[j + 1], k, &rq, &cq, &qm);
+      if (h->prm.u1) q[j] = qm;
       BufPtr B = make_buf((size_t)k * d * chi[j + 1] * sizeof(cplx));
       CK(scale_rows(h->st, B->c(), pr->c(), vin->d(), k, (long long)d * chi[j + 1]));
       gemm(h, OP_N, OP_N, chi[j - 1] * d, k, chi[j], A[j - 1]->c(), chi[j], pl->c(), k, tmp->c(), k);
@@ -1705,6 +1995,7 @@ void reorthonormalize(tdvp_ctx* h) {
     h->h_psi = std::move(hpsi);
     h->h_lam = std::move(hlam);
     h->h_chi = chi;
+    if (h->prm.u1) h->h_q = q;
     h->envs_valid = false;
     h->layout_p = 0;  // re-layout: upload + sequential environment build at the next call
   }
@@ -1865,6 +2156,21 @@ int tdvp_set_params(tdvp_t h, const tdvp_params* p) {
   } catch (const TdvpError& e) {
     return fail(h, e);
   }
+  if (p->u1 && h->d != 2) {
+    h->err = "u1 needs d = 2 (spin-1/2 charges)";
+    return TDVP_EARG;
+  }
+  if (!!p->u1 != !!h->prm.u1 && h->layout_p != 0) {
+    // switching the U(1) mode re-lays the state out (charges inferred / dropped)
+    try {
+      if (h->have_mps && local_mode(h)) download_state(h);
+    } catch (const TdvpError& e) {
+      return fail(h, e);
+    }
+    h->layout_p = 0;
+    h->envs_valid = false;
+    h->h_q.clear();
+  }
   h->prm = *p;
   h->prm.n_devices = (int)h->devs.size();
   h->prm.device_ids = h->devs.data();
@@ -1939,6 +2245,7 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     for (int j = 0; j < L; ++j) h->h_psi[j].assign(Psi[j], Psi[j] + (size_t)chi[j] * d * chi[j + 1] * 2);
     for (int b = 0; b < L - 1; ++b) h->h_lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
     h->h_chi.assign(chi, chi + L + 1);
+    h->h_q.clear();  // U(1) charges are re-inferred at the next layout
     h->have_mps = true;
     h->evolved = false;
     h->envs_valid = false;

@@ -40,7 +40,7 @@ class TdvpError(RuntimeError):
 class tdvp_params(C.Structure):
     _fields_ = [("eps", C.c_double), ("w_max", C.c_double), ("krylov_k", C.c_int), ("krylov_tol", C.c_double),
                 ("multiplet_delta", C.c_double), ("timing", C.c_int), ("n_devices", C.c_int),
-                ("device_ids", C.POINTER(C.c_int)), ("rebalance", C.c_double)]
+                ("device_ids", C.POINTER(C.c_int)), ("rebalance", C.c_double), ("u1", C.c_int)]
 
 
 class tdvp_stats(C.Structure):
@@ -156,11 +156,11 @@ class Tdvp:
     __del__ = close
 
     def set_params(self, eps=1e-12, w_max=0.0, krylov_k=8, multiplet_delta=1e-6, timing=False, krylov_tol=0.0,
-                   rebalance=0.0):
+                   rebalance=0.0, u1=False):
         nd = len(self.devices)
         ids = (C.c_int * max(1, nd))(*(self.devices or [0]))
         p = tdvp_params(eps, w_max, krylov_k, krylov_tol, multiplet_delta, int(bool(timing)), nd if nd > 1 else 1,
-                        ids, float(rebalance))
+                        ids, float(rebalance), int(bool(u1)))
         _check(lib().tdvp_set_params(self.h, C.byref(p)), self.h)
 
     def set_mpo(self, W):
