@@ -225,6 +225,33 @@ def timed_steps(t, dt, p, k):
     return out
 
 
+def secondary_u1(pkg, steps, warmup):
+    """configs[4] shapes with a state of definite S^z_tot (the Neel sector of
+    configs 1/2/3/5): a saturated random U(1) MPS (L = 24, chi_max = 1024), the
+    dense path vs the U(1) block-sparse splits."""
+    import tdvp_inputs as ti
+    L, chi, dt = 24, 1024, 0.05
+    mps = ti.random_u1_mps(L, chi, seed=2)
+    W = ti.mpo_xxz_nn(L, 1.0)
+    res = {"desc": "L=24 XXX D=5 chi_max=1024 eps=1e-12 dt=0.05, seeded random S^z_tot=0 MPS at saturated chi "
+                   "(tdvp_inputs.random_u1_mps)", "chi_profile": [1] + [len(x) for x in mps.lam] + [1]}
+    for u1 in (False, True):
+        t = pkg.Tdvp(L, 2, 5, chi)
+        t.set_params(eps=1e-12, u1=u1)
+        t.set_mpo(W)
+        t.set_mps(mps.psi, mps.lam)
+        for _ in range(warmup):
+            t.step(dt, 1)
+        per = timed_steps(t, dt, 1, steps)
+        t.set_params(eps=1e-12, u1=u1, timing=True)
+        pt = timed_steps(t, dt, 1, 1)[0]
+        res["u1" if u1 else "dense"] = {"ms_per_step": float(np.mean([x["step_ms"] for x in per])),
+                                       "svd_ms_per_step": pt["svd_ms"], "steps": steps}
+        t.close()
+    res["speedup"] = res["dense"]["ms_per_step"] / res["u1"]["ms_per_step"]
+    return res
+
+
 def secondary_c2sat(pkg, steps, warmup):
     """Round 1's chi=128 headline (configs[1] shapes), serial and as 8 segment lanes on this GPU."""
     wl = workload_inputs("c2sat")
@@ -437,6 +464,7 @@ def main():
     }
     if not args.no_extras and world == 1 and n_gpus == 1:
         line["secondary_c2sat"] = secondary_c2sat(pkg, max(1, min(args.steps, 5)), 2)
+        line["secondary_u1"] = secondary_u1(pkg, 2, 1)
     if not args.no_cpu_baseline and world == 1 and n_gpus == 1:
         line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line))
