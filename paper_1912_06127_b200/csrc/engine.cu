@@ -198,6 +198,15 @@ struct tdvp_ctx {
   int L = 0, d = 0, Dmpo = 0, chi_max = 0;
   tdvp_params prm{};
   const double* cur_skip = nullptr;  // inside a paper-mode Lanczos: its device "converged" flag
+  // U(1) mode: block masks of the first and last GEMM of the H_eff matvec in
+  // progress (set around a Lanczos exponential, nullptr otherwise)
+  const GemmMask* cur_mask[2] = {nullptr, nullptr};
+  struct MaskSet {
+    std::vector<unsigned char> ha, hb;
+    BufPtr da, db;
+    GemmMask g;
+  } masks[2];
+  std::vector<std::vector<int>> h_r;  // MPO channel charges per bond position (U(1)); empty = not conserving
   int dev = 0;
   // devices of a multi-device handle (tdvp_params.n_devices / device_ids):
   // segment q of a p-segment step lives on devs[q * n / p]; devs[0] = dev
@@ -302,9 +311,9 @@ int ev_record(tdvp_ctx* h) {
 }
 
 void gemm(tdvp_ctx* h, int opA, int opB, int M, int N, int K, const cplx* A, long long lda, const cplx* B,
-          long long ldb, cplx* C, long long ldc) {
+          long long ldb, cplx* C, long long ldc, const GemmMask* mask = nullptr) {
   CK(zgemm(h->st, opA, opB, M, N, K, ONE, A, lda, B, ldb, ZERO, C, ldc, 1, 0, 0, 0, h->gemm_work->c(),
-           (size_t)h->work_elems, h->cur_skip));
+           (size_t)h->work_elems, h->cur_skip, mask));
   g_gemm_count++;
   g_launch_count++;
 }
@@ -441,13 +450,15 @@ void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, 
   cplx* T1 = h->T1->c();
   cplx* T2 = h->T2->c();
   // stage 1: T1[(a,w),(t1,t2,b')] = L[(a,w),a'] x[a',(t1,t2,b')]
-  gemm(h, OP_N, OP_N, cl * Dl, d * d * cr, cl, Lenv, cl, x, (long long)d * d * cr, T1, (long long)d * d * cr);
+  gemm(h, OP_N, OP_N, cl * Dl, d * d * cr, cl, Lenv, cl, x, (long long)d * d * cr, T1, (long long)d * d * cr,
+       h->cur_mask[0]);
   if (W1.has12) {
     // stages 2+3 in one pass: T3[a][s1][s2][w''][b'] = sum W12[(w,t1,t2) -> (s1,s2,w'')] T1[a][w][t1][t2][b']
     cmix(h, W1.cm12, cl, cr, T1, (long long)Dl * d * d * cr, 1,
          Strides3{(long long)d * d * cr, (long long)d * cr, (long long)cr}, T2, (long long)d * d * Dr * cr, 1,
          Strides3{(long long)d * Dr * cr, (long long)Dr * cr, (long long)cr});
-    gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+    gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr,
+         h->cur_mask[1]);
     return;
   }
   // stage 2: T2[a][s1][w'][(t2,b')] = sum W1[w,s1,t1,w'] T1[a][w][t1][(t2,b')]
@@ -457,7 +468,8 @@ void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, 
   cmix(h, W2.cmL, cl * d, cr, T2, (long long)Dm * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T1,
        (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
   // stage 4: y[(a,s1,s2), b] = T3[(a,s1,s2),(w'',b')] R[b,(w'',b')]^T
-  gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T1, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+  gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T1, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr,
+       h->cur_mask[1]);
 }
 
 // H_eff^(1) x: x, y (cl, d, cr)
@@ -465,10 +477,10 @@ void heff1(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W, const cplx* Renv, in
   const int d = h->d, Dl = W.Dl, Dr = W.Dr;
   cplx* T1 = h->T1->c();
   cplx* T2 = h->T2->c();
-  gemm(h, OP_N, OP_N, cl * Dl, d * cr, cl, Lenv, cl, x, (long long)d * cr, T1, (long long)d * cr);
+  gemm(h, OP_N, OP_N, cl * Dl, d * cr, cl, Lenv, cl, x, (long long)d * cr, T1, (long long)d * cr, h->cur_mask[0]);
   cmix(h, W.cmL, cl, cr, T1, (long long)Dl * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T2,
        (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
-  gemm(h, OP_N, OP_T, cl * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr);
+  gemm(h, OP_N, OP_T, cl * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr, h->cur_mask[1]);
 }
 
 // beta'[b,w',b'] = sum conj(A[a,s,b]) beta[a,w,a'] W[w,s,t,w'] A[a',t,b']
@@ -730,7 +742,14 @@ void u1_svd_split(tdvp_ctx* h, const cplx* M, int m, int n, const std::vector<in
   while (chi > 1 && chi < r && all[chi - 1].s - all[chi].s <= tp.delta * all[chi - 1].s + 1e-13 * s1) --chi;
   w = 0.0;
   for (int k = chi; k < r; ++k) w += all[k].s * all[k].s;
-  // scatter the kept triplets; lam / V / charges in the global order
+  // the kept triplets ordered by charge (ascending), then sigma (descending):
+  // every bond basis stays sorted by charge, so the U(1) blocks of the next
+  // contractions are contiguous and the GEMM block masks skip them whole
+  std::stable_sort(all.begin(), all.begin() + chi, [&](const Ent& a, const Ent& b) {
+    if (ss[a.sec].Q != ss[b.sec].Q) return ss[a.sec].Q < ss[b.sec].Q;
+    return a.s > b.s;
+  });
+  // scatter the kept triplets; lam / V / charges in that order
   CK(cudaMemsetAsync(psiL, 0, (size_t)m * chi * sizeof(cplx), h->st));
   CK(cudaMemsetAsync(psiR, 0, (size_t)chi * n * sizeof(cplx), h->st));
   std::vector<int> kmap(offL > 0 ? 0 : 0);
@@ -783,6 +802,96 @@ void u1_pair_charges(const Segment& g, int j, int d, std::vector<int>& rq, std::
     for (int b = 0; b < cr; ++b) cq[(size_t)s * cr + b] = qc[b] - U1_C[s];
 }
 
+// Block masks of op(A) = rows x k and op(B) = k x cols for a U(1)-blocked
+// product: an element of op(A) can be nonzero only if its row charge equals
+// its k charge, of op(B) only if its k charge equals its column charge
+// (charges in one common frame; INT_MIN = unknown = matches every charge).
+// 32-row / 8-k / 32-column blocks as GemmMask expects; uploaded on h->st.
+void build_mask(tdvp_ctx* h, tdvp_ctx::MaskSet& ms, const std::vector<int>& rq, const std::vector<int>& kq,
+                const std::vector<int>& cq) {
+  const int M = (int)rq.size(), K = (int)kq.size(), N = (int)cq.size();
+  const int mb = (M + 31) / 32, kb = (K + 7) / 8, nb = (N + 31) / 32;
+  int lo = 0, hi = 0;
+  bool first = true;
+  for (const auto* v : {&rq, &kq, &cq})
+    for (int x : *v)
+      if (x != std::numeric_limits<int>::min()) {
+        lo = first ? x : std::min(lo, x);
+        hi = first ? x : std::max(hi, x);
+        first = false;
+      }
+  const int W = (hi - lo) / 64 + 1;
+  auto sets = [&](const std::vector<int>& q, int blk, int nblk) {
+    std::vector<uint64_t> out((size_t)nblk * W, 0);
+    for (int i = 0; i < (int)q.size(); ++i) {
+      uint64_t* w = out.data() + (size_t)(i / blk) * W;
+      if (q[i] == std::numeric_limits<int>::min()) {
+        for (int k = 0; k < W; ++k) w[k] = ~0ull;
+      } else {
+        const int o = q[i] - lo;
+        w[o / 64] |= 1ull << (o % 64);
+      }
+    }
+    return out;
+  };
+  const std::vector<uint64_t> sr = sets(rq, 32, mb), sk = sets(kq, 8, kb), sc = sets(cq, 32, nb);
+  auto meet = [&](const uint64_t* a, const uint64_t* b) {
+    for (int k = 0; k < W; ++k)
+      if (a[k] & b[k]) return 1;
+    return 0;
+  };
+  ms.ha.assign((size_t)mb * kb, 0);
+  ms.hb.assign((size_t)kb * nb, 0);
+  for (int r = 0; r < mb; ++r)
+    for (int k = 0; k < kb; ++k) ms.ha[(size_t)r * kb + k] = (unsigned char)meet(&sr[(size_t)r * W], &sk[(size_t)k * W]);
+  for (int k = 0; k < kb; ++k)
+    for (int c = 0; c < nb; ++c) ms.hb[(size_t)k * nb + c] = (unsigned char)meet(&sk[(size_t)k * W], &sc[(size_t)c * W]);
+  if (!ms.da || ms.da->bytes < ms.ha.size()) ms.da = make_buf(ms.ha.size() + 64);
+  if (!ms.db || ms.db->bytes < ms.hb.size()) ms.db = make_buf(ms.hb.size() + 64);
+  CK(cudaMemcpyAsync(ms.da->p, ms.ha.data(), ms.ha.size(), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(ms.db->p, ms.hb.data(), ms.hb.size(), cudaMemcpyHostToDevice, h->st));
+  ms.g.a = reinterpret_cast<const unsigned char*>(ms.da->p);
+  ms.g.b = reinterpret_cast<const unsigned char*>(ms.db->p);
+  ms.g.ldA = kb;
+  ms.g.ldB = nb;
+}
+
+// the masks of the two dense GEMMs of H_eff^(2) (pair j) or H_eff^(1) (site j)
+// in U(1) mode (charge frames derived in DESIGN.md §N1): stage 1
+// beta[(a,w),a'] theta[a',(t..,b')]: rows q(a) - r(w), k q(a'), columns
+// q(b') - sum c(t); last stage T[(a,s..),(w',b')] R^T[(w',b'),b]: rows
+// q(a) + sum c(s), k q(b') + r(w'), columns q(b).  Returns false (dense) when
+// the MPO's channel charges are unknown.
+bool set_heff_masks(tdvp_ctx* h, const Segment& g, int j, int nsite) {
+  const int d = h->d, L = h->L;
+  const tdvp_ctx* root = h->parent ? h->parent : h;
+  if (!h->prm.u1 || (int)root->h_r.size() != L + 1) return false;
+  const std::vector<int>& qa = g.qb[j];
+  const std::vector<int>& qb = g.qb[j + nsite];
+  const std::vector<int>& rl = root->h_r[j];
+  const std::vector<int>& rr = root->h_r[j + nsite];
+  const int cl = g.cb[j], cr = g.cb[j + nsite], Dl = (int)rl.size(), Dr = (int)rr.size();
+  if ((int)qa.size() != cl || (int)qb.size() != cr) return false;
+  const int UNK = std::numeric_limits<int>::min();
+  const int ns = nsite == 2 ? d * d : d;
+  auto csum = [&](int idx) { return nsite == 2 ? U1_C[idx / d] + U1_C[idx % d] : U1_C[idx]; };
+  std::vector<int> rq((size_t)cl * Dl), kq(qa.begin(), qa.end()), cq((size_t)ns * cr);
+  for (int a = 0; a < cl; ++a)
+    for (int w = 0; w < Dl; ++w) rq[(size_t)a * Dl + w] = rl[w] == UNK ? UNK : qa[a] - rl[w];
+  for (int t = 0; t < ns; ++t)
+    for (int b = 0; b < cr; ++b) cq[(size_t)t * cr + b] = qb[b] - csum(t);
+  build_mask(h, h->masks[0], rq, kq, cq);
+  std::vector<int> rq2((size_t)cl * ns), kq2((size_t)Dr * cr);
+  for (int a = 0; a < cl; ++a)
+    for (int t = 0; t < ns; ++t) rq2[(size_t)a * ns + t] = qa[a] + csum(t);
+  for (int w = 0; w < Dr; ++w)
+    for (int b = 0; b < cr; ++b) kq2[(size_t)w * cr + b] = rr[w] == UNK ? UNK : qb[b] + rr[w];
+  build_mask(h, h->masks[1], rq2, kq2, qb);
+  h->cur_mask[0] = &h->masks[0].g;
+  h->cur_mask[1] = &h->masks[1].g;
+  return true;
+}
+
 // the split of a two-site update: dense or sector-wise (U(1))
 cudaError_t split_theta(tdvp_ctx* h, Segment& g, int j, const cplx* th2, int cl, int cr, const TruncParams& tp,
                         int& chi, double& w, int& r, int& chi_eps, int& sweeps, float* jac_ms, double* jac_flop) {
@@ -823,9 +932,11 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   }
   cplx* th2 = h->tmpB->c();
   const int el0 = h->prm.timing ? ev_record(h) : -1;
+  set_heff_masks(h, g, j, 2);
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, 0.0, -tau,
       h->prm.krylov_k, 2, fl);
+  h->cur_mask[0] = h->cur_mask[1] = nullptr;
   if (el0 >= 0) h->ev_lz2.emplace_back(el0, ev_record(h));
   // a4: truncated SVD split
   int e0 = -1;
@@ -911,9 +1022,11 @@ void dmrg_pair(tdvp_ctx* h, Segment& g, int j, int build, int restarts) {
   const cplx* Lenv = P(g.beta[j]);
   const cplx* Renv = P(g.gamma[j + 1]);
   cplx* th2 = h->tmpB->c();
+  set_heff_masks(h, g, j, 2);
   ground_lanczos(
       h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, h->prm.krylov_k,
       restarts);
+  h->cur_mask[0] = h->cur_mask[1] = nullptr;
   TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
   int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
   double w = 0.0;
@@ -946,9 +1059,11 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   g_launch_count++;
   const double fl = flops_heff1(cl, cr, d, W.Dl, W.Dr, nnz_of(W));
   const int el0 = h->prm.timing ? ev_record(h) : -1;
+  set_heff_masks(h, g, j, 1);
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff1(h, Lenv, W, Renv, cl, cr, x, y); }, h->tmpB->c(), P(g.psi[j]), n, 0.0,
       0.5 * dt, h->prm.krylov_k, 1, fl);
+  h->cur_mask[0] = h->cur_mask[1] = nullptr;
   if (el0 >= 0) h->ev_lz1.emplace_back(el0, ev_record(h));
   h->stats.n_back++;
 }
@@ -2203,6 +2318,32 @@ int tdvp_set_mpo(tdvp_t h, const int* D, const double* const* W) {
     build_mpo_tables(mpo, L, d, h->h_D, hw);
     h->h_W = std::move(hw);
     h->mpo = std::move(mpo);
+    // U(1): channel charges r(w') = r(w) + c(s) - c(t) over the nonzero W[w,s,t,w'];
+    // inconsistent -> the MPO does not conserve S^z (masks off; u1 steps still exact)
+    h->h_r.clear();
+    if (d == 2) {
+      const int UNK = std::numeric_limits<int>::min();
+      std::vector<std::vector<int>> r(L + 1);
+      r[0] = {0};
+      bool ok = true;
+      for (int j = 0; j < L && ok; ++j) {
+        r[j + 1].assign(D[j + 1], UNK);
+        const auto& Wj = h->h_W[j];
+        for (int w = 0; w < D[j] && ok; ++w) {
+          if (r[j][w] == UNK) continue;
+          for (int s2 = 0; s2 < 2; ++s2)
+            for (int t = 0; t < 2; ++t)
+              for (int w2 = 0; w2 < D[j + 1]; ++w2) {
+                const cplx v = Wj[(((size_t)w * 2 + s2) * 2 + t) * D[j + 1] + w2];
+                if (v.x == 0.0 && v.y == 0.0) continue;
+                const int val = r[j][w] + U1_C[s2] - U1_C[t];
+                if (r[j + 1][w2] == UNK) r[j + 1][w2] = val;
+                else if (r[j + 1][w2] != val) ok = false;
+              }
+        }
+      }
+      if (ok) h->h_r = std::move(r);
+    }
     h->lanes.clear();  // lanes of a multi-device handle hold per-device copies of the tables
     h->have_mpo = true;
     h->envs_valid = false;
@@ -2437,6 +2578,40 @@ int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
   if (!h || !Psi) return TDVP_EARG;
   try {
     if (!h->have_mps) throw TdvpError(TDVP_ESTATE, "MPS not set");
+    if (h->prm.u1) {
+      // U(1) mode keeps every bond basis sorted by charge; the ABI returns
+      // descending Lambda: permute each bond on the host copy on the way out
+      const int L = h->L, d = h->d;
+      if (h->layout_p != 0) download_state(h);
+      std::vector<std::vector<double>> ps = h->h_psi;
+      std::vector<std::vector<double>> lm = h->h_lam;
+      const std::vector<int>& chi = h->h_chi;
+      for (int b = 0; b + 1 < L; ++b) {
+        const int n = chi[b + 1];
+        std::vector<int> perm(n);
+        for (int i = 0; i < n; ++i) perm[i] = i;
+        std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return lm[b][x] > lm[b][y]; });
+        std::vector<double> nl(n);
+        for (int i = 0; i < n; ++i) nl[i] = lm[b][perm[i]];
+        lm[b] = nl;
+        // Psi_b: right index; Psi_{b+1}: left index
+        const int cl = chi[b], cr2 = chi[b + 2];
+        std::vector<double> a2(ps[b].size()), b2(ps[b + 1].size());
+        for (int a = 0; a < cl * d; ++a)
+          for (int i = 0; i < n; ++i) {
+            a2[((size_t)a * n + i) * 2] = ps[b][((size_t)a * n + perm[i]) * 2];
+            a2[((size_t)a * n + i) * 2 + 1] = ps[b][((size_t)a * n + perm[i]) * 2 + 1];
+          }
+        const size_t row = (size_t)d * cr2 * 2;
+        for (int i = 0; i < n; ++i) std::memcpy(&b2[i * row], &ps[b + 1][perm[i] * row], row * sizeof(double));
+        ps[b] = std::move(a2);
+        ps[b + 1] = std::move(b2);
+      }
+      for (int j = 0; j < L; ++j) std::memcpy(Psi[j], ps[j].data(), ps[j].size() * sizeof(double));
+      if (Lambda)
+        for (int b = 0; b + 1 < L; ++b) std::memcpy(Lambda[b], lm[b].data(), lm[b].size() * sizeof(double));
+      return TDVP_OK;
+    }
     if (h->layout_p != 0 && local_mode(h)) {
       // device state authoritative: straight into the caller's buffers (no host staging copy)
       const int L = h->L, d = h->d;

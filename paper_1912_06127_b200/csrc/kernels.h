@@ -13,10 +13,21 @@ extern int g_num_sms;
 // op(A) is M x K (A stored M x K for N/R, K x M for T/C); op(B) is K x N.
 // `work` (optional) enables deterministic split-K for small M x N.
 enum { OP_N = 0, OP_T = 1, OP_C = 2, OP_R = 3 };
+// Structural block masks of op(A) (M x K) and op(B) (K x N) for block-sparse
+// operands (U(1) charge blocks): a[(m/32) * ldA + k/8] != 0 when the
+// 32-row x 8-column block of op(A) may be nonzero, b[(k/8) * ldB + n/32]
+// likewise for op(B); a CTA visits only the k-chunks where both its A rows
+// and its B columns may be nonzero (exact zeros elsewhere, so the product is
+// unchanged).  Device pointers; nullptr = dense.
+struct GemmMask {
+  const unsigned char* a = nullptr;
+  const unsigned char* b = nullptr;
+  int ldA = 0, ldB = 0;
+};
 cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
                   const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch = 1, long long sA = 0,
                   long long sB = 0, long long sC = 0, cplx* work = nullptr, size_t work_elems = 0,
-                  const double* skip = nullptr);
+                  const double* skip = nullptr, const GemmMask* mask = nullptr);
 
 // -------------------------------------------------------------- chanmix.cu
 // Sparse MPO-channel contraction:

@@ -32,7 +32,9 @@ struct GemmArgs {
   int ksplit, kchunk;
   cplx* work;  // split-K partials [batch*ksplit][M][N]
   const double* skip;  // != 0 on device: return at once (Lanczos converged, krylov_tol > 0)
+  GemmMask mask;       // block-sparse operands: visit only the k-chunks both masks allow
 };
+constexpr int MAXKL = 1024;  // k-chunk list capacity (K <= 8192 with masks)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -118,10 +120,43 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
 #pragma unroll
     for (int j = 0; j < NTL; ++j) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
 
-  const int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+  // k-chunks to visit: all, or (block-sparse operands) those where this CTA's
+  // rows of op(A) and columns of op(B) may both be nonzero, compacted in order
+  __shared__ int s_kl[MAXKL];
+  __shared__ int s_wcnt[NT / 32];
+  const bool masked = g.mask.a != nullptr;
+  int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+  if (masked) {
+    const int kc0 = kbeg / BK, nkc = nk;
+    const int r0 = m0 / 32, r1 = min((M - 1) / 32, (m0 + BM - 1) / 32);
+    const int c0 = n0 / 32, c1 = min((N - 1) / 32, (n0 + BN - 1) / 32);
+    int cnt = 0;
+    for (int base = 0; base < nkc; base += NT) {
+      const int kc = kc0 + base + tid;
+      bool on = false;
+      if (base + tid < nkc) {
+        bool a = false, b = false;
+        for (int r = r0; r <= r1; ++r) a |= g.mask.a[(long long)r * g.mask.ldA + kc] != 0;
+        for (int c = c0; c <= c1; ++c) b |= g.mask.b[(long long)kc * g.mask.ldB + c] != 0;
+        on = a && b;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = cnt;
+      for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+      if (on) s_kl[off + __popc(bal & ((1u << lane) - 1u))] = kc - kc0;
+      int tot = 0;
+      for (int w = 0; w < NT / 32; ++w) tot += s_wcnt[w];
+      cnt += tot;
+      __syncthreads();
+    }
+    nk = cnt;
+  }
+  auto kt_of = [&](int kt) { return masked ? s_kl[kt] : kt; };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_tile(s, s);
+    if (s < nk) load_tile(s, kt_of(s));
     cp_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -129,7 +164,7 @@ __global__ void __launch_bounds__(NT, 2) zgemm_dmma_kernel(GemmArgs g) {
     __syncthreads();
     {
       const int nt = kt + STAGES - 1;
-      if (nt < nk) load_tile(nt % STAGES, nt);
+      if (nt < nk) load_tile(nt % STAGES, kt_of(nt));
       cp_commit();
     }
     const cplx* a_s = sA + (kt % STAGES) * A_ST;
@@ -274,7 +309,8 @@ int g_num_sms = 148;
 
 cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx alpha, const cplx* A, long long lda,
                   const cplx* B, long long ldb, cplx beta, cplx* C, long long ldc, int batch, long long sA,
-                  long long sB, long long sC, cplx* work, size_t work_elems, const double* skip) {
+                  long long sB, long long sC, cplx* work, size_t work_elems, const double* skip,
+                  const GemmMask* mask) {
   if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
   if (K <= 0) {
     for (int b = 0; b < batch; ++b) {
@@ -290,6 +326,7 @@ cudaError_t zgemm(cudaStream_t st, int opA, int opB, int M, int N, int K, cplx a
   g.C = C; g.ldc = ldc; g.sC = sC;
   g.work = work;
   g.skip = skip;
+  if (mask != nullptr && mask->a != nullptr && mask->b != nullptr && (K + BK - 1) / BK <= MAXKL) g.mask = *mask;
   // tile choice: 64x64 when that gives >= 2 waves of CTAs, else 32x32 (4x more CTAs)
   const long long tiles64 = (long long)((M + 63) / 64) * ((N + 63) / 64) * batch;
   const bool small = tiles64 < 2LL * g_num_sms;
