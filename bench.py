@@ -49,6 +49,17 @@ WORKLOADS = {
 }
 
 
+def bjac_traffic(launches, steps):
+    """DRAM bytes (read + write) per bjac_kernel launch of this workload from the
+    committed ncu --set full capture (profiles/r2_ncu_bjac_c5sat.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_bjac_c5sat.json")) as f:
+            m = json.load(f)["metrics"]
+        return float(m["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def workload_inputs(name):
     import tdvp_inputs as ti
     L, Delta, chi, eps, dt, desc = WORKLOADS[name]
@@ -425,6 +436,16 @@ def main():
               "flop_per_unit": "per sweep nc(nc-1)/2 * (16 mr + 24 (mr + nc)), sweeps counted on device",
               "share_of_step": jac_ms / bstep_ms if bstep_ms > 0 else None,
               "svd_calls": n_svd, "sweeps_per_svd": sweeps / n_svd if n_svd else None}
+    bj_ms, bj_fl, bj_n = S("svd_bj_ms"), S("svd_bj_flop"), S("svd_bj_calls")
+    bj_tf = tf(bj_fl, bj_ms)
+    rf_bj = {"kernel": "bjac_kernel (block one-sided Jacobi SVD on the DMMA pipe, > 1024 columns)", "bound": "tensor",
+             "achieved": bj_tf, "peak": zpeak, "unit": "TFLOP/s",
+             "frac": (bj_tf / zpeak) if (bj_tf and zpeak) else None, "traffic": bjac_traffic(bj_n, nb),
+             "peak_source": f"measured in this run: cuBLAS ZGEMM {zpeak} TFLOP/s (MEASURED_PEAKS.json has no FP64 entry)",
+             "flop_per_unit": "executed per block pair and round: Gram 8 xr 32^2 10/16 + rotation 8 (xr+nc) 32^2 "
+                              "(8 flop per complex MAC, counted on the device)",
+             "launches_per_step": bj_n / nb, "ms_per_launch": bj_ms / bj_n if bj_n else None,
+             "share_of_step": bj_ms / bstep_ms if bstep_ms > 0 else None}
     rf_h = {"kernel": "H_eff^(2)+H_eff^(1) matvecs (DMMA zgemm + sparse channel pass)", "bound": "tensor",
             "achieved": tf(h2_fl + h1_fl, h2_ms + h1_ms), "peak": zpeak, "unit": "TFLOP/s",
             "frac": (tf(h2_fl + h1_fl, h2_ms + h1_ms) / zpeak) if (zpeak and h2_ms + h1_ms > 0) else None,
@@ -432,7 +453,10 @@ def main():
             "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
             "flop_per_unit": "SURVEY §8(d): 8[d^2 cl cr (Dl cl + Dr cr) + d cl cr (nnzW_j + nnzW_j+1)] per H2 matvec",
             "share_of_step": (h2_ms + h1_ms) / bstep_ms if bstep_ms > 0 else None}
-    roof = rf_jac if jac_ms >= h2_ms + h1_ms else rf_h
+    # the dominant kernel: the ncu launch list of this workload puts bjac_kernel
+    # first (profiles/r2a_launches_c5sat.txt); report it when it ran, else the larger
+    cands = [c for c in (rf_bj, rf_h, rf_jac) if c.get("share_of_step")]
+    roof = rf_bj if bj_n > 0 else max(cands, key=lambda c: c["share_of_step"])
     bins = {}
     for name, ms_, fl_ in zip(("chi<=128", "chi<=256", "chi<=512", "chi<=1024"), bins_ms, bins_fl):
         if ms_ > 0:
@@ -443,7 +467,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
         "roofline": roof,
-        "roofline_other": rf_h if roof is rf_jac else rf_jac,
+        "roofline_other": [c for c in (rf_bj, rf_h, rf_jac) if c is not roof],
         "heff2_tflops_by_chi": bins,
         "heff2": {"achieved": h2_tf, "peak": zpeak, "frac": (h2_tf / zpeak) if (h2_tf and zpeak) else None,
                   "share_of_step": h2_ms / bstep_ms if bstep_ms > 0 else None},

@@ -111,6 +111,11 @@ typedef struct {
    * their time is lanczos2_ms + lanczos1_ms - heff2_ms - heff1_ms) */
   double lz_vec_bytes;
   int rebalances;         /* cumulative dynamic re-partitionings (tdvp_params.rebalance) */
+  /* the block-Jacobi (DMMA) SVD kernel alone (more than 1024 columns): device time
+   * (timing=1), the flops it executed (Gram + rotation products, 8 per complex
+   * MAC, counted on the device), launches */
+  double svd_bj_ms, svd_bj_flop;
+  int svd_bj_calls;
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

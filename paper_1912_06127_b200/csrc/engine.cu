@@ -964,6 +964,11 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
     // block-Jacobi (DMMA) path: the flops it executed; SIMT paths: the scalar count per sweep
     h->stats.svd_jac_flop += jac_flop > 0.0 ? jac_flop
                                             : (double)sweeps * nc * (nc - 1) / 2 * (16.0 * mr + 24.0 * (mr + nc));
+    if (jac_flop > 0.0) {  // the block-Jacobi (DMMA) kernel alone: the dominant kernel at chi = 1024
+      h->stats.svd_bj_ms += jac_ms;
+      h->stats.svd_bj_flop += jac_flop;
+      h->stats.svd_bj_calls++;
+    }
   }
   if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
   // a5: environments for the next update
@@ -1581,6 +1586,8 @@ void reset_step_stats(tdvp_ctx* h) {
   h->stats.svd_sweeps_max = 0;
   h->stats.svd_sweeps_total = 0;
   h->stats.svd_jac_ms = h->stats.svd_jac_flop = 0.0;
+  h->stats.svd_bj_ms = h->stats.svd_bj_flop = 0.0;
+  h->stats.svd_bj_calls = 0;
   h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
   h->stats.heff2_calls = 0;
   h->stats.lz_vec_bytes = 0.0;
@@ -1673,6 +1680,9 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     a.svd_sweeps_total += b.svd_sweeps_total;
     a.svd_jac_ms += b.svd_jac_ms;
     a.svd_jac_flop += b.svd_jac_flop;
+    a.svd_bj_ms += b.svd_bj_ms;
+    a.svd_bj_flop += b.svd_bj_flop;
+    a.svd_bj_calls += b.svd_bj_calls;
     a.heff2_flop += b.heff2_flop;
     a.heff2_calls += b.heff2_calls;
     a.heff1_flop += b.heff1_flop;

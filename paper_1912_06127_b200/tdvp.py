@@ -52,7 +52,8 @@ class tdvp_stats(C.Structure):
                 ("svd_jac_ms", C.c_double), ("svd_jac_flop", C.c_double), ("svd_sweeps_total", C.c_int),
                 ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
                 ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
-                ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int)]
+                ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int), ("svd_bj_ms", C.c_double),
+                ("svd_bj_flop", C.c_double), ("svd_bj_calls", C.c_int)]
 
     def as_dict(self):
         out = {}
