@@ -1778,6 +1778,7 @@ void do_step(tdvp_ctx* h, double dt, int p) {
       for (int q = 1; q < p; ++q) {
         // summed device time over lanes (concurrent: may exceed step_ms)
         tdvp_ctx* ln = h->lanes[q - 1].get();
+        DeviceGuard dg(ln->dev);  // its events live on its device
         finish_timing(ln);
         h->stats.heff2_ms += ln->stats.heff2_ms;
         h->stats.heff1_ms += ln->stats.heff1_ms;
