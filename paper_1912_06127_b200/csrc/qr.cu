@@ -114,15 +114,19 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_kernel(cplx* A, long long lda,
     __syncthreads();
   }
   // ---- T (zlarft forward/columnwise): T_ii = tau_i, T[0:i, i] = -tau_i T[0:i,0:i] z[0:i, i]
-  if (tid == 0) {
+  if (wid == 0) {  // column i depends on the earlier columns; its rows r < i are independent (lane r)
     for (int i = 0; i < kb; ++i) {
-      s_T[i][i] = s_tau[i];
-      for (int r = 0; r < i; ++r) {
+      const int r = lane;
+      if (r < i) {
         cplx acc = cmk(0.0, 0.0);
         for (int c = r; c < i; ++c) acc = cadd(acc, cmul(s_T[r][c], s_z[c][i]));
         s_T[r][i] = cmul(cmk(-s_tau[i].x, -s_tau[i].y), acc);
+      } else if (r == i) {
+        s_T[i][i] = s_tau[i];
+      } else if (r < kb) {
+        s_T[r][i] = cmk(0.0, 0.0);
       }
-      for (int r = i + 1; r < kb; ++r) s_T[r][i] = cmk(0.0, 0.0);
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -275,16 +279,21 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
     }
     __syncthreads();
   }
-  // ---- T (zlarft forward/columnwise) on CTA 0
-  if (crank == 0 && tid == 0) {
+  // ---- T (zlarft forward/columnwise) on CTA 0, one warp: column i of T
+  // depends on the earlier columns; its rows r < i are independent (lane r)
+  if (crank == 0 && wid == 0) {
     for (int i = 0; i < kb; ++i) {
-      s_T[i][i] = s_tau[i];
-      for (int r = 0; r < i; ++r) {
+      const int r = lane;
+      if (r < i) {
         cplx acc = cmk(0.0, 0.0);
         for (int c = r; c < i; ++c) acc = cadd(acc, cmul(s_T[r][c], s_z[c][i]));
         s_T[r][i] = cmul(cmk(-s_tau[i].x, -s_tau[i].y), acc);
+      } else if (r == i) {
+        s_T[i][i] = s_tau[i];
+      } else if (r < kb) {
+        s_T[r][i] = cmk(0.0, 0.0);
       }
-      for (int r = i + 1; r < kb; ++r) s_T[r][i] = cmk(0.0, 0.0);
+      __syncwarp();
     }
   }
   __syncthreads();

@@ -43,6 +43,7 @@ constexpr int PC = 2 * BB;    // columns per block pair
 constexpr int NTB = 256;      // threads per CTA (8 warps)
 constexpr int GP = PC + 1;    // padded row length of the shared PC x PC matrices
 constexpr int NUT = 10;       // upper-triangular 8 x 8 tiles of a 32 x 32 Gram matrix
+constexpr int NUB = (PC / 2) * (PC / 2 + 1) / 2;  // upper-triangular 2 x 2 blocks of the inner rotation rounds
 
 struct BjArgs {
   cplx* Y;
@@ -113,6 +114,7 @@ struct Smem {
   cplx sn[PC / 2];
   int rp[PC / 2], rq[PC / 2];
   int col[PC];       // global column of pair column i (-1: absent)
+  unsigned char ut_a[136], ut_b[136];  // upper-triangle 2 x 2 block u -> (row pair, column pair)
   double offw[8];
   int any;
 };
@@ -136,6 +138,16 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
   int xr0, xr1, vr0, vr1;
   split(a.xr, xr0, xr1);
   split(a.nc, vr0, vr1);
+  if (tid == 0) {
+    int u = 0;
+    for (int ra = 0; ra < PC / 2; ++ra)
+      for (int rb = ra; rb < PC / 2; ++rb) {
+        sm.ut_a[u] = (unsigned char)ra;
+        sm.ut_b[u] = (unsigned char)rb;
+        ++u;
+      }
+  }
+  __syncthreads();
   unsigned long long round_g = 0;  // rounds completed (all sweeps), for the monotonic counters
   const bool prof = a.prof && blockIdx.x == 0 && tid == 0;
   unsigned long long pt = clock64();
@@ -332,108 +344,87 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
           sm.Q[i][j] = cmk(i == j ? 1.0 : 0.0, 0.0);
         }
         const double tol2q = tol4 * tol4;
-        // absolute noise floor of the updated G entries: the first inner sweep
-        // works on the freshly computed G (accurate relative to the column
-        // norms), later sweeps on G after rotations, whose entries carry
-        // rounding ~ u max_i g_ii; below that floor a rotation only chases noise
-        double gmax = 0.0;
-        for (int i = 0; i < PC; ++i) gmax = fmax(gmax, sm.G[i][i].x);
-        const double floor2 = (64.0 * DBL_EPSILON * gmax) * (64.0 * DBL_EPSILON * gmax);
-        // Round of 16 disjoint rotations: threads 0..15 compute the rotation
-        // parameters (rsqrt only) into shared memory; then every thread
-        // updates one 2 x 2 block of the upper triangle of G (row pair ra <=
-        // column pair rb; the lower triangle is its mirror) and the Q entries
-        // of rows 2 ra, 2 ra + 1 in column pair rb.
-        const int ra = tid >> 4, rb = tid & 15;
-        for (int isw = 0; isw < a.inner_max; ++isw) {
-          if (tid == 0) sm.any = 0;
-          if (tid < 8) sm.offw[tid] = 0.0;
-          __syncthreads();
-          double smax = 0.0;
-          for (int rd = 0; rd < PC - 1; ++rd) {
-            if (tid < PC / 2) {
-              int p, q;
-              rr_pair(PC, rd, tid, p, q);
-              double cs = 1.0;
-              cplx sn = cmk(0.0, 0.0);
-              const double ga = sm.G[p][p].x, gc = sm.G[q][q].x;
-              const cplx g = sm.G[p][q];
-              const double ag2 = cabs2(g);
-              const double gg = ga * gc;
-              if (ga > 0.0 && gc > 0.0 && ag2 > 1e-300) {
-                smax = fmax(smax, ag2 / gg);
-                if (ag2 > tol2q * gg && (isw == 0 || ag2 > floor2)) {
-                  // zero g = x_p^H x_q by x_p' = cs x_p - conj(sn) x_q, x_q' = sn x_p + cs x_q:
-                  // cos^2 = (1 + |w| / D) / 2, sn = sgn(w) g / (D cs), D = sqrt(w^2 + 4 |g|^2)
-                  const double w = gc - ga;
-                  const double rD = rsqrt(fma(w, w, 4.0 * ag2));
-                  const double qq = 0.5 * fma(fabs(w), rD, 1.0);
-                  const double rcs = rsqrt(qq);
-                  cs = qq * rcs;
-                  const double f = copysign(rD * rcs, w);
-                  sn = cmk(f * g.x, f * g.y);
-                  sm.any = 1;
-                }
-              }
-              sm.rp[tid] = p;
-              sm.rq[tid] = q;
-              sm.cs[tid] = cs;
-              sm.sn[tid] = sn;
+        // ONE cyclic sweep of 31 rounds of 16 disjoint rotations (the outer
+        // iteration converges as fast as with more inner sweeps, measured).
+        // Per round: threads 0..15 compute the rotation parameters (rsqrt
+        // only); then threads 0..135 each update one 2 x 2 block of the upper
+        // triangle of G (row pair ra <= column pair rb, packed into the first
+        // 4.25 warps so the others skip the branch; the lower triangle is the
+        // mirror), and every thread updates two (row, column pair) entries of Q.
+        for (int rd = 0; rd < PC - 1; ++rd) {
+          if (tid < PC / 2) {
+            int p, q;
+            rr_pair(PC, rd, tid, p, q);
+            double cs = 1.0;
+            cplx sn = cmk(0.0, 0.0);
+            const double ga = sm.G[p][p].x, gc = sm.G[q][q].x;
+            const cplx g = sm.G[p][q];
+            const double ag2 = cabs2(g);
+            const double gg = ga * gc;
+            if (ga > 0.0 && gc > 0.0 && ag2 > 1e-300 && ag2 > tol2q * gg) {
+              // zero g = x_p^H x_q by x_p' = cs x_p - conj(sn) x_q, x_q' = sn x_p + cs x_q:
+              // cos^2 = (1 + |w| / D) / 2, sn = sgn(w) g / (D cs), D = sqrt(w^2 + 4 |g|^2)
+              const double w = gc - ga;
+              const double rD = rsqrt(fma(w, w, 4.0 * ag2));
+              const double qq = 0.5 * fma(fabs(w), rD, 1.0);
+              const double rcs = rsqrt(qq);
+              cs = qq * rcs;
+              const double f = copysign(rD * rcs, w);
+              sn = cmk(f * g.x, f * g.y);
             }
-            __syncthreads();
-            {
-              const int p1 = sm.rp[ra], q1 = sm.rq[ra], p2 = sm.rp[rb], q2 = sm.rq[rb];
-              const double ca = sm.cs[ra], cb = sm.cs[rb];
-              const cplx sa = sm.sn[ra], sb = sm.sn[rb];
-              if (ra <= rb) {
-                const cplx b00 = sm.G[p1][p2], b01 = sm.G[p1][q2], b10 = sm.G[q1][p2], b11 = sm.G[q1][q2];
-                // B <- J_a^H B J_b ; rows: p' = ca p - sa q, q' = conj(sa) p + ca q
-                const cplx r00 = csub(cscale(b00, ca), cmul(sa, b10));
-                const cplx r01 = csub(cscale(b01, ca), cmul(sa, b11));
-                const cplx r10 = cadd(cmul(cconj(sa), b00), cscale(b10, ca));
-                const cplx r11 = cadd(cmul(cconj(sa), b01), cscale(b11, ca));
-                // columns: p' = cb p - conj(sb) q ; q' = sb p + cb q
-                cplx n00 = csub(cscale(r00, cb), cmul(cconj(sb), r01));
-                cplx n01 = cadd(cmul(sb, r00), cscale(r01, cb));
-                cplx n10 = csub(cscale(r10, cb), cmul(cconj(sb), r11));
-                cplx n11 = cadd(cmul(sb, r10), cscale(r11, cb));
-                if (ra == rb) {
-                  if (sa.x != 0.0 || sa.y != 0.0) n01 = n10 = cmk(0.0, 0.0);
-                  n00.y = n11.y = 0.0;
-                  n10 = cconj(n01);
-                }
-                sm.G[p1][p2] = n00;
-                sm.G[p1][q2] = n01;
-                sm.G[q1][p2] = n10;
-                sm.G[q1][q2] = n11;
-                if (ra != rb) {  // mirror: G[b][a] = G[a][b]^H
-                  sm.G[p2][p1] = cconj(n00);
-                  sm.G[q2][p1] = cconj(n01);
-                  sm.G[p2][q1] = cconj(n10);
-                  sm.G[q2][q1] = cconj(n11);
-                }
-              }
-              // Q <- Q J_b on rows 2 ra, 2 ra + 1
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int row = 2 * ra + h;
-                const cplx qp = sm.Q[row][p2], qq = sm.Q[row][q2];
-                sm.Q[row][p2] = csub(cscale(qp, cb), cmul(cconj(sb), qq));
-                sm.Q[row][q2] = cadd(cmul(sb, qp), cscale(qq, cb));
-              }
-            }
-            __syncthreads();
+            sm.rp[tid] = p;
+            sm.rq[tid] = q;
+            sm.cs[tid] = cs;
+            sm.sn[tid] = sn;
           }
-          // stop after a sweep without rotations, or when the largest coupling
-          // of the sweep was so small that the next sweep's are below tol / 4
-          if (tid < PC / 2) atomic_max_nonneg(&sm.offw[0], smax);
           __syncthreads();
-          const double sw = sm.offw[0];
-          const int any = sm.any;
+          if (tid < NUB) {
+            const int ra = sm.ut_a[tid], rb = sm.ut_b[tid];
+            const int p1 = sm.rp[ra], q1 = sm.rq[ra], p2 = sm.rp[rb], q2 = sm.rq[rb];
+            const double ca = sm.cs[ra], cb = sm.cs[rb];
+            const cplx sa = sm.sn[ra], sb = sm.sn[rb];
+            const cplx b00 = sm.G[p1][p2], b01 = sm.G[p1][q2], b10 = sm.G[q1][p2], b11 = sm.G[q1][q2];
+            // B <- J_a^H B J_b ; rows: p' = ca p - sa q, q' = conj(sa) p + ca q
+            const cplx r00 = csub(cscale(b00, ca), cmul(sa, b10));
+            const cplx r01 = csub(cscale(b01, ca), cmul(sa, b11));
+            const cplx r10 = cadd(cmul(cconj(sa), b00), cscale(b10, ca));
+            const cplx r11 = cadd(cmul(cconj(sa), b01), cscale(b11, ca));
+            // columns: p' = cb p - conj(sb) q ; q' = sb p + cb q
+            cplx n00 = csub(cscale(r00, cb), cmul(cconj(sb), r01));
+            cplx n01 = cadd(cmul(sb, r00), cscale(r01, cb));
+            cplx n10 = csub(cscale(r10, cb), cmul(cconj(sb), r11));
+            cplx n11 = cadd(cmul(sb, r10), cscale(r11, cb));
+            if (ra == rb) {
+              if (sa.x != 0.0 || sa.y != 0.0) n01 = cmk(0.0, 0.0);
+              n00.y = n11.y = 0.0;
+              n10 = cconj(n01);
+            }
+            sm.G[p1][p2] = n00;
+            sm.G[p1][q2] = n01;
+            sm.G[q1][p2] = n10;
+            sm.G[q1][q2] = n11;
+            if (ra != rb) {  // mirror: G[b][a] = G[a][b]^H
+              sm.G[p2][p1] = cconj(n00);
+              sm.G[q2][p1] = cconj(n01);
+              sm.G[p2][q1] = cconj(n10);
+              sm.G[q2][q1] = cconj(n11);
+            }
+          }
+          // Q <- Q J_b: units (row, column pair) = tid, tid + 256
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int u = tid + h * NTB;
+            const int row = u >> 4, rb = u & 15;
+            const int p2 = sm.rp[rb], q2 = sm.rq[rb];
+            const double cb = sm.cs[rb];
+            const cplx sb = sm.sn[rb];
+            const cplx qp = sm.Q[row][p2], qq = sm.Q[row][q2];
+            sm.Q[row][p2] = csub(cscale(qp, cb), cmul(cconj(sb), qq));
+            sm.Q[row][q2] = cadd(cmul(sb, qp), cscale(qq, cb));
+          }
           __syncthreads();
-          if (prof) g_bj_prof[6]++;
-          if (!any || sw * sw <= 0.01 * tol2q) break;
         }
+        if (prof) g_bj_prof[6]++;
         if (prof) g_bj_prof[7]++;
         mark(2);
         // ---- 4. [X_p ; V_p] <- [X_p ; V_p] Q on the DMMA pipe, this CTA's rows
@@ -460,13 +451,19 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
         for (int part = 0; part < 2; ++part) {
           const int rb0 = part == 0 ? xr0 : a.vofs + vr0;
           const int rb1 = part == 0 ? xr1 : a.vofs + vr1;
-          for (int r0 = rb0 + wid * 8; r0 < rb1; r0 += 64) {
+          cplx av[8], nx[8];
+          auto load_chunk = [&](int r0, cplx (&dst)[8]) {
             const int r = r0 + (lane >> 2);
             const bool rv = r < rb1;
-            cplx av[8];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              av[ks] = (rv && cc[ks] >= 0) ? __ldcg(Y + (long long)cc[ks] * ldy + r) : cmk(0.0, 0.0);
+              dst[ks] = (rv && cc[ks] >= 0) ? __ldcg(Y + (long long)cc[ks] * ldy + r) : cmk(0.0, 0.0);
+          };
+          if (rb0 + wid * 8 < rb1) load_chunk(rb0 + wid * 8, nx);
+          for (int r0 = rb0 + wid * 8; r0 < rb1; r0 += 64) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) av[ks] = nx[ks];
+            if (r0 + 64 < rb1) load_chunk(r0 + 64, nx);  // next chunk in flight during the DMMAs
             double c1[4][2], c2[4][2], c3[4][2];
 #pragma unroll
             for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
