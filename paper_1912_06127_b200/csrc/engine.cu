@@ -1302,10 +1302,13 @@ void send_left_local(tdvp_ctx* h, Segment& b, Segment& a) {
 }
 
 // NCCL mode
+// The header (chi) is host-known on the sender: stream-ordered, no host
+// synchronisation (a pageable-memory H2D copy has consumed `v` when it
+// returns; the next header's copy is ordered after this send on the stream).
+// The receiver needs chi on the host to size its receives, so it waits.
 void nccl_send_ints(tdvp_ctx* h, const int* v, int n, int peer) {
   CK(cudaMemcpyAsync(h->hdr->p, v, n * sizeof(int), cudaMemcpyHostToDevice, h->st));
   NK(nccl().Send(h->hdr->p, n, ncclInt32, peer, h->comm, h->st));
-  CK(cudaStreamSynchronize(h->st));
 }
 void nccl_recv_ints(tdvp_ctx* h, int* v, int n, int peer) {
   NK(nccl().Recv(h->hdr->p, n, ncclInt32, peer, h->comm, h->st));
@@ -1605,7 +1608,7 @@ void reset_step_stats(tdvp_ctx* h) {
 // both half-steps of segment q on its lane (the per-rank program of the NCCL
 // executor, with lane messages in place of send/recv)
 void lane_program(tdvp_ctx* h, int q, double dt, const std::set<int>& merged, const std::atomic<bool>& abort) {
-  tdvp_ctx* ln = lane_of(h, q);
+  tdvp_ctx* ln = q == 0 ? h : h->lanes[q - 1].get();
   Segment& g = h->segs[q];
   const int L = h->L, p = h->layout_p;
   for (int hh = 1; hh <= 2; ++hh)
@@ -1636,7 +1639,9 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
   std::vector<std::exception_ptr> errs(p);
   auto body = [&](int q) {
     try {
-      CK(cudaSetDevice(q == 0 ? h->dev : lane_of(h, q)->dev));
+      // lanes were created (and their devices checked) above, on this thread:
+      // the workers only read h->lanes
+      CK(cudaSetDevice(q == 0 ? h->dev : h->lanes[q - 1]->dev));
       lane_program(h, q, dt, merged, abort);
     } catch (...) {
       errs[q] = std::current_exception();
