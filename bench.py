@@ -399,6 +399,8 @@ def main():
     sweeps, n_svd = int(S("svd_sweeps_total")), int(S("n_pair"))
     bins_ms = np.sum([s["heff2_ms_bin"] for s in per_t], axis=0)
     bins_fl = np.sum([s["heff2_flop_bin"] for s in per_t], axis=0)
+    lzb_ms = np.sum([s["lz_ms_bin"] for s in per_t], axis=0)
+    lzb_by = np.sum([s["lz_bytes_bin"] for s in per_t], axis=0)
     zpeak = peaks.get("zgemm") if peaks else None
 
     # e2e: the same step through the C-ABI with HOST buffers (set_mps H2D incl.
@@ -462,6 +464,11 @@ def main():
         if ms_ > 0:
             v = tf(fl_, ms_)
             bins[name] = {"tflops": v, "frac_of_zgemm_peak": (v / zpeak) if zpeak else None, "ms_per_step": ms_ / nb}
+    lz_bins = {}
+    for name, ms_, by_ in zip(("chi<=128", "chi<=256", "chi<=512", "chi<=1024"), lzb_ms, lzb_by):
+        if ms_ > 0:
+            g = by_ / (ms_ * 1e-3) / 1e9
+            lz_bins[name] = {"gbs": g, "frac_of_hbm": (g / hbm) if hbm else None, "ms_per_step": ms_ / nb}
     line = {
         "metric": METRIC, "value": ms_per_step, "unit": "ms/step", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
@@ -473,7 +480,8 @@ def main():
                   "share_of_step": h2_ms / bstep_ms if bstep_ms > 0 else None},
         "lanczos_vectors": {"achieved_gbs": lz_gbs, "peak_gbs": hbm, "frac": (lz_gbs / hbm) if lz_gbs else None,
                             "bytes_per_step": lz_bytes / nb, "ms_per_step": lz_vec_ms / nb,
-                            "bytes": "algorithmic: per exponential 16 n [3 + sum_{k<K-1}(3(k+1)+6) + (K+1) + (K+1)]"},
+                            "bytes": "algorithmic: per exponential 16 n [3 + sum_{k<K-1}(3(k+1)+6) + (K+1) + (K+1)]",
+                            "by_chi": lz_bins},
         "svd_share_of_step": svd_ms / bstep_ms if bstep_ms > 0 else None,
         "breakdown_ms_per_step_instrumented": bstep_ms / nb,
         "breakdown_ms_per_step": {"svd_total": svd_ms / nb, "svd_jacobi_kernel": jac_ms / nb,

@@ -116,6 +116,11 @@ typedef struct {
    * MAC, counted on the device), launches */
   double svd_bj_ms, svd_bj_flop;
   int svd_bj_calls;
+  /* the Lanczos vector passes (everything of the Krylov exponentials but the
+   * matvecs) binned like heff2_*_bin by max(chi_L, chi_R): device time and
+   * algorithmic bytes (timing=1) */
+  double lz_ms_bin[4];
+  double lz_bytes_bin[4];
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

@@ -248,6 +248,13 @@ struct tdvp_ctx {
   size_t ev_used = 0;
   std::vector<std::pair<int, int>> ev_h2, ev_h1, ev_svd, ev_lz2, ev_lz1, ev_env;
   std::vector<int> ev_h2_bin;  // chi bin of every ev_h2 entry (tdvp_stats.heff2_*_bin)
+  // one record per timed Krylov exponential: its whole span, its chi bin and
+  // the range of its matvec events in ev_h2 (which = 2) or ev_h1 (which = 1)
+  struct LzRec {
+    int ea, eb, bin, which;
+    size_t mv0, mv1;
+  };
+  std::vector<LzRec> ev_lzrec;
   int cur_bin = 0;             // chi bin of the pair update in progress
   cudaEvent_t ev_step0 = nullptr, ev_step1 = nullptr;
   // NCCL
@@ -522,6 +529,9 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
                   long long n, double tre, double tim, int K, int which /*2: heff2 1: heff1 0: other*/, double mv_flop) {
   cplx* V = h->krylov->c();
   cplx* w = h->wvec->c();
+  const bool tm = h->prm.timing && which;
+  const int lz_ea = tm ? ev_record(h) : -1;
+  const size_t lz_mv0 = which == 2 ? h->ev_h2.size() : h->ev_h1.size();
   CK(lz_start(h->st, h->lz, x, V, n));
   g_launch_count += 2;
   // paper mode (krylov_tol > 0): the convergence test runs on
@@ -557,10 +567,14 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
     double units = 3.0 + (double)(K + 1) + (double)(K + 1);
     for (int k = 0; k + 1 < K; ++k) units += 3.0 * (k + 1) + 6.0;
     h->stats.lz_vec_bytes += units * 16.0 * (double)n;
+    h->stats.lz_bytes_bin[h->cur_bin] += units * 16.0 * (double)n;
   }
   CK(lz_tridiag_exp(h->st, h->lz, K, tre, tim));
   CK(lz_combine(h->st, h->lz, V, n, K, out, n));
   g_launch_count += 2;
+  if (tm)
+    h->ev_lzrec.push_back({lz_ea, ev_record(h), h->cur_bin, which, lz_mv0,
+                           which == 2 ? h->ev_h2.size() : h->ev_h1.size()});
 }
 
 // --------------------------------------------------------- local updates
@@ -1063,6 +1077,10 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), n));
   g_launch_count++;
   const double fl = flops_heff1(cl, cr, d, W.Dl, W.Dr, nnz_of(W));
+  {
+    const int cx = std::max(cl, cr);
+    h->cur_bin = cx <= 128 ? 0 : cx <= 256 ? 1 : cx <= 512 ? 2 : 3;
+  }
   const int el0 = h->prm.timing ? ev_record(h) : -1;
   set_heff_masks(h, g, j, 1);
   expm_lanczos(
@@ -1595,6 +1613,8 @@ void reset_step_stats(tdvp_ctx* h) {
   h->stats.heff2_calls = 0;
   h->stats.lz_vec_bytes = 0.0;
   for (int i = 0; i < 4; ++i) h->stats.heff2_ms_bin[i] = h->stats.heff2_flop_bin[i] = 0.0;
+  for (int i = 0; i < 4; ++i) h->stats.lz_ms_bin[i] = h->stats.lz_bytes_bin[i] = 0.0;
+  h->ev_lzrec.clear();
   h->ev_used = 0;
   h->ev_h2.clear();
   h->ev_h2_bin.clear();
@@ -1693,6 +1713,7 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     a.heff1_flop += b.heff1_flop;
     a.lz_vec_bytes += b.lz_vec_bytes;
     for (int i = 0; i < 4; ++i) a.heff2_flop_bin[i] += b.heff2_flop_bin[i];
+    for (int i = 0; i < 4; ++i) a.lz_bytes_bin[i] += b.lz_bytes_bin[i];
   }
 }
 
@@ -1717,6 +1738,17 @@ void finish_timing(tdvp_ctx* h) {
   h->stats.lanczos2_ms = sum(h->ev_lz2);
   h->stats.lanczos1_ms = sum(h->ev_lz1);
   h->stats.env_ms = sum(h->ev_env);
+  for (const auto& r : h->ev_lzrec) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev_pool[r.ea], h->ev_pool[r.eb]));
+    double t = ms;
+    const auto& mv = r.which == 2 ? h->ev_h2 : h->ev_h1;
+    for (size_t i = r.mv0; i < r.mv1 && i < mv.size(); ++i) {
+      CK(cudaEventElapsedTime(&ms, h->ev_pool[mv[i].first], h->ev_pool[mv[i].second]));
+      t -= ms;
+    }
+    h->stats.lz_ms_bin[r.bin] += t;
+  }
 }
 
 int balanced_partition(int L, int p, const int* chi, int* s, int* e, double* best);
@@ -1791,6 +1823,8 @@ void do_step(tdvp_ctx* h, double dt, int p) {
         h->stats.lanczos2_ms += ln->stats.lanczos2_ms;
         h->stats.lanczos1_ms += ln->stats.lanczos1_ms;
         h->stats.env_ms += ln->stats.env_ms;
+        for (int i = 0; i < 4; ++i) h->stats.lz_ms_bin[i] += ln->stats.lz_ms_bin[i];
+        for (int i = 0; i < 4; ++i) h->stats.heff2_ms_bin[i] += ln->stats.heff2_ms_bin[i];
       }
   }
 }

@@ -46,10 +46,19 @@ __global__ void __launch_bounds__(TPB) lz_norm_kernel(LanczosDev d, const cplx* 
     s_last = (atomicAdd(d.counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)d.partials)[b];
+  if (!s_last) return;
+  // the last block: all its threads sum the partials (strided, then the warp
+  // and warp-order tree: a fixed order), no L2-latency chain of length gridDim
+  __threadfence();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += TPB) t += __ldcg(d.partials + b);
+  t = warp_sum(t);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = 0.0;
+    for (int ww = 0; ww < NW; ++ww) t += s_red[ww];
     for (int i = 0; i < 2 * KMAX; ++i) d.scal[i] = 0.0;
     d.scal[LZ_N0] = sqrt(t);
     d.scal[LZ_BRK] = 0.0;
@@ -280,26 +289,53 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
       P[(long long)blockIdx.x * nq + tid] = t;
     }
   };
+  // every block sums the G partials of each value in the same fixed order:
+  // thread (j, q) over blocks b = j (mod J), then a pairwise tree over j
+  // (J a power of two), so all blocks hold identical totals; the loads of
+  // one thread are independent (no L2-latency chain of length G)
+  __shared__ double s_part[TPB];
   auto grid_total = [&](int nq, const double* P) {
-    if (tid < nq) {
+    int J = 1;
+    while (2 * J * nq <= TPB) J *= 2;
+    const int q = tid % nq, j = tid / nq;
+    if (j < J) {
       double t = 0.0;
-      for (int b = 0; b < G; ++b) t += __ldcg(P + (long long)b * nq + tid);
-      s_tot[tid] = t;
+      for (int b = j; b < G; b += J) t += __ldcg(P + (long long)b * nq + q);
+      s_part[j * nq + q] = t;
     }
+    __syncthreads();
+    for (int h = J / 2; h >= 1; h /= 2) {
+      if (j < h) s_part[j * nq + q] += s_part[(j + h) * nq + q];
+      __syncthreads();
+    }
+    if (tid < nq) s_tot[tid] = s_part[tid];
     __syncthreads();
   };
   double acc[NQ];
   // ---- phase 1
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
-    const cplx we = w[e];
+  // U independent elements per thread and trip: more loads in flight for
+  // few basis vectors (HBM latency x bandwidth per SM)
+  constexpr int U = NV <= 2 ? 4 : NV <= 4 ? 2 : 1;
+  for (long long e0 = blockIdx.x * (long long)TPB + tid; e0 < n; e0 += stride * U) {
+    cplx we[U], v[U][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const cplx p = cdotc(V[i * ldv + e], we);
-      acc[2 * i] += p.x;
-      acc[2 * i + 1] += p.y;
+    for (int u = 0; u < U; ++u) {
+      const long long e = e0 + u * stride;
+      const bool ok = e < n;
+      we[u] = ok ? w[e] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[u][i] = ok ? V[i * ldv + e] : cmk(0.0, 0.0);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const cplx p = cdotc(v[u][i], we[u]);
+        acc[2 * i] += p.x;
+        acc[2 * i + 1] += p.y;
+      }
   }
   block_reduce_store(acc, NQ, PA);
   grid.sync();
@@ -311,19 +347,28 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
   // ---- phase 2
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
-    cplx we = w[e];
-    cplx v[NV];
+  for (long long e0 = blockIdx.x * (long long)TPB + tid; e0 < n; e0 += stride * U) {
+    cplx we[U], v[U][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = V[i * ldv + e];
+    for (int u = 0; u < U; ++u) {
+      const long long e = e0 + u * stride;
+      const bool ok = e < n;
+      we[u] = ok ? w[e] : cmk(0.0, 0.0);
 #pragma unroll
-    for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], v[i]));
-    w[e] = we;
+      for (int i = 0; i < NV; ++i) v[u][i] = ok ? V[i * ldv + e] : cmk(0.0, 0.0);
+    }
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const cplx p = cdotc(v[i], we);
-      acc[2 * i] += p.x;
-      acc[2 * i + 1] += p.y;
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) we[u] = csub(we[u], cmul(s_c[i], v[u][i]));
+      const long long e = e0 + u * stride;
+      if (e < n) w[e] = we[u];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const cplx p = cdotc(v[u][i], we[u]);
+        acc[2 * i] += p.x;
+        acc[2 * i + 1] += p.y;
+      }
     }
   }
   block_reduce_store(acc, NQ, PB);
@@ -333,12 +378,24 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
   __syncthreads();
   // ---- phase 3
   acc[0] = 0.0;
-  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) {
-    cplx we = w[e];
+  for (long long e0 = blockIdx.x * (long long)TPB + tid; e0 < n; e0 += stride * U) {
+    cplx we[U], v[U][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) we = csub(we, cmul(s_c[i], V[i * ldv + e]));
-    w[e] = we;
-    acc[0] += cabs2(we);
+    for (int u = 0; u < U; ++u) {
+      const long long e = e0 + u * stride;
+      const bool ok = e < n;
+      we[u] = ok ? w[e] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[u][i] = ok ? V[i * ldv + e] : cmk(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) we[u] = csub(we[u], cmul(s_c[i], v[u][i]));
+      const long long e = e0 + u * stride;
+      if (e < n) w[e] = we[u];
+      acc[0] += cabs2(we[u]);
+    }
   }
   block_reduce_store(acc, 1, PA);
   grid.sync();
@@ -372,7 +429,19 @@ __global__ void __launch_bounds__(TPB) lz_iter_kernel(LanczosDev d, const cplx* 
   }
   // ---- phase 4
   const double inv = brk ? 0.0 : 1.0 / b;
-  for (long long e = blockIdx.x * (long long)TPB + tid; e < n; e += stride) vnext[e] = cscale(w[e], inv);
+  for (long long e0 = blockIdx.x * (long long)TPB + tid; e0 < n; e0 += stride * 4) {
+    cplx we[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long e = e0 + u * stride;
+      we[u] = e < n ? w[e] : cmk(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long e = e0 + u * stride;
+      if (e < n) vnext[e] = cscale(we[u], inv);
+    }
+  }
 }
 
 // Lowest eigenpair of the symmetric tridiagonal T = tridiag(alpha, beta) (one
@@ -490,10 +559,12 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
   // grid-wide barriers get cheaper with fewer blocks: 64 blocks for small
   // vectors (measured: the non-matvec Lanczos time at chi = 128 drops by a
   // third against 296 blocks), more once a vector exceeds 16K elements/block
-  const long long want = std::max<long long>(64, n / 16384);
+  // (measured: 2K elements per block keeps HBM busy from chi = 512 up)
+  const long long want = std::max<long long>(64, n / 2048);
+  // every block sums all G partials (deterministic order): G <= 2 * SMs
+  const long long cap = (long long)std::min(occ[nv], 2) * g_num_sms;
   const int G = (int)std::max<long long>(
-      1, std::min<long long>(std::min<long long>(nblk_for(n), (long long)occ[nv] * g_num_sms),
-                             std::min<long long>(want, 2LL * g_num_sms)));
+      1, std::min<long long>(std::min<long long>((n + TPB - 1) / TPB, cap), want));
   void* args[] = {(void*)&d,    (void*)&V,   (void*)&ldv, (void*)&w,      (void*)&vnext, (void*)&n,
                   (void*)&k,    (void*)&last, (void*)&tol, (void*)&tau_re, (void*)&tau_im};
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(TPB), args, 0, st);

@@ -53,7 +53,8 @@ class tdvp_stats(C.Structure):
                 ("lanczos2_ms", C.c_double), ("lanczos1_ms", C.c_double),
                 ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
                 ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int), ("svd_bj_ms", C.c_double),
-                ("svd_bj_flop", C.c_double), ("svd_bj_calls", C.c_int)]
+                ("svd_bj_flop", C.c_double), ("svd_bj_calls", C.c_int), ("lz_ms_bin", C.c_double * 4),
+                ("lz_bytes_bin", C.c_double * 4)]
 
     def as_dict(self):
         out = {}
