@@ -106,8 +106,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
+// per-warp cp.async ring: NST stages of 8 rows x PC columns (column-major,
+// row index swizzled by sw(col) so both the Gram's and the apply's fragment
+// reads are bank-conflict free)
+constexpr int NST = 4;
+constexpr int STG = 8 * PC;  // complex elements per stage
+__device__ __forceinline__ int sw(int col) { return ((col & 1) << 2) | (col & 2); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 struct Smem {
-  cplx red[4][PC * GP];  // warp-tree reduction of the Gram tiles
+  union {
+    cplx red[4][PC * GP];       // warp-tree reduction of the Gram tiles
+    cplx ring[8][NST][STG];     // cp.async staging of X / V rows (Gram and apply loops)
+  };
   cplx G[PC][GP];
   cplx Q[PC][GP];
   double cs[PC / 2];
@@ -187,48 +207,68 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
         sm.col[tid] = (blk < a.nb && c < a.nc) ? c : -1;
       }
       __syncthreads();
-      // ---- 1. partial Gram over rows [xr0, xr1) of X: warp w takes 4-row steps w, w+8, ...
+      // ---- 1. partial Gram over rows [xr0, xr1) of X: warp w takes 8-row
+      // stages w, w+8, ... streamed through its cp.async ring (NST - 1 stages
+      // in flight), two 4-row DMMA k-steps per stage
       // 3M products: conj(a) b = (P1 + P2) + i (P3 - P1 + P2) with P1 = ar br,
       // P2 = ai bi, P3 = (ar - ai)(br + bi): three real DMMAs per complex MAC
       double g1[NUT][2], g2[NUT][2], g3[NUT][2];
 #pragma unroll
       for (int t = 0; t < NUT; ++t) g1[t][0] = g1[t][1] = g2[t][0] = g2[t][1] = g3[t][0] = g3[t][1] = 0.0;
       {
-        int cc[4];
+        // this lane's cp.async chunks: c = lane + 32 k -> column c >> 3, row c & 7
+        int ccol[8];
 #pragma unroll
-        for (int cb = 0; cb < 4; ++cb) cc[cb] = sm.col[cb * 8 + (lane >> 2)];
-        const int nsteps = (xr1 - xr0 + 3) / 4;
-        constexpr int U = 2;  // steps in flight per warp
-        for (int st0 = wid; st0 < nsteps; st0 += 8 * U) {
-          cplx x[U][4];
+        for (int k = 0; k < 8; ++k) ccol[k] = sm.col[(lane >> 3) + 4 * k];
+        cplx* ring = &sm.ring[wid][0][0];
+        const int nstage = (xr1 - xr0 + 7) / 8;
+        auto issue = [&](int j, int slot) {
+          const int rb = xr0 + 8 * j;
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int r = xr0 + (st0 + 8 * u) * 4 + (lane & 3);
-            const bool rv = (st0 + 8 * u) < nsteps && r < xr1;
-#pragma unroll
-            for (int cb = 0; cb < 4; ++cb)
-              x[u][cb] = (rv && cc[cb] >= 0) ? __ldcg(Y + (long long)cc[cb] * ldy + r) : cmk(0.0, 0.0);
+          for (int k = 0; k < 8; ++k) {
+            const int col = (lane >> 3) + 4 * k, r = lane & 7, row = rb + r;
+            const bool v = j < nstage && ccol[k] >= 0 && row < xr1;
+            cp_async16(ring + slot * STG + col * 8 + (r ^ sw(col)), v ? (const void*)(Y + (long long)ccol[k] * ldy + row)
+                                                                      : (const void*)Y, v);
           }
+          cp_commit();
+        };
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            double xs[4], xd[4];
+        for (int i = 0; i < NST - 1; ++i) issue(wid + 8 * i, i);
+        int slot = 0;
+        for (int j = wid; j < nstage; j += 8) {
+          cp_wait<NST - 2>();
+          __syncwarp();
+          // refill the slot consumed in the previous iteration, NST - 1 stages ahead
+          issue(j + 8 * (NST - 1), slot == 0 ? NST - 1 : slot - 1);
+          const cplx* st = ring + slot * STG;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            double xr_[4], xi_[4], xs[4], xd[4];
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb) {
-              xs[cb] = x[u][cb].x + x[u][cb].y;
-              xd[cb] = x[u][cb].x - x[u][cb].y;
+              const int col = cb * 8 + (lane >> 2), r = 4 * t + (lane & 3);
+              const cplx v = st[col * 8 + (r ^ sw(col))];
+              xr_[cb] = v.x;
+              xi_[cb] = v.y;
+              xs[cb] = v.x + v.y;
+              xd[cb] = v.x - v.y;
             }
 #pragma unroll
-            for (int t = 0; t < NUT; ++t) {
+            for (int tt = 0; tt < NUT; ++tt) {
               int ti, tj;
-              ut_tile(t, ti, tj);
+              ut_tile(tt, ti, tj);
               // G[i][j] += conj(x_ki) x_kj : A from x[ti] (row-major 8x4), B from x[tj] (col-major 4x8)
-              dmma(g1[t][0], g1[t][1], x[u][ti].x, x[u][tj].x);
-              dmma(g2[t][0], g2[t][1], x[u][ti].y, x[u][tj].y);
-              dmma(g3[t][0], g3[t][1], xd[ti], xs[tj]);
+              dmma(g1[tt][0], g1[tt][1], xr_[ti], xr_[tj]);
+              dmma(g2[tt][0], g2[tt][1], xi_[ti], xi_[tj]);
+              dmma(g3[tt][0], g3[tt][1], xd[ti], xs[tj]);
             }
           }
+          slot = slot + 1 == NST ? 0 : slot + 1;
         }
+        cp_wait<0>();
       }
+      __syncthreads();  // every warp is done with its ring (aliases the reduction buffer)
       double gR[NUT][2], gI[NUT][2];
 #pragma unroll
       for (int t = 0; t < NUT; ++t)
@@ -441,60 +481,80 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
             bqi[ks][jt] = q.y;
             bqs[ks][jt] = q.x + q.y;
           }
-        int cc[8], cs_[4][2];
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) cc[ks] = sm.col[ks * 4 + (lane & 3)];
+        int cs_[4][2];
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt)
 #pragma unroll
           for (int h = 0; h < 2; ++h) cs_[jt][h] = sm.col[jt * 8 + 2 * (lane & 3) + h];
-        for (int part = 0; part < 2; ++part) {
-          const int rb0 = part == 0 ? xr0 : a.vofs + vr0;
-          const int rb1 = part == 0 ? xr1 : a.vofs + vr1;
-          cplx av[8], nx[8];
-          auto load_chunk = [&](int r0, cplx (&dst)[8]) {
-            const int r = r0 + (lane >> 2);
-            const bool rv = r < rb1;
+        int ccol[8];
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
-              dst[ks] = (rv && cc[ks] >= 0) ? __ldcg(Y + (long long)cc[ks] * ldy + r) : cmk(0.0, 0.0);
-          };
-          if (rb0 + wid * 8 < rb1) load_chunk(rb0 + wid * 8, nx);
-          for (int r0 = rb0 + wid * 8; r0 < rb1; r0 += 64) {
+        for (int k = 0; k < 8; ++k) ccol[k] = sm.col[(lane >> 3) + 4 * k];
+        cplx* ring = &sm.ring[wid][0][0];
+        // X rows then V rows, 8-row stages, warp w takes stages w, w+8, ...
+        const int nsx = (xr1 - xr0 + 7) / 8, nsv = (vr1 - vr0 + 7) / 8, nstage = nsx + nsv;
+        auto srow = [&](int j, int& rb, int& re) {
+          if (j < nsx) {
+            rb = xr0 + 8 * j;
+            re = xr1;
+          } else {
+            rb = a.vofs + vr0 + 8 * (j - nsx);
+            re = a.vofs + vr1;
+          }
+        };
+        auto issue = [&](int j, int slot) {
+          int rb = 0, re = 0;
+          if (j < nstage) srow(j, rb, re);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks) av[ks] = nx[ks];
-            if (r0 + 64 < rb1) load_chunk(r0 + 64, nx);  // next chunk in flight during the DMMAs
-            double c1[4][2], c2[4][2], c3[4][2];
+          for (int k = 0; k < 8; ++k) {
+            const int col = (lane >> 3) + 4 * k, r = lane & 7, row = rb + r;
+            const bool v = j < nstage && ccol[k] >= 0 && row < re;
+            cp_async16(ring + slot * STG + col * 8 + (r ^ sw(col)), v ? (const void*)(Y + (long long)ccol[k] * ldy + row)
+                                                                      : (const void*)Y, v);
+          }
+          cp_commit();
+        };
 #pragma unroll
-            for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
+        for (int i = 0; i < NST - 1; ++i) issue(wid + 8 * i, i);
+        int slot = 0;
+        for (int j = wid; j < nstage; j += 8) {
+          cp_wait<NST - 2>();
+          __syncwarp();
+          issue(j + 8 * (NST - 1), slot == 0 ? NST - 1 : slot - 1);
+          const cplx* st = ring + slot * STG;
+          cplx av[8];
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-              const double as = av[ks].x + av[ks].y;
+          for (int ks = 0; ks < 8; ++ks) {
+            const int col = ks * 4 + (lane & 3), r = lane >> 2;
+            av[ks] = st[col * 8 + (r ^ sw(col))];
+          }
+          double c1[4][2], c2[4][2], c3[4][2];
 #pragma unroll
-              for (int jt = 0; jt < 4; ++jt) {
-                dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
-                dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
-                dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
-              }
+          for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double as = av[ks].x + av[ks].y;
+#pragma unroll
+            for (int jt = 0; jt < 4; ++jt) {
+              dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
+              dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
+              dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
             }
-            double cR[4][2], cI[4][2];
+          }
+          slot = slot + 1 == NST ? 0 : slot + 1;
+          int rb, re;
+          srow(j, rb, re);
+          const int ro = rb + (lane >> 2);
+          if (ro < re) {
 #pragma unroll
             for (int jt = 0; jt < 4; ++jt)
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                cR[jt][h] = c1[jt][h] - c2[jt][h];
-                cI[jt][h] = c3[jt][h] - c1[jt][h] - c2[jt][h];
-              }
-            const int ro = r0 + (lane >> 2);
-            if (ro < rb1) {
-#pragma unroll
-              for (int jt = 0; jt < 4; ++jt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-                  if (cs_[jt][h] >= 0) __stcg(Y + (long long)cs_[jt][h] * ldy + ro, cmk(cR[jt][h], cI[jt][h]));
-            }
+              for (int h = 0; h < 2; ++h)
+                if (cs_[jt][h] >= 0)
+                  __stcg(Y + (long long)cs_[jt][h] * ldy + ro,
+                         cmk(c1[jt][h] - c2[jt][h], c3[jt][h] - c1[jt][h] - c2[jt][h]));
           }
         }
+        cp_wait<0>();
       }
       mark(3);
       __syncthreads();
