@@ -144,12 +144,19 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_kernel(cplx* A, long long lda,
 
 // Panel [k0, k0+kb) of column-major A (rows k0..m-1, kb <= 32) factored by ONE
 // thread-block cluster of C CTAs: CTA c holds rows [c*rc, (c+1)*rc) of the
-// panel in its shared memory.  Per reflector i two cluster barriers: (1) the
-// partial norms of column i below the pivot (and the pivot alpha from its
-// owner) are summed by every CTA in rank order through DSMEM -> identical
-// zlarfg (beta, tau, 1/(alpha-beta)) everywhere; (2) the partial dots
-// w_j = v_i^H a_j (j > i) and z_j = v_j^H v_i (j < i, for T) are summed the
-// same way, then every CTA updates its rows of a_j -= conj(tau) v_i w_j.
+// panel in its shared memory.  ONE cluster barrier per reflector i: every CTA
+// forms, over its rows g >= i, the partial sums
+//   s_j = x^H a_j (j > i),  s_j = v_j^H x (j < i),  s_i = |x below the pivot|^2
+// with x = column i BEFORE the reflector is known, and the owner of pivot row
+// i publishes that row (alpha = x_i, a_j[i], v_j[i]); after the barrier every
+// CTA sums the C partials in rank order (identical everywhere) and forms
+// zlarfg (beta, tau, scale = 1/(alpha - beta)) and, since v = (x - beta e_i) scale,
+//   w_j = v^H a_j = conj(scale) (s_j - beta a_j[i])          (j > i)
+//   z_j = v_j^H v = scale (s_j - beta conj(v_j[i]))           (j < i, for T)
+// (algebraically the LAPACK dots with the explicit v; |scale| <= 1/||x|| keeps
+// the rounding at eps ||a_j||), then updates its rows of a_j -= conj(tau) v w_j.
+// The DSMEM slots are double-buffered by reflector parity, so the next
+// reflector's partials never overwrite ones a slower CTA is still reading.
 // Output as qr_panel_kernel (R / reflector tails in A, explicit rows Vc, tau, T).
 constexpr int QPW = 32;   // max panel width
 constexpr int QPNT = 256;
@@ -161,19 +168,17 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
   const int crank = (int)cluster.block_rank();
   extern __shared__ __align__(16) unsigned char qr_sm[];
   cplx* P = reinterpret_cast<cplx*>(qr_sm);  // [kb][rc] column j at P + j*rc
-  __shared__ double s_nrm[2];                 // partial |x|^2 below the pivot; [1] unused
-  __shared__ cplx s_alpha;                    // pivot value (owner CTA)
-  __shared__ cplx s_w[QPW];                   // partial dots of this CTA
-  __shared__ cplx s_wt[QPW];                  // summed dots
+  __shared__ cplx s_w[2][QPW];                // partial sums of this CTA (by reflector parity)
+  __shared__ cplx s_row[2][QPW];              // pivot row (owner CTA, by parity)
+  __shared__ cplx s_pw[QPW][16];              // partial sums of all CTAs
+  __shared__ cplx s_rowt[QPW];                // pivot row fetched from its owner
+  __shared__ cplx s_wt[QPW];                  // w_j (j > i)
   __shared__ cplx s_z[QPW][QPW + 1];          // (CTA 0) z[j][i] = v_j^H v_i
   __shared__ cplx s_tau[QPW];
   __shared__ cplx s_T[QPW][QPW + 1];
-  __shared__ double s_red[8];
   __shared__ cplx s_scale;
+  __shared__ double s_beta;
   __shared__ int s_refl;
-  __shared__ double s_pn[16];       // partial norms of all CTAs
-  __shared__ cplx s_al;
-  __shared__ cplx s_pw[QPW][16];    // partial dots of all CTAs
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int rows = m - k0;
   const int r0 = crank * rc;                       // first panel row of this CTA
@@ -183,98 +188,135 @@ __global__ void __launch_bounds__(QPNT, 1) qr_panel_cl_kernel(cplx* A, long long
     P[j * rc + r] = (r < nr) ? A[(long long)(k0 + j) * lda + k0 + r0 + r] : cmk(0.0, 0.0);
   }
   __syncthreads();
+  // thread (h, rr): rows rr and rr + 128 of this CTA, panel columns [16 h, 16 h + 16)
+  const int h = tid >> 7, rr = tid & 127;
+  __shared__ double s_red[QPNT / 32][32];
   for (int i = 0; i < kb; ++i) {
-    const int pr = i;  // pivot row within the panel
+    const int pr = i, par = i & 1;  // pivot row within the panel
     cplx* vi = P + i * rc;
-    // ---- (1) partial norm of column i below the pivot
+    // ---- (1) partial sums over this CTA's rows g >= pr: 16 columns per thread,
+    // then a warp reduce-scatter (lane l: value l) and the 4 warps of a half
     {
-      double x = 0.0;
-      for (int r = tid; r < nr; r += QPNT)
-        if (r0 + r > pr) x += cabs2(vi[r]);
-      x = warp_sum(x);
-      if (lane == 0) s_red[wid] = x;
-      __syncthreads();
-      if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < QPNT / 32; ++w) t += s_red[w];
-        s_nrm[0] = t;
-        if (pr >= r0 && pr < r0 + nr) s_alpha = vi[pr - r0];
+      double val[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) val[u] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = rr + 128 * q, g = r0 + r;
+        if (r >= nr || g < pr) continue;
+        const cplx x = vi[r];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = 16 * h + jj;
+          if (j >= kb) continue;
+          const cplx a = P[j * rc + r];
+          cplx t;
+          if (j > i) t = cdotc(x, a);
+          else if (j < i) t = cdotc(a, x);
+          else t = cmk(g > pr ? cabs2(x) : 0.0, 0.0);
+          val[2 * jj] += t.x;
+          val[2 * jj + 1] += t.y;
+        }
       }
+#pragma unroll
+      for (int lev = 0; lev < 5; ++lev) {
+        const int msk = 16 >> lev, hh = 16 >> lev;
+        const bool up = (lane & msk) != 0;
+#pragma unroll
+        for (int u = 0; u < hh; ++u) {
+          const double send = up ? val[u] : val[u + hh];
+          const double keep = up ? val[u + hh] : val[u];
+          val[u] = keep + __shfl_xor_sync(0xffffffffu, send, msk);
+        }
+      }
+      s_red[wid][lane] = val[0];
     }
-    cluster.sync();
-    // the C partial norms fetched in parallel (one DSMEM round trip), summed in rank order
-    if (tid < C) s_pn[tid] = *cluster.map_shared_rank(&s_nrm[0], tid);
-    if (tid == 32) s_al = *cluster.map_shared_rank(&s_alpha, pr / rc);
     __syncthreads();
-    if (tid == 0) {
-      double xn2 = 0.0;
-      for (int c = 0; c < C; ++c) xn2 += s_pn[c];
-      const cplx al = s_al;
+    if (tid < 64) {
+      const int hh = tid >> 5, l = tid & 31, j = 16 * hh + (l >> 1);
+      const double t = ((s_red[4 * hh][l] + s_red[4 * hh + 1][l]) + s_red[4 * hh + 2][l]) + s_red[4 * hh + 3][l];
+      if (j < kb) reinterpret_cast<double*>(&s_w[par][j])[l & 1] = t;
+    } else if (tid < 64 + kb) {
+      if (pr >= r0 && pr < r0 + nr) s_row[par][tid - 64] = P[(tid - 64) * rc + pr - r0];
+    }
+    __syncthreads();
+    cluster.sync();
+    // kb x C partials and the pivot row fetched in parallel (one DSMEM round trip)
+    for (int e = tid; e < kb * C; e += QPNT) {
+      const int j = e / C, c = e - j * C;
+      s_pw[j][c] = *cluster.map_shared_rank(&s_w[par][j], c);
+    }
+    if (tid >= QPNT - QPW && tid - (QPNT - QPW) < kb)
+      s_rowt[tid - (QPNT - QPW)] = *cluster.map_shared_rank(&s_row[par][tid - (QPNT - QPW)], pr / rc);
+    // every thread keeps its rows of x (column i) for step (3)
+    cplx xq[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = rr + 128 * q;
+      xq[q] = r < nr ? vi[r] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    // ---- (2) zlarfg and the dots, every CTA (identical sums in a fixed
+    // pairwise order over the C = 8 or 16 ranks, identical results)
+    if (tid < kb) {
+      cplx t[16];
+      double xn[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        t[c] = c < C ? s_pw[tid][c] : cmk(0.0, 0.0);
+        xn[c] = c < C ? s_pw[i][c].x : 0.0;
+      }
+#pragma unroll
+      for (int w = 1; w < 16; w *= 2)
+#pragma unroll
+        for (int c = 0; c + w < 16; c += 2 * w) {
+          t[c] = cadd(t[c], t[c + w]);
+          xn[c] += xn[c + w];
+        }
+      const cplx sj = t[0];
+      const double xn2 = xn[0];
+      const cplx al = s_rowt[i];
       const double ar = al.x, ai = al.y;
       cplx t_i = cmk(0.0, 0.0), scale = cmk(1.0, 0.0);
       double beta = ar;
       const bool refl = !(xn2 == 0.0 && ai == 0.0);
       if (refl) {
         beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
-        t_i = cmk((beta - ar) / beta, -ai / beta);
+        const double ib = 1.0 / beta;
+        t_i = cmk((beta - ar) * ib, -ai * ib);
         const double dr = ar - beta, di = ai;
-        const double den = dr * dr + di * di;
-        scale = cmk(dr / den, -di / den);  // 1 / (alpha - beta)
+        const double iden = 1.0 / (dr * dr + di * di);
+        scale = cmk(dr * iden, -di * iden);  // 1 / (alpha - beta)
       }
-      s_tau[i] = t_i;
-      s_scale = scale;
-      s_refl = refl;
-      if (pr >= r0 && pr < r0 + nr) vi[pr - r0] = cmk(beta, 0.0);  // R_pp; v_p = 1 implicitly
+      if (tid > i) {
+        s_wt[tid] = cmul(cconj(t_i), cmul(cconj(scale), csub(sj, cscale(s_rowt[tid], beta))));  // conj(tau) w_j
+      } else if (tid < i) {
+        if (crank == 0) s_z[tid][i] = cmul(scale, csub(sj, cscale(cconj(s_rowt[tid]), beta)));
+      } else {
+        s_tau[i] = t_i;
+        s_scale = scale;
+        s_beta = beta;
+        s_refl = refl;
+      }
     }
     __syncthreads();
-    if (s_refl) {
+    // ---- (3) v_i = (x - beta e_pr) scale; a_j -= v_i conj(tau) w_j (j > i);
+    // the half holding column i writes v_i (R_pp = beta at the pivot)
+    {
       const cplx sc = s_scale;
-      for (int r = tid; r < nr; r += QPNT)
-        if (r0 + r > pr) vi[r] = cmul(vi[r], sc);
-    }
-    __syncthreads();
-    // ---- (2) partial dots: w_j = v_i^H a_j (j > i), z_j = v_j^H v_i (j < i)
-    for (int j = wid; j < kb; j += QPNT / 32) {
-      if (j == i) continue;
-      const cplx* aj = P + j * rc;
-      double dr = 0.0, di = 0.0;
-      for (int r = lane; r < nr; r += 32) {
-        const int g = r0 + r;
-        if (g < pr) continue;
-        const cplx v = (g == pr) ? cmk(1.0, 0.0) : vi[r];
-        const cplx x = (j > i) ? cdotc(v, aj[r]) : cdotc((g == j) ? cmk(1.0, 0.0) : aj[r], v);
-        dr += x.x;
-        di += x.y;
-      }
-      dr = warp_sum(dr);
-      di = warp_sum(di);
-      if (lane == 0) s_w[j] = cmk(dr, di);
-    }
-    __syncthreads();
-    cluster.sync();
-    // kb x C partial dots fetched in parallel, then summed per column in rank order
-    for (int e = tid; e < kb * C; e += QPNT) {
-      const int j = e / C, c = e - j * C;
-      if (j != i) s_pw[j][c] = *cluster.map_shared_rank(&s_w[j], c);
-    }
-    __syncthreads();
-    if (tid < kb && tid != i) {
-      cplx t = cmk(0.0, 0.0);
-      for (int c = 0; c < C; ++c) t = cadd(t, s_pw[tid][c]);
-      s_wt[tid] = t;
-      if (crank == 0 && tid < i) s_z[tid][i] = t;
-    }
-    __syncthreads();
-    const cplx ct = cconj(s_tau[i]);
-    for (int j = wid; j < kb; j += QPNT / 32) {
-      if (j <= i) continue;
-      cplx* aj = P + j * rc;
-      const cplx f = cmul(ct, s_wt[j]);
-      for (int r = lane; r < nr; r += 32) {
-        const int g = r0 + r;
-        if (g < pr) continue;
-        const cplx v = (g == pr) ? cmk(1.0, 0.0) : vi[r];
-        aj[r] = csub(aj[r], cmul(v, f));
+      const bool refl = s_refl != 0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = rr + 128 * q, g = r0 + r;
+        if (r >= nr || g < pr) continue;
+        const cplx v = (g == pr) ? cmk(1.0, 0.0) : (refl ? cmul(xq[q], sc) : xq[q]);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = 16 * h + jj;
+          if (j <= i || j >= kb) continue;
+          P[j * rc + r] = csub(P[j * rc + r], cmul(v, s_wt[j]));
+        }
+        if (h == (i >> 4)) vi[r] = (g == pr) ? cmk(s_beta, 0.0) : v;
       }
     }
     __syncthreads();
