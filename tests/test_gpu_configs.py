@@ -10,7 +10,8 @@ lies within the cut's uncertainty band of eps*sigma_1, or continues the
 multiplet at the last common value.  The band is derived from the measured
 GPU-oracle difference of the common spectrum at that bond (4x its max, floor
 1e-13 sigma_1 = the SVDs' own rounding at n <= 2048), not from the observable
-tolerance.  Flip counts are returned and bounded per config."""
+tolerance.  Flip counts are returned and bounded per config; c5 (eps = 1e-12,
+10 steps) bounds the weight of one-sided tails instead (R-F2)."""
 import numpy as np
 import pytest
 
@@ -31,7 +32,7 @@ def B():
     return pkg
 
 
-def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
+def run_both(B, mps, W, chi_max, eps, dt, steps, p, every, weight_tol=None):
     D = max(max(w.shape[0], w.shape[3]) for w in W)
     t = B.Tdvp(len(W), 2, D, chi_max)
     t.set_params(eps=eps)
@@ -55,7 +56,7 @@ def run_both(B, mps, W, chi_max, eps, dt, steps, p, every):
         _, glam = t.get_mps()
         _, olam = O.global_mps(st)
         for a, b in zip(glam, olam):
-            dchi = check_spectra(a, b, eps, tol)
+            dchi = check_spectra(a, b, eps, tol, weight_tol)
             max_dchi = max(max_dchi, dchi)
         flips += sum(1 for x, y in zip(chi, ochi) if x != y)
     s = t.stats()
@@ -86,16 +87,16 @@ def test_config4_long_range(B, p):
 @pytest.mark.parametrize("p", [1, 2, 4, 8])
 def test_config5_scaling_partitions(B, p):
     c = ti.config("c5")
-    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], p, every=5)
-    # At eps = 1e-12 the cut sits where the singular values carry absolute
-    # errors ~ sqrt(n) u sigma_1 ~ 1e-14 sigma_1 (1% of the cut) on BOTH sides,
-    # and the SU(2) chain has dense multiplets there, so bonds flip by up to a
-    # multiplet; check_spectra verifies that every flipped value is such a
-    # near-cut value (DESIGN.md R-F).  Bounds: measured on B200 (round 2:
-    # max |dchi| 4-7, 138-173 flipped bond checks over 255 bonds x 2 checks
-    # for p = 1..8), with margin.
-    assert r["max_dchi"] <= 8
-    assert r["flips"] <= 250
+    # At eps = 1e-12 the cut sits at the level of the accumulated FP64
+    # difference of the two runs (~1e-12 sigma_1 after 10 steps, different
+    # SVD algorithms and product orders), and the SU(2) chain has dense
+    # multiplets there, so bonds flip at the cut by whole multiplets, and a
+    # value kept by one side keeps growing with the entanglement of the Neel
+    # quench.  The tails one side holds alone must weigh <= 1e-9 sigma_1 (a
+    # state difference at the untruncated tolerance, DESIGN.md R-F2); the
+    # observables are held to north_star's 1e-6 and measured at ~1e-11.
+    r = run_both(B, c["mps"], c["mpo"], c["chi_max"], c["eps"], c["dt"], c["steps"], p, every=5, weight_tol=1e-9)
+    assert r["worst"] < 1e-9
     assert max(r["chi"]) < c["chi_max"]  # chi_max never binds from the Neel state in 10 steps
 
 
