@@ -401,7 +401,15 @@ def main():
     bins_fl = np.sum([s["heff2_flop_bin"] for s in per_t], axis=0)
     lzb_ms = np.sum([s["lz_ms_bin"] for s in per_t], axis=0)
     lzb_by = np.sum([s["lz_bytes_bin"] for s in per_t], axis=0)
-    zpeak = peaks.get("zgemm") if peaks else None
+    # the library's complex GEMMs (zgemm.cu) and the block-Jacobi Gram / rotation
+    # products (svd_bjac.cu) execute 3 real DMMA products per complex MAC (3M);
+    # their algorithmic rate (8 flop per complex MAC) is therefore held against
+    # 4/3 x the measured cuBLAS ZGEMM (4M) rate: the same DMMA pipe throughput
+    zpeak4 = peaks.get("zgemm") if peaks else None
+    zpeak = zpeak4 * 4.0 / 3.0 if zpeak4 else None
+    zsrc = (f"measured in this run: cuBLAS ZGEMM {zpeak4} TFLOP/s (4 real DMMA products per complex MAC) x 4/3 "
+            f"for 3M kernels (3 products per complex MAC, 8 algorithmic flop) = {zpeak}; "
+            f"MEASURED_PEAKS.json has no FP64 entry")
 
     # e2e: the same step through the C-ABI with HOST buffers (set_mps H2D incl.
     # the sequential environment build, step, get_mps D2H) every step
@@ -443,7 +451,7 @@ def main():
     rf_bj = {"kernel": "bjac_kernel (block one-sided Jacobi SVD on the DMMA pipe, > 1024 columns)", "bound": "tensor",
              "achieved": bj_tf, "peak": zpeak, "unit": "TFLOP/s",
              "frac": (bj_tf / zpeak) if (bj_tf and zpeak) else None, "traffic": bjac_traffic(bj_n, nb),
-             "peak_source": f"measured in this run: cuBLAS ZGEMM {zpeak} TFLOP/s (MEASURED_PEAKS.json has no FP64 entry)",
+             "peak_source": zsrc,
              "flop_per_unit": "executed per block pair and round: Gram 8 xr 32^2 10/16 + rotation 8 (xr+nc) 32^2 "
                               "(8 flop per complex MAC, counted on the device)",
              "launches_per_step": bj_n / nb, "ms_per_launch": bj_ms / bj_n if bj_n else None,
@@ -452,7 +460,7 @@ def main():
             "achieved": tf(h2_fl + h1_fl, h2_ms + h1_ms), "peak": zpeak, "unit": "TFLOP/s",
             "frac": (tf(h2_fl + h1_fl, h2_ms + h1_ms) / zpeak) if (zpeak and h2_ms + h1_ms > 0) else None,
             "traffic": None,
-            "peak_source": f"measured in this run: cuBLAS FP64 {json.dumps(peaks)} (MEASURED_PEAKS.json has no FP64 entry)",
+            "peak_source": zsrc + f" (cuBLAS FP64 measured: {json.dumps(peaks)})",
             "flop_per_unit": "SURVEY §8(d): 8[d^2 cl cr (Dl cl + Dr cr) + d cl cr (nnzW_j + nnzW_j+1)] per H2 matvec",
             "share_of_step": (h2_ms + h1_ms) / bstep_ms if bstep_ms > 0 else None}
     # the dominant kernel: the ncu launch list of this workload puts bjac_kernel
@@ -463,7 +471,7 @@ def main():
     for name, ms_, fl_ in zip(("chi<=128", "chi<=256", "chi<=512", "chi<=1024"), bins_ms, bins_fl):
         if ms_ > 0:
             v = tf(fl_, ms_)
-            bins[name] = {"tflops": v, "frac_of_zgemm_peak": (v / zpeak) if zpeak else None, "ms_per_step": ms_ / nb}
+            bins[name] = {"tflops": v, "frac_of_dmma_peak_3m": (v / zpeak) if zpeak else None, "ms_per_step": ms_ / nb}
     lz_bins = {}
     for name, ms_, by_ in zip(("chi<=128", "chi<=256", "chi<=512", "chi<=1024"), lzb_ms, lzb_by):
         if ms_ > 0:
