@@ -268,6 +268,22 @@ struct tdvp_ctx {
   // round-robin executor on one stream.
   tdvp_ctx* parent = nullptr;
   bool lanes_on = true;
+  // U(1) split: workers that run the sector SVDs concurrently (own stream and
+  // SVD workspace each; allocated on the first U(1) split)
+  struct U1Worker {
+    cudaStream_t st = nullptr;
+    BufPtr Y, Q, F, sigma, order, perm, bj, off, ires, dres;
+    double* h_pin = nullptr;
+    int* h_ipin = nullptr;
+    SvdDev sv{};
+    ~U1Worker() {
+      if (st) cudaStreamSynchronize(st);
+      if (h_pin) cudaFreeHost(h_pin);
+      if (h_ipin) cudaFreeHost(h_ipin);
+      if (st) cudaStreamDestroy(st);
+    }
+  };
+  std::vector<std::unique_ptr<U1Worker>> u1w;
   std::vector<std::unique_ptr<tdvp_ctx>> lanes;  // lanes 1 .. p-1
   std::vector<std::unique_ptr<LaneMsg>> msg_r, msg_l;  // per segment: to q+1, to q-1
   ~tdvp_ctx();
@@ -282,6 +298,7 @@ tdvp_ctx::~tdvp_ctx() {
   if (prev != dev) cudaSetDevice(dev);  // this context's stream, events and buffers live on `dev`
   if (st) cudaStreamSynchronize(st);
   lanes.clear();
+  u1w.clear();
   msg_r.clear();
   msg_l.clear();
   segs.clear();
@@ -676,7 +693,7 @@ void u1_svd_split(tdvp_ctx* h, const cplx* M, int m, int n, const std::vector<in
   for (int k = 0; k < n; ++k) sec[cq[k]].second.push_back(k);
   struct Sector {
     int Q, mq, nq, kq = 0, idx_off = 0;
-    long long offL = 0, offR = 0;
+    long long offL = 0, offR = 0, goff = 0, koff = 0;
     std::vector<double> sig;
   };
   std::vector<Sector> ss;
@@ -699,30 +716,107 @@ void u1_svd_split(tdvp_ctx* h, const cplx* M, int m, int n, const std::vector<in
   const TruncParams full{std::max(m, n), 0.0, 0.0, 0.0};
   cplx* stL = h->T1->c();
   cplx* stR = h->T2->c();
-  long long offL = 0, offR = 0;
-  sweeps_sum = 0;
-  for (auto& t : ss) {
-    CK(cudaStreamSynchronize(h->st));  // idx upload / previous host reads done
-    u1_gather_kernel<<<u1_grid((long long)t.mq * t.nq), 256, 0, h->st>>>(M, n, didx + t.idx_off,
-                                                                         didx + t.idx_off + t.mq, t.mq, t.nq,
-                                                                         h->tmpA->c());
-    CK(cudaGetLastError());
-    int k = 0, rr = 0, ce = 0, sw = 0;
-    double ww = 0.0;
-    t.offL = offL;
-    t.offR = offR;
-    cudaError_t se = svd_truncate_split(h->st, h->sv, h->tmpA->c(), t.mq, t.nq, full, stL + offL, stR + offR,
-                                        h->u1_lam->d(), h->u1_vinv->d(), &k, &ww, &rr, &ce, &sw);
-    if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in a U(1) sector");
-    CK(se);
-    sweeps_sum += std::max(sw, 0);
-    t.kq = k;
-    t.sig.resize(k);
-    CK(cudaMemcpyAsync(t.sig.data(), h->u1_lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    offL += (long long)t.mq * k;
-    offR += (long long)k * t.nq;
+  // every sector gets its own regions: the gathered block in tmpA, its factors
+  // in T1 / T2 and its spectrum in u1_lam / u1_vinv, sized by kmax = min(mq, nq)
+  // (sum mq nq <= m n and sum kmax <= min(m, n): the sectors partition rows and columns)
+  {
+    long long go = 0, lo = 0, ro = 0, ko = 0;
+    for (auto& t : ss) {
+      const int kmax = std::min(t.mq, t.nq);
+      t.offL = lo;
+      t.offR = ro;
+      t.goff = go;
+      t.koff = ko;
+      go += (long long)t.mq * t.nq;
+      lo += (long long)t.mq * kmax;
+      ro += (long long)kmax * t.nq;
+      ko += kmax;
+    }
   }
+  // sector SVDs run concurrently: NW worker threads, each with its own stream
+  // and SVD workspace (svd_truncate_split reads chi back on the host), sectors
+  // handed out largest first; the workers wait on the index upload
+  constexpr int NW = 4;
+  if (h->u1w.empty()) {
+    const long long ncmax = (long long)h->d * h->chi_max;
+    const size_t nflags = (size_t)4 * ncmax + 64;
+    for (int w = 0; w < NW; ++w) {
+      auto u = std::make_unique<tdvp_ctx::U1Worker>();
+      CK(cudaStreamCreateWithFlags(&u->st, cudaStreamNonBlocking));
+      u->Y = make_buf((size_t)h->svdmax * sizeof(cplx));
+      u->Q = make_buf(h->svdQ->bytes);
+      u->F = make_buf(nflags * sizeof(unsigned));
+      u->sigma = make_buf(ncmax * sizeof(double) + 64);
+      u->order = make_buf(ncmax * sizeof(int) + 64);
+      u->perm = make_buf(2 * ncmax * sizeof(int) + 64);
+      u->bj = make_buf(svd_bjac_work_elems(g_num_sms) * sizeof(cplx));
+      u->off = make_buf(64);
+      u->ires = make_buf(64);
+      u->dres = make_buf(64);
+      CK(cudaMallocHost(&u->h_pin, 16 * sizeof(double)));
+      CK(cudaMallocHost(&u->h_ipin, 16 * sizeof(int)));
+      u->sv = SvdDev{u->Y->c(), 0, u->sigma->d(), u->order->i(), u->off->d(), u->ires->i(), u->dres->d(),
+                     u->h_pin, u->h_ipin, {nullptr, nullptr}, u->Q->c(), h->svdQ->bytes / sizeof(cplx),
+                     reinterpret_cast<unsigned*>(u->F->p), nflags, 1, u->perm->i(), u->bj->c(),
+                     svd_bjac_work_elems(g_num_sms)};
+      h->u1w.push_back(std::move(u));
+    }
+  }
+  cudaEvent_t ev_in = ev_get(h);
+  CK(cudaEventRecord(ev_in, h->st));
+  std::vector<int> order(ss.size());
+  for (size_t i = 0; i < ss.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a_, int b_) {
+    return (long long)ss[a_].mq * ss[a_].nq > (long long)ss[b_].mq * ss[b_].nq;
+  });
+  std::atomic<int> next{0};
+  std::vector<int> sws(ss.size(), 0);
+  std::vector<std::string> errs(NW);
+  std::vector<int> errc(NW, 0);
+  const int dev = h->dev;
+  auto work = [&](int w) {
+    try {
+      DeviceGuard dg(dev);
+      tdvp_ctx::U1Worker& u = *h->u1w[w];
+      CK(cudaStreamWaitEvent(u.st, ev_in, 0));
+      for (int i = next.fetch_add(1); i < (int)ss.size(); i = next.fetch_add(1)) {
+        Sector& t = ss[order[i]];
+        cplx* blk = h->tmpA->c() + t.goff;
+        u1_gather_kernel<<<u1_grid((long long)t.mq * t.nq), 256, 0, u.st>>>(M, n, didx + t.idx_off,
+                                                                          didx + t.idx_off + t.mq, t.mq, t.nq, blk);
+        CK(cudaGetLastError());
+        int k = 0, rr = 0, ce = 0, sw = 0;
+        double ww = 0.0;
+        cudaError_t se = svd_truncate_split(u.st, u.sv, blk, t.mq, t.nq, full, stL + t.offL, stR + t.offR,
+                                            h->u1_lam->d() + t.koff, h->u1_vinv->d() + t.koff, &k, &ww, &rr, &ce,
+                                            &sw);
+        if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in a U(1) sector");
+        CK(se);
+        sws[order[i]] = std::max(sw, 0);
+        t.kq = k;
+        t.sig.resize(k);
+        CK(cudaMemcpyAsync(t.sig.data(), h->u1_lam->d() + t.koff, k * sizeof(double), cudaMemcpyDeviceToHost, u.st));
+        CK(cudaStreamSynchronize(u.st));
+      }
+    } catch (const TdvpError& e) {
+      errc[w] = e.code;
+      errs[w] = e.what();
+    } catch (const std::exception& e) {
+      errc[w] = TDVP_ECUDA;
+      errs[w] = e.what();
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (int w = 1; w < NW; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& x : th) x.join();
+  }
+  for (int w = 0; w < NW; ++w)
+    if (errc[w]) throw TdvpError(errc[w], errs[w]);
+  sweeps_sum = 0;
+  for (int x : sws) sweeps_sum += x;
+  g_launch_count += 2 * (long long)ss.size();
   // global order: descending sigma, ties by sector charge then index (oracle/u1.py)
   struct Ent { double s; int sec, k; };
   std::vector<Ent> all;
@@ -766,7 +860,6 @@ void u1_svd_split(tdvp_ctx* h, const cplx* M, int m, int n, const std::vector<in
   // scatter the kept triplets; lam / V / charges in that order
   CK(cudaMemsetAsync(psiL, 0, (size_t)m * chi * sizeof(cplx), h->st));
   CK(cudaMemsetAsync(psiR, 0, (size_t)chi * n * sizeof(cplx), h->st));
-  std::vector<int> kmap(offL > 0 ? 0 : 0);
   std::vector<std::vector<int>> km(ss.size());
   for (int si = 0; si < (int)ss.size(); ++si) km[si].assign(ss[si].kq, -1);
   std::vector<double> hl(chi), hv(chi);
