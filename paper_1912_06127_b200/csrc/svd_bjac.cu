@@ -13,11 +13,19 @@
 //      warps in a fixed tree, CTAs in index order through global memory);
 //   2. measures the pair's largest scaled coupling c = |g_ij| / sqrt(g_ii g_jj)
 //      (the one-sided convergence test, relative, so tiny columns count);
-//   3. if c > tol / 4: diagonalises G by cyclic two-sided Jacobi rotations in
-//      shared memory (each of the 256 threads updates one 2 x 2 block of G per
-//      round), accumulating the unitary Q (every S CTA of the pair does this
-//      redundantly on the identical G, so no broadcast is needed), and
-//   4. applies [X_p ; V_p] <- [X_p ; V_p] Q on the DMMA pipe over its rows.
+//   3. if c > tol / 4: rotates G by two-sided Jacobi rotations in shared
+//      memory -- every column pair of the matrix exactly once per outer sweep:
+//      a full cyclic sweep over the pair's 32 columns in the sweep's round 0,
+//      the 16 x 16 cross-block pairs in the other rounds -- accumulating the
+//      unitary Q (every S CTA of the pair does this redundantly on the
+//      identical G, so no broadcast is needed), and
+//   4. applies X_p <- X_p Q on the DMMA pipe over its rows (all 8 warps).
+// The inner solve (step 3) runs on warps 0..3 only; meanwhile warps 4..7
+// replay the CTA's PREVIOUS round on V (V_p <- V_p Q_prev on its V rows, the
+// same DMMA products in the same round order per block, so V is bit-identical
+// to an in-round update), ordered by their own per-(block, slice) flags.  The
+// V half of the rotation work thus overlaps the latency-bound inner solve
+// instead of following it.
 // The inner solve only has to produce a unitary Q that orthogonalises the
 // pair well; the result's accuracy is set by the outer test, computed from
 // the actual columns every round (one-sided Jacobi's relative accuracy).
@@ -41,6 +49,8 @@ namespace {
 constexpr int BB = 16;        // columns per block
 constexpr int PC = 2 * BB;    // columns per block pair
 constexpr int NTB = 256;      // threads per CTA (8 warps)
+constexpr int NIW = 4;        // warps of the inner solve (the other NVW replay V meanwhile)
+constexpr int NVW = NTB / 32 - NIW;
 constexpr int GP = PC + 1;    // padded row length of the shared PC x PC matrices
 constexpr int NUT = 10;       // upper-triangular 8 x 8 tiles of a 32 x 32 Gram matrix
 constexpr int NUB = (PC / 2) * (PC / 2 + 1) / 2;  // upper-triangular 2 x 2 blocks of the inner rotation rounds
@@ -55,7 +65,8 @@ struct BjArgs {
   cplx* part;      // [2][P][S][PC * PC] partial Gram matrices (double-buffered by round parity)
   unsigned* pcnt;  // [P] monotonic pair counters
   unsigned* gbar;  // [1] monotonic grid-barrier counter (end of every sweep)
-  unsigned* done;  // [nbe][S] rounds completed on row slice s of block b (monotonic)
+  unsigned* done;  // [nbe][S] X-phase rounds completed on row slice s of block b (monotonic)
+  unsigned* vdone; // [nbe][S] V-phase rounds completed on row slice s of block b (monotonic)
   double* offb;    // [3] per-sweep max scaled coupling
   int* sweeps_out;
   double* flop_out;  // algorithmic DMMA flops executed (Gram + apply)
@@ -88,6 +99,10 @@ __device__ __forceinline__ void ut_tile(int t, int& ti, int& tj) {
   constexpr int TJ[NUT] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
   ti = TI[t];
   tj = TJ[t];
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
@@ -130,10 +145,12 @@ struct Smem {
   };
   cplx G[PC][GP];
   cplx Q[PC][GP];
+  cplx Qp[PC][GP];   // the previous round's Q (pending V update)
   double cs[PC / 2];
   cplx sn[PC / 2];
   int rp[PC / 2], rq[PC / 2];
   int col[PC];       // global column of pair column i (-1: absent)
+  int colp[PC];      // the previous round's columns (pending V update)
   unsigned char ut_a[136], ut_b[136];  // upper-triangle 2 x 2 block u -> (row pair, column pair)
   double offw[8];
   int any;
@@ -176,6 +193,194 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
       const unsigned long long t = clock64();
       g_bj_prof[i] += t - pt;
       pt = t;
+    }
+  };
+  // Y_p rows [rb0, re0) <- Y_p Q (sm.Q, columns sm.col) on the DMMA pipe:
+  // 8-row stages, warp w takes stages w, w+8, ... through its cp.async ring.
+  // 3M products: a q = (P1 - P2) + i (P3 - P1 - P2) with P1 = ar qr,
+  // P2 = ai qi, P3 = (ar + ai)(qr + qi)
+  // Warps wl = 0 .. nw - 1 of the calling group (wl = wid - first warp).
+  auto apply_rows = [&](int rb0, int re0, const cplx (*Qm)[GP], const int* colv, int wl, int nw) {
+    double bqr[8][4], bqi[8][4], bqs[8][4];  // B fragments of Q: [k-step][j-tile]
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+        const cplx q = Qm[ks * 4 + (lane & 3)][jt * 8 + (lane >> 2)];
+        bqr[ks][jt] = q.x;
+        bqi[ks][jt] = q.y;
+        bqs[ks][jt] = q.x + q.y;
+      }
+    int cs_[4][2];
+#pragma unroll
+    for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) cs_[jt][h] = colv[jt * 8 + 2 * (lane & 3) + h];
+    int ccol[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ccol[k] = colv[(lane >> 3) + 4 * k];
+    cplx* ring = &sm.ring[wid][0][0];
+    const int nstage = (re0 - rb0 + 7) / 8;
+    auto issue = [&](int j, int slot) {
+      const int rb = rb0 + 8 * j;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int col = (lane >> 3) + 4 * k, r = lane & 7, row = rb + r;
+        const bool v = j < nstage && ccol[k] >= 0 && row < re0;
+        cp_async16(ring + slot * STG + col * 8 + (r ^ sw(col)), v ? (const void*)(Y + (long long)ccol[k] * ldy + row)
+                                                                  : (const void*)Y, v);
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < NST - 1; ++i) issue(wl + nw * i, i);
+    int slot = 0;
+    for (int j = wl; j < nstage; j += nw) {
+      cp_wait<NST - 2>();
+      __syncwarp();
+      issue(j + nw * (NST - 1), slot == 0 ? NST - 1 : slot - 1);
+      const cplx* st = ring + slot * STG;
+      cplx av[8];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int col = ks * 4 + (lane & 3), r = lane >> 2;
+        av[ks] = st[col * 8 + (r ^ sw(col))];
+      }
+      double c1[4][2], c2[4][2], c3[4][2];
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const double as = av[ks].x + av[ks].y;
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+          dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
+          dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
+          dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
+        }
+      }
+      slot = slot + 1 == NST ? 0 : slot + 1;
+      const int ro = rb0 + 8 * j + (lane >> 2);
+      if (ro < re0) {
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (cs_[jt][h] >= 0)
+              __stcg(Y + (long long)cs_[jt][h] * ldy + ro,
+                     cmk(c1[jt][h] - c2[jt][h], c3[jt][h] - c1[jt][h] - c2[jt][h]));
+      }
+    }
+    cp_wait<0>();
+  };
+  // V update pending from this CTA's previous round (warps 4..7 replay it
+  // during the next round's inner solve): blocks, global round index, whether
+  // the pair rotated; its Q and columns wait in sm.Qp / sm.colp
+  bool pv = false, pv_rot = false;
+  int pvI = 0, pvJ = 0;
+  unsigned long long pv_g = 0;
+  double vflops = 0.0;
+  // V rows [rb0, re0) <- V Q_prev (sm.Qp, columns sm.colp) by warps 4..7
+  // (wl = wid - NIW), like apply_rows over the warp's own cp.async ring (an
+  // 8-stage ring borrowing the idle inner warp's stages measured the same:
+  // the V stream is bound by DMMA issue of one warp per SM sub-partition)
+  constexpr int NSV = NST;
+  auto v_stream = [&](int rb0, int re0) {
+    const int wl = wid - NIW;
+    double bqr[8][4], bqi[8][4], bqs[8][4];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+        const cplx q = sm.Qp[ks * 4 + (lane & 3)][jt * 8 + (lane >> 2)];
+        bqr[ks][jt] = q.x;
+        bqi[ks][jt] = q.y;
+        bqs[ks][jt] = q.x + q.y;
+      }
+    int cs_[4][2];
+#pragma unroll
+    for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) cs_[jt][h] = sm.colp[jt * 8 + 2 * (lane & 3) + h];
+    int ccol[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ccol[k] = sm.colp[(lane >> 3) + 4 * k];
+    cplx* const rbase = &sm.ring[wid][0][0];
+    auto slot_ptr = [&](int slot) -> cplx* { return rbase + slot * STG; };
+    const int nstage = (re0 - rb0 + 7) / 8;
+    auto issue = [&](int j, int slot) {
+      const int rb = rb0 + 8 * j;
+      cplx* dst = slot_ptr(slot);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int col = (lane >> 3) + 4 * k, r = lane & 7, row = rb + r;
+        const bool v = j < nstage && ccol[k] >= 0 && row < re0;
+        cp_async16(dst + col * 8 + (r ^ sw(col)), v ? (const void*)(Y + (long long)ccol[k] * ldy + row) : (const void*)Y,
+                   v);
+      }
+      cp_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < NSV - 1; ++i) issue(wl + NVW * i, i);
+    int slot = 0;
+    for (int j = wl; j < nstage; j += NVW) {
+      cp_wait<NSV - 2>();
+      __syncwarp();
+      issue(j + 4 * (NSV - 1), slot == 0 ? NSV - 1 : slot - 1);
+      const cplx* st = slot_ptr(slot);
+      cplx av[8];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int col = ks * 4 + (lane & 3), r = lane >> 2;
+        av[ks] = st[col * 8 + (r ^ sw(col))];
+      }
+      double c1[4][2], c2[4][2], c3[4][2];
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const double as = av[ks].x + av[ks].y;
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+          dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
+          dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
+          dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
+        }
+      }
+      const int ro = rb0 + 8 * j + (lane >> 2);
+      if (ro < re0) {
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (cs_[jt][h] >= 0)
+              __stcg(Y + (long long)cs_[jt][h] * ldy + ro,
+                     cmk(c1[jt][h] - c2[jt][h], c3[jt][h] - c1[jt][h] - c2[jt][h]));
+      }
+      slot = slot + 1 == NSV ? 0 : slot + 1;
+    }
+    cp_wait<0>();
+  };
+  // the pending update's blocks finished their previous V round on slice s
+  auto v_wait = [&]() {
+    for (const int blk : {pvI, pvJ}) {
+      const unsigned* f = a.vdone + (long long)blk * a.S + s;
+      while (true) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int)(v - (unsigned)pv_g) >= 0) break;
+        __nanosleep(20);
+      }
+    }
+  };
+  auto v_release = [&]() {  // after a __syncthreads that follows every v_stream
+    if (tid == NIW * 32) {
+      __threadfence();
+      for (const int blk : {pvI, pvJ}) {
+        unsigned* f = a.vdone + (long long)blk * a.S + s;
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"((unsigned)(pv_g + 1)) : "memory");
+      }
+      if (s == 0 && pv_rot) vflops += 8.0 * (double)a.nc * PC * PC;
     }
   };
   double flops = 0.0;
@@ -377,24 +582,36 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
         atomic_max_nonneg(off_cur, cpair);
         flops += 8.0 * (double)a.xr * PC * PC * (double)NUT / 16.0;
       }
-      if (cpair > tol4) {
-        // ---- 3. two-sided cyclic Jacobi on G (shared memory), Q accumulated
-        for (int e = tid; e < PC * PC; e += NTB) {
+      const bool rotate = cpair > tol4;
+      if (wid < NIW) {
+        if (rotate) {
+        // ---- 3. two-sided cyclic Jacobi on G (shared memory), Q accumulated,
+        // by warps 0..3 (named barrier 1) while warps 4..7 replay the previous
+        // round's rotation on this CTA's V rows
+        for (int e = tid; e < PC * PC; e += NIW * 32) {
           const int i = e / PC, j = e - i * PC;
           sm.Q[i][j] = cmk(i == j ? 1.0 : 0.0, 0.0);
         }
         const double tol2q = tol4 * tol4;
-        // ONE cyclic sweep of 31 rounds of 16 disjoint rotations (the outer
-        // iteration converges as fast as with more inner sweeps, measured).
-        // Per round: threads 0..15 compute the rotation parameters (rsqrt
-        // only); then threads 0..135 each update one 2 x 2 block of the upper
-        // triangle of G (row pair ra <= column pair rb, packed into the first
-        // 4.25 warps so the others skip the branch; the lower triangle is the
-        // mirror), and every thread updates two (row, column pair) entries of Q.
-        for (int rd = 0; rd < PC - 1; ++rd) {
+        // Each column pair once per outer sweep (as svd_rjac.cu): in the
+        // sweep's round 0 (where every block sits in exactly one pair) a full
+        // cyclic sweep over the 32 columns, 31 rotation rounds of 16 disjoint
+        // rotations (intra-block and cross pairs); in the other rounds only
+        // the 16 cross-block rotation rounds (i, 16 + (i + rd) mod 16).
+        // Per rotation round: threads 0..15 compute the parameters (rsqrt
+        // only); then the inner warps update the 136 2 x 2 blocks of the upper
+        // triangle of G (row pair ra <= column pair rb; the lower triangle is
+        // the mirror) and the (row, column pair) entries of Q.
+        const int nrd = round == 0 ? PC - 1 : BB;
+        for (int rd = 0; rd < nrd; ++rd) {
           if (tid < PC / 2) {
             int p, q;
-            rr_pair(PC, rd, tid, p, q);
+            if (round == 0) {
+              rr_pair(PC, rd, tid, p, q);
+            } else {
+              p = tid;
+              q = BB + ((tid + rd) & (BB - 1));
+            }
             double cs = 1.0;
             cplx sn = cmk(0.0, 0.0);
             const double ga = sm.G[p][p].x, gc = sm.G[q][q].x;
@@ -417,9 +634,9 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
             sm.cs[tid] = cs;
             sm.sn[tid] = sn;
           }
-          __syncthreads();
-          if (tid < NUB) {
-            const int ra = sm.ut_a[tid], rb = sm.ut_b[tid];
+          named_bar(1, NIW * 32);
+          for (int ub = tid; ub < NUB; ub += NIW * 32) {
+            const int ra = sm.ut_a[ub], rb = sm.ut_b[ub];
             const int p1 = sm.rp[ra], q1 = sm.rq[ra], p2 = sm.rp[rb], q2 = sm.rq[rb];
             const double ca = sm.cs[ra], cb = sm.cs[rb];
             const cplx sa = sm.sn[ra], sb = sm.sn[rb];
@@ -450,10 +667,10 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
               sm.G[q2][q1] = cconj(n11);
             }
           }
-          // Q <- Q J_b: units (row, column pair) = tid, tid + 256
+          // Q <- Q J_b: units (row, column pair) = tid + 128 h
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int u = tid + h * NTB;
+          for (int h = 0; h < PC * PC / 2 / (NIW * 32); ++h) {
+            const int u = tid + h * NIW * 32;
             const int row = u >> 4, rb = u & 15;
             const int p2 = sm.rp[rb], q2 = sm.rq[rb];
             const double cb = sm.cs[rb];
@@ -462,99 +679,26 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
             sm.Q[row][p2] = csub(cscale(qp, cb), cmul(cconj(sb), qq));
             sm.Q[row][q2] = cadd(cmul(sb, qp), cscale(qq, cb));
           }
-          __syncthreads();
+          named_bar(1, NIW * 32);
         }
+        }
+      } else if (pv) {
+        const bool vprof = a.prof && blockIdx.x == 0 && tid == NIW * 32;
+        const unsigned long long t0 = vprof ? clock64() : 0;
+        if (tid == NIW * 32) v_wait();
+        named_bar(2, NVW * 32);
+        if (pv_rot) v_stream(a.vofs + vr0, a.vofs + vr1);
+        if (vprof) g_bj_prof[5] += clock64() - t0;
+      }
+      __syncthreads();
+      if (pv) v_release();
+      if (rotate) {
         if (prof) g_bj_prof[6]++;
         if (prof) g_bj_prof[7]++;
         mark(2);
-        // ---- 4. [X_p ; V_p] <- [X_p ; V_p] Q on the DMMA pipe, this CTA's rows
-        if (s == 0 && tid == 0) flops += 8.0 * (double)(a.xr + a.nc) * PC * PC;
-        // 3M products: a q = (P1 - P2) + i (P3 - P1 - P2) with P1 = ar qr,
-        // P2 = ai qi, P3 = (ar + ai)(qr + qi)
-        double bqr[8][4], bqi[8][4], bqs[8][4];  // B fragments of Q: [k-step][j-tile]
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-          for (int jt = 0; jt < 4; ++jt) {
-            const cplx q = sm.Q[ks * 4 + (lane & 3)][jt * 8 + (lane >> 2)];
-            bqr[ks][jt] = q.x;
-            bqi[ks][jt] = q.y;
-            bqs[ks][jt] = q.x + q.y;
-          }
-        int cs_[4][2];
-#pragma unroll
-        for (int jt = 0; jt < 4; ++jt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) cs_[jt][h] = sm.col[jt * 8 + 2 * (lane & 3) + h];
-        int ccol[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) ccol[k] = sm.col[(lane >> 3) + 4 * k];
-        cplx* ring = &sm.ring[wid][0][0];
-        // X rows then V rows, 8-row stages, warp w takes stages w, w+8, ...
-        const int nsx = (xr1 - xr0 + 7) / 8, nsv = (vr1 - vr0 + 7) / 8, nstage = nsx + nsv;
-        auto srow = [&](int j, int& rb, int& re) {
-          if (j < nsx) {
-            rb = xr0 + 8 * j;
-            re = xr1;
-          } else {
-            rb = a.vofs + vr0 + 8 * (j - nsx);
-            re = a.vofs + vr1;
-          }
-        };
-        auto issue = [&](int j, int slot) {
-          int rb = 0, re = 0;
-          if (j < nstage) srow(j, rb, re);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int col = (lane >> 3) + 4 * k, r = lane & 7, row = rb + r;
-            const bool v = j < nstage && ccol[k] >= 0 && row < re;
-            cp_async16(ring + slot * STG + col * 8 + (r ^ sw(col)), v ? (const void*)(Y + (long long)ccol[k] * ldy + row)
-                                                                      : (const void*)Y, v);
-          }
-          cp_commit();
-        };
-#pragma unroll
-        for (int i = 0; i < NST - 1; ++i) issue(wid + 8 * i, i);
-        int slot = 0;
-        for (int j = wid; j < nstage; j += 8) {
-          cp_wait<NST - 2>();
-          __syncwarp();
-          issue(j + 8 * (NST - 1), slot == 0 ? NST - 1 : slot - 1);
-          const cplx* st = ring + slot * STG;
-          cplx av[8];
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
-            const int col = ks * 4 + (lane & 3), r = lane >> 2;
-            av[ks] = st[col * 8 + (r ^ sw(col))];
-          }
-          double c1[4][2], c2[4][2], c3[4][2];
-#pragma unroll
-          for (int jt = 0; jt < 4; ++jt) c1[jt][0] = c1[jt][1] = c2[jt][0] = c2[jt][1] = c3[jt][0] = c3[jt][1] = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
-            const double as = av[ks].x + av[ks].y;
-#pragma unroll
-            for (int jt = 0; jt < 4; ++jt) {
-              dmma(c1[jt][0], c1[jt][1], av[ks].x, bqr[ks][jt]);
-              dmma(c2[jt][0], c2[jt][1], av[ks].y, bqi[ks][jt]);
-              dmma(c3[jt][0], c3[jt][1], as, bqs[ks][jt]);
-            }
-          }
-          slot = slot + 1 == NST ? 0 : slot + 1;
-          int rb, re;
-          srow(j, rb, re);
-          const int ro = rb + (lane >> 2);
-          if (ro < re) {
-#pragma unroll
-            for (int jt = 0; jt < 4; ++jt)
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-                if (cs_[jt][h] >= 0)
-                  __stcg(Y + (long long)cs_[jt][h] * ldy + ro,
-                         cmk(c1[jt][h] - c2[jt][h], c3[jt][h] - c1[jt][h] - c2[jt][h]));
-          }
-        }
-        cp_wait<0>();
+        // ---- 4. X_p <- X_p Q on the DMMA pipe over this CTA's rows (all warps)
+        if (s == 0 && tid == 0) flops += 8.0 * (double)a.xr * PC * PC;
+        apply_rows(xr0, xr1, sm.Q, sm.col, wid, 8);
       }
       mark(3);
       __syncthreads();
@@ -566,14 +710,33 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
           asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
         }
       }
+      // this round's V update becomes pending (replayed during the next
+      // round's inner solve, or after the last sweep)
+      if (rotate)
+        for (int e = tid; e < PC * PC; e += NTB) sm.Qp[e / PC][e % PC] = sm.Q[e / PC][e % PC];
+      if (tid < PC) sm.colp[tid] = sm.col[tid];
+      pv = true;
+      pv_rot = rotate;
+      pvI = bI;
+      pvJ = bJ;
+      pv_g = round_g;
+      __syncthreads();
     }
     grid_barrier(a.gbar, (unsigned)((sweep + 1) * (unsigned long long)G_));
     mark(4);
     const double off = __ldcg(off_cur);
     if (!(off > tol) || off * off <= 0.01 * tol) break;
   }
+  if (pv) {  // the last round's V update
+    if (tid == NIW * 32) v_wait();
+    __syncthreads();
+    if (pv_rot && wid >= NIW) v_stream(a.vofs + vr0, a.vofs + vr1);
+    __syncthreads();
+    v_release();
+  }
   if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = min(sweep + 1, a.max_sweeps);
   if (s == 0 && tid == 0 && flops > 0.0) atomicAdd(a.flop_out, flops);
+  if (s == 0 && tid == NIW * 32 && vflops > 0.0) atomicAdd(a.flop_out, vflops);
 }
 
 }  // namespace
@@ -598,11 +761,14 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   // S CTAs per pair (row slices) so that the grid fills the SMs once
   const int S = std::max(1, std::min(16, occ * g_num_sms / P));
   if (P * S > occ * g_num_sms) return cudaErrorNotSupported;
-  const size_t nfl = (size_t)P + 1 + (size_t)nbe * S;
-  if ((size_t)2 * P * S * PC * PC > d.bjwork_elems || nfl > d.flags_elems) return cudaErrorNotSupported;
+  const size_t nfl = (size_t)P + 1 + (size_t)2 * nbe * S;
+  const size_t npart = (size_t)2 * P * S * PC * PC;
+  if (npart > d.bjwork_elems || nfl > d.flags_elems)
+    return cudaErrorNotSupported;
   unsigned* pcnt = d.flags;
   unsigned* gbar = d.flags + P;
   unsigned* done = d.flags + P + 1;
+  unsigned* vdone = done + (size_t)nbe * S;
   if ((e = cudaMemsetAsync(d.flags, 0, nfl * sizeof(unsigned), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(d.offmax, 0, 4 * sizeof(double), st)) != cudaSuccess) return e;
   BjArgs a;
@@ -618,6 +784,7 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   a.tol = tol;
   a.max_sweeps = 60;
   a.part = d.bjwork;
+  a.vdone = vdone;
   a.pcnt = pcnt;
   a.gbar = gbar;
   a.done = done;
@@ -639,9 +806,9 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
     cudaMemcpyFromSymbolAsync(z, g_bj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     std::fprintf(stderr,
-                 "bjac prof xr=%d nc=%d P=%d S=%d cycles: gram %llu pairsum %llu inner %llu apply %llu gridbar %llu | "
+                 "bjac prof xr=%d nc=%d P=%d S=%d cycles: gram %llu pairsum %llu inner %llu apply %llu gridbar %llu vphase %llu | "
                  "inner sweeps %llu in %llu rounds\n",
-                 xr, nc, P, S, z[0], z[1], z[2], z[3], z[4], z[6], z[7]);
+                 xr, nc, P, S, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[7]);
   }
   return e;
 }
