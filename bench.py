@@ -51,9 +51,9 @@ WORKLOADS = {
 
 def bjac_traffic(launches, steps):
     """DRAM bytes (read + write) per bjac_kernel launch of this workload from the
-    committed ncu --set full capture (profiles/r2_ncu_bjac_c5sat.json), else None."""
+    committed ncu --set full capture (profiles/r2f_ncu_bjac_c5sat.json), else None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r2_ncu_bjac_c5sat.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2f_ncu_bjac_c5sat.json")) as f:
             m = json.load(f)["metrics"]
         return float(m["dram_bytes_per_launch"])
     except (OSError, KeyError, ValueError):

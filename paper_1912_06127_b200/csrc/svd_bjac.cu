@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
     for (int j = wl; j < nstage; j += NVW) {
       cp_wait<NSV - 2>();
       __syncwarp();
-      issue(j + 4 * (NSV - 1), slot == 0 ? NSV - 1 : slot - 1);
+      issue(j + NVW * (NSV - 1), slot == 0 ? NSV - 1 : slot - 1);
       const cplx* st = slot_ptr(slot);
       cplx av[8];
 #pragma unroll
@@ -669,8 +669,9 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
           }
           // Q <- Q J_b: units (row, column pair) = tid + 128 h
 #pragma unroll
-          for (int h = 0; h < PC * PC / 2 / (NIW * 32); ++h) {
+          for (int h = 0; h < (PC * PC / 2 + NIW * 32 - 1) / (NIW * 32); ++h) {
             const int u = tid + h * NIW * 32;
+            if (u >= PC * PC / 2) break;
             const int row = u >> 4, rb = u & 15;
             const int p2 = sm.rp[rb], q2 = sm.rq[rb];
             const double cb = sm.cs[rb];
