@@ -1184,6 +1184,156 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   h->stats.n_back++;
 }
 
+// ------------------------------------------------------ one-site TDVP
+// Serial 1TDVP, the integrator the hybrid scheme of PAPER.md:697 switches to
+// once chi_max is saturated (reading R-1TDVP in DESIGN.md; oracle/tdvp1.py
+// step1 is the same algorithm step by step).  Storage stays the paper's
+// inverse-canonical product Psi_0 V_0 Psi_1 ...; every
+// bond split is the 2TDVP truncated SVD (O-7).
+
+// H_eff^(0) C (bond matrix): y[a, b] = sum L[a, w, a'] R[b, w, b'] x[a', b']
+// (the one-site Fig 5b contraction, without a site tensor):
+// two DMMA GEMMs, T[(a, w), b'] = L[(a, w), a'] x[a', b'], y = T R^T over (w, b')
+void heff0(tdvp_ctx* h, const cplx* Lenv, const cplx* Renv, int D, int cl, int cr, const cplx* x, cplx* y) {
+  cplx* T1 = h->T1->c();
+  gemm(h, OP_N, OP_N, cl * D, cr, cl, Lenv, cl, x, cr, T1, cr);
+  gemm(h, OP_N, OP_T, cl, cr, D * cr, T1, (long long)D * cr, Renv, (long long)D * cr, y, cr);
+}
+
+double flops_heff0(int cl, int cr, int D) { return 8.0 * ((double)D * cl * cl * cr + (double)D * cl * cr * cr); }
+
+// forward one-site step Psi_j <- exp(-i t H_eff^(1)) Psi_j
+void site_forward(tdvp_ctx* h, Segment& g, int j, double t) {
+  const int d = h->d, cl = g.cb[j], cr = g.cb[j + 1];
+  const MpoSite& W = h->mpo[j];
+  const long long n = (long long)cl * d * cr;
+  const cplx* Lenv = P(g.beta[j]);
+  const cplx* Renv = P(g.gamma[j]);
+  CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), n));
+  g_launch_count++;
+  expm_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff1(h, Lenv, W, Renv, cl, cr, x, y); }, h->tmpB->c(), P(g.psi[j]), n, 0.0,
+      -t, h->prm.krylov_k, 0, flops_heff1(cl, cr, d, W.Dl, W.Dr, nnz_of(W)));
+}
+
+// truncated SVD of an m x n matrix into (U S, S W^dag), Lambda / V of bond b
+int split_bond(tdvp_ctx* h, Segment& g, int b, const cplx* M, int m, int n, cplx* US, cplx* SWh) {
+  TruncParams tp{h->chi_max, h->prm.eps, h->prm.w_max, h->prm.multiplet_delta};
+  int chi = 0, r = 0, chi_eps = 0, sweeps = 0;
+  double w = 0.0;
+  cudaError_t se = svd_truncate_split(h->st, h->sv, M, m, n, tp, US, SWh, g.lam[b]->d(), g.vinv[b]->d(), &chi, &w, &r,
+                                      &chi_eps, &sweeps);
+  if (se == cudaErrorUnknown) throw TdvpError(TDVP_ENUMERIC, "non-finite or zero spectrum in SVD at bond " + std::to_string(b));
+  CK(se);
+  g_launch_count += 5;
+  if (chi > h->cbmax[b + 1]) throw TdvpError(TDVP_ECUDA, "internal: chi exceeds allocation");
+  h->stats.w_step += w;
+  h->stats.svd_sweeps_max = std::max(h->stats.svd_sweeps_max, sweeps);
+  h->stats.svd_sweeps_total += sweeps;
+  if (chi < std::min(chi_eps, r)) h->stats.trunc_active = 1;
+  return chi;
+}
+
+void step1_serial(tdvp_ctx* h, double dt) {
+  Segment& g = h->segs[0];
+  const int L = h->L, d = h->d, K = h->prm.krylov_k;
+  const double tau = 0.5 * dt;
+  // bond matrix C (<= max chi_b^2 <= the two-site buffer) and its evolved copy
+  // C2 in tmpB (free between the environment update and the next site step)
+  cplx* C = h->theta->c();
+  cplx* C2 = h->tmpB->c();
+  // left to right (the last site by the merged dt)
+  for (int j = 0; j < L; ++j) {
+    site_forward(h, g, j, j == L - 1 ? dt : tau);
+    if (j == L - 1) break;
+    const int cl = g.cb[j], cr = g.cb[j + 1], cr2 = g.cb[j + 2];
+    const MpoSite& W = h->mpo[j];
+    // B = diag(V_j) Psi_{j+1} (right-canonical), before V_j is replaced
+    CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), cr, (long long)d * cr2));
+    CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
+    g_launch_count += 2;
+    const int chi = split_bond(h, g, j, h->tmpB->c(), cl * d, cr, P(g.psi[j]), C);
+    g.cb[j + 1] = chi;
+    // beta_{j+1} from U = Psi_j diag(V_j)
+    CK(scale_cols(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
+    g_launch_count++;
+    env_left(h, P(g.beta[j]), h->tmpB->c(), W, cl, chi, P(g.beta[j + 1]));
+    // C <- exp(+i tau H_eff^(0)(beta_{j+1}, gamma_j)) C
+    const cplx* Le = P(g.beta[j + 1]);
+    const cplx* Re = P(g.gamma[j]);
+    expm_lanczos(
+        h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dr, chi, cr, x, y); }, C, C2, (long long)chi * cr, 0.0,
+        tau, K, 0, flops_heff0(chi, cr, W.Dr));
+    // Psi_{j+1} = C B
+    gemm(h, OP_N, OP_N, chi, d * cr2, cr, C2, cr, h->tmpA->c(), (long long)d * cr2, P(g.psi[j + 1]),
+         (long long)d * cr2);
+  }
+  // right to left (the last site was evolved by dt above)
+  for (int j = L - 1; j >= 0; --j) {
+    if (j < L - 1) site_forward(h, g, j, tau);
+    if (j == 0) break;
+    const int cl2 = g.cb[j - 1], cl = g.cb[j], cr = g.cb[j + 1];
+    const MpoSite& W = h->mpo[j];
+    // A = Psi_{j-1} diag(V_{j-1}) (left-canonical), before V_{j-1} is replaced
+    CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j - 1]), g.vinv[j - 1]->d(), (long long)cl2 * d, cl));
+    CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
+    g_launch_count += 2;
+    const int chi = split_bond(h, g, j - 1, h->tmpB->c(), cl, d * cr, C, P(g.psi[j]));
+    g.cb[j] = chi;
+    // gamma_{j-1} from W^dag = diag(V_{j-1}) Psi_j
+    CK(scale_rows(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j - 1]->d(), chi, (long long)d * cr));
+    g_launch_count++;
+    env_right(h, P(g.gamma[j]), h->tmpB->c(), W, chi, cr, P(g.gamma[j - 1]));
+    // C <- exp(+i tau H_eff^(0)(beta_j, gamma_{j-1})) C
+    const cplx* Le = P(g.beta[j]);
+    const cplx* Re = P(g.gamma[j - 1]);
+    expm_lanczos(
+        h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dl, cl, chi, x, y); }, C, C2, (long long)cl * chi, 0.0,
+        tau, K, 0, flops_heff0(cl, chi, W.Dl));
+    // Psi_{j-1} = A C
+    gemm(h, OP_N, OP_N, cl2 * d, chi, cl, h->tmpA->c(), cl, C2, chi, P(g.psi[j - 1]), chi);
+  }
+}
+
+// hybrid switch rule: every bond at min(chi_max, d^(j+1), d^(L-j-1))
+bool chi_saturated(tdvp_ctx* h) {
+  const Segment& g = h->segs[0];
+  for (int j = 0; j + 1 < h->L; ++j) {
+    long long cap = 1;
+    const int k = std::min(j + 1, h->L - j - 1);
+    for (int i = 0; i < k && cap < h->chi_max; ++i) cap *= h->d;
+    if (g.cb[j + 1] < std::min<long long>(cap, h->chi_max)) return false;
+  }
+  return true;
+}
+
+void layout(tdvp_ctx* h, int p);
+bool local_mode(tdvp_ctx* h);
+void reset_step_stats(tdvp_ctx* h);
+void finish_timing(tdvp_ctx* h);
+
+void do_step1(tdvp_ctx* h, double dt) {
+  if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step1");
+  if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
+  if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "tdvp_step1 runs on a single-process handle");
+  if (h->prm.u1) throw TdvpError(TDVP_EARG, "tdvp_step1 runs in dense mode (u1 = 0)");
+  if (h->layout_p != 1 || !h->envs_valid) layout(h, 1);
+  reset_step_stats(h);
+  h->evolved = true;
+  const long long l0 = g_launch_count, g0 = g_gemm_count;
+  CK(cudaEventRecord(h->ev_step0, h->st));
+  step1_serial(h, dt);
+  CK(cudaEventRecord(h->ev_step1, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev_step0, h->ev_step1));
+  h->stats.step_ms = ms;
+  h->stats.w_total += h->stats.w_step;
+  h->stats.kernel_launches = g_launch_count - l0;
+  h->stats.gemm_launches = g_gemm_count - g0;
+  if (h->prm.timing) finish_timing(h);
+}
+
 // ------------------------------------------------------------ layout / init
 void alloc_segment(tdvp_ctx* h, Segment& g, int q, int s, int e, int dev) {
   const int L = h->L, d = h->d;
@@ -2544,6 +2694,38 @@ int tdvp_step(tdvp_t h, double dt, int n_segments) {
   if (!h) return TDVP_EARG;
   try {
     do_step(h, dt, n_segments);
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_step1(tdvp_t h, double dt) {
+  if (!h) return TDVP_EARG;
+  try {
+    do_step1(h, dt);
+  } catch (const TdvpError& e) {
+    return fail(h, e);
+  }
+  return TDVP_OK;
+}
+
+int tdvp_step_hybrid(tdvp_t h, double dt, int n_segments, int* used) {
+  if (!h) return TDVP_EARG;
+  try {
+    bool one = false;
+    if (n_segments == 1 && h->have_mps && local_mode(h) && !h->prm.u1) {
+      if (h->layout_p != 1 || !h->envs_valid) {
+        if (!h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step_hybrid");
+        layout(h, 1);
+      }
+      one = chi_saturated(h);
+    }
+    if (one)
+      do_step1(h, dt);
+    else
+      do_step(h, dt, n_segments);
+    if (used) *used = one ? 1 : 2;
   } catch (const TdvpError& e) {
     return fail(h, e);
   }

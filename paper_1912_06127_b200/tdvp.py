@@ -75,6 +75,8 @@ _SIGS = {
     "tdvp_set_mpo": (C.c_int, [C.c_void_p, _I, _PD]),
     "tdvp_set_mps": (C.c_int, [C.c_void_p, _I, _PD, _PD]),
     "tdvp_step": (C.c_int, [C.c_void_p, C.c_double, C.c_int]),
+    "tdvp_step1": (C.c_int, [C.c_void_p, C.c_double]),
+    "tdvp_step_hybrid": (C.c_int, [C.c_void_p, C.c_double, C.c_int, _I]),
     "tdvp_measure_sz": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_norm": (C.c_int, [C.c_void_p, _D]),
@@ -181,6 +183,16 @@ class Tdvp:
 
     def step(self, dt, n_segments=1):
         _check(lib().tdvp_step(self.h, float(dt), int(n_segments)), self.h)
+
+    def step1(self, dt):
+        """One serial one-site TDVP step (tdvp_step1)."""
+        _check(lib().tdvp_step1(self.h, float(dt)), self.h)
+
+    def step_hybrid(self, dt, n_segments=1):
+        """One hybrid 2TDVP -> 1TDVP step (tdvp_step_hybrid); returns 1 or 2."""
+        used = C.c_int()
+        _check(lib().tdvp_step_hybrid(self.h, float(dt), int(n_segments), C.byref(used)), self.h)
+        return used.value
 
     def measure_sz(self):
         out = np.zeros(self.L)
