@@ -263,6 +263,26 @@ def secondary_u1(pkg, steps, warmup):
     return res
 
 
+def secondary_1tdvp(pkg, steps, warmup):
+    """The headline workload (c5sat: chi_max = 1024 saturated on bonds 10..14)
+    advanced by the hybrid scheme's one-site integrator (tdvp_step1, PAPER.md:697
+    "1TDVP is faster") vs the 2TDVP step, same state, same handle."""
+    wl = workload_inputs("c5sat")
+    t = pkg.Tdvp(wl["L"], 2, wl["D"], wl["chi"])
+    t.set_params(eps=wl["eps"])
+    t.set_mpo(wl["mpo"])
+    t.set_mps(wl["mps"].psi, wl["mps"].lam)
+    for _ in range(warmup):
+        t.step1(wl["dt"])
+    ms = []
+    for _ in range(steps):
+        t.step1(wl["dt"])
+        ms.append(t.stats()["step_ms"])
+    t.close()
+    return {"desc": wl["desc"] + "; one-site TDVP steps (tdvp_step1)", "ms_per_step": float(np.mean(ms)),
+            "steps": steps}
+
+
 def secondary_c2sat(pkg, steps, warmup):
     """Round 1's chi=128 headline (configs[1] shapes), serial and as 8 segment lanes on this GPU."""
     wl = workload_inputs("c2sat")
@@ -505,6 +525,8 @@ def main():
     if not args.no_extras and world == 1 and n_gpus == 1:
         line["secondary_c2sat"] = secondary_c2sat(pkg, max(1, min(args.steps, 5)), 2)
         line["secondary_u1"] = secondary_u1(pkg, 2, 1)
+        line["secondary_1tdvp"] = secondary_1tdvp(pkg, 2, 1)
+        line["secondary_1tdvp"]["speedup_vs_2tdvp"] = line["ms_per_step"] / line["secondary_1tdvp"]["ms_per_step"]
     if not args.no_cpu_baseline and world == 1 and n_gpus == 1:
         line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line))
