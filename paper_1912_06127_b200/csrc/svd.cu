@@ -950,15 +950,19 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   int sweeps = 0;
   const bool tj = jac_ms_out != nullptr && d.ev_jac[0] != nullptr;
   if (tj && (e = cudaEventRecord(d.ev_jac[0], st)) != cudaSuccess) return e;
-  // block Jacobi on DMMA (svd_bjac.cu) beyond 1024 columns (chi = 1024 two-site
-  // matrices: 290 vs 674 ms at n = 2048); up to 1024 the register-resident
-  // rjac is as fast (microbench.py --svd: 15.6 vs 17.1 ms at 512, 50.5 vs 53.3
-  // at 1024).  TDVP_SVD_BJ_MIN lowers the threshold (parity tests run both).
-  static int bj_min = -1;
-  if (bj_min < 0) {
+  // block Jacobi on DMMA (svd_bjac.cu) from 300 columns (tools/svd_once.py,
+  // random n x n: 384 9.8 vs 11.3 ms for the register-resident rjac, 512 13.8
+  // vs 15.6, 768 27.4 vs 34.1, 1024 42.3 vs 48.1; 256 and below rjac is as
+  // fast or faster).  With several SVDs in flight (d.throughput: segment lanes,
+  // U(1) sector workers) the grid-filling bjac would serialise them, so there
+  // it only takes what rjac cannot (> 1024 columns).  TDVP_SVD_BJ_MIN
+  // overrides the threshold (the parity tests force both paths).
+  static int bj_env = -2;
+  if (bj_env == -2) {
     const char* ev = std::getenv("TDVP_SVD_BJ_MIN");
-    bj_min = ev ? std::atoi(ev) : 1025;
+    bj_env = ev ? std::atoi(ev) : -1;
   }
+  const int bj_min = bj_env >= 0 ? bj_env : (d.throughput ? 1025 : 300);
   if ((e = cudaMemsetAsync(d.dres + 2, 0, sizeof(double), st)) != cudaSuccess) return e;
   bool bj = false;
   if (nc >= bj_min && (e = svd_bjac_run(st, d, x_rows, mr, nc, ldy, tol, d.ires + 4, d.dres + 2)) !=

@@ -326,13 +326,26 @@ def test_paper_mode_krylov_tol_matches_oracle(B, p):
 
 
 def test_svd_block_jacobi_forced_small(B):
-    """The DMMA block-Jacobi SVD path (svd_bjac.cu, default only beyond 1024
+    """The DMMA block-Jacobi SVD path (svd_bjac.cu, by default from 300
     columns) forced down to 32 columns (TDVP_SVD_BJ_MIN, read once per process,
     hence a subprocess): every SVD parity test above on ragged small shapes."""
     import os
     import subprocess
     import sys
     env = dict(os.environ, TDVP_SVD_BJ_MIN="32")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "svd and not forced",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_svd_register_jacobi_forced_large(B):
+    """The register-resident Jacobi (svd_rjac.cu) kept for every width up to
+    1024 columns (TDVP_SVD_BJ_MIN = 1025, the segment-lane / U(1)-worker
+    rule): every SVD parity test above, 300..1024 columns included."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TDVP_SVD_BJ_MIN="1025")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "svd and not forced",
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
