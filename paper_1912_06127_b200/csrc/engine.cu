@@ -1448,6 +1448,48 @@ void download_state(tdvp_ctx* h) {
 void build_envs(tdvp_ctx* h) {
   const int L = h->L, d = h->d;
   const std::vector<int>& chi = h->h_chi;
+  bool on_lead = local_mode(h);
+  for (const auto& g : h->segs) on_lead = on_lead && g.dev == h->dev;
+  if (on_lead) {
+    // every segment on this handle's device: the state was just uploaded
+    // (upload_state), so the chains read the owners' device tensors -- no
+    // second host upload, no host synchronisation per site
+    const cplx one = ONE;
+    cplx* cur = h->envA->c();
+    cplx* nxt = h->envB->c();
+    auto store = [&](bool left, int j, const cplx* src, long long n) {
+      for (auto& g : h->segs) {
+        const BufPtr& b = left ? g.beta[j] : g.gamma[j];
+        if (b) CK(cudaMemcpyAsync(b->p, src, n * sizeof(cplx), cudaMemcpyDeviceToDevice, h->st));
+      }
+    };
+    CK(cudaMemcpyAsync(cur, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+    store(true, 0, cur, 1);
+    // serial layout: every step, DMRG sweep and 1TDVP step starts with a
+    // left-to-right sweep, which rebuilds beta_1..beta_{L-1} as it goes
+    // (the initial envs a sweep needs are the ones ahead of it)
+    const int left_end = h->layout_p == 1 ? 0 : L - 1;
+    for (int j = 0; j < left_end; ++j) {
+      const Segment& o = h->segs[owner_of(h, j)];
+      CK(scale_cols(h->st, h->tmpA->c(), P(o.psi[j]), o.vinv[j]->d(), (long long)chi[j] * d, chi[j + 1]));
+      env_left(h, cur, h->tmpA->c(), h->mpo[j], chi[j], chi[j + 1], nxt);
+      std::swap(cur, nxt);
+      store(true, j + 1, cur, (long long)chi[j + 1] * h->mpo[j].Dr * chi[j + 1]);
+    }
+    cur = h->envA->c();
+    nxt = h->envB->c();
+    CK(cudaMemcpyAsync(cur, &one, sizeof(cplx), cudaMemcpyHostToDevice, h->st));
+    store(false, L - 1, cur, 1);
+    for (int j = L - 1; j > 0; --j) {
+      const Segment& o = h->segs[owner_of(h, j)];
+      CK(scale_rows(h->st, h->tmpA->c(), P(o.psi[j]), o.vinv[j - 1]->d(), chi[j], (long long)d * chi[j + 1]));
+      env_right(h, cur, h->tmpA->c(), h->mpo[j], chi[j], chi[j + 1], nxt);
+      std::swap(cur, nxt);
+      store(false, j - 1, cur, (long long)chi[j] * h->mpo[j].Dl * chi[j]);
+    }
+    CK(cudaStreamSynchronize(h->st));
+    return;
+  }
   // scratch: running env (envA/envB ping-pong), site tensor upload (T2 reused), scaled tensor (tmpA)
   DevBuf psi_tmp, lam_tmp, vinv_tmp;
   psi_tmp.alloc((size_t)h->n1max * sizeof(cplx));
