@@ -114,3 +114,54 @@ def test_step1_rejects_u1(B):
     with pytest.raises(B.TdvpError):
         t.step1(0.05)
     t.close()
+
+
+@pytest.mark.parametrize("L,chi", [(2, 2), (3, 2), (5, 1), (9, 4)])
+def test_step1_edge_shapes(B, L, chi):
+    """Shortest chains (one bond; the turnaround site is also the first),
+    chi = 1 (a product state stays a product state: the mean-field limit of
+    1TDVP), and an odd length."""
+    W = ti.mpo_xxz_nn(L, 0.7)
+    mps = ti.bloch_mps(L, seed=1) if chi == 1 else ti.random_canonical_mps(L, chi, seed=8)
+    t, st = _pair(B, mps, W, chi, 1e-14)
+    for _ in range(3):
+        t.step1(0.05)
+        T1.step1(st, 0.05)
+    _compare(t, st, 1e-10)
+    if chi == 1:
+        assert t.chi() == [1] * (L + 1)
+    t.close()
+
+
+def test_step1_zero_dt_is_identity(B):
+    L = 8
+    W = ti.mpo_xxz_nn(L, 1.0)
+    mps = ti.random_canonical_mps(L, 8, seed=9)
+    t, st = _pair(B, mps, W, 8, 1e-14)
+    sz0 = O.measure(st)["sz"]
+    t.step1(0.0)
+    assert np.abs(t.measure_sz() - sz0).max() < 1e-12
+    t.close()
+
+
+def test_step1_bench_workload_invariants(B):
+    """bench.py's secondary_1tdvp launch configuration at its full size
+    (c5sat: L = 24, chi = 1024 on bonds 10..14, 2048 x 1024 splits through
+    the block-Jacobi SVD): properties that hold at any size -- the energy and
+    the norm are conserved and no bond grows (a value below eps * sigma_1 may
+    be cut by the split's O-7 rule, as in the oracle; the oracle cannot run
+    this size in a test)."""
+    L, chi = 24, 1024
+    mps = ti.random_canonical_mps(L, chi, seed=2)
+    W = ti.mpo_xxz_nn(L, 1.0)
+    t = B.Tdvp(L, 2, 5, chi)
+    t.set_params(eps=1e-12)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    E0, n0, chi0 = t.measure_energy(), t.measure_norm(), t.chi()
+    t.step1(0.05)
+    assert abs(t.measure_energy() - E0) < 1e-9 * max(1.0, abs(E0))
+    assert abs(t.measure_norm() - n0) < 1e-10
+    assert all(c <= c0 for c, c0 in zip(t.chi(), chi0))
+    assert sum(chi0) - sum(t.chi()) <= 4
+    t.close()
