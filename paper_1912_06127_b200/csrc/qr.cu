@@ -383,14 +383,14 @@ cudaError_t qr_factor(cudaStream_t st, const QrWork& w, cplx* A, long long lda, 
     const int rows = m - k0;
     cplx* T = w.T + (long long)p * KBm * KBm;
     cudaError_t e;
-    if (rows <= 256) {
+    if (rows <= 64) {
       const size_t smem = (size_t)rows * kb * sizeof(cplx);
       if ((e = set_smem_attr(reinterpret_cast<const void*>(qr_panel_kernel<32, 256>), 128 * 1024)) != cudaSuccess)
         return e;
       qr_panel_kernel<32, 256><<<1, 256, smem, st>>>(A, lda, m, k0, kb, w.tau, w.Vc, w.ldv, T);
     } else {
       // cluster panel: C CTAs of rc rows each (rc * kb * 16 B of shared memory)
-      const int C = rows <= 1024 ? 8 : 16;
+      const int C = rows <= 512 ? 4 : rows <= 1024 ? 8 : 16;
       const int rc = (rows + C - 1) / C;
       const size_t smem = (size_t)rc * kb * sizeof(cplx);
       if ((e = set_smem_attr(reinterpret_cast<const void*>(qr_panel_cl_kernel), (int)std::max<size_t>(smem, 48 * 1024))) !=
