@@ -39,6 +39,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -151,11 +153,16 @@ struct Smem {
   int rp[PC / 2], rq[PC / 2];
   int col[PC];       // global column of pair column i (-1: absent)
   int colp[PC];      // the previous round's columns (pending V update)
+  cplx part[2][PC * PC];  // CL: this CTA's partial Gram (by round parity), read by the pair's cluster
   unsigned char ut_a[136], ut_b[136];  // upper-triangle 2 x 2 block u -> (row pair, column pair)
   double offw[8];
   int any;
 };
 
+// CL: the S CTAs of a pair form one thread-block cluster and exchange their
+// partial Grams through distributed shared memory (one cluster barrier per
+// round); else through global memory and a per-pair counter
+template <bool CL>
 __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
@@ -520,39 +527,57 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
       __syncthreads();
       if (wid == 0) {
         tile_add(sm.red[0]);
-        // this CTA's partial -> global slot (upper tiles only)
-        cplx* dst = a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + s) * (PC * PC);
+        // this CTA's partial -> its slot (upper tiles only)
+        cplx* dst = CL ? sm.part[round_g & 1]
+                       : a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + s) * (PC * PC);
 #pragma unroll
         for (int t = 0; t < NUT; ++t) {
           int ti, tj;
           ut_tile(t, ti, tj);
           const int r = ti * 8 + (lane >> 2);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) __stcg(dst + r * PC + tj * 8 + 2 * (lane & 3) + h, cmk(gR[t][h], gI[t][h]));
+          for (int h = 0; h < 2; ++h) {
+            cplx* q = dst + r * PC + tj * 8 + 2 * (lane & 3) + h;
+            if (CL) *q = cmk(gR[t][h], gI[t][h]);
+            else __stcg(q, cmk(gR[t][h], gI[t][h]));
+          }
         }
       }
       // pair barrier: all S partials of this pair written
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(a.pcnt + pair, 1u);
-        const unsigned target = (unsigned)((round_g + 1) * (unsigned long long)a.S);
-        while (true) {
-          unsigned v;
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.pcnt + pair) : "memory");
-          if ((int)(v - target) >= 0) break;
-          __nanosleep(20);
+      if (CL) {
+        // the partial slots are double-buffered by round parity: a CTA writes
+        // round r + 2's only after this barrier of round r + 1, which the
+        // others pass only after their reads of round r
+        cooperative_groups::this_cluster().sync();
+      } else {
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(a.pcnt + pair, 1u);
+          const unsigned target = (unsigned)((round_g + 1) * (unsigned long long)a.S);
+          while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.pcnt + pair) : "memory");
+            if ((int)(v - target) >= 0) break;
+            __nanosleep(20);
+          }
+          __threadfence();
         }
-        __threadfence();
+        __syncthreads();
       }
-      __syncthreads();
       // ---- sum the S partials in index order -> G (Hermitian, both triangles)
       for (int e = tid; e < PC * PC; e += NTB) {
         const int i = e / PC, j = e - i * PC;
         if (i <= j) {
           cplx v = cmk(0.0, 0.0);
-          for (int q = 0; q < a.S; ++q)
-            v = cadd(v, __ldcg(a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + q) * (PC * PC) + e));
+          for (int q = 0; q < a.S; ++q) {
+            if (CL) {
+              cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+              v = cadd(v, *cl.map_shared_rank(&sm.part[round_g & 1][e], q));
+            } else {
+              v = cadd(v, __ldcg(a.part + (((long long)(round_g & 1) * a.P + pair) * a.S + q) * (PC * PC) + e));
+            }
+          }
           if (i == j) v.y = 0.0;
           sm.G[i][j] = v;
           sm.G[j][i] = cconj(v);
@@ -738,6 +763,7 @@ __global__ void __launch_bounds__(NTB, 1) bjac_kernel(BjArgs a) {
   if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = min(sweep + 1, a.max_sweeps);
   if (s == 0 && tid == 0 && flops > 0.0) atomicAdd(a.flop_out, flops);
   if (s == 0 && tid == NIW * 32 && vflops > 0.0) atomicAdd(a.flop_out, vflops);
+  if (CL) cooperative_groups::this_cluster().sync();  // partners may still read this CTA's partials
 }
 
 }  // namespace
@@ -752,12 +778,15 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   const int nb = (nc + BB - 1) / BB;
   const int nbe = nb + (nb & 1);
   const int P = nbe / 2;
-  const void* fn = reinterpret_cast<const void*>(bjac_kernel);
+  const void* fn = reinterpret_cast<const void*>(bjac_kernel<false>);
+  const void* fnc = reinterpret_cast<const void*>(bjac_kernel<true>);
   const size_t smem = sizeof(Smem);
   cudaError_t e;
   if ((e = set_smem_attr(fn, (int)smem)) != cudaSuccess) return e;
+  if ((e = set_smem_attr(fnc, (int)smem)) != cudaSuccess) return e;
+  if ((e = set_cluster_nonportable(fnc)) != cudaSuccess) return e;
   int occ = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bjac_kernel, NTB, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bjac_kernel<false>, NTB, smem)) != cudaSuccess) return e;
   if (occ < 1) return cudaErrorNotSupported;
   // S CTAs per pair (row slices) so that the grid fills the SMs once
   const int S = std::max(1, std::min(16, occ * g_num_sms / P));
@@ -801,7 +830,40 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
     cudaMemcpyToSymbolAsync(g_bj_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
   void* args[] = {(void*)&a};
-  e = cudaLaunchCooperativeKernel(fn, dim3(P * S), dim3(NTB), args, smem, st);
+  // cluster variant when the P clusters of S CTAs can all be resident at once
+  // (a cooperative launch needs every CTA co-resident for the sweep barrier)
+  bool cl = false;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    cfg.gridDim = dim3(P * S);
+    cfg.blockDim = dim3(NTB);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    static int use_cl = -1;
+    if (use_cl < 0) {
+      const char* ev = std::getenv("TDVP_BJ_CLUSTER");
+      use_cl = ev ? std::atoi(ev) : 1;
+    }
+    if (use_cl && S > 1 && cudaOccupancyMaxActiveClusters(&ncl, fnc, &cfg) == cudaSuccess && ncl >= P) {
+      cfg.numAttrs = 2;
+      e = cudaLaunchKernelEx(&cfg, bjac_kernel<true>, a);
+      cl = e == cudaSuccess;
+      if (!cl) cudaGetLastError();  // not launchable as a cooperative cluster grid: the global-memory exchange
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (!cl) e = cudaLaunchCooperativeKernel(fn, dim3(P * S), dim3(NTB), args, smem, st);
   if (e == cudaSuccess && prof) {
     unsigned long long z[8];
     cudaMemcpyFromSymbolAsync(z, g_bj_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);

@@ -349,3 +349,16 @@ def test_svd_register_jacobi_forced_large(B):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "svd and not forced",
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_svd_block_jacobi_forced_global_exchange(B):
+    """The block Jacobi with its pair exchange through global memory (the
+    fallback when the pair clusters cannot all be co-resident;
+    TDVP_BJ_CLUSTER=0) forced down to 32 columns: every SVD parity test."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TDVP_SVD_BJ_MIN="32", TDVP_BJ_CLUSTER="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "svd and not forced",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
