@@ -8,7 +8,8 @@ enable a parallel version of the hybrid method ..., whereby a simulation
 starts with 2TDVP and switches to 1TDVP when chi_max is saturated.  1TDVP is
 faster".  The paper gives no p1TDVP algorithm; what is built here is the
 serial one-site integrator the hybrid switches to, in the paper's own
-building blocks and storage (reading R-1TDVP in DESIGN.md):
+building blocks and storage (reading R-1TDVP in DESIGN.md), and its
+segment-parallel form (step1p, reading R-P1TDVP, below):
 
 * the state is kept in the inverse-canonical product form
   Psi_0 V_0 Psi_1 ... Psi_{L-1}, every bond split by the
@@ -113,6 +114,144 @@ def step1(st: State, dt: float):
         seg.gamma[j - 1] = env_right(seg.gamma[j], Wh, W[j])
         C = bwd_bond(seg.beta[j], seg.gamma[j - 1], US)
         seg.psi[j - 1] = np.tensordot(A, C, axes=(2, 0))
+    st.stats.w_total += st.stats.w_step
+
+
+# ----------------------------------------------------------------------------
+# segment-parallel one-site TDVP (p1TDVP, reading R-P1TDVP in DESIGN.md)
+# ----------------------------------------------------------------------------
+#
+# PAPER.md:697 expects "a parallel variant of one-site TDVP (p1TDVP) could be
+# developed using the same approach" as p2TDVP.  Reading: the App. A half-step
+# programs unchanged at the segment boundaries -- D and C phases keep the
+# paper's two-site Lambda^-1-merged boundary pair updates, the
+# D-phase backward one-site step and the half-1/half-2 merge of full-dt
+# boundary pairs -- and every segment's interior sweep one-site:
+#   RIGHT over [s, e]: [back(s) if q > 0]; site_right(j) for j = s .. e-1
+#     (forward Psi_j by dt/2 unless merged, split bond j, beta_{j+1}, backward
+#     bond j by dt/2, absorb into Psi_{j+1}); at the chain end e = L-1 the last
+#     site forward by dt in half 1 (merged: skipped in half 2), dt/2 in half 2
+#   LEFT over [s, e]: [back(e) if q < p-1]; site_left(j) for j = e .. s+1
+#     (mirror: split bond j-1, gamma_{j-1}, absorb into Psi_{j-1}); at the
+#     chain start s = 0 site 0 forward by dt in half 1, dt/2 in half 2.
+# Per step every site is evolved forward by dt and every interior bond
+# backward by dt, as in serial 1TDVP; every boundary as in p2TDVP.  p = 1 is
+# exactly step1.
+
+
+def _fwd(st, seg, j, t):
+    p = st.params
+    info = {}
+    seg.psi[j] = expm_lanczos(lambda x: apply_h1(seg.beta[j], st.W[j], seg.gamma[j], x), seg.psi[j], -1j * t,
+                              p.krylov_k, p.krylov_tol, info)
+    st.stats.krylov_breakdowns += int(info.get("breakdown", False))
+
+
+def _bond_back(st, Lenv, Renv, C, tau):
+    p = st.params
+    info = {}
+    out = expm_lanczos(lambda x: apply_h0(Lenv, Renv, x), C, 1j * tau, p.krylov_k, p.krylov_tol, info)
+    st.stats.krylov_breakdowns += int(info.get("breakdown", False))
+    return out
+
+
+def _site_right(st, seg, j, t_fwd, tau):
+    """Forward site j by t_fwd (None: already evolved), split bond j, beta_{j+1},
+    bond j backward by tau, absorb into site j+1."""
+    if t_fwd is not None:
+        _fwd(st, seg, j, t_fwd)
+    cl, d, cr = seg.psi[j].shape
+    B = (1.0 / seg.lam[j])[:, None, None] * seg.psi[j + 1]
+    US, S, SWh, w = _split(seg.psi[j].reshape(cl * d, cr), st.params)
+    st.stats.w_step += w
+    seg.psi[j] = US.reshape(cl, d, len(S))
+    seg.lam[j] = S
+    seg.beta[j + 1] = env_left(seg.beta[j], seg.psi[j] * (1.0 / S)[None, None, :], st.W[j])
+    C = _bond_back(st, seg.beta[j + 1], seg.gamma[j], SWh, tau)
+    seg.psi[j + 1] = np.tensordot(C, B, axes=(1, 0))
+
+
+def _site_left(st, seg, j, t_fwd, tau):
+    """Forward site j by t_fwd (None: already evolved), split bond j-1,
+    gamma_{j-1}, bond j-1 backward by tau, absorb into site j-1."""
+    if t_fwd is not None:
+        _fwd(st, seg, j, t_fwd)
+    cl, d, cr = seg.psi[j].shape
+    A = seg.psi[j - 1] * (1.0 / seg.lam[j - 1])[None, None, :]
+    US, S, SWh, w = _split(seg.psi[j].reshape(cl, d * cr), st.params)
+    st.stats.w_step += w
+    seg.psi[j] = SWh.reshape(len(S), d, cr)
+    seg.lam[j - 1] = S
+    seg.gamma[j - 1] = env_right(seg.gamma[j], (1.0 / S)[:, None, None] * seg.psi[j], st.W[j])
+    C = _bond_back(st, seg.beta[j], seg.gamma[j - 1], US, tau)
+    seg.psi[j - 1] = np.tensordot(A, C, axes=(2, 0))
+
+
+def _half1(st: State, dt: float, h: int, merged_pairs: set, merged_sites: set):
+    """Half h of a p1TDVP step, phase by phase (the structure of tdvp._half)."""
+    from .tdvp import LEFT, RIGHT, _back, _pair, directions
+    L, p = st.L, st.p
+    dirs = directions(p, h)
+    th, tf = 0.5 * dt, dt
+    tau_h, tau_f = -0.5j * dt, -1.0j * dt
+    new_pairs, new_sites = set(), set()
+    # ---- D-phase: unchanged two-site boundary updates (PAPER.md:484)
+    for q in range(p - 1):
+        if dirs[q] == LEFT and dirs[q + 1] == RIGHT:
+            a, b = st.segs[q], st.segs[q + 1]
+            e = a.e
+            if e not in merged_pairs:
+                _pair(st, a, e, tau_h, True, True)
+                b.psi[e + 1] = a.psi[e + 1].copy()
+                b.lam[e] = a.lam[e].copy()
+                b.beta[e + 1] = a.beta[e + 1].copy()
+    # ---- sweep phase: one-site interiors
+    for seg in st.segs:
+        q, s, e = seg.q, seg.s, seg.e
+        if dirs[q] == RIGHT:
+            if q > 0:
+                _back(st, seg, s, dt)
+            for j in range(s, e):
+                _site_right(st, seg, j, None if j in merged_sites else th, th)
+            if e == L - 1 and (L - 1) not in merged_sites:
+                _fwd(st, seg, L - 1, tf if h == 1 else th)
+                if h == 1:
+                    new_sites.add(L - 1)
+        else:
+            if q < p - 1:
+                _back(st, seg, e, dt)
+            for j in range(e, s, -1):
+                _site_left(st, seg, j, None if j in merged_sites else th, th)
+            if s == 0 and 0 not in merged_sites:
+                _fwd(st, seg, 0, tf if h == 1 else th)
+                if h == 1:
+                    new_sites.add(0)
+    # ---- C-phase: unchanged two-site boundary updates
+    for q in range(p - 1):
+        if dirs[q] == RIGHT and dirs[q + 1] == LEFT:
+            a, b = st.segs[q], st.segs[q + 1]
+            e, s = a.e, b.s
+            a.psi[s] = b.psi[s].copy()
+            a.gamma[s] = b.gamma[s].copy()
+            tau = tau_f if h == 1 else tau_h
+            _pair(st, a, e, tau, True, True)
+            if tau == tau_f:
+                new_pairs.add(e)
+            b.psi[s] = a.psi[s].copy()
+            b.lam[e] = a.lam[e].copy()
+            b.beta[s] = a.beta[s].copy()
+    return new_pairs, new_sites
+
+
+def step1p(st: State, dt: float):
+    """One p1TDVP step (half 1 + half 2) on a State of any p (reading above);
+    p = 1 is step1."""
+    if st.params.u1:
+        raise ValueError("p1TDVP runs in dense mode")
+    st.stats.w_step = 0.0
+    st.stats.trunc_active = False
+    mp, ms = _half1(st, dt, 1, set(), set())
+    _half1(st, dt, 2, mp, ms)
     st.stats.w_total += st.stats.w_step
 
 
