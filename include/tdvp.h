@@ -150,23 +150,27 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
  * n_segments rebuilds the environments (sequential section). */
 int tdvp_step(tdvp_t h, double dt, int n_segments);
 
-/* One serial one-site TDVP (1TDVP) step dt: the integrator of the hybrid
- * scheme PAPER.md:697 describes ("starts with 2TDVP and switches to 1TDVP
- * when chi_max is saturated"; the paper gives no parallel p1TDVP algorithm,
- * reading R-1TDVP in DESIGN.md).  Left-to-right then right-to-left sweep with
- * tau = dt/2: forward one-site steps exp(-i tau H_eff^(1)) (the last site
- * once by dt, the turnaround merge of PAPER.md:430), each bond split by the
- * truncated SVD of tdvp_step (O-7; bond dimensions never grow)
- * and evolved backwards by exp(+i tau H_eff^(0)), H_eff^(0) C[a,b] =
- * sum L[a,w,a'] R[b,w,b'] C[a',b'].  The state stays in the inverse-canonical
- * product form of tdvp_set_mps.  Single-process handles, dense mode (u1 = 0):
- * TDVP_ESTATE / TDVP_EARG otherwise; a handle laid out for n_segments > 1 is
- * re-laid out serially (environment rebuild).  Stats as for tdvp_step (n_pair
- * = n_back = 0). */
-int tdvp_step1(tdvp_t h, double dt);
+/* One one-site TDVP step dt with n_segments partitions: the integrator of
+ * the hybrid scheme PAPER.md:697 describes ("starts with 2TDVP and switches
+ * to 1TDVP when chi_max is saturated"), and its segment-parallel form p1TDVP
+ * ("could be developed using the same approach"; the paper gives no
+ * algorithm: readings R-1TDVP / R-P1TDVP in DESIGN.md).  n_segments = 1:
+ * serial 1TDVP -- left-to-right then right-to-left sweep with tau = dt/2:
+ * forward one-site steps exp(-i tau H_eff^(1)) (the last site once by dt, the
+ * turnaround merge of PAPER.md:430), each bond split by the truncated SVD of
+ * tdvp_step (O-7; interior bond dimensions never grow) and
+ * evolved backwards by exp(+i tau H_eff^(0)), H_eff^(0) C[a,b] =
+ * sum L[a,w,a'] R[b,w,b'] C[a',b'].  n_segments = p > 1: the p2TDVP
+ * half-step programs of tdvp_step with their boundary phases unchanged (the
+ * two-site Lambda^-1-merged boundary pair updates, which may
+ * grow the boundary bonds up to chi_max) and one-site segment interiors.
+ * The state stays in the inverse-canonical product form of tdvp_set_mps.
+ * Partition, executors and devices as for tdvp_step; dense mode only
+ * (TDVP_EARG with u1 = 1).  Stats as for tdvp_step. */
+int tdvp_step1(tdvp_t h, double dt, int n_segments);
 
-/* One step of the hybrid scheme: tdvp_step1 when
- * n_segments = 1, the handle is single-process dense, and every bond j is
+/* One step of the hybrid scheme: tdvp_step1(h, dt,
+ * n_segments) when the handle is single-process dense and every bond j is
  * saturated (chi_j = min(chi_max, d^(j+1), d^(L-j-1))); tdvp_step(h, dt,
  * n_segments) otherwise.  *used (may be NULL) = 1 or 2, the integrator run. */
 int tdvp_step_hybrid(tdvp_t h, double dt, int n_segments, int* used);

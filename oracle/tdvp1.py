@@ -268,11 +268,12 @@ def saturated(chi, L: int, d: int, chi_max: int) -> bool:
 
 
 def step_hybrid(st: State, dt: float, d: int = 2) -> int:
-    """One step of the hybrid scheme: 2TDVP until chi_max is saturated on every
-    bond, then 1TDVP.  Returns 1 or 2 (the integrator used)."""
+    """One step of the hybrid scheme: (p)2TDVP until chi_max is saturated on
+    every bond, then (p)1TDVP on the same partition (R-P1TDVP).  Returns 1 or
+    2 (the integrator used)."""
     from .tdvp import chi_profile, step
-    if st.p == 1 and saturated(chi_profile(st), st.L, d, st.params.chi_max):
-        step1(st, dt)
+    if saturated(chi_profile(st), st.L, d, st.params.chi_max):
+        step1p(st, dt)
         return 1
     step(st, dt)
     return 2

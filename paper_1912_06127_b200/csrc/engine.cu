@@ -223,6 +223,11 @@ struct tdvp_ctx {
   bool have_mpo = false, have_mps = false, envs_valid = false;
   bool evolved = false;  // stepped since the last tdvp_set_mps (the host copy h_psi is stale in rank mode)
   int layout_p = 0;  // segments currently laid out (0: the host copy h_psi/h_lam is authoritative)
+  // the step in progress runs the p1TDVP programs (tdvp_step1; reading
+  // R-P1TDVP) instead of the p2TDVP ones; msites: chain-end sites evolved by dt
+  // at the end of its half 1
+  bool one_site = false;
+  std::set<int> msites;
   int alloc_p = 0;   // segments whose device buffers are allocated (kept across tdvp_set_mps)
   std::vector<std::pair<int, int>> bounds;
   std::vector<std::pair<int, int>> custom;  // tdvp_set_partition: explicit bounds for n_segments = custom.size()
@@ -1234,104 +1239,77 @@ int split_bond(tdvp_ctx* h, Segment& g, int b, const cplx* M, int m, int n, cplx
   return chi;
 }
 
-void step1_serial(tdvp_ctx* h, double dt) {
-  Segment& g = h->segs[0];
-  const int L = h->L, d = h->d, K = h->prm.krylov_k;
+// one-site interior operations of the p1TDVP programs (schedule.h
+// OP_SITE_R / OP_SITE_L / OP_FWD; oracle/tdvp1.py _site_right/_site_left)
+// bond matrix C in theta (<= max chi_b^2 <= the two-site buffer), its evolved
+// copy C2 in tmpB (free between the environment update and the next site step)
+void site_right(tdvp_ctx* h, Segment& g, int j, bool done, double dt) {
+  const int d = h->d, K = h->prm.krylov_k;
   const double tau = 0.5 * dt;
-  // bond matrix C (<= max chi_b^2 <= the two-site buffer) and its evolved copy
-  // C2 in tmpB (free between the environment update and the next site step)
+  if (!done) site_forward(h, g, j, tau);
   cplx* C = h->theta->c();
   cplx* C2 = h->tmpB->c();
-  // left to right (the last site by the merged dt)
-  for (int j = 0; j < L; ++j) {
-    site_forward(h, g, j, j == L - 1 ? dt : tau);
-    if (j == L - 1) break;
-    const int cl = g.cb[j], cr = g.cb[j + 1], cr2 = g.cb[j + 2];
-    const MpoSite& W = h->mpo[j];
-    // B = diag(V_j) Psi_{j+1} (right-canonical), before V_j is replaced
-    CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), cr, (long long)d * cr2));
-    CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
-    g_launch_count += 2;
-    const int chi = split_bond(h, g, j, h->tmpB->c(), cl * d, cr, P(g.psi[j]), C);
-    g.cb[j + 1] = chi;
-    // beta_{j+1} from U = Psi_j diag(V_j)
-    CK(scale_cols(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
-    g_launch_count++;
-    env_left(h, P(g.beta[j]), h->tmpB->c(), W, cl, chi, P(g.beta[j + 1]));
-    // C <- exp(+i tau H_eff^(0)(beta_{j+1}, gamma_j)) C
-    const cplx* Le = P(g.beta[j + 1]);
-    const cplx* Re = P(g.gamma[j]);
-    expm_lanczos(
-        h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dr, chi, cr, x, y); }, C, C2, (long long)chi * cr, 0.0,
-        tau, K, 0, flops_heff0(chi, cr, W.Dr));
-    // Psi_{j+1} = C B
-    gemm(h, OP_N, OP_N, chi, d * cr2, cr, C2, cr, h->tmpA->c(), (long long)d * cr2, P(g.psi[j + 1]),
-         (long long)d * cr2);
-  }
-  // right to left (the last site was evolved by dt above)
-  for (int j = L - 1; j >= 0; --j) {
-    if (j < L - 1) site_forward(h, g, j, tau);
-    if (j == 0) break;
-    const int cl2 = g.cb[j - 1], cl = g.cb[j], cr = g.cb[j + 1];
-    const MpoSite& W = h->mpo[j];
-    // A = Psi_{j-1} diag(V_{j-1}) (left-canonical), before V_{j-1} is replaced
-    CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j - 1]), g.vinv[j - 1]->d(), (long long)cl2 * d, cl));
-    CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
-    g_launch_count += 2;
-    const int chi = split_bond(h, g, j - 1, h->tmpB->c(), cl, d * cr, C, P(g.psi[j]));
-    g.cb[j] = chi;
-    // gamma_{j-1} from W^dag = diag(V_{j-1}) Psi_j
-    CK(scale_rows(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j - 1]->d(), chi, (long long)d * cr));
-    g_launch_count++;
-    env_right(h, P(g.gamma[j]), h->tmpB->c(), W, chi, cr, P(g.gamma[j - 1]));
-    // C <- exp(+i tau H_eff^(0)(beta_j, gamma_{j-1})) C
-    const cplx* Le = P(g.beta[j]);
-    const cplx* Re = P(g.gamma[j - 1]);
-    expm_lanczos(
-        h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dl, cl, chi, x, y); }, C, C2, (long long)cl * chi, 0.0,
-        tau, K, 0, flops_heff0(cl, chi, W.Dl));
-    // Psi_{j-1} = A C
-    gemm(h, OP_N, OP_N, cl2 * d, chi, cl, h->tmpA->c(), cl, C2, chi, P(g.psi[j - 1]), chi);
-  }
+  const int cl = g.cb[j], cr = g.cb[j + 1], cr2 = g.cb[j + 2];
+  const MpoSite& W = h->mpo[j];
+  // B = diag(V_j) Psi_{j+1} (right-canonical), before V_j is replaced
+  CK(scale_rows(h->st, h->tmpA->c(), P(g.psi[j + 1]), g.vinv[j]->d(), cr, (long long)d * cr2));
+  CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
+  g_launch_count += 2;
+  const int chi = split_bond(h, g, j, h->tmpB->c(), cl * d, cr, P(g.psi[j]), C);
+  g.cb[j + 1] = chi;
+  // beta_{j+1} from U = Psi_j diag(V_j)
+  CK(scale_cols(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j]->d(), (long long)cl * d, chi));
+  g_launch_count++;
+  env_left(h, P(g.beta[j]), h->tmpB->c(), W, cl, chi, P(g.beta[j + 1]));
+  // C <- exp(+i tau H_eff^(0)(beta_{j+1}, gamma_j)) C
+  const cplx* Le = P(g.beta[j + 1]);
+  const cplx* Re = P(g.gamma[j]);
+  expm_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dr, chi, cr, x, y); }, C, C2, (long long)chi * cr, 0.0,
+      tau, K, 0, flops_heff0(chi, cr, W.Dr));
+  // Psi_{j+1} = C B
+  gemm(h, OP_N, OP_N, chi, d * cr2, cr, C2, cr, h->tmpA->c(), (long long)d * cr2, P(g.psi[j + 1]),
+       (long long)d * cr2);
+}
+
+void site_left(tdvp_ctx* h, Segment& g, int j, bool done, double dt) {
+  const int d = h->d, K = h->prm.krylov_k;
+  const double tau = 0.5 * dt;
+  if (!done) site_forward(h, g, j, tau);
+  cplx* C = h->theta->c();
+  cplx* C2 = h->tmpB->c();
+  const int cl2 = g.cb[j - 1], cl = g.cb[j], cr = g.cb[j + 1];
+  const MpoSite& W = h->mpo[j];
+  // A = Psi_{j-1} diag(V_{j-1}) (left-canonical), before V_{j-1} is replaced
+  CK(scale_cols(h->st, h->tmpA->c(), P(g.psi[j - 1]), g.vinv[j - 1]->d(), (long long)cl2 * d, cl));
+  CK(copy_cplx(h->st, h->tmpB->c(), P(g.psi[j]), (long long)cl * d * cr));
+  g_launch_count += 2;
+  const int chi = split_bond(h, g, j - 1, h->tmpB->c(), cl, d * cr, C, P(g.psi[j]));
+  g.cb[j] = chi;
+  // gamma_{j-1} from W^dag = diag(V_{j-1}) Psi_j
+  CK(scale_rows(h->st, h->tmpB->c(), P(g.psi[j]), g.vinv[j - 1]->d(), chi, (long long)d * cr));
+  g_launch_count++;
+  env_right(h, P(g.gamma[j]), h->tmpB->c(), W, chi, cr, P(g.gamma[j - 1]));
+  // C <- exp(+i tau H_eff^(0)(beta_j, gamma_{j-1})) C
+  const cplx* Le = P(g.beta[j]);
+  const cplx* Re = P(g.gamma[j - 1]);
+  expm_lanczos(
+      h, [&](const cplx* x, cplx* y) { heff0(h, Le, Re, W.Dl, cl, chi, x, y); }, C, C2, (long long)cl * chi, 0.0,
+      tau, K, 0, flops_heff0(cl, chi, W.Dl));
+  // Psi_{j-1} = A C
+  gemm(h, OP_N, OP_N, cl2 * d, chi, cl, h->tmpA->c(), cl, C2, chi, P(g.psi[j - 1]), chi);
 }
 
 // hybrid switch rule: every bond at min(chi_max, d^(j+1), d^(L-j-1))
+int owner_of(tdvp_ctx* h, int j);
 bool chi_saturated(tdvp_ctx* h) {
-  const Segment& g = h->segs[0];
   for (int j = 0; j + 1 < h->L; ++j) {
     long long cap = 1;
     const int k = std::min(j + 1, h->L - j - 1);
     for (int i = 0; i < k && cap < h->chi_max; ++i) cap *= h->d;
-    if (g.cb[j + 1] < std::min<long long>(cap, h->chi_max)) return false;
+    if (h->segs[owner_of(h, j)].cb[j + 1] < std::min<long long>(cap, h->chi_max)) return false;
   }
   return true;
-}
-
-void layout(tdvp_ctx* h, int p);
-bool local_mode(tdvp_ctx* h);
-void reset_step_stats(tdvp_ctx* h);
-void finish_timing(tdvp_ctx* h);
-
-void do_step1(tdvp_ctx* h, double dt) {
-  if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step1");
-  if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
-  if (!local_mode(h)) throw TdvpError(TDVP_ESTATE, "tdvp_step1 runs on a single-process handle");
-  if (h->prm.u1) throw TdvpError(TDVP_EARG, "tdvp_step1 runs in dense mode (u1 = 0)");
-  if (h->layout_p != 1 || !h->envs_valid) layout(h, 1);
-  reset_step_stats(h);
-  h->evolved = true;
-  const long long l0 = g_launch_count, g0 = g_gemm_count;
-  CK(cudaEventRecord(h->ev_step0, h->st));
-  step1_serial(h, dt);
-  CK(cudaEventRecord(h->ev_step1, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, h->ev_step0, h->ev_step1));
-  h->stats.step_ms = ms;
-  h->stats.w_total += h->stats.w_step;
-  h->stats.kernel_launches = g_launch_count - l0;
-  h->stats.gemm_launches = g_gemm_count - g0;
-  if (h->prm.timing) finish_timing(h);
 }
 
 // ------------------------------------------------------------ layout / init
@@ -1670,6 +1648,17 @@ void recv_right_nccl(tdvp_ctx* h, Segment& a) {
 void exec_compute(tdvp_ctx* h, Segment& g, const SchedOp& op, double dt) {
   if (op.kind == OP_PAIR) pair_update(h, g, op.j, dt, op.full, op.build);
   else if (op.kind == OP_BACK) back_update(h, g, op.j, dt);
+  else if (op.kind == OP_SITE_R) site_right(h, g, op.j, op.full != 0, dt);
+  else if (op.kind == OP_SITE_L) site_left(h, g, op.j, op.full != 0, dt);
+  else if (op.kind == OP_FWD) site_forward(h, g, op.j, op.full ? dt : 0.5 * dt);
+}
+
+// the program of segment q in half hh of the step in progress (p2TDVP, or
+// p1TDVP when h->one_site)
+std::vector<SchedOp> program_of(tdvp_ctx* h, int hh, int q, const std::set<int>& merged) {
+  const int L = h->L, p = h->layout_p;
+  return h->one_site ? segment_program1(L, p, hh, q, h->bounds[q], merged, h->msites)
+                     : segment_program(L, p, hh, q, h->bounds[q], merged);
 }
 
 // one half-step
@@ -1677,7 +1666,7 @@ void run_half(tdvp_ctx* h, int hh, double dt, const std::set<int>& merged) {
   const int L = h->L, p = h->layout_p;
   if (!local_mode(h)) {
     Segment& g = h->segs[0];
-    for (const SchedOp& op : segment_program(L, p, hh, g.q, h->bounds[g.q], merged)) {
+    for (const SchedOp& op : program_of(h, hh, g.q, merged)) {
       switch (op.kind) {
         case OP_SEND_R: send_right_nccl(h, g); break;
         case OP_RECV_L: recv_left_nccl(h, g); break;
@@ -1693,7 +1682,7 @@ void run_half(tdvp_ctx* h, int hh, double dt, const std::set<int>& merged) {
   std::vector<std::vector<SchedOp>> prog(p);
   std::vector<size_t> pc(p, 0);
   std::vector<int> msg_from_left(p, 0), msg_from_right(p, 0);
-  for (int q = 0; q < p; ++q) prog[q] = segment_program(L, p, hh, q, h->bounds[q], merged);
+  for (int q = 0; q < p; ++q) prog[q] = program_of(h, hh, q, merged);
   size_t done = 0;
   while (done < (size_t)p) {
     bool progress = false;
@@ -1917,7 +1906,7 @@ void lane_program(tdvp_ctx* h, int q, double dt, const std::set<int>& merged, co
   Segment& g = h->segs[q];
   const int L = h->L, p = h->layout_p;
   for (int hh = 1; hh <= 2; ++hh)
-    for (const SchedOp& op : segment_program(L, p, hh, q, h->bounds[q], merged)) {
+    for (const SchedOp& op : program_of(h, hh, q, merged)) {
       if (abort.load()) throw TdvpError(TDVP_ECUDA, "segment lane aborted");
       switch (op.kind) {
         case OP_SEND_R: lane_send_right(ln, g, *h->msg_r[q], abort); break;
@@ -2040,9 +2029,10 @@ int balanced_partition(int L, int p, const int* chi, int* s, int* e, double* bes
 double partition_cost(int L, const int* chi, const std::vector<std::pair<int, int>>& bounds);
 void reorthonormalize(tdvp_ctx* h);
 
-void do_step(tdvp_ctx* h, double dt, int p) {
+void do_step(tdvp_ctx* h, double dt, int p, bool one_site = false) {
   if (!h->have_mpo || !h->have_mps) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step");
   if (!std::isfinite(dt)) throw TdvpError(TDVP_EARG, "dt must be finite");
+  if (one_site && h->prm.u1) throw TdvpError(TDVP_EARG, "tdvp_step1 runs in dense mode (u1 = 0)");
   if (h->prm.u1 && !local_mode(h)) throw TdvpError(TDVP_EARG, "u1 is not supported across ranks (use one process)");
   // dynamic load balancing ("dynamic load balancer"):
   // before the step, re-partition when the chi-weighted optimum beats the
@@ -2076,7 +2066,14 @@ void do_step(tdvp_ctx* h, double dt, int p) {
   h->evolved = true;
   const long long l0 = g_launch_count, g0 = g_gemm_count;
   CK(cudaEventRecord(h->ev_step0, h->st));
-  const std::set<int> merged = merged_pairs(h->L, p, h->bounds);
+  std::set<int> merged;
+  h->one_site = one_site;
+  if (one_site) merged1(h->L, p, h->bounds, merged, h->msites);
+  else merged = merged_pairs(h->L, p, h->bounds);
+  struct OneSiteReset {
+    tdvp_ctx* h;
+    ~OneSiteReset() { h->one_site = false; }
+  } reset_one_site{h};
   const bool lanes = local_mode(h) && p > 1 && (h->lanes_on || h->multi_dev);
   if (lanes) {
     if ((int)h->msg_r.size() != p) alloc_msgs(h);
@@ -2742,10 +2739,10 @@ int tdvp_step(tdvp_t h, double dt, int n_segments) {
   return TDVP_OK;
 }
 
-int tdvp_step1(tdvp_t h, double dt) {
+int tdvp_step1(tdvp_t h, double dt, int n_segments) {
   if (!h) return TDVP_EARG;
   try {
-    do_step1(h, dt);
+    do_step(h, dt, n_segments, true);
   } catch (const TdvpError& e) {
     return fail(h, e);
   }
@@ -2756,17 +2753,21 @@ int tdvp_step_hybrid(tdvp_t h, double dt, int n_segments, int* used) {
   if (!h) return TDVP_EARG;
   try {
     bool one = false;
-    if (n_segments == 1 && h->have_mps && local_mode(h) && !h->prm.u1) {
-      if (h->layout_p != 1 || !h->envs_valid) {
-        if (!h->have_mpo) throw TdvpError(TDVP_ESTATE, "MPO and MPS must be set before tdvp_step_hybrid");
-        layout(h, 1);
+    if (h->have_mps && h->have_mpo && local_mode(h) && !h->prm.u1) {
+      if (h->layout_p == 0) {
+        // nothing laid out yet: the host copy's bond dimensions
+        one = true;
+        for (int j = 0; j + 1 < h->L; ++j) {
+          long long cap = 1;
+          const int k = std::min(j + 1, h->L - j - 1);
+          for (int i = 0; i < k && cap < h->chi_max; ++i) cap *= h->d;
+          if (h->h_chi[j + 1] < std::min<long long>(cap, h->chi_max)) one = false;
+        }
+      } else {
+        one = chi_saturated(h);
       }
-      one = chi_saturated(h);
     }
-    if (one)
-      do_step1(h, dt);
-    else
-      do_step(h, dt, n_segments);
+    do_step(h, dt, n_segments, one);
     if (used) *used = one ? 1 : 2;
   } catch (const TdvpError& e) {
     return fail(h, e);

@@ -8,7 +8,15 @@
 #include <utility>
 #include <vector>
 
-enum OpKind { OP_PAIR = 1, OP_BACK = 2, OP_SEND_R = 3, OP_RECV_L = 4, OP_SEND_L = 5, OP_RECV_R = 6 };
+enum OpKind {
+  OP_PAIR = 1, OP_BACK = 2, OP_SEND_R = 3, OP_RECV_L = 4, OP_SEND_L = 5, OP_RECV_R = 6,
+  // one-site interior operations of the p1TDVP programs (reading R-P1TDVP):
+  // SITE_R j: forward site j by dt/2 (skipped if full = 1: evolved by dt at the
+  // end of half 1), split bond j, beta_{j+1}, bond j backward by dt/2, absorb
+  // into site j+1; SITE_L j: the mirror onto bond j-1 / site j-1; FWD j: site j
+  // forward by dt (full = 1) or dt/2
+  OP_SITE_R = 7, OP_SITE_L = 8, OP_FWD = 9
+};
 enum { BUILD_BETA = 1, BUILD_GAMMA = 2 };
 
 struct SchedOp {
@@ -96,4 +104,57 @@ inline std::set<int> merged_pairs(int L, int p, const std::vector<std::pair<int,
     for (const SchedOp& op : segment_program(L, p, 1, q, bounds[q], {}))
       if (op.kind == OP_PAIR && op.full) m.insert(op.j);
   return m;
+}
+
+// p1TDVP half-step programs (reading R-P1TDVP; oracle/tdvp1.py _half1): the
+// App. A programs with the boundary phases unchanged (two-site Lambda^-1-merged
+// boundary pairs, D-phase backward steps, merged full-dt boundary pairs) and
+// one-site segment interiors.  merged: boundary pairs evolved by dt in half 1;
+// msites: chain-end sites evolved by dt in half 1 (both skipped in half 2).
+inline std::vector<SchedOp> segment_program1(int L, int p, int h, int q, const std::pair<int, int>& se,
+                                             const std::set<int>& merged, const std::set<int>& msites) {
+  std::vector<SchedOp> ops;
+  const int s = se.first, e = se.second;
+  auto is_merged = [&](int j) { return h == 2 && merged.count(j) > 0; };
+  auto site_done = [&](int j) { return h == 2 && msites.count(j) > 0; };
+  if (sweeps_right(p, h, q)) {
+    if (q > 0) {
+      if (!is_merged(s - 1)) ops.push_back({OP_RECV_L, s - 1, 0, 0});
+      ops.push_back({OP_BACK, s, 0, 0});
+    }
+    for (int j = s; j < e; ++j) ops.push_back({OP_SITE_R, j, site_done(j) ? 1 : 0, BUILD_BETA});
+    if (e == L - 1 && !site_done(L - 1)) ops.push_back({OP_FWD, L - 1, h == 1 ? 1 : 0, 0});
+    if (q < p - 1) {
+      ops.push_back({OP_RECV_R, e, 0, 0});
+      ops.push_back({OP_PAIR, e, h == 1 ? 1 : 0, BUILD_BETA | BUILD_GAMMA});
+      ops.push_back({OP_SEND_R, e, 0, 0});
+    }
+  } else {
+    if (q < p - 1) {
+      if (!is_merged(e)) {
+        ops.push_back({OP_PAIR, e, 0, BUILD_BETA | BUILD_GAMMA});
+        ops.push_back({OP_SEND_R, e, 0, 0});
+      }
+      ops.push_back({OP_BACK, e, 0, 0});
+    }
+    for (int j = e; j > s; --j) ops.push_back({OP_SITE_L, j, site_done(j) ? 1 : 0, BUILD_GAMMA});
+    if (s == 0 && !site_done(0)) ops.push_back({OP_FWD, 0, h == 1 ? 1 : 0, 0});
+    if (q > 0) {
+      ops.push_back({OP_SEND_L, s, 0, 0});
+      ops.push_back({OP_RECV_L, s - 1, 0, 0});
+    }
+  }
+  return ops;
+}
+
+// the boundary pairs and chain-end sites a p1TDVP half 1 evolves by dt
+inline void merged1(int L, int p, const std::vector<std::pair<int, int>>& bounds, std::set<int>& pairs,
+                    std::set<int>& sites) {
+  pairs.clear();
+  sites.clear();
+  for (int q = 0; q < p; ++q)
+    for (const SchedOp& op : segment_program1(L, p, 1, q, bounds[q], {}, {})) {
+      if (op.kind == OP_PAIR && op.full) pairs.insert(op.j);
+      if (op.kind == OP_FWD && op.full) sites.insert(op.j);
+    }
 }

@@ -75,7 +75,7 @@ _SIGS = {
     "tdvp_set_mpo": (C.c_int, [C.c_void_p, _I, _PD]),
     "tdvp_set_mps": (C.c_int, [C.c_void_p, _I, _PD, _PD]),
     "tdvp_step": (C.c_int, [C.c_void_p, C.c_double, C.c_int]),
-    "tdvp_step1": (C.c_int, [C.c_void_p, C.c_double]),
+    "tdvp_step1": (C.c_int, [C.c_void_p, C.c_double, C.c_int]),
     "tdvp_step_hybrid": (C.c_int, [C.c_void_p, C.c_double, C.c_int, _I]),
     "tdvp_measure_sz": (C.c_int, [C.c_void_p, _D]),
     "tdvp_measure_energy": (C.c_int, [C.c_void_p, _D]),
@@ -184,9 +184,9 @@ class Tdvp:
     def step(self, dt, n_segments=1):
         _check(lib().tdvp_step(self.h, float(dt), int(n_segments)), self.h)
 
-    def step1(self, dt):
-        """One serial one-site TDVP step (tdvp_step1)."""
-        _check(lib().tdvp_step1(self.h, float(dt)), self.h)
+    def step1(self, dt, n_segments=1):
+        """One one-site TDVP step (tdvp_step1): serial 1TDVP, or p1TDVP with n_segments > 1."""
+        _check(lib().tdvp_step1(self.h, float(dt), int(n_segments)), self.h)
 
     def step_hybrid(self, dt, n_segments=1):
         """One hybrid 2TDVP -> 1TDVP step (tdvp_step_hybrid); returns 1 or 2."""

@@ -95,14 +95,61 @@ def test_hybrid_matches_oracle(B):
     t.close()
 
 
-def test_hybrid_segments_stay_two_site(B):
-    """n_segments > 1: the hybrid step is the p2TDVP step (1TDVP is serial)."""
+def _pair_p(B, mps, W, chi_max, eps, p, devices=None):
+    D_ = max(max(w.shape[0], w.shape[3]) for w in W)
+    t = B.Tdvp(len(W), 2, D_, chi_max, devices=devices)
+    t.set_params(eps=eps)
+    t.set_mpo(W)
+    t.set_mps(mps.psi, mps.lam)
+    st = O.init_state(mps, W, O.Params(chi_max=chi_max, eps=eps), p)
+    return t, st
+
+
+@pytest.mark.parametrize("p,chi_max", [(2, 16), (4, 16), (2, 64), (4, 64)])
+def test_p1tdvp_matches_oracle(B, p, chi_max):
+    """Segment-parallel one-site TDVP (tdvp_step1 with n_segments = p,
+    reading R-P1TDVP) vs oracle step1p: saturated interiors (chi 16), and
+    chi_max above the state's chi so the two-site boundary updates grow their
+    bonds (64); the serial p1 case is the tests above."""
+    L = 16
+    mps = ti.random_canonical_mps(L, 16, seed=12)
+    W = ti.mpo_xxz_nn(L, 0.8)
+    t, st = _pair_p(B, mps, W, chi_max, 1e-12, p)
+    for _ in range(3):
+        t.step1(0.05, p)
+        T1.step1p(st, 0.05)
+    _compare(t, st, 1e-9)
+    t.close()
+
+
+def test_p1tdvp_multi_device_lanes(B):
+    """The multi-device executor (segment lanes, repeated device ids on this
+    GPU) running the p1TDVP programs, p = 4."""
+    L = 16
+    mps = ti.random_canonical_mps(L, 16, seed=13)
+    W = ti.mpo_xxz_nn(L, 1.0)
+    t, st = _pair_p(B, mps, W, 32, 1e-12, 4, devices=[0, 0, 0, 0])
+    for _ in range(2):
+        t.step1(0.05, 4)
+        T1.step1p(st, 0.05)
+    _compare(t, st, 1e-9)
+    t.close()
+
+
+def test_hybrid_segments(B):
+    """n_segments = 2: 2TDVP (p2) until saturated, then p1TDVP; same sequence
+    and results as the oracle's hybrid on the same partition."""
     L, chi = 12, 8
     W = ti.mpo_xxz_nn(L, 1.0)
-    mps = ti.random_canonical_mps(L, chi, seed=6)
-    t, _ = _pair(B, mps, W, chi, 1e-12)
-    assert t.step_hybrid(0.05, 2) == 2
-    assert t.step_hybrid(0.05, 1) == 1
+    t, st = _pair_p(B, ti.neel_mps(L), W, chi, 1e-12, 2)
+    used_g, used_o = [], []
+    trunc = False
+    for _ in range(12):
+        used_g.append(t.step_hybrid(0.05, 2))
+        used_o.append(T1.step_hybrid(st, 0.05))
+        trunc = trunc or st.stats.trunc_active
+    assert used_g == used_o and used_g[-1] == 1
+    _compare(t, st, 1e-6 if trunc else 1e-9)
     t.close()
 
 
