@@ -241,6 +241,9 @@ int tdvp_comm_init(tdvp_t h, int rank, int world, const unsigned char* id128);
  * (Psi_{e+1}, Lambda_e, beta_{e+1} -> q+1), 4 RECV_L, 5 SEND_L (Psi_s,
  * gamma_s -> q-1), 6 RECV_R.  build: bit0 beta_{j+1}, bit1 gamma_j. */
 int tdvp_plan(int L, int p, int h, int q, int* ops, int max_ops);
+/* The same for the p1TDVP programs of tdvp_step1 (reading R-P1TDVP): kinds
+ * additionally 7 = SITE_R, 8 = SITE_L, 9 = FWD (schedule.h). */
+int tdvp_plan1(int L, int p, int h, int q, int* ops, int max_ops);
 /* Segment bounds [s, e] of segment q (SURVEY O-3). */
 int tdvp_partition(int L, int p, int* s, int* e);
 

@@ -3056,6 +3056,24 @@ int tdvp_plan(int L, int p, int hh, int q, int* ops, int max_ops) {
   return (int)prog.size();
 }
 
+int tdvp_plan1(int L, int p, int hh, int q, int* ops, int max_ops) {
+  std::vector<std::pair<int, int>> b;
+  std::string err;
+  if (!plan_partition(L, p, b, err)) return TDVP_EPARTITION;
+  if (hh < 1 || hh > 2 || q < 0 || q >= p) return TDVP_EARG;
+  std::set<int> pairs, sites;
+  merged1(L, p, b, pairs, sites);
+  const std::vector<SchedOp> prog = segment_program1(L, p, hh, q, b[q], pairs, sites);
+  if ((int)prog.size() > max_ops) return TDVP_EARG;
+  for (size_t i = 0; i < prog.size(); ++i) {
+    ops[4 * i] = prog[i].kind;
+    ops[4 * i + 1] = prog[i].j;
+    ops[4 * i + 2] = prog[i].full;
+    ops[4 * i + 3] = prog[i].build;
+  }
+  return (int)prog.size();
+}
+
 int tdvp_set_partition(tdvp_t h, int p, const int* s) {
   if (!h) return TDVP_EARG;
   try {

@@ -93,6 +93,7 @@ _SIGS = {
     "tdvp_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "tdvp_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
     "tdvp_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, C.c_int]),
+    "tdvp_plan1": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, C.c_int]),
     "tdvp_partition": (C.c_int, [C.c_int, C.c_int, _I, _I]),
     "tdvp_get_partition": (C.c_int, [C.c_void_p, _I, _I, _I]),
     "tdvp_dmrg": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _D]),
@@ -296,9 +297,10 @@ def nccl_unique_id() -> bytes:
 
 
 # ---------------------------------------------------------------- host-only
-def plan(L, p, h, q):
+def plan(L, p, h, q, one_site=False):
+    """Per-segment op list of tdvp_step (tdvp_plan) or of tdvp_step1 (tdvp_plan1)."""
     buf = (C.c_int * (4 * 8 * (L + 8)))()
-    n = lib().tdvp_plan(L, p, h, q, buf, 8 * (L + 8))
+    n = (lib().tdvp_plan1 if one_site else lib().tdvp_plan)(L, p, h, q, buf, 8 * (L + 8))
     if n < 0:
         raise TdvpError(n, f"tdvp_plan(L={L}, p={p})")
     return [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]

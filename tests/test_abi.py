@@ -77,6 +77,43 @@ def test_plan_counts_and_messages(L, p):
     assert n_fwd == 2 * (L - 1)
 
 
+@pytest.mark.parametrize("L,p", [(2, 1), (9, 1), (8, 2), (12, 4), (16, 8), (10, 2), (100, 4), (64, 8)])
+def test_plan1_protocol(L, p):
+    """p1TDVP programs (tdvp_plan1, reading R-P1TDVP): (a) the message
+    protocol of every segment and half is the p2TDVP one op for op (the NCCL
+    and lane executors need nothing new); (b) per step every site is evolved
+    forward by exactly dt and every bond that is not a segment boundary
+    backward by exactly dt (time in units of dt/2: PAIR +1 per site, +2 when
+    full; BACK -1; SITE_R/SITE_L +1 on the site unless skipped, -1 on the bond;
+    FWD +2 when full else +1)."""
+    comm = (3, 4, 5, 6)
+    site = [0] * L
+    bond = [0] * (L - 1)
+    bounds = B.partition(L, p)
+    boundary = {e for _, e in bounds[:-1]}
+    for h in (1, 2):
+        for q in range(p):
+            p1, p2 = B.plan(L, p, h, q, one_site=True), B.plan(L, p, h, q)
+            assert [op for op in p1 if op[0] in comm] == [op for op in p2 if op[0] in comm]
+            for kind, j, full, build in p1:
+                if kind == 1:
+                    site[j] += 2 if full else 1
+                    site[j + 1] += 2 if full else 1
+                elif kind == 2:
+                    site[j] -= 1
+                elif kind == 7:
+                    site[j] += 0 if full else 1
+                    bond[j] -= 1
+                elif kind == 8:
+                    site[j] += 0 if full else 1
+                    bond[j - 1] -= 1
+                elif kind == 9:
+                    site[j] += 2 if full else 1
+    assert site == [2] * L
+    assert all(bond[b] == -2 for b in range(L - 1) if b not in boundary), bond
+    assert all(bond[b] == 0 for b in boundary)
+
+
 def test_plan_serial_is_paper_sweep():
     # PAPER.md:430: L->R pairs with backward singles, rightmost pair by the full dt
     L = 6
