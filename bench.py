@@ -315,6 +315,16 @@ def secondary_c2sat(pkg, steps, warmup):
             t.step(wl["dt"], p)
         ms = [s["step_ms"] for s in timed_steps(t, wl["dt"], p, steps)]
         res["serial_ms_per_step" if p == 1 else "lanes8_ms_per_step"] = float(np.mean(ms))
+    # the same state by the segment-parallel one-site integrator (tdvp_step1,
+    # p1TDVP: one-site interiors, two-site boundary updates), 8 lanes
+    t.set_mps(wl["mps"].psi, wl["mps"].lam)
+    for _ in range(warmup):
+        t.step1(wl["dt"], 8)
+    ms = []
+    for _ in range(steps):
+        t.step1(wl["dt"], 8)
+        ms.append(t.stats()["step_ms"])
+    res["p1tdvp_lanes8_ms_per_step"] = float(np.mean(ms))
     t.close()
     res["desc"] = wl["desc"]
     return res
