@@ -121,6 +121,11 @@ typedef struct {
    * algorithmic bytes (timing=1) */
   double lz_ms_bin[4];
   double lz_bytes_bin[4];
+  /* the flops the H_eff^(2) / H_eff^(1) matvecs executed (timing=1): the
+   * algorithmic counts heff2_flop / heff1_flop (every MPO
+   * channel) minus the environments' identity channels, which are copied
+   * instead of contracted (MpoSite::lid / rid) */
+  double heff2_flop_exec, heff1_flop_exec;
 } tdvp_stats;
 
 /* Create a handle for an L-site chain of local dimension d, MPO bond dimension

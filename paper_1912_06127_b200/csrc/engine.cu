@@ -148,6 +148,13 @@ struct MpoSite {
   // H_eff^(2)'s two channel stages in one pass when its inputs fit the gather kernel
   ChanMix cm12;
   bool has12 = false;
+  // identity channels of the environments at this site (build_mpo_tables):
+  // lid: beta_j[:, Dl-1, :] = A^dag A = I (the "not started" channel: beta_0 = 1
+  // and every W_k, k < j, feeds column Dr-1 only from row Dl-1 with the
+  // identity); rid: gamma_j[:, 0, :] = B B^dag = I (the "done" channel, rows 0
+  // of every W_k, k > j).  Exact for the canonical A = U, B = W^dag of every
+  // split; H_eff then copies instead of contracting those channels
+  bool lid = false, rid = false;
   std::vector<BufPtr> store;
 };
 
@@ -473,21 +480,58 @@ size_t nnz_of(const MpoSite& ms) { return (size_t)ms.cmL.nnz; }
 
 // ---------------------------------------------------------- contractions
 // H_eff^(2) x: x, y (cl, d, d, cr)
+// stage 1 of the H_eff matvecs: T1[(a, w), :] = L[(a, w), a'] x[a', :] (n
+// columns); with the left identity channel (lid) its rows w = Dl-1 are x
+// itself (a strided copy) and the GEMM runs over the other Dl-1 channels
+// (batched by channel)
+void heff_stage1(tdvp_ctx* h, const cplx* Lenv, int Dl, bool lid, int cl, long long n, const cplx* x, cplx* T1) {
+  if (!lid || h->cur_mask[0] != nullptr) {
+    gemm(h, OP_N, OP_N, cl * Dl, (int)n, cl, Lenv, cl, x, n, T1, n, h->cur_mask[0]);
+    return;
+  }
+  CK(cudaMemcpy2DAsync(T1 + (long long)(Dl - 1) * n, (size_t)Dl * n * sizeof(cplx), x, (size_t)n * sizeof(cplx),
+                       (size_t)n * sizeof(cplx), cl, cudaMemcpyDeviceToDevice, h->st));
+  if (Dl > 1) {
+    CK(zgemm(h->st, OP_N, OP_N, cl, (int)n, cl, ONE, Lenv, (long long)Dl * cl, x, n, ZERO, T1, (long long)Dl * n,
+             Dl - 1, cl, 0, n, h->gemm_work->c(), (size_t)h->work_elems, h->cur_skip, nullptr));
+    g_gemm_count++;
+    g_launch_count++;
+  }
+}
+
+// last stage: y[r, b] = sum_{(w, b')} T[r, (w, b')] R[b, (w, b')] (rows r);
+// with the right identity channel (rid) the w = 0 term is T[r, (0, b)] (a
+// strided copy into y) and the GEMM accumulates the other Dr-1 channels
+void heff_stage_last(tdvp_ctx* h, const cplx* T, int rows, int Dr, bool rid, int cr, const cplx* Renv, cplx* y) {
+  const long long K = (long long)Dr * cr;
+  if (!rid || h->cur_mask[1] != nullptr) {
+    gemm(h, OP_N, OP_T, rows, cr, (int)K, T, K, Renv, K, y, cr, h->cur_mask[1]);
+    return;
+  }
+  CK(cudaMemcpy2DAsync(y, (size_t)cr * sizeof(cplx), T, (size_t)K * sizeof(cplx), (size_t)cr * sizeof(cplx), rows,
+                       cudaMemcpyDeviceToDevice, h->st));
+  if (Dr > 1) {
+    CK(zgemm(h->st, OP_N, OP_T, rows, cr, (int)(K - cr), ONE, T + cr, K, Renv + cr, K, ONE, y, cr, 1, 0, 0, 0,
+             h->gemm_work->c(), (size_t)h->work_elems, h->cur_skip, nullptr));
+    g_gemm_count++;
+    g_launch_count++;
+  }
+}
+
+// H_eff^(2) x: x, y (cl, d, d, cr)
 void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, const cplx* Renv, int cl, int cr,
            const cplx* x, cplx* y) {
   const int d = h->d, Dl = W1.Dl, Dm = W1.Dr, Dr = W2.Dr;
   cplx* T1 = h->T1->c();
   cplx* T2 = h->T2->c();
   // stage 1: T1[(a,w),(t1,t2,b')] = L[(a,w),a'] x[a',(t1,t2,b')]
-  gemm(h, OP_N, OP_N, cl * Dl, d * d * cr, cl, Lenv, cl, x, (long long)d * d * cr, T1, (long long)d * d * cr,
-       h->cur_mask[0]);
+  heff_stage1(h, Lenv, Dl, W1.lid, cl, (long long)d * d * cr, x, T1);
   if (W1.has12) {
     // stages 2+3 in one pass: T3[a][s1][s2][w''][b'] = sum W12[(w,t1,t2) -> (s1,s2,w'')] T1[a][w][t1][t2][b']
     cmix(h, W1.cm12, cl, cr, T1, (long long)Dl * d * d * cr, 1,
          Strides3{(long long)d * d * cr, (long long)d * cr, (long long)cr}, T2, (long long)d * d * Dr * cr, 1,
          Strides3{(long long)d * Dr * cr, (long long)Dr * cr, (long long)cr});
-    gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr,
-         h->cur_mask[1]);
+    heff_stage_last(h, T2, cl * d * d, Dr, W2.rid, cr, Renv, y);
     return;
   }
   // stage 2: T2[a][s1][w'][(t2,b')] = sum W1[w,s1,t1,w'] T1[a][w][t1][(t2,b')]
@@ -497,8 +541,7 @@ void heff2(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W1, const MpoSite& W2, 
   cmix(h, W2.cmL, cl * d, cr, T2, (long long)Dm * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T1,
        (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
   // stage 4: y[(a,s1,s2), b] = T3[(a,s1,s2),(w'',b')] R[b,(w'',b')]^T
-  gemm(h, OP_N, OP_T, cl * d * d, cr, Dr * cr, T1, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr,
-       h->cur_mask[1]);
+  heff_stage_last(h, T1, cl * d * d, Dr, W2.rid, cr, Renv, y);
 }
 
 // H_eff^(1) x: x, y (cl, d, cr)
@@ -506,10 +549,10 @@ void heff1(tdvp_ctx* h, const cplx* Lenv, const MpoSite& W, const cplx* Renv, in
   const int d = h->d, Dl = W.Dl, Dr = W.Dr;
   cplx* T1 = h->T1->c();
   cplx* T2 = h->T2->c();
-  gemm(h, OP_N, OP_N, cl * Dl, d * cr, cl, Lenv, cl, x, (long long)d * cr, T1, (long long)d * cr, h->cur_mask[0]);
+  heff_stage1(h, Lenv, Dl, W.lid, cl, (long long)d * cr, x, T1);
   cmix(h, W.cmL, cl, cr, T1, (long long)Dl * d * cr, 1, Strides3{(long long)d * cr, (long long)cr, 0}, T2,
        (long long)d * Dr * cr, 1, Strides3{(long long)Dr * cr, (long long)cr, 0});
-  gemm(h, OP_N, OP_T, cl * d, cr, Dr * cr, T2, (long long)Dr * cr, Renv, (long long)Dr * cr, y, cr, h->cur_mask[1]);
+  heff_stage_last(h, T2, cl * d, Dr, W.rid, cr, Renv, y);
 }
 
 // beta'[b,w',b'] = sum conj(A[a,s,b]) beta[a,w,a'] W[w,s,t,w'] A[a',t,b']
@@ -542,13 +585,25 @@ double flops_heff2(int cl, int cr, int d, int Dl, int Dr, size_t nnz1, size_t nn
   return 8.0 * ((double)d * d * cl * cr * ((double)Dl * cl + (double)Dr * cr) +
                 (double)d * cl * cr * (double)(nnz1 + nnz2));
 }
+// flops the H_eff matvecs execute: the identity channels (MpoSite::lid/rid)
+// are copied, not contracted
+double flops_heff2_exec(int cl, int cr, int d, int Dl, int Dr, size_t nnz1, size_t nnz2, bool lid, bool rid) {
+  return 8.0 * ((double)d * d * cl * cr * ((double)(Dl - (lid ? 1 : 0)) * cl + (double)(Dr - (rid ? 1 : 0)) * cr) +
+                (double)d * cl * cr * (double)(nnz1 + nnz2));
+}
+double flops_heff1_exec(int cl, int cr, int d, int Dl, int Dr, size_t nnz, bool lid, bool rid) {
+  return 8.0 * ((double)d * cl * cr * ((double)(Dl - (lid ? 1 : 0)) * cl + (double)(Dr - (rid ? 1 : 0)) * cr) +
+                (double)cl * cr * (double)nnz);
+}
 double flops_heff1(int cl, int cr, int d, int Dl, int Dr, size_t nnz) {
   return 8.0 * ((double)d * cl * cr * ((double)Dl * cl + (double)Dr * cr) + (double)cl * cr * (double)nnz);
 }
 
 // exp(tau H) x -> out, device-resident Lanczos (SURVEY O-10)
 void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& matvec, const cplx* x, cplx* out,
-                  long long n, double tre, double tim, int K, int which /*2: heff2 1: heff1 0: other*/, double mv_flop) {
+                  long long n, double tre, double tim, int K, int which /*2: heff2 1: heff1 0: other*/, double mv_flop,
+                  double mv_flop_exec = -1.0) {
+  if (mv_flop_exec < 0.0) mv_flop_exec = mv_flop;
   cplx* V = h->krylov->c();
   cplx* w = h->wvec->c();
   const bool tm = h->prm.timing && which;
@@ -571,11 +626,13 @@ void expm_lanczos(tdvp_ctx* h, const std::function<void(const cplx*, cplx*)>& ma
       (which == 2 ? h->ev_h2 : h->ev_h1).emplace_back(e0, e1);
       if (which == 2) {
         h->stats.heff2_flop += mv_flop;
+        h->stats.heff2_flop_exec += mv_flop_exec;
         h->stats.heff2_calls++;
         h->stats.heff2_flop_bin[h->cur_bin] += mv_flop;
         h->ev_h2_bin.push_back(h->cur_bin);
       } else {
         h->stats.heff1_flop += mv_flop;
+        h->stats.heff1_flop_exec += mv_flop_exec;
       }
     }
     CK(lz_iter(h->st, h->lz, V, n, k + 1, w, V + (long long)(k + 1) * n, n, k, k + 1 == K ? 1 : 0, ktol, tre, tim));
@@ -1047,7 +1104,8 @@ void pair_update(tdvp_ctx* h, Segment& g, int j, double dt, int full, int build)
   set_heff_masks(h, g, j, 2);
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff2(h, Lenv, W1, W2, Renv, cl, cr, x, y); }, th, th2, n, 0.0, -tau,
-      h->prm.krylov_k, 2, fl);
+      h->prm.krylov_k, 2, fl,
+      h->prm.u1 ? fl : flops_heff2_exec(cl, cr, d, W1.Dl, W2.Dr, nnz_of(W1), nnz_of(W2), W1.lid, W2.rid));
   h->cur_mask[0] = h->cur_mask[1] = nullptr;
   if (el0 >= 0) h->ev_lz2.emplace_back(el0, ev_record(h));
   // a4: truncated SVD split
@@ -1183,7 +1241,8 @@ void back_update(tdvp_ctx* h, Segment& g, int j, double dt) {
   set_heff_masks(h, g, j, 1);
   expm_lanczos(
       h, [&](const cplx* x, cplx* y) { heff1(h, Lenv, W, Renv, cl, cr, x, y); }, h->tmpB->c(), P(g.psi[j]), n, 0.0,
-      0.5 * dt, h->prm.krylov_k, 1, fl);
+      0.5 * dt, h->prm.krylov_k, 1, fl,
+      h->prm.u1 ? fl : flops_heff1_exec(cl, cr, d, W.Dl, W.Dr, nnz_of(W), W.lid, W.rid));
   h->cur_mask[0] = h->cur_mask[1] = nullptr;
   if (el0 >= 0) h->ev_lz1.emplace_back(el0, ev_record(h));
   h->stats.n_back++;
@@ -1884,6 +1943,7 @@ void reset_step_stats(tdvp_ctx* h) {
   h->stats.svd_bj_ms = h->stats.svd_bj_flop = 0.0;
   h->stats.svd_bj_calls = 0;
   h->stats.heff2_flop = h->stats.heff1_flop = 0.0;
+  h->stats.heff2_flop_exec = h->stats.heff1_flop_exec = 0.0;
   h->stats.heff2_calls = 0;
   h->stats.lz_vec_bytes = 0.0;
   for (int i = 0; i < 4; ++i) h->stats.heff2_ms_bin[i] = h->stats.heff2_flop_bin[i] = 0.0;
@@ -1985,6 +2045,8 @@ void run_step_lanes(tdvp_ctx* h, double dt, const std::set<int>& merged) {
     a.heff2_flop += b.heff2_flop;
     a.heff2_calls += b.heff2_calls;
     a.heff1_flop += b.heff1_flop;
+    a.heff2_flop_exec += b.heff2_flop_exec;
+    a.heff1_flop_exec += b.heff1_flop_exec;
     a.lz_vec_bytes += b.lz_vec_bytes;
     for (int i = 0; i < 4; ++i) a.heff2_flop_bin[i] += b.heff2_flop_bin[i];
     for (int i = 0; i < 4; ++i) a.lz_bytes_bin[i] += b.lz_bytes_bin[i];
@@ -2191,6 +2253,27 @@ void build_mpo_tables(std::vector<MpoSite>& mpo, int L, int d, const std::vector
   mpo.resize(L);
   for (int j = 0; j < L; ++j) build_site(mpo[j], D[j], D[j + 1], d, W[j]);
   for (int j = 0; j + 1 < L; ++j) build_pair(mpo[j], D[j], D[j + 1], D[j + 2], d, W[j], W[j + 1]);
+  // identity-channel structure (MpoSite::lid / rid)
+  auto at = [&](int j, int w, int s, int t, int w2) { return W[j][(((size_t)w * d + s) * d + t) * D[j + 1] + w2]; };
+  auto is = [](cplx v, double x) { return v.x == x && v.y == 0.0; };
+  auto col_last_identity = [&](int j) {  // column D_{j+1}-1 fed only by row D_j-1 with the identity
+    for (int w = 0; w < D[j]; ++w)
+      for (int s = 0; s < d; ++s)
+        for (int t = 0; t < d; ++t)
+          if (!is(at(j, w, s, t, D[j + 1] - 1), (w == D[j] - 1 && s == t) ? 1.0 : 0.0)) return false;
+    return true;
+  };
+  auto row0_identity = [&](int j) {  // row 0 feeds only column 0 with the identity
+    for (int w2 = 0; w2 < D[j + 1]; ++w2)
+      for (int s = 0; s < d; ++s)
+        for (int t = 0; t < d; ++t)
+          if (!is(at(j, 0, s, t, w2), (w2 == 0 && s == t) ? 1.0 : 0.0)) return false;
+    return true;
+  };
+  mpo[0].lid = true;
+  for (int j = 1; j < L; ++j) mpo[j].lid = mpo[j - 1].lid && col_last_identity(j - 1);
+  mpo[L - 1].rid = true;
+  for (int j = L - 2; j >= 0; --j) mpo[j].rid = mpo[j + 1].rid && row0_identity(j + 1);
 }
 
 // ------------------------------------------------------------ workspace

@@ -54,7 +54,7 @@ class tdvp_stats(C.Structure):
                 ("env_ms", C.c_double), ("heff2_ms_bin", C.c_double * 4), ("heff2_flop_bin", C.c_double * 4),
                 ("lz_vec_bytes", C.c_double), ("rebalances", C.c_int), ("svd_bj_ms", C.c_double),
                 ("svd_bj_flop", C.c_double), ("svd_bj_calls", C.c_int), ("lz_ms_bin", C.c_double * 4),
-                ("lz_bytes_bin", C.c_double * 4)]
+                ("lz_bytes_bin", C.c_double * 4), ("heff2_flop_exec", C.c_double), ("heff1_flop_exec", C.c_double)]
 
     def as_dict(self):
         out = {}
