@@ -34,6 +34,57 @@
 #include "kernels.h"
 #include "schedule.h"
 
+// Page-locked host storage for the full-state host copy: tdvp_set_mps /
+// upload_state / download_state move up to d chi_max^2 L complex values per
+// call, which DMA straight from pinned pages (no staging through the driver's
+// bounce buffers); the pages are kept while the shapes stay (assign / resize
+// of an equal size does not reallocate).
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable) != cudaSuccess || !p) {
+      cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+using hvec = std::vector<double, PinnedAlloc<double>>;
+
+// f(k, i0, i1) over the concatenated element ranges [0, sizes[k]), split
+// evenly over up to 8 host threads (the full-state validation and copy of
+// tdvp_set_mps: d chi_max^2 L doubles, memory-bandwidth bound on one core)
+template <class F>
+void host_parallel(const std::vector<size_t>& sizes, F f) {
+  size_t total = 0;
+  for (size_t n : sizes) total += n;
+  const unsigned hc = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const int T = (int)std::max<size_t>(1, std::min<size_t>(hc, total >> 20));
+  auto work = [&](int t) {
+    const size_t lo = total * t / T, hi = total * (t + 1) / T;
+    size_t base = 0;
+    for (size_t k = 0; k < sizes.size() && base < hi; base += sizes[k], ++k) {
+      const size_t a = std::max(lo, base), b = std::min(hi, base + sizes[k]);
+      if (a < b) f(k, a - base, b - base);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
 namespace {
 
 // ------------------------------------------------------------------ errors
@@ -240,7 +291,8 @@ struct tdvp_ctx {
   std::vector<std::pair<int, int>> custom;  // tdvp_set_partition: explicit bounds for n_segments = custom.size()
   std::vector<Segment> segs;
   // full-state host copy (multi-process initialisation)
-  std::vector<std::vector<double>> h_psi, h_lam;
+  std::vector<hvec> h_psi;  // pinned
+  std::vector<std::vector<double>> h_lam;
   std::vector<int> h_chi;
   std::vector<std::vector<int>> h_q;  // U(1) mode: bond charges of the host copy (positions 0..L)
   BufPtr u1_idx, u1_lam, u1_vinv;     // U(1) split: sector index lists, per-sector spectra
@@ -714,7 +766,7 @@ std::vector<std::vector<int>> infer_charges(const tdvp_ctx* h) {
   const int UNSET = std::numeric_limits<int>::min();
   for (int j = 0; j < L; ++j) {
     const int cl = h->h_chi[j], cr = h->h_chi[j + 1];
-    const std::vector<double>& t = h->h_psi[j];
+    const hvec& t = h->h_psi[j];
     q[j + 1].assign(cr, UNSET);
     for (int a = 0; a < cl; ++a)
       for (int s = 0; s < d; ++s)
@@ -2504,7 +2556,7 @@ void reorthonormalize(tdvp_ctx* h) {
       chi[j] = k;
     }
     // download, normalise, Psi_0 = A_0 / n, Lambda /= n, Psi_j = Lambda_{j-1} B_j
-    std::vector<std::vector<double>> hpsi(L);
+    std::vector<hvec> hpsi(L);
     for (int j = 0; j < L; ++j) {
       hpsi[j].resize((size_t)chi[j] * d * chi[j + 1] * 2);
       CK(cudaMemcpyAsync(hpsi[j].data(), A[j]->p, hpsi[j].size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
@@ -2782,14 +2834,19 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     // validate everything first (the handle keeps its state on error), then
     // copy into the existing host vectors (their pages are reused: no
     // allocation or page faults per call for the same shapes)
+    std::vector<size_t> sz(L);
     for (int j = 0; j < L; ++j) {
       if (!Psi[j]) throw TdvpError(TDVP_EARG, "null Psi");
-      const size_t n = (size_t)chi[j] * d * chi[j + 1] * 2;
+      sz[j] = (size_t)chi[j] * d * chi[j + 1] * 2;
+    }
+    std::atomic<bool> bad{false};
+    host_parallel(sz, [&](size_t j, size_t i0, size_t i1) {
       const double* src = Psi[j];
       bool fin = true;
-      for (size_t i = 0; i < n; ++i) fin &= std::isfinite(src[i]);
-      if (!fin) throw TdvpError(TDVP_ENONFINITE, "non-finite Psi entry");
-    }
+      for (size_t i = i0; i < i1; ++i) fin &= std::isfinite(src[i]);
+      if (!fin) bad = true;
+    });
+    if (bad) throw TdvpError(TDVP_ENONFINITE, "non-finite Psi entry");
     for (int b = 0; b < L - 1; ++b) {
       if (!Lambda[b]) throw TdvpError(TDVP_EARG, "null Lambda");
       for (int i = 0; i < chi[b + 1]; ++i)
@@ -2798,7 +2855,14 @@ int tdvp_set_mps(tdvp_t h, const int* chi, const double* const* Psi, const doubl
     }
     h->h_psi.resize(L);
     h->h_lam.resize(L - 1);
-    for (int j = 0; j < L; ++j) h->h_psi[j].assign(Psi[j], Psi[j] + (size_t)chi[j] * d * chi[j + 1] * 2);
+    for (int j = 0; j < L; ++j)
+      if (h->h_psi[j].size() != sz[j]) {
+        h->h_psi[j].clear();
+        h->h_psi[j].resize(sz[j]);
+      }
+    host_parallel(sz, [&](size_t j, size_t i0, size_t i1) {
+      std::memcpy(h->h_psi[j].data() + i0, Psi[j] + i0, (i1 - i0) * sizeof(double));
+    });
     for (int b = 0; b < L - 1; ++b) h->h_lam[b].assign(Lambda[b], Lambda[b] + chi[b + 1]);
     h->h_chi.assign(chi, chi + L + 1);
     h->h_q.clear();  // U(1) charges are re-inferred at the next layout
@@ -3034,7 +3098,8 @@ int tdvp_get_mps(tdvp_t h, double** Psi, double** Lambda) {
       // descending Lambda: permute each bond on the host copy on the way out
       const int L = h->L, d = h->d;
       if (h->layout_p != 0) download_state(h);
-      std::vector<std::vector<double>> ps = h->h_psi;
+      std::vector<std::vector<double>> ps;
+      for (const hvec& v : h->h_psi) ps.emplace_back(v.begin(), v.end());
       std::vector<std::vector<double>> lm = h->h_lam;
       const std::vector<int>& chi = h->h_chi;
       for (int b = 0; b + 1 < L; ++b) {

@@ -267,10 +267,21 @@ class Tdvp:
         _check(lib().tdvp_get_chi(self.h, out), self.h)
         return list(out)
 
-    def get_mps(self):
+    def get_mps(self, out=None):
+        """The current MPS (inverse-canonical Psi_j, Lambda_b).  out = (psi, lam):
+        caller-owned C-contiguous arrays (e.g. pinned host memory) filled in
+        place when their shapes match the current bond dimensions."""
         chi = self.chi()
-        psi = [np.zeros((chi[j], self.d, chi[j + 1]), dtype=np.complex128) for j in range(self.L)]
-        lam = [np.zeros(chi[b + 1]) for b in range(self.L - 1)]
+        shp = [(chi[j], self.d, chi[j + 1]) for j in range(self.L)]
+        if (out is not None and len(out[0]) == self.L and len(out[1]) == self.L - 1
+                and all(o.shape == s and o.dtype == np.complex128 and o.flags.c_contiguous
+                        for o, s in zip(out[0], shp))
+                and all(o.shape == (chi[b + 1],) and o.dtype == np.float64 and o.flags.c_contiguous
+                        for b, o in enumerate(out[1]))):
+            psi, lam = out
+        else:
+            psi = [np.zeros(s, dtype=np.complex128) for s in shp]
+            lam = [np.zeros(chi[b + 1]) for b in range(self.L - 1)]
         pa = (_D * self.L)(*[p.ctypes.data_as(_D) for p in psi])
         la = (_D * max(1, self.L - 1))(*[l.ctypes.data_as(_D) for l in lam])
         _check(lib().tdvp_get_mps(self.h, pa, la), self.h)

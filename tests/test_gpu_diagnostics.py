@@ -199,3 +199,46 @@ def test_set_partition_validation(B):
     t.step(0.05, 2)
     assert abs(t.measure_norm() - 1.0) < 1e-9
     t.close()
+
+
+def test_set_get_mps_pinned_buffers(B):
+    """set_mps from page-locked host arrays, get_mps into caller-owned pinned
+    buffers (the bench's e2e path): same state as the default allocating
+    get_mps after a step, buffers filled in place; mismatched out buffers
+    fall back to fresh arrays; a non-finite entry is rejected (the threaded
+    validation) and the handle keeps its state."""
+    import torch
+    L, chi_max = 12, 16
+    W = ti.mpo_xxz_nn(L, 0.7)
+    mps = ti.random_canonical_mps(L, chi_max, seed=11)
+
+    def pin(a):
+        x = torch.empty(a.shape, dtype=torch.complex128 if np.iscomplexobj(a) else torch.float64,
+                        pin_memory=True).numpy()
+        x[...] = a
+        return x
+
+    t = handle(B, W, mps, chi_max, eps=1e-14)
+    t.set_mps([pin(x) for x in mps.psi], [pin(x) for x in mps.lam])
+    t.step(0.05, 2)
+    ref_psi, ref_lam = t.get_mps()
+    chi = t.chi()
+    out = ([pin(np.zeros((chi[j], 2, chi[j + 1]), np.complex128)) for j in range(L)],
+           [pin(np.zeros(chi[b + 1])) for b in range(L - 1)])
+    psi, lam = t.get_mps(out)
+    assert all(a is b for a, b in zip(psi, out[0])) and all(a is b for a, b in zip(lam, out[1]))
+    for a, b in zip(psi, ref_psi):
+        assert np.array_equal(a, b)
+    for a, b in zip(lam, ref_lam):
+        assert np.array_equal(a, b)
+    bad = ([np.zeros((1, 2, 1), np.complex128)] * L, out[1])
+    psi2, _ = t.get_mps(bad)
+    assert psi2[0] is not bad[0] and all(np.array_equal(a, b) for a, b in zip(psi2, ref_psi))
+    # non-finite input: rejected, the evolved state is kept
+    nf = [x.copy() for x in ref_psi]
+    nf[L // 2].flat[-1] = np.nan
+    with pytest.raises(B.TdvpError):
+        t.set_mps(nf, ref_lam)
+    psi3, _ = t.get_mps()
+    assert all(np.array_equal(a, b) for a, b in zip(psi3, ref_psi))
+    t.close()
