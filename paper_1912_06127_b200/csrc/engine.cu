@@ -120,23 +120,24 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (tried) return api;
-  tried = true;
-  void* hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
-  if (!hd) hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!hd) return api;
-  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(hd, "ncclGetUniqueId");
-  api.CommInitRank = (decltype(api.CommInitRank))dlsym(hd, "ncclCommInitRank");
-  api.CommDestroy = (decltype(api.CommDestroy))dlsym(hd, "ncclCommDestroy");
-  api.Send = (decltype(api.Send))dlsym(hd, "ncclSend");
-  api.Recv = (decltype(api.Recv))dlsym(hd, "ncclRecv");
-  api.GroupStart = (decltype(api.GroupStart))dlsym(hd, "ncclGroupStart");
-  api.GroupEnd = (decltype(api.GroupEnd))dlsym(hd, "ncclGroupEnd");
-  api.GetErrorString = (decltype(api.GetErrorString))dlsym(hd, "ncclGetErrorString");
-  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
-           api.GroupEnd && api.GetErrorString;
+  // resolved once, thread-safe (function-local static initialisation)
+  static NcclApi api = [] {
+    NcclApi a;
+    void* hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!hd) hd = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!hd) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(hd, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(hd, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(hd, "ncclCommDestroy");
+    a.Send = (decltype(a.Send))dlsym(hd, "ncclSend");
+    a.Recv = (decltype(a.Recv))dlsym(hd, "ncclRecv");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(hd, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(hd, "ncclGroupEnd");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(hd, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd &&
+           a.GetErrorString;
+    return a;
+  }();
   return api;
 }
 
@@ -2590,8 +2591,8 @@ int fail(tdvp_ctx* h, const TdvpError& e) {
 }
 
 void init_device_globals() {
-  static bool done = false;
-  if (done) return;
+  static std::atomic<bool> done{false};
+  if (done.load()) return;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     int sms = 0;

@@ -12,6 +12,7 @@
 // all four in ONE cooperative launch per iteration (lz_iter_kernel).
 // then an on-device K x K symmetric tridiagonal eigen-decomposition
 // (cyclic Jacobi) for y = n0 Q exp(tau mu) Q^T e_1 and v' = V y.
+#include <atomic>
 #include <cstdlib>
 #include <cooperative_groups.h>
 #include "common.cuh"
@@ -540,7 +541,7 @@ cudaError_t lz_tridiag_ground(cudaStream_t st, const LanczosDev& d, int K) {
 }
 cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long long ldv, int nv, cplx* w, cplx* vnext,
                     long long n, int k, int last, double tol, double tau_re, double tau_im) {
-  static int occ[KMAX + 1] = {0};
+  static std::atomic<int> occ[KMAX + 1];  // per-variant occupancy, set once (lanes call concurrently)
   void* fn = nullptr;
   switch (nv) {
 #define LZI(NVV) case NVV: fn = (void*)lz_iter_kernel<NVV>; break;
@@ -550,10 +551,10 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e;
-  if (occ[nv] == 0) {
+  if (occ[nv].load(std::memory_order_relaxed) == 0) {
     int o = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, TPB, 0)) != cudaSuccess) return e;
-    occ[nv] = std::max(1, o);
+    occ[nv].store(std::max(1, o), std::memory_order_relaxed);
   }
   // partials: two buffers of G * 2 * (KMAX + 1) doubles inside d.partials (4 * SMs blocks' worth)
   // grid-wide barriers get cheaper with fewer blocks: 64 blocks for small
@@ -562,7 +563,7 @@ cudaError_t lz_iter(cudaStream_t st, const LanczosDev& d, const cplx* V, long lo
   // (measured: 2K elements per block keeps HBM busy from chi = 512 up)
   const long long want = std::max<long long>(64, n / 2048);
   // every block sums all G partials (deterministic order): G <= 2 * SMs
-  const long long cap = (long long)std::min(occ[nv], 2) * g_num_sms;
+  const long long cap = (long long)std::min(occ[nv].load(std::memory_order_relaxed), 2) * g_num_sms;
   const int G = (int)std::max<long long>(
       1, std::min<long long>(std::min<long long>((n + TPB - 1) / TPB, cap), want));
   void* args[] = {(void*)&d,    (void*)&V,   (void*)&ldv, (void*)&w,      (void*)&vnext, (void*)&n,

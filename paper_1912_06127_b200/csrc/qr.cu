@@ -1088,8 +1088,7 @@ cudaError_t qr_factor_cluster(cudaStream_t st, cplx* A, long long lda, int m, in
   }
   unsigned* nog = nullptr;
   e = cudaLaunchKernelEx(&cfg, fn, A, lda, m, n, cw, tau, RH, ldrh, rh_rows, nog);
-  static int prof = -1;
-  if (prof < 0) prof = std::getenv("TDVP_QR_PROF") ? 1 : 0;
+  static const int prof = std::getenv("TDVP_QR_PROF") ? 1 : 0;  // thread-safe once (lanes call this concurrently)
   if (prof && e == cudaSuccess) {
     unsigned long long z[16][4];
     cudaMemcpyFromSymbolAsync(z, g_qr_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);

@@ -957,11 +957,10 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
   // U(1) sector workers) the grid-filling bjac would serialise them, so there
   // it only takes what rjac cannot (> 1024 columns).  TDVP_SVD_BJ_MIN
   // overrides the threshold (the parity tests force both paths).
-  static int bj_env = -2;
-  if (bj_env == -2) {
+  static const int bj_env = [] {  // thread-safe once (segment lanes / U(1) workers call this concurrently)
     const char* ev = std::getenv("TDVP_SVD_BJ_MIN");
-    bj_env = ev ? std::atoi(ev) : -1;
-  }
+    return ev ? std::atoi(ev) : -1;
+  }();
   const int bj_min = bj_env >= 0 ? bj_env : (d.throughput ? 1025 : 300);
   if ((e = cudaMemsetAsync(d.dres + 2, 0, sizeof(double), st)) != cudaSuccess) return e;
   bool bj = false;
@@ -1013,8 +1012,7 @@ cudaError_t svd_truncate_split(cudaStream_t st, const SvdDev& d, const cplx* the
     int occ = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nth, dsm)) != cudaSuccess) return e;
     const int grid = std::max(1, std::min(nbe / 2, occ * g_num_sms));
-    static int prof = -1;
-    if (prof < 0) prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;
+    static const int prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;  // thread-safe once
     if (prof) {
       unsigned long long z[8] = {0};
       cudaMemcpyToSymbolAsync(g_svd_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);

@@ -821,8 +821,7 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
   a.offb = d.offmax;
   a.sweeps_out = sweeps_dev;
   a.flop_out = flop_dev;
-  static int prof = -1;
-  if (prof < 0) prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;
+  static const int prof = std::getenv("TDVP_SVD_PROF") ? 1 : 0;  // thread-safe once
   a.prof = prof;
   a.inner_max = 1;  // one inner sweep per round (measured fastest: the outer sweep count does not grow)
   if (prof) {
@@ -849,11 +848,10 @@ cudaError_t svd_bjac_run(cudaStream_t st, const SvdDev& d, int xr, int vofs, int
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int ncl = 0;
-    static int use_cl = -1;
-    if (use_cl < 0) {
+    static const int use_cl = [] {  // thread-safe once
       const char* ev = std::getenv("TDVP_BJ_CLUSTER");
-      use_cl = ev ? std::atoi(ev) : 1;
-    }
+      return ev ? std::atoi(ev) : 1;
+    }();
     if (use_cl && S > 1 && cudaOccupancyMaxActiveClusters(&ncl, fnc, &cfg) == cudaSuccess && ncl >= P) {
       cfg.numAttrs = 2;
       e = cudaLaunchKernelEx(&cfg, bjac_kernel<true>, a);

@@ -869,11 +869,10 @@ bool rows_ok(int row, int mr, int nc) {
 // cudaErrorNotSupported when no register-resident variant fits the shape.
 cudaError_t svd_rjac_run(cudaStream_t st, const SvdDev& d, int mr, int vofs, int nc, long long ldy, double tol,
                          int* sweeps_dev) {
-  static int prof = -1;
-  if (prof < 0) {
+  static const int prof = [] {  // thread-safe once
     const char* pe = std::getenv("TDVP_SVD_PROF");  // per-phase cycle counts on stderr (diagnostics only)
-    prof = pe ? std::max(1, std::atoi(pe)) : 0;
-  }
+    return pe ? std::max(1, std::atoi(pe)) : 0;
+  }();
   constexpr int full_rounds = 0, fastp = 0;
   int row = -1;
   {
